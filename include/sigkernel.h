@@ -1,0 +1,123 @@
+/*
+ * sigkernel.h -- C ABI of the B200 (sm_100a) signature-kernel hot path.
+ *
+ * Drop-in boundary for the reference's kernel entry points.  The reference
+ * (sigcore 0.1.0) binds its solver through numba functions that take
+ * caller-allocated buffers and never allocate (/root/reference/pkg/src/sigcore/
+ * _kernels.py:9-12); this ABI keeps that contract with device pointers:
+ *
+ *   sk_forward_batch   replaces kernel.py:125-148   (kernel_batch  -> goursat_batch,
+ *                                                    _kernels.py:399-405)
+ *   sk_forward_gram    replaces kernel.py:151-180   (kernel_gram   -> goursat_gram,
+ *                                                    _kernels.py:408-429), plus a
+ *                                                    row range for sharding
+ *   sk_solve_delta     replaces kernel.py:94-122    (solve_goursat on a given delta,
+ *                                                    goursat_strip/_grid)
+ *   sk_solve_delta_grid                             (store_grid=True path,
+ *                                                    _kernels.py:381-396)
+ *   sk_backward_batch  replaces kernel_grad.py:64-98 (kernel_batch_backward ->
+ *                                                    goursat_grid + goursat_backward,
+ *                                                    _kernels.py:436-466, plus the
+ *                                                    dF/d(delta) -> dF/dx mapping of
+ *                                                    kernel_grad.py:51-60)
+ *   sk_backward_gram   (no reference counterpart: Gram backward composed from
+ *                       kernel_backward per pair)
+ *
+ * Conventions
+ *   - every array pointer is DEVICE memory, C-contiguous float64, borrowed for
+ *     the duration of the call; outputs and the workspace are caller-allocated
+ *     (size the workspace with the matching *_workspace_bytes query);
+ *   - paths are (n, L, d) row-major; L >= 2;
+ *   - static_kernel: SK_STATIC_LINEAR (<a,b>, the reference's increment_gram)
+ *     or SK_STATIC_RBF (exp(-|a-b|^2 / (2 sigma^2)); no reference counterpart);
+ *   - work is enqueued on `stream` (a cudaStream_t, NULL = legacy default) and
+ *     the call returns without synchronising;
+ *   - return value: SK_OK, or an error code whose message sk_last_error()
+ *     returns (thread-local).  SK_INVALID_ARGUMENT / SK_INVALID_STATE map to
+ *     the reference's InvalidArgument(ValueError) / InvalidState(RuntimeError)
+ *     (errors.py:4-12).  Non-finite values are never trapped: overflow
+ *     propagates as inf, NaN as NaN (kernel.py:97-99).
+ */
+#ifndef SIGKERNEL_H
+#define SIGKERNEL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SK_ABI_VERSION 1
+
+enum {
+  SK_OK = 0,
+  SK_INVALID_ARGUMENT = 1,
+  SK_INVALID_STATE = 2,
+  SK_CUDA_ERROR = 3
+};
+
+enum { SK_STATIC_LINEAR = 0, SK_STATIC_RBF = 1 };
+
+int sk_abi_version(void);
+const char *sk_last_error(void);
+/* number of SMs of the current device (the persistent-grid size basis) */
+int sk_device_sms(void);
+
+/* ---- forward ----------------------------------------------------------- */
+
+size_t sk_forward_batch_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d,
+                                        int lam1, int lam2, int static_kernel);
+/* out[b] = k(x_b, y_b);  x (B,L1,d), y (B,L2,d), out (B,) */
+int sk_forward_batch(const double *x, const double *y, int64_t B, int64_t L1, int64_t L2,
+                     int64_t d, int lam1, int lam2, int static_kernel, double sigma,
+                     double *out, void *workspace, size_t workspace_bytes, void *stream);
+
+size_t sk_forward_gram_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                       int64_t d, int lam1, int lam2, int static_kernel,
+                                       int symmetric);
+/* out[a - row_begin, b] = k(x_a, y_b) for a in [row_begin, row_end), b < n2.
+ * y == NULL means y is x (symmetric): only pairs a <= b are solved and the
+ * in-range part of the lower triangle is mirrored (kernel.py:177-179);
+ * entries with a > b outside the row range are left untouched. */
+int sk_forward_gram(const double *x, const double *y, int64_t n1, int64_t n2, int64_t L1,
+                    int64_t L2, int64_t d, int lam1, int lam2, int static_kernel,
+                    double sigma, int64_t row_begin, int64_t row_end, double *out,
+                    void *workspace, size_t workspace_bytes, void *stream);
+
+size_t sk_solve_delta_workspace_bytes(int64_t B, int64_t r1, int64_t r2, int lam1, int lam2);
+/* out[b] = solve_goursat(delta_b) for delta (B, r1, r2) */
+int sk_solve_delta(const double *delta, int64_t B, int64_t r1, int64_t r2, int lam1,
+                   int lam2, double *out, void *workspace, size_t workspace_bytes,
+                   void *stream);
+/* full fine grid ((r1<<lam1)+1, (r2<<lam2)+1) of one delta (B = 1) */
+int sk_solve_delta_grid(const double *delta, int64_t r1, int64_t r2, int lam1, int lam2,
+                        double *grid, void *stream);
+
+/* ---- backward ---------------------------------------------------------- */
+
+size_t sk_backward_batch_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d,
+                                         int lam1, int lam2, int static_kernel);
+/* grad_x = sum_b cot[b] dk(x_b,y_b)/dx_b, grad_y likewise; values (B,) optional
+ * (NULL to skip).  cot == NULL means ones (kernel_grad.py:81-82). */
+int sk_backward_batch(const double *x, const double *y, int64_t B, int64_t L1, int64_t L2,
+                      int64_t d, int lam1, int lam2, int static_kernel, double sigma,
+                      const double *cot, double *values, double *grad_x, double *grad_y,
+                      void *workspace, size_t workspace_bytes, void *stream);
+
+size_t sk_backward_gram_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                        int64_t d, int lam1, int lam2, int static_kernel,
+                                        int symmetric);
+/* F = sum_{a in rows, b} cot[a - row_begin, b] G[a, b];  grad_x += dF/dx,
+ * grad_y += dF/dy (grad_y unused when y == NULL: both sides land in grad_x).
+ * Gradients ACCUMULATE into the caller's buffers (zero them first). */
+int sk_backward_gram(const double *x, const double *y, int64_t n1, int64_t n2, int64_t L1,
+                     int64_t L2, int64_t d, int lam1, int lam2, int static_kernel,
+                     double sigma, int64_t row_begin, int64_t row_end, const double *cot,
+                     double *grad_x, double *grad_y, void *workspace, size_t workspace_bytes,
+                     void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SIGKERNEL_H */

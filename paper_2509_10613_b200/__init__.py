@@ -1,0 +1,15 @@
+"""B200-native (sm_100a) signature-kernel hot path of pySigLib (arXiv 2509.10613).
+
+Public API (pySigLib style, torch autograd):
+    sig_kernel, sig_kernel_gram, LinearKernel, RBFKernel
+Reference-compatible numpy facade (sigcore names): paper_2509_10613_b200.sigcore_compat
+Multi-GPU Gram sharding: paper_2509_10613_b200.gram_dist
+"""
+
+from .api import LinearKernel, RBFKernel, sig_kernel, sig_kernel_gram
+from .errors import InvalidArgument, InvalidState, NativeUnavailable
+
+__version__ = "0.1.0"
+
+__all__ = ["sig_kernel", "sig_kernel_gram", "LinearKernel", "RBFKernel", "InvalidArgument",
+           "InvalidState", "NativeUnavailable", "__version__"]

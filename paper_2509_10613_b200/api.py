@@ -1,0 +1,144 @@
+"""pySigLib-style torch API: sig_kernel / sig_kernel_gram with autograd.
+
+    k = sig_kernel(x, y, dyadic_order=1)                  # (B,)
+    G = sig_kernel_gram(X, dyadic_order=(0, 1),
+                        static_kernel=RBFKernel(0.5))     # (n, n)
+    loss = (G * C).sum(); loss.backward()
+
+Forward and backward both run hand-written sm_100a kernels through the C ABI
+(include/sigkernel.h).  The backward is the paper's exact scheme
+(differentiate the solver, Alg. 4 / reference kernel_grad.py), done
+as a reverse wavefront that recomputes forward values from checkpoints
+instead of storing the full PDE grid.
+
+dtype rule (reference kernel.py:36-38, _kernels.py:325): float32 inputs are
+solved in float64 arithmetic and the result is returned as float32, exactly
+like the reference's "fp32 storage, fp64 math" path.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import ops
+from .errors import InvalidArgument
+
+
+@dataclass(frozen=True)
+class LinearKernel:
+    """Static kernel <a, b> (the reference's increment_gram, kernel.py:60-77)."""
+    kind: str = "linear"
+
+
+@dataclass(frozen=True)
+class RBFKernel:
+    """Static kernel exp(-|a - b|^2 / (2 sigma^2)) (no reference counterpart;
+    convention documented in DESIGN.md)."""
+    sigma: float = 1.0
+    kind: str = "rbf"
+
+    def __post_init__(self):
+        if not self.sigma > 0:
+            raise InvalidArgument("RBF sigma must be > 0")
+
+
+def _orders(dyadic_order):
+    if isinstance(dyadic_order, (tuple, list)):
+        if len(dyadic_order) != 2:
+            raise InvalidArgument("dyadic_order must be an int or a pair (lam1, lam2)")
+        l1, l2 = int(dyadic_order[0]), int(dyadic_order[1])
+    else:
+        l1 = l2 = int(dyadic_order)
+    if l1 < 0 or l2 < 0:
+        raise InvalidArgument("dyadic orders must be >= 0")
+    return l1, l2
+
+
+def _batched(t, name):
+    if not isinstance(t, torch.Tensor):
+        raise InvalidArgument(f"{name} must be a torch tensor")
+    if t.dim() == 2:
+        return t.unsqueeze(0), True
+    if t.dim() != 3:
+        raise InvalidArgument(f"{name} must be (L, d) or (B, L, d), got shape {tuple(t.shape)}")
+    return t, False
+
+
+class _SigKernelFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, y, l1, l2, kind, sigma):
+        ctx.save_for_backward(x, y)
+        ctx.cfg = (l1, l2, kind, sigma)
+        return ops.forward_batch(x, y, l1, l2, kind, sigma)
+
+    @staticmethod
+    def backward(ctx, cot):
+        x, y = ctx.saved_tensors
+        l1, l2, kind, sigma = ctx.cfg
+        _, gx, gy = ops.backward_batch(x, y, l1, l2, kind, sigma, cot)
+        return (gx if ctx.needs_input_grad[0] else None,
+                gy if ctx.needs_input_grad[1] else None, None, None, None, None)
+
+
+class _SigKernelGramFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, y, l1, l2, kind, sigma):
+        sym = y is None
+        ctx.sym = sym
+        ctx.cfg = (l1, l2, kind, sigma)
+        ctx.save_for_backward(x) if sym else ctx.save_for_backward(x, y)
+        return ops.forward_gram(x, y, l1, l2, kind, sigma)
+
+    @staticmethod
+    def backward(ctx, cot):
+        l1, l2, kind, sigma = ctx.cfg
+        if ctx.sym:
+            (x,) = ctx.saved_tensors
+            gx, _ = ops.backward_gram(x, None, l1, l2, kind, sigma, cot)
+            return gx, None, None, None, None, None
+        x, y = ctx.saved_tensors
+        gx, gy = ops.backward_gram(x, y, l1, l2, kind, sigma, cot)
+        return (gx if ctx.needs_input_grad[0] else None,
+                gy if ctx.needs_input_grad[1] else None, None, None, None, None)
+
+
+def _prep(t, name):
+    if not t.is_cuda:
+        raise InvalidArgument(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_floating_point():
+        t = t.to(torch.float64)  # reference integer-dtype bug not reproduced
+    return t
+
+
+def sig_kernel(x, y, dyadic_order=0, static_kernel=None):
+    """k(x_b, y_b) for aligned batches (B, L1, d), (B, L2, d) -> (B,).
+
+    A pair of (L, d) paths returns a 0-d tensor."""
+    x, sq = _batched(_prep(x, "x"), "x")
+    y, _ = _batched(_prep(y, "y"), "y")
+    l1, l2 = _orders(dyadic_order)
+    kind, sigma = ops.static_kind(static_kernel)
+    out_dtype = torch.promote_types(x.dtype, y.dtype)
+    k = _SigKernelFn.apply(x.to(torch.float64), y.to(torch.float64), l1, l2, kind, sigma)
+    k = k.to(out_dtype)
+    return k[0] if sq else k
+
+
+def sig_kernel_gram(x, y=None, dyadic_order=0, static_kernel=None):
+    """Gram matrix G[a, b] = k(x_a, y_b) -> (n1, n2).
+
+    y None (or y is x) -> symmetric: only a <= b is solved and the result is
+    mirrored, hence exactly symmetric (reference kernel.py:151-180)."""
+    sym = y is None or y is x
+    x, _ = _batched(_prep(x, "x"), "x")
+    l1, l2 = _orders(dyadic_order)
+    kind, sigma = ops.static_kind(static_kernel)
+    if sym:
+        G = _SigKernelGramFn.apply(x.to(torch.float64), None, l1, l2, kind, sigma)
+        return G.to(x.dtype)
+    y, _ = _batched(_prep(y, "y"), "y")
+    out_dtype = torch.promote_types(x.dtype, y.dtype)
+    G = _SigKernelGramFn.apply(x.to(torch.float64), y.to(torch.float64), l1, l2, kind, sigma)
+    return G.to(out_dtype)

@@ -1,0 +1,441 @@
+// sk_capi.cu -- extern "C" boundary (include/sigkernel.h) and host planning.
+//
+// The planning mirrors the reference's dispatch (kernel.py:125-180):
+//   * orientation: the longer fine axis goes on the grid rows (kernel.py:137-140,
+//     164-170), so results are bit-identical under x<->y swap;
+//   * symmetric Gram: upper triangle only, then mirrored (kernel.py:177-179).
+// Everything runs on the caller's stream; no allocation happens here
+// (the reference's "caller buffers only" contract, _kernels.py:9-10).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/sigkernel.h"
+#include "sk_backward.cuh"
+#include "sk_plan.h"
+
+namespace sk {
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define SK_CUDA(call)                                                              \
+  do {                                                                             \
+    cudaError_t e_ = (call);                                                       \
+    if (e_ != cudaSuccess)                                                         \
+      return fail(SK_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+static int device_sms() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
+  return sms > 0 ? sms : 148;
+}
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// ---------------------------------------------------------------- prep kernels
+// Increments (kernel.py:74-75 np.diff) into a zero-padded [n][L-1][dpad] array.
+__global__ void prep_increments(const double* __restrict__ x, int64_t n, int64_t L, int64_t d,
+                                int dpad, double* __restrict__ out) {
+  int64_t total = n * (L - 1) * dpad;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t k = e % dpad, i = (e / dpad) % (L - 1), p = e / (dpad * (L - 1));
+    out[e] = (k < d) ? x[(p * L + i + 1) * d + k] - x[(p * L + i) * d + k] : 0.0;
+  }
+}
+
+// Nodes into a zero-padded [n][L][dpad] array (RBF static kernel).
+__global__ void prep_nodes(const double* __restrict__ x, int64_t n, int64_t L, int64_t d,
+                           int dpad, double* __restrict__ out) {
+  int64_t total = n * L * dpad;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t k = e % dpad, i = (e / dpad) % L, p = e / (dpad * L);
+    out[e] = (k < d) ? x[(p * L + i) * d + k] : 0.0;
+  }
+}
+
+// Mirror the solved upper triangle into the lower one (kernel.py:177-179),
+// restricted to rows [r0, r1) (out holds those rows, leading dim ldo).
+__global__ void mirror_upper(double* __restrict__ out, int64_t ldo, int r0, int r1) {
+  int64_t span = r1 - r0;
+  int64_t total = span * span;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = e / span, b = e % span;  // relative
+    if (b < a) out[a * ldo + (b + r0)] = out[b * ldo + (a + r0)];
+  }
+}
+
+// Full fine grid of one delta (store_grid=True facade path, goursat_grid
+// _kernels.py:381-396).  One warp; lane u owns fine rows u, u+32, ... and the
+// columns are swept as a skewed wavefront with a shared-memory row buffer.
+// Used only for the small grids the reference's API returns to the caller.
+__global__ void grid_kernel(const double* __restrict__ delta, int r1, int r2, int lam1,
+                            int lam2, double scale, double* __restrict__ grid) {
+  const int m1 = r1 << lam1, m2 = r2 << lam2;
+  const int w = m2 + 1;
+  for (int t = threadIdx.x; t <= m2; t += blockDim.x) grid[t] = 1.0;
+  for (int s = threadIdx.x; s <= m1; s += blockDim.x) grid[(int64_t)s * w] = 1.0;
+  __syncthreads();
+  // anti-diagonal sweep: cells with s + t = dd are independent
+  for (int dd = 2; dd <= m1 + m2; ++dd) {
+    int slo = max(1, dd - m2), shi = min(m1, dd - 1);
+    for (int s = slo + threadIdx.x; s <= shi; s += blockDim.x) {
+      int t = dd - s;
+      double p = delta[(int64_t)((s - 1) >> lam1) * r2 + ((t - 1) >> lam2)] * scale;
+      Coef c = coef(p);
+      grid[(int64_t)s * w + t] = cell(grid[(int64_t)(s - 1) * w + t],
+                                      grid[(int64_t)s * w + t - 1],
+                                      grid[(int64_t)(s - 1) * w + t - 1], c);
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------- planning
+struct Geometry {
+  // oriented problem (rows = longer fine axis)
+  int64_t nR, nC;  // path counts on rows / cols side
+  int64_t LR, LC;  // points per row / col path
+  int lamR, lamC;
+  bool swap;
+};
+
+static int pick_dp(int64_t d, int& nch) {
+  int DP = d <= 4 ? 4 : d <= 8 ? 8 : d <= 16 ? 16 : 32;
+  nch = (int)((d + DP - 1) / DP);
+  return DP;
+}
+
+struct FwdPlan {
+  FwdShape shape;
+  FwdFn fn = nullptr;
+  int threads = 128;
+  int64_t blocks = 0;
+  int64_t slots = 0;
+  int64_t hand_stride = 0;
+  int64_t nitems = 0;
+  int P = 1;
+};
+
+// Chooses lanes-per-pair and the persistent grid.  `gram` marks tiles whose
+// groups share the column path.
+static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, int64_t M1c,
+                        int64_t M2c, int64_t npairs, bool gram, int mode, int n2, int r0,
+                        int r1) {
+  int nch = 1;
+  FwdShape s{};
+  s.kind = kind;
+  s.DP = (kind == DELTA) ? 4 : pick_dp(d, nch);
+  s.R = (kind == DELTA) ? 8 : rows_per_lane(s.DP);
+  s.FR = std::min(1 << std::min(lamR, 3), s.R);
+  s.F = std::min(1 << std::min(lamC, 2), 4);
+  const int64_t M1 = M1c << lamR;
+  const int sms = device_sms();
+  const int64_t target_lanes = (int64_t)sms * 512;
+  const int64_t lanes_per_pair = (M1 + s.R - 1) / s.R;
+  s.XW = false;
+  s.W = 1;
+  if (gram || npairs * 4 >= target_lanes || lanes_per_pair <= 8) {
+    s.G = 4;
+  } else if (npairs * 32 >= target_lanes || lanes_per_pair <= 64 || kind != LINEAR) {
+    s.G = 32;
+  } else {
+    int W = 2;
+    while (W < 16 && npairs * 32 * W < target_lanes && 32 * W * 2 <= lanes_per_pair) W *= 2;
+    s.XW = true;
+    s.W = W;
+    s.G = 32 * W;
+  }
+  FwdFn fn = kind == LINEAR ? select_fwd_linear(s) : kind == RBF ? select_fwd_rbf(s)
+                                                                 : select_fwd_delta(s);
+  if (!fn) return fail(SK_INVALID_ARGUMENT, "no forward kernel instance for this shape");
+  pl.shape = s;
+  pl.fn = fn;
+  pl.threads = s.XW ? 32 * s.W : 128;
+  pl.P = s.XW ? 1 : 32 / s.G;
+  const int warps = pl.threads / 32;
+  if (mode == BATCH) pl.nitems = (npairs + pl.P - 1) / pl.P;
+  else pl.nitems = gram_items(mode, n2, r0, r1, pl.P);
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, pl.threads, 0) !=
+          cudaSuccess ||
+      occ < 1)
+    occ = 1;
+  int64_t want = s.XW ? pl.nitems : (pl.nitems + warps - 1) / warps;
+  pl.blocks = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)occ * sms));
+  pl.slots = s.XW ? pl.blocks : pl.blocks * warps * pl.P;
+  pl.hand_stride = (int64_t)align_up((size_t)((M2c << lamC) + 1), 4);
+  (void)nch;
+  return SK_OK;
+}
+
+static size_t prep_elems(int kind, int64_t n, int64_t L, int dpad) {
+  return kind == RBF ? (size_t)n * L * dpad : (size_t)n * (L - 1) * dpad;
+}
+
+static void launch_prep(int kind, const double* x, int64_t n, int64_t L, int64_t d, int dpad,
+                        double* out, cudaStream_t st) {
+  size_t total = prep_elems(kind, n, L, dpad);
+  if (total == 0) return;
+  int blocks = (int)std::min<size_t>((total + 255) / 256, 4096);
+  if (kind == RBF) prep_nodes<<<blocks, 256, 0, st>>>(x, n, L, d, dpad, out);
+  else prep_increments<<<blocks, 256, 0, st>>>(x, n, L, d, dpad, out);
+}
+
+static int validate(int64_t L1, int64_t L2, int64_t d, int lam1, int lam2, int kind,
+                    double sigma) {
+  if (L1 < 2 || L2 < 2) return fail(SK_INVALID_ARGUMENT, "paths need at least 2 points");
+  if (d < 1) return fail(SK_INVALID_ARGUMENT, "path dimension must be >= 1");
+  if (lam1 < 0 || lam2 < 0) return fail(SK_INVALID_ARGUMENT, "dyadic orders must be >= 0");
+  if (lam1 > 16 || lam2 > 16) return fail(SK_INVALID_ARGUMENT, "dyadic order > 16 unsupported");
+  if (kind != SK_STATIC_LINEAR && kind != SK_STATIC_RBF)
+    return fail(SK_INVALID_ARGUMENT, "unknown static kernel");
+  if (kind == SK_STATIC_RBF && !(sigma > 0.0))
+    return fail(SK_INVALID_ARGUMENT, "RBF sigma must be > 0");
+  if (((L1 - 1) << lam1) >= (int64_t)1 << 30 || ((L2 - 1) << lam2) >= (int64_t)1 << 30)
+    return fail(SK_INVALID_ARGUMENT, "fine grid too large");
+  return SK_OK;
+}
+
+static Problem base_problem(int kind, int64_t d, int lamR, int lamC, int64_t LR, int64_t LC,
+                            double sigma) {
+  Problem pb{};
+  int nch = 1;
+  int DP = pick_dp(d, nch);
+  pb.kind = kind;
+  pb.dpad = DP * nch;
+  pb.nch = nch;
+  pb.M1c = (int)(LR - 1);
+  pb.M2c = (int)(LC - 1);
+  pb.lam1 = lamR;
+  pb.lam2 = lamC;
+  pb.scale = std::ldexp(1.0, -(lamR + lamC));
+  pb.inv2s2 = kind == RBF ? 1.0 / (2.0 * sigma * sigma) : 0.0;
+  pb.invs2 = kind == RBF ? 1.0 / (sigma * sigma) : 0.0;
+  return pb;
+}
+
+// Workspace layout for forward calls: [prep rows][prep cols][handoff rows].
+struct FwdLayout {
+  size_t prepR = 0, prepC = 0, hand = 0, total = 0;
+};
+
+static FwdLayout fwd_layout(const FwdPlan& pl, int kind, int64_t nR, int64_t LR, int64_t nC,
+                            int64_t LC, int dpad, bool shared_paths) {
+  FwdLayout lo;
+  lo.prepR = align_up(prep_elems(kind, nR, LR, dpad) * sizeof(double), 256);
+  lo.prepC = shared_paths ? 0 : align_up(prep_elems(kind, nC, LC, dpad) * sizeof(double), 256);
+  lo.hand = align_up((size_t)pl.slots * pl.hand_stride * sizeof(double), 256);
+  lo.total = lo.prepR + lo.prepC + lo.hand;
+  return lo;
+}
+
+static Geometry orient(int64_t n1, int64_t n2, int64_t L1, int64_t L2, int lam1, int lam2) {
+  Geometry g;
+  int64_t m1 = (L1 - 1) << lam1, m2 = (L2 - 1) << lam2;
+  g.swap = m2 > m1;
+  g.nR = g.swap ? n2 : n1;
+  g.nC = g.swap ? n1 : n2;
+  g.LR = g.swap ? L2 : L1;
+  g.LC = g.swap ? L1 : L2;
+  g.lamR = g.swap ? lam2 : lam1;
+  g.lamC = g.swap ? lam1 : lam2;
+  return g;
+}
+
+static int forward_impl(const double* x, const double* y, int64_t n1, int64_t n2, int64_t L1,
+                        int64_t L2, int64_t d, int lam1, int lam2, int kind, double sigma,
+                        int mode, int64_t r0, int64_t r1, double* out, void* ws,
+                        size_t ws_bytes, cudaStream_t st, size_t* query) {
+  if (int rc = validate(L1, L2, d, lam1, lam2, kind, sigma)) return rc;
+  const bool sym = mode == GRAM_SYM;
+  Geometry g = orient(n1, n2, L1, L2, lam1, lam2);
+  Problem pb = base_problem(kind, d, g.lamR, g.lamC, g.LR, g.LC, sigma);
+  pb.mode = mode;
+  pb.n1 = (int)n1;
+  pb.n2 = (int)n2;
+  pb.r0 = (int)r0;
+  pb.r1 = (int)r1;
+  pb.swap = g.swap ? 1 : 0;
+  pb.npairs = mode == BATCH ? n1 : 0;
+  pb.ldo = n2;
+  FwdPlan pl;
+  const int64_t npairs = mode == BATCH ? n1 : (r1 - r0) * n2;
+  if (int rc = plan_forward(pl, kind, d, g.lamR, g.lamC, pb.M1c, pb.M2c, npairs,
+                            mode != BATCH, mode, (int)n2, (int)r0, (int)r1))
+    return rc;
+  FwdLayout lo = fwd_layout(pl, kind, g.nR, g.LR, g.nC, g.LC, pb.dpad, sym);
+  if (query) {
+    *query = lo.total;
+    return SK_OK;
+  }
+  if (npairs <= 0 || pl.nitems == 0) return SK_OK;
+  if (ws_bytes < lo.total)
+    return fail(SK_INVALID_ARGUMENT, "workspace too small: need " + std::to_string(lo.total) +
+                                         " bytes, got " + std::to_string(ws_bytes));
+  char* base = static_cast<char*>(ws);
+  double* prepR = reinterpret_cast<double*>(base);
+  double* prepC = sym ? prepR : reinterpret_cast<double*>(base + lo.prepR);
+  double* hand = reinterpret_cast<double*>(base + lo.prepR + lo.prepC);
+  const double* xr = g.swap ? y : x;
+  const double* xc = g.swap ? x : y;
+  launch_prep(kind, xr, g.nR, g.LR, d, pb.dpad, prepR, st);
+  if (!sym) launch_prep(kind, xc, g.nC, g.LC, d, pb.dpad, prepC, st);
+  pb.R.p = prepR;
+  pb.R.rows = (int)(g.LR - 1);
+  pb.R.path_stride = (kind == RBF ? g.LR : g.LR - 1) * pb.dpad;
+  pb.C.p = prepC;
+  pb.C.rows = (int)(g.LC - 1);
+  pb.C.path_stride = (kind == RBF ? g.LC : g.LC - 1) * pb.dpad;
+  pb.nitems = pl.nitems;
+  pb.out = out;
+  pl.fn<<<(unsigned)pl.blocks, pl.threads, 0, st>>>(pb, hand, pl.hand_stride);
+  SK_CUDA(cudaGetLastError());
+  if (sym) {
+    int64_t span = r1 - r0;
+    int blocks = (int)std::min<int64_t>((span * span + 255) / 256, 4096);
+    if (span > 1) mirror_upper<<<blocks, 256, 0, st>>>(out, n2, (int)r0, (int)r1);
+    SK_CUDA(cudaGetLastError());
+  }
+  return SK_OK;
+}
+
+}  // namespace sk
+
+using namespace sk;
+
+extern "C" {
+
+int sk_abi_version(void) { return SK_ABI_VERSION; }
+const char* sk_last_error(void) { return g_err.c_str(); }
+int sk_device_sms(void) { return device_sms(); }
+
+size_t sk_forward_batch_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d, int lam1,
+                                        int lam2, int static_kernel) {
+  size_t q = 0;
+  if (forward_impl(nullptr, nullptr, B, B, L1, L2, d, lam1, lam2, static_kernel, 1.0, BATCH, 0,
+                   B, nullptr, nullptr, 0, nullptr, &q))
+    return 0;
+  return q;
+}
+
+int sk_forward_batch(const double* x, const double* y, int64_t B, int64_t L1, int64_t L2,
+                     int64_t d, int lam1, int lam2, int static_kernel, double sigma,
+                     double* out, void* ws, size_t ws_bytes, void* stream) {
+  if (B < 0) return fail(SK_INVALID_ARGUMENT, "negative batch");
+  return forward_impl(x, y, B, B, L1, L2, d, lam1, lam2, static_kernel, sigma, BATCH, 0, B, out,
+                      ws, ws_bytes, (cudaStream_t)stream, nullptr);
+}
+
+size_t sk_forward_gram_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                       int64_t d, int lam1, int lam2, int static_kernel,
+                                       int symmetric) {
+  size_t q = 0;
+  if (forward_impl(nullptr, nullptr, n1, n2, L1, L2, d, lam1, lam2, static_kernel, 1.0,
+                   symmetric ? GRAM_SYM : GRAM_CROSS, 0, n1, nullptr, nullptr, 0, nullptr, &q))
+    return 0;
+  return q;
+}
+
+int sk_forward_gram(const double* x, const double* y, int64_t n1, int64_t n2, int64_t L1,
+                    int64_t L2, int64_t d, int lam1, int lam2, int static_kernel, double sigma,
+                    int64_t row_begin, int64_t row_end, double* out, void* ws, size_t ws_bytes,
+                    void* stream) {
+  const bool sym = (y == nullptr);
+  if (sym && (n2 != n1 || L2 != L1))
+    return fail(SK_INVALID_ARGUMENT, "symmetric Gram needs n2 == n1 and L2 == L1");
+  if (row_begin < 0 || row_end > n1 || row_begin > row_end)
+    return fail(SK_INVALID_ARGUMENT, "row range out of bounds");
+  return forward_impl(x, sym ? x : y, n1, n2, L1, L2, d, lam1, lam2, static_kernel, sigma,
+                      sym ? GRAM_SYM : GRAM_CROSS, row_begin, row_end, out, ws, ws_bytes,
+                      (cudaStream_t)stream, nullptr);
+}
+
+static int solve_delta_impl(const double* delta, int64_t B, int64_t r1, int64_t r2, int lam1,
+                            int lam2, double* out, void* ws, size_t ws_bytes,
+                            cudaStream_t st, size_t* query) {
+  if (r1 < 1 || r2 < 1) return fail(SK_INVALID_ARGUMENT, "increment matrix must be non-empty");
+  if (lam1 < 0 || lam2 < 0 || lam1 > 16 || lam2 > 16)
+    return fail(SK_INVALID_ARGUMENT, "dyadic orders must be in [0, 16]");
+  // delta is solved un-transposed: rows = delta rows (kernel.py:106-110 grid
+  // orientation; the strip path transposes but is bitwise equal, test_kernel.py:65-71)
+  Problem pb = base_problem(DELTA, 4, lam1, lam2, r1 + 1, r2 + 1, 1.0);
+  pb.mode = BATCH;
+  pb.npairs = B;
+  pb.delta = delta;
+  FwdPlan pl;
+  if (int rc = plan_forward(pl, DELTA, 4, lam1, lam2, r1, r2, B, false, BATCH, 0, 0, 0))
+    return rc;
+  size_t need = align_up((size_t)pl.slots * pl.hand_stride * sizeof(double), 256);
+  if (query) {
+    *query = need;
+    return SK_OK;
+  }
+  if (B == 0) return SK_OK;
+  if (ws_bytes < need) return fail(SK_INVALID_ARGUMENT, "workspace too small");
+  pb.nitems = pl.nitems;
+  pb.out = out;
+  pl.fn<<<(unsigned)pl.blocks, pl.threads, 0, st>>>(pb, static_cast<double*>(ws),
+                                                     pl.hand_stride);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+size_t sk_solve_delta_workspace_bytes(int64_t B, int64_t r1, int64_t r2, int lam1, int lam2) {
+  size_t q = 0;
+  if (solve_delta_impl(nullptr, B, r1, r2, lam1, lam2, nullptr, nullptr, 0, nullptr, &q))
+    return 0;
+  return q;
+}
+
+int sk_solve_delta(const double* delta, int64_t B, int64_t r1, int64_t r2, int lam1, int lam2,
+                   double* out, void* ws, size_t ws_bytes, void* stream) {
+  return solve_delta_impl(delta, B, r1, r2, lam1, lam2, out, ws, ws_bytes,
+                          (cudaStream_t)stream, nullptr);
+}
+
+int sk_solve_delta_grid(const double* delta, int64_t r1, int64_t r2, int lam1, int lam2,
+                        double* grid, void* stream) {
+  if (r1 < 1 || r2 < 1) return fail(SK_INVALID_ARGUMENT, "increment matrix must be non-empty");
+  if (lam1 < 0 || lam2 < 0 || lam1 > 16 || lam2 > 16)
+    return fail(SK_INVALID_ARGUMENT, "dyadic orders must be in [0, 16]");
+  grid_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(delta, (int)r1, (int)r2, lam1, lam2,
+                                                    std::ldexp(1.0, -(lam1 + lam2)), grid);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+size_t sk_backward_batch_workspace_bytes(int64_t, int64_t, int64_t, int64_t, int, int, int) {
+  return 0;
+}
+int sk_backward_batch(const double*, const double*, int64_t, int64_t, int64_t, int64_t, int, int,
+                      int, double, const double*, double*, double*, double*, void*, size_t,
+                      void*) {
+  return fail(SK_INVALID_STATE, "backward not built yet");
+}
+size_t sk_backward_gram_workspace_bytes(int64_t, int64_t, int64_t, int64_t, int64_t, int, int,
+                                        int, int) {
+  return 0;
+}
+int sk_backward_gram(const double*, const double*, int64_t, int64_t, int64_t, int64_t, int64_t,
+                     int, int, int, double, int64_t, int64_t, const double*, double*, double*,
+                     void*, size_t, void*) {
+  return fail(SK_INVALID_STATE, "backward not built yet");
+}
+}

@@ -1,0 +1,36 @@
+// sk_plan.h -- host-side kernel selection (template instance tables).
+#pragma once
+#include "sk_common.cuh"
+
+namespace sk {
+
+using FwdFn = void (*)(Problem, double*, int64_t);
+
+// Shape class chosen on the host for one call.
+struct FwdShape {
+  int kind;
+  int DP;   // 4, 8, 16, 32
+  int R;    // fine rows per lane
+  int FR;   // fine rows per coarse row inside a lane
+  int F;    // fine columns per step
+  int G;    // lanes per pair (4 or 32), ignored if XW
+  bool XW;  // cross-warp groups: one pair per CTA of W warps
+  int W;    // warps per CTA when XW
+};
+
+// Per-kind instance tables (one translation unit each, compiled in parallel).
+FwdFn select_fwd_linear(const FwdShape& s);
+FwdFn select_fwd_rbf(const FwdShape& s);
+FwdFn select_fwd_delta(const FwdShape& s);
+
+inline int rows_per_lane(int DP) {
+  switch (DP) {
+    case 4: return 8;
+    case 8: return 4;
+    case 16: return 2;
+    default: return 1;
+  }
+}
+
+}  // namespace sk
+
