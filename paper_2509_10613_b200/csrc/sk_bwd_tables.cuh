@@ -1,0 +1,50 @@
+// sk_bwd_tables.cuh -- maps a runtime BwdShape to a backward kernel instance.
+#pragma once
+#include "sk_backward.cuh"
+#include "sk_plan.h"
+
+namespace sk {
+
+template <int KIND, int DP, int R, int FR, int F>
+inline void sk_bwd_leaf(BwdFn& fn, int& smem_doubles) {
+  constexpr int CB = 8 / F;
+  constexpr int MAP = (KIND == LINEAR) ? FUSED : DBUF;
+  fn = bwd_kernel<KIND, DP, R, FR, F, CB, MAP>;
+  smem_doubles = BlockSmem<R, R / FR, F, CB>::TOTAL * 32;
+}
+
+template <int KIND, int DP, int R, int FR>
+inline void sk_bwd_f(const BwdShape& s, BwdFn& fn, int& sm) {
+  switch (s.F) {
+    case 1: sk_bwd_leaf<KIND, DP, R, FR, 1>(fn, sm); break;
+    case 2: sk_bwd_leaf<KIND, DP, R, FR, 2>(fn, sm); break;
+    case 4: sk_bwd_leaf<KIND, DP, R, FR, 4>(fn, sm); break;
+    default: break;
+  }
+}
+
+template <int KIND, int DP, int R>
+inline void sk_bwd_table(const BwdShape& s, BwdFn& fn, int& sm) {
+  switch (s.FR) {
+    case 1: sk_bwd_f<KIND, DP, R, 1>(s, fn, sm); break;
+    case 2: if constexpr (R >= 2) sk_bwd_f<KIND, DP, R, 2>(s, fn, sm); break;
+    case 4: if constexpr (R >= 4) sk_bwd_f<KIND, DP, R, 4>(s, fn, sm); break;
+    case 8: if constexpr (R >= 8) sk_bwd_f<KIND, DP, R, 8>(s, fn, sm); break;
+    default: break;
+  }
+}
+
+template <int KIND>
+inline BwdFn sk_bwd_select(const BwdShape& s, int& smem_doubles) {
+  BwdFn fn = nullptr;
+  switch (s.DP) {
+    case 4: sk_bwd_table<KIND, 4, 8>(s, fn, smem_doubles); break;
+    case 8: sk_bwd_table<KIND, 8, 4>(s, fn, smem_doubles); break;
+    case 16: sk_bwd_table<KIND, 16, 2>(s, fn, smem_doubles); break;
+    case 32: sk_bwd_table<KIND, 32, 1>(s, fn, smem_doubles); break;
+    default: break;
+  }
+  return fn;
+}
+
+}  // namespace sk

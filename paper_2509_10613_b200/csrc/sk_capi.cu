@@ -420,22 +420,203 @@ int sk_solve_delta_grid(const double* delta, int64_t r1, int64_t r2, int lam1, i
 
 }  // extern "C"
 
+
+// ====================================================================== backward
+namespace sk {
+
+struct BwdPlan {
+  BwdShape shape;
+  BwdFn fn = nullptr;
+  int smem_bytes = 0;
+  int threads = 128;
+  int64_t blocks = 0, slots = 0, nitems = 0;
+  int64_t rowck_stride = 0, colck_stride = 0, row_stride = 0, dbuf_stride = 0;
+};
+
+static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, int64_t M1c,
+                         int64_t M2c, int mode, int64_t npairs, int n2, int r0, int r1) {
+  int nch = 1;
+  BwdShape s{};
+  s.kind = kind;
+  s.DP = pick_dp(d, nch);
+  if (nch > 1) return fail(SK_INVALID_ARGUMENT, "backward supports d <= 32");
+  s.R = rows_per_lane(s.DP);
+  s.FR = std::min(1 << std::min(lamR, 3), s.R);
+  s.F = std::min(1 << std::min(lamC, 2), 4);
+  int smd = 0;
+  BwdFn fn = kind == LINEAR ? select_bwd_linear(s, smd) : select_bwd_rbf(s, smd);
+  if (!fn) return fail(SK_INVALID_ARGUMENT, "no backward kernel instance for this shape");
+  pl.shape = s;
+  pl.fn = fn;
+  pl.threads = 128;
+  const int warps = pl.threads / 32;
+  pl.smem_bytes = smd * (int)sizeof(double) * warps;
+  if (pl.smem_bytes > 48 * 1024) {
+    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             pl.smem_bytes) != cudaSuccess)
+      (void)cudaGetLastError();
+  }
+  pl.nitems = mode == BATCH ? npairs : gram_items(mode, n2, r0, r1, 1);
+  const int sms = device_sms();
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, pl.threads,
+                                                    pl.smem_bytes) != cudaSuccess ||
+      occ < 1) {
+    (void)cudaGetLastError();
+    occ = 1;
+  }
+  pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + warps - 1) / warps,
+                                                     (int64_t)occ * sms));
+  pl.slots = pl.blocks * warps;
+  const int64_t M1 = M1c << lamR, M2 = M2c << lamC;
+  const int64_t NS = M2 / s.F, NT = NS + 31, CB = 8 / s.F, NB = (NT + CB - 1) / CB;
+  const int64_t nstrips = (M1 + 32 * s.R - 1) / (32 * s.R);
+  pl.rowck_stride = (int64_t)align_up((size_t)(nstrips * NT * s.F * 32), 32);
+  pl.colck_stride = (int64_t)align_up((size_t)(nstrips * NB * s.R * 32), 32);
+  pl.row_stride = (int64_t)align_up((size_t)(M2 + 1), 32);
+  pl.dbuf_stride = kind == RBF ? (int64_t)align_up((size_t)(M1c * M2c), 32) : 0;
+  return SK_OK;
+}
+
+struct BwdLayout {
+  size_t prepR = 0, prepC = 0, rowck = 0, colck = 0, rows = 0, dbuf = 0, total = 0;
+};
+
+static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n2, int64_t L1,
+                         int64_t L2, int64_t d, int lam1, int lam2, int kind, double sigma,
+                         int mode, int64_t r0, int64_t r1, const double* cot, double* values,
+                         double* grad_x, double* grad_y, void* ws, size_t ws_bytes,
+                         cudaStream_t st, size_t* query) {
+  if (int rc = validate(L1, L2, d, lam1, lam2, kind, sigma)) return rc;
+  const bool sym = mode == GRAM_SYM;
+  Geometry g = orient(n1, n2, L1, L2, lam1, lam2);
+  Problem pb = base_problem(kind, d, g.lamR, g.lamC, g.LR, g.LC, sigma);
+  pb.mode = mode;
+  pb.n1 = (int)n1;
+  pb.n2 = (int)n2;
+  pb.r0 = (int)r0;
+  pb.r1 = (int)r1;
+  pb.swap = g.swap ? 1 : 0;
+  pb.npairs = mode == BATCH ? n1 : 0;
+  pb.ldo = n2;
+  BwdPlan pl;
+  const int64_t npairs = mode == BATCH ? n1 : (r1 - r0) * n2;
+  if (int rc = plan_backward(pl, kind, d, g.lamR, g.lamC, pb.M1c, pb.M2c, mode, npairs,
+                             (int)n2, (int)r0, (int)r1))
+    return rc;
+  BwdLayout lo;
+  lo.prepR = align_up(prep_elems(kind, g.nR, g.LR, pb.dpad) * sizeof(double), 256);
+  lo.prepC = sym ? 0 : align_up(prep_elems(kind, g.nC, g.LC, pb.dpad) * sizeof(double), 256);
+  lo.rowck = align_up((size_t)pl.slots * pl.rowck_stride * sizeof(double), 256);
+  lo.colck = align_up((size_t)pl.slots * pl.colck_stride * sizeof(double), 256);
+  lo.rows = align_up((size_t)pl.slots * pl.row_stride * 2 * sizeof(double), 256);
+  lo.dbuf = align_up((size_t)pl.slots * pl.dbuf_stride * sizeof(double), 256);
+  lo.total = lo.prepR + lo.prepC + lo.rowck + lo.colck + lo.rows + lo.dbuf;
+  if (query) {
+    *query = lo.total;
+    return SK_OK;
+  }
+  if (mode == BATCH) {
+    // batch gradients are written (not accumulated): zero them first
+    if (grad_x) SK_CUDA(cudaMemsetAsync(grad_x, 0, sizeof(double) * n1 * L1 * d, st));
+    if (grad_y) SK_CUDA(cudaMemsetAsync(grad_y, 0, sizeof(double) * n2 * L2 * d, st));
+  }
+  if (npairs <= 0 || pl.nitems == 0) return SK_OK;
+  if (ws_bytes < lo.total)
+    return fail(SK_INVALID_ARGUMENT, "workspace too small: need " + std::to_string(lo.total) +
+                                         " bytes, got " + std::to_string(ws_bytes));
+  if (!grad_x || (!sym && !grad_y)) return fail(SK_INVALID_ARGUMENT, "gradient buffers missing");
+  char* base = static_cast<char*>(ws);
+  double* prepR = reinterpret_cast<double*>(base);
+  double* prepC = sym ? prepR : reinterpret_cast<double*>(base + lo.prepR);
+  char* p = base + lo.prepR + lo.prepC;
+  BwdArgs ba{};
+  ba.rowck = reinterpret_cast<double*>(p);
+  ba.rowck_stride = pl.rowck_stride;
+  p += lo.rowck;
+  ba.colck = reinterpret_cast<double*>(p);
+  ba.colck_stride = pl.colck_stride;
+  p += lo.colck;
+  ba.hand = reinterpret_cast<double*>(p);
+  ba.adj = ba.hand + pl.slots * pl.row_stride;
+  ba.row_stride = pl.row_stride;
+  p += lo.rows;
+  ba.dbuf = reinterpret_cast<double*>(p);
+  ba.dbuf_stride = pl.dbuf_stride;
+  const double* xr = g.swap ? y : x;
+  const double* xc = g.swap ? x : y;
+  launch_prep(kind, xr, g.nR, g.LR, d, pb.dpad, prepR, st);
+  if (!sym) launch_prep(kind, xc, g.nC, g.LC, d, pb.dpad, prepC, st);
+  pb.R.p = prepR;
+  pb.R.rows = (int)(g.LR - 1);
+  pb.R.path_stride = (kind == RBF ? g.LR : g.LR - 1) * pb.dpad;
+  pb.C.p = prepC;
+  pb.C.rows = (int)(g.LC - 1);
+  pb.C.path_stride = (kind == RBF ? g.LC : g.LC - 1) * pb.dpad;
+  pb.nitems = pl.nitems;
+  pb.out = values;
+  // GRAM_SYM keeps (rows, cols) = (X_a, X_b): both sides land in grad_x
+  double* gx_rows = sym ? grad_x : (g.swap ? grad_y : grad_x);
+  double* gx_cols = sym ? grad_x : (g.swap ? grad_x : grad_y);
+  ba.gradR = gx_rows;
+  ba.gradC = gx_cols;
+  ba.gR_path = g.LR * d;
+  ba.gC_path = g.LC * d;
+  ba.d = (int)d;
+  ba.atomic = mode == BATCH ? 0 : 1;
+  ba.cot = cot;
+  ba.values = values;
+  pl.fn<<<(unsigned)pl.blocks, pl.threads, pl.smem_bytes, st>>>(pb, ba);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+}  // namespace sk
+
 extern "C" {
-size_t sk_backward_batch_workspace_bytes(int64_t, int64_t, int64_t, int64_t, int, int, int) {
-  return 0;
+
+size_t sk_backward_batch_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d,
+                                         int lam1, int lam2, int static_kernel) {
+  size_t q = 0;
+  if (backward_impl(nullptr, nullptr, B, B, L1, L2, d, lam1, lam2, static_kernel, 1.0, BATCH, 0,
+                    B, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, &q))
+    return 0;
+  return q;
 }
-int sk_backward_batch(const double*, const double*, int64_t, int64_t, int64_t, int64_t, int, int,
-                      int, double, const double*, double*, double*, double*, void*, size_t,
-                      void*) {
-  return fail(SK_INVALID_STATE, "backward not built yet");
+
+int sk_backward_batch(const double* x, const double* y, int64_t B, int64_t L1, int64_t L2,
+                      int64_t d, int lam1, int lam2, int static_kernel, double sigma,
+                      const double* cot, double* values, double* grad_x, double* grad_y,
+                      void* ws, size_t ws_bytes, void* stream) {
+  if (B < 0) return fail(SK_INVALID_ARGUMENT, "negative batch");
+  return backward_impl(x, y, B, B, L1, L2, d, lam1, lam2, static_kernel, sigma, BATCH, 0, B, cot,
+                       values, grad_x, grad_y, ws, ws_bytes, (cudaStream_t)stream, nullptr);
 }
-size_t sk_backward_gram_workspace_bytes(int64_t, int64_t, int64_t, int64_t, int64_t, int, int,
-                                        int, int) {
-  return 0;
+
+size_t sk_backward_gram_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                        int64_t d, int lam1, int lam2, int static_kernel,
+                                        int symmetric) {
+  size_t q = 0;
+  if (backward_impl(nullptr, nullptr, n1, n2, L1, L2, d, lam1, lam2, static_kernel, 1.0,
+                    symmetric ? GRAM_SYM : GRAM_CROSS, 0, n1, nullptr, nullptr, nullptr,
+                    nullptr, nullptr, 0, nullptr, &q))
+    return 0;
+  return q;
 }
-int sk_backward_gram(const double*, const double*, int64_t, int64_t, int64_t, int64_t, int64_t,
-                     int, int, int, double, int64_t, int64_t, const double*, double*, double*,
-                     void*, size_t, void*) {
-  return fail(SK_INVALID_STATE, "backward not built yet");
+
+int sk_backward_gram(const double* x, const double* y, int64_t n1, int64_t n2, int64_t L1,
+                     int64_t L2, int64_t d, int lam1, int lam2, int static_kernel,
+                     double sigma, int64_t row_begin, int64_t row_end, const double* cot,
+                     double* grad_x, double* grad_y, void* ws, size_t ws_bytes, void* stream) {
+  const bool sym = (y == nullptr);
+  if (sym && (n2 != n1 || L2 != L1))
+    return fail(SK_INVALID_ARGUMENT, "symmetric Gram needs n2 == n1 and L2 == L1");
+  if (row_begin < 0 || row_end > n1 || row_begin > row_end)
+    return fail(SK_INVALID_ARGUMENT, "row range out of bounds");
+  if (!cot) return fail(SK_INVALID_ARGUMENT, "Gram backward needs the cotangent matrix");
+  return backward_impl(x, sym ? x : y, n1, n2, L1, L2, d, lam1, lam2, static_kernel, sigma,
+                       sym ? GRAM_SYM : GRAM_CROSS, row_begin, row_end, cot, nullptr, grad_x,
+                       grad_y, ws, ws_bytes, (cudaStream_t)stream, nullptr);
 }
-}
+
+}  // extern "C"

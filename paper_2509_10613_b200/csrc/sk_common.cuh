@@ -39,7 +39,7 @@ struct Problem {
   int nch;       // number of DP-chunks of the dimension
   int M1c, M2c;  // coarse rows / cols of every pair
   int lam1, lam2;
-  double scale;   // 2^-(lam1+lam2); LINEAR has it folded into R.p already
+  double scale;   // 2^-(lam1+lam2), applied to every coarse p (exact: power of two)
   double inv2s2;  // RBF: 1/(2 sigma^2)
   double invs2;   // RBF: 1/sigma^2
   // pair mapping
@@ -52,6 +52,28 @@ struct Problem {
   // output
   double* out;
   int64_t ldo;
+};
+
+// Backward scratch and outputs (see sk_backward.cuh).
+struct BwdArgs {
+  // per-slot scratch
+  double* rowck;
+  int64_t rowck_stride;
+  double* colck;
+  int64_t colck_stride;
+  double* hand;  // forward handoff rows
+  double* adj;   // reverse handoff rows (messages between strips)
+  int64_t row_stride;
+  double* dbuf;  // DBUF: per-slot coarse adjoint [M1c][M2c]
+  int64_t dbuf_stride;
+  // outputs (point gradients, real dimension d)
+  double* gradR;  // gradient of the grid-row path set
+  double* gradC;  // gradient of the grid-column path set
+  int64_t gR_path, gC_path;  // elements per path (L * d)
+  int d;
+  int atomic;  // accumulate with atomics (Gram: several pairs share a path)
+  const double* cot;  // BATCH: [npairs] (nullptr = ones); GRAM: [n1][n2]
+  double* values;     // BATCH: optional kernel values
 };
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -18,6 +18,16 @@ struct FwdShape {
   int W;    // warps per CTA when XW
 };
 
+using BwdFn = void (*)(Problem, BwdArgs);
+
+struct BwdShape {
+  int kind;
+  int DP, R, FR, F;  // as FwdShape; lanes per pair fixed at 32, CB = 8 / F
+};
+
+BwdFn select_bwd_linear(const BwdShape& s, int& smem_doubles);
+BwdFn select_bwd_rbf(const BwdShape& s, int& smem_doubles);
+
 // Per-kind instance tables (one translation unit each, compiled in parallel).
 FwdFn select_fwd_linear(const FwdShape& s);
 FwdFn select_fwd_rbf(const FwdShape& s);

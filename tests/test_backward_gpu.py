@@ -1,0 +1,179 @@
+"""GPU parity of the reverse-wavefront backward against the reference-pinned
+golden vectors, the C oracle (fp64, 1e-10) and torch.autograd.gradcheck."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden, make_paths, rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def sk():
+    import paper_2509_10613_b200 as sk
+    from paper_2509_10613_b200 import ops
+    return sk, ops
+
+
+def cu(a):
+    return torch.as_tensor(np.asarray(a, dtype=np.float64), device="cuda")
+
+
+def bwd(ops, x, y, l1, l2, cot=None, static=(0, 1.0)):
+    v, gx, gy = ops.backward_batch(cu(x), cu(y), l1, l2, static[0], static[1],
+                                   None if cot is None else cu(cot), want_values=True)
+    return v.cpu().numpy(), gx.cpu().numpy(), gy.cpu().numpy()
+
+
+def test_single_cell_hand_value(sk):
+    _, ops = sk
+    x = np.array([[[0.0], [1.0]]])
+    v, gx, gy = bwd(ops, x, x, 0, 0)
+    assert v[0] == 2.25
+    np.testing.assert_allclose(gx[0], [[-1.5], [1.5]], rtol=1e-15)
+    np.testing.assert_allclose(gy[0], [[-1.5], [1.5]], rtol=1e-15)
+
+
+def test_batch_backward_golden(sk):
+    _, ops = sk
+    g = golden("batch_backward_small")
+    for l1, l2 in ((0, 0), (1, 2), (2, 1), (0, 3)):
+        v, gx, gy = bwd(ops, g["x"], g["y"], l1, l2, g["cot"])
+        assert rel_err(v, g[f"v_{l1}{l2}"]) < TOL
+        assert rel_err(gx, g[f"gx_{l1}{l2}"]) < TOL, (l1, l2)
+        assert rel_err(gy, g[f"gy_{l1}{l2}"]) < TOL, (l1, l2)
+
+
+def test_c2_linear_golden(sk):
+    _, ops = sk
+    g = golden("c2_linear_pairs")
+    v, gx, gy = bwd(ops, g["x"], g["y"], 2, 2)
+    assert rel_err(v, g["v"]) < TOL
+    assert rel_err(gx, g["gx"]) < TOL
+    assert rel_err(gy, g["gy"]) < TOL
+
+
+def test_c5_pair_golden(sk):
+    _, ops = sk
+    g = golden("c5_pair_grad")
+    v, gx, gy = bwd(ops, g["x"][None], g["y"][None], 0, 0)
+    assert rel_err(v, [float(g["value"])]) < TOL
+    assert rel_err(gx[0], g["gx"]) < TOL
+    assert rel_err(gy[0], g["gy"]) < TOL
+
+
+@pytest.mark.parametrize("B,L1,L2,d,l1,l2", [
+    (3, 2, 2, 1, 0, 0), (4, 5, 40, 2, 0, 0), (3, 70, 33, 5, 1, 0), (2, 17, 17, 9, 2, 3),
+    (3, 129, 100, 16, 0, 1), (2, 300, 5, 3, 0, 4), (2, 40, 37, 4, 3, 1), (2, 65, 66, 8, 0, 0),
+    (1, 520, 200, 6, 0, 0), (2, 33, 35, 12, 1, 1)])
+def test_random_vs_oracle(sk, oracle, B, L1, L2, d, l1, l2):
+    _, ops = sk
+    rng = np.random.default_rng(B * 1000 + L1 + L2)
+    x = make_paths(rng, B, L1, d)
+    y = make_paths(rng, B, L2, d)
+    cot = rng.standard_normal(B)
+    wv, wx, wy = oracle.kernel_batch_backward(x, y, l1, l2, cot)
+    v, gx, gy = bwd(ops, x, y, l1, l2, cot)
+    assert rel_err(v, wv) < TOL
+    assert rel_err(gx, wx) < TOL
+    assert rel_err(gy, wy) < TOL
+
+
+@pytest.mark.parametrize("lam", [(0, 0), (2, 2), (1, 3)])
+def test_rbf_vs_oracle(sk, oracle, lam):
+    _, ops = sk
+    rng = np.random.default_rng(77)
+    x = make_paths(rng, 3, 30, 4)
+    y = make_paths(rng, 3, 23, 4)
+    cot = rng.standard_normal(3)
+    wv, wx, wy = oracle.kernel_batch_backward(x, y, *lam, cot, ("rbf", 0.9))
+    v, gx, gy = bwd(ops, x, y, *lam, cot, static=(1, 0.9))
+    assert rel_err(v, wv) < TOL
+    assert rel_err(gx, wx) < TOL
+    assert rel_err(gy, wy) < TOL
+
+
+def test_batch_equals_single_bitwise(sk):
+    _, ops = sk
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((3, 40, 2)) * 0.5
+    y = rng.standard_normal((3, 60, 2)) * 0.5
+    v, gx, gy = bwd(ops, x, y, 1, 0)
+    for b in range(3):
+        vb, gxb, gyb = bwd(ops, x[b:b + 1], y[b:b + 1], 1, 0)
+        assert v[b] == vb[0]
+        np.testing.assert_array_equal(gx[b], gxb[0])
+        np.testing.assert_array_equal(gy[b], gyb[0])
+
+
+def test_linear_in_cotangent(sk):
+    _, ops = sk
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((2, 30, 3)) * 0.5
+    y = rng.standard_normal((2, 50, 3)) * 0.5
+    _, g1x, g1y = bwd(ops, x, y, 1, 1, np.ones(2))
+    _, g2x, g2y = bwd(ops, x, y, 1, 1, -2.5 * np.ones(2))
+    assert rel_err(g2x, -2.5 * g1x) < 1e-13
+    assert rel_err(g2y, -2.5 * g1y) < 1e-13
+
+
+@pytest.mark.parametrize("n,L,d,lam", [(5, 9, 2, (1, 1)), (13, 40, 8, (0, 0)),
+                                       (6, 70, 16, (0, 0)), (4, 20, 3, (2, 1))])
+def test_gram_sym_vs_oracle(sk, oracle, n, L, d, lam):
+    _, ops = sk
+    rng = np.random.default_rng(n + L)
+    X = make_paths(rng, n, L, d)
+    C = rng.standard_normal((n, n))
+    want = oracle.gram_backward(X, None, C, *lam)
+    gx, _ = ops.backward_gram(cu(X), None, *lam, 0, 1.0, cu(C))
+    assert rel_err(gx.cpu().numpy(), want) < TOL
+
+
+def test_gram_cross_vs_oracle(sk, oracle):
+    _, ops = sk
+    rng = np.random.default_rng(5)
+    X = make_paths(rng, 5, 20, 3)
+    Y = make_paths(rng, 7, 31, 3)
+    C = rng.standard_normal((5, 7))
+    for lam in ((0, 0), (0, 1), (2, 0)):
+        wx, wy = oracle.gram_backward(X, Y, C, *lam)
+        gx, gy = ops.backward_gram(cu(X), cu(Y), *lam, 0, 1.0, cu(C))
+        assert rel_err(gx.cpu().numpy(), wx) < TOL
+        assert rel_err(gy.cpu().numpy(), wy) < TOL
+
+
+def test_gram_rbf_vs_oracle(sk, oracle):
+    _, ops = sk
+    rng = np.random.default_rng(8)
+    X = make_paths(rng, 6, 15, 3)
+    C = rng.standard_normal((6, 6))
+    want = oracle.gram_backward(X, None, C, 1, 1, ("rbf", 0.7))
+    gx, _ = ops.backward_gram(cu(X), None, 1, 1, 1, 0.7, cu(C))
+    assert rel_err(gx.cpu().numpy(), want) < TOL
+
+
+def test_autograd_gradcheck(sk):
+    s, _ = sk
+    torch.manual_seed(0)
+    x = (torch.randn(2, 6, 2, dtype=torch.float64, device="cuda") * 0.4).requires_grad_()
+    y = (torch.randn(2, 5, 2, dtype=torch.float64, device="cuda") * 0.4).requires_grad_()
+    assert torch.autograd.gradcheck(lambda a, b: s.sig_kernel(a, b, (1, 0)), (x, y))
+    assert torch.autograd.gradcheck(
+        lambda a, b: s.sig_kernel(a, b, 1, s.RBFKernel(0.8)), (x, y))
+    X = (torch.randn(3, 5, 2, dtype=torch.float64, device="cuda") * 0.4).requires_grad_()
+    assert torch.autograd.gradcheck(lambda a: s.sig_kernel_gram(a, dyadic_order=1), (X,))
+    assert torch.autograd.gradcheck(lambda a, b: s.sig_kernel_gram(a, b, (0, 1)), (X, y))
+
+
+def test_autograd_loss_backward(sk, oracle):
+    s, _ = sk
+    rng = np.random.default_rng(3)
+    X = make_paths(rng, 8, 30, 4)
+    C = rng.standard_normal((8, 8))
+    Xt = cu(X).requires_grad_()
+    G = s.sig_kernel_gram(Xt, dyadic_order=0)
+    (G * cu(C)).sum().backward()
+    assert rel_err(Xt.grad.cpu().numpy(), oracle.gram_backward(X, None, C)) < TOL
