@@ -1,0 +1,384 @@
+"""Benchmark: signature-kernel Gram forward+backward (fp64) on B200.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` prints ONE
+JSON line on rank 0.  N>1 runs under torchrun, one rank per GPU (NCCL).
+
+Workload (default --config c3, BASELINE.json configs[2]): symmetric
+sig_kernel_gram of 1024 Brownian paths, L=512, d=16, dyadic order 0, linear
+static kernel, fp64 forward + exact backward with cotangent ones (the
+reference default, kernel_grad.py:81-82).  A "step" = forward Gram + backward
+gradient of the whole Gram.  With N GPUs the same Gram is sharded by
+balanced row blocks (strong scaling) and assembled with NCCL all-gathers.
+
+  value  = solved PDE cells per second (device-resident inputs, device timed,
+           max over ranks); Gram entries/s reported beside it
+  e2e    = the same step through the public API (sig_kernel_gram + autograd)
+           from pinned host memory: H2D of X and D2H of G and dF/dX inside
+           the timed region
+  roofline: dominant kernel (backward wavefront) vs the FP64 FMA pipe,
+           algorithmic DP instructions per cell from SURVEY.md 8d, peak
+           measured live with a DFMA probe on this GPU
+  cpu_baseline: the C oracle (restatement of the reference algorithm,
+           OpenMP over pairs, all host threads) on a bounded sub-Gram
+
+`--impl reference` times the reference's CPU algorithm (the oracle port; the
+reference itself is Python+numba and is not installed on the GPU box) on the
+same metric with all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("sig-kernel PDE cells/sec and Gram entries/sec (fwd+bwd, fp64) vs roofline & CPU")
+
+CONFIGS = {
+    # name: (n, L, d, lam, description)
+    "c3": (1024, 512, 16, 0,
+           "sig_kernel_gram 1024x1024, length=512, dim=16, fp64 forward+backward on 1xB200 "
+           "(BASELINE configs[2])"),
+    "c5": (8192, 1024, 8, 0,
+           "sig_kernel_gram 8192x8192, length=1024, dim=8, forward+backward sharded "
+           "(BASELINE configs[4])"),
+}
+
+
+def make_paths(rng, batch, length, dim):
+    """Reference bench generator (sigcore/bench.py:53-56), fp64."""
+    steps = rng.standard_normal((batch, length, dim)) / np.sqrt(max(length, 1))
+    return np.cumsum(steps, axis=1, dtype=np.float64)
+
+
+def dp_instr_per_cell(d, lam1, lam2):
+    """Algorithmic FP64 instructions per fine cell:
+    I_fwd = 3 + (d+4)/2^(l1+l2),  I_bwd = 7 + (2d+2)/2^(l1+l2)."""
+    s = 2.0 ** (lam1 + lam2)
+    return 3 + (d + 4) / s, 7 + (2 * d + 2) / s
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(n_sample, L, d, lam, budget_s=10.0):
+    """Oracle (C restatement of the reference, OpenMP) fwd+bwd on a sub-Gram."""
+    from oracle import oracle as orc
+    orc.build()
+    rng = np.random.default_rng(0)
+    X = make_paths(rng, n_sample, L, d)
+    C = np.ones((n_sample, n_sample))
+    threads = os.cpu_count() or 1
+    orc.gram_backward(X[:2], None, C[:2, :2], lam, lam, threads=threads)  # warm
+    pairs = n_sample * (n_sample + 1) // 2
+    cells = pairs * ((L - 1) << lam) ** 2
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        orc.gram_backward(X, None, C, lam, lam, threads=threads)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or reps >= 50:
+            break
+    return {"value": cells * reps / el, "unit": "cells/s", "cores": threads, "kind": "port",
+            "sample": f"symmetric sub-Gram {n_sample}x{n_sample} (L={L}, d={d}, lambda={lam}) "
+                      f"fwd+bwd, {reps} rep(s) in {el:.1f}s; oracle/sk_oracle.c (restates "
+                      f"sigcore goursat_grid+goursat_backward per pair)",
+            "entries_per_s": n_sample * n_sample * reps / el}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference CPU algorithm (oracle port), rank 0 only."""
+    if rank != 0:
+        return
+    n, L, d, lam, desc = CONFIGS[args.config]
+    n_sample = 24 if args.config == "c3" else 8
+    from oracle import oracle as orc
+    orc.build()
+    rng = np.random.default_rng(0)
+    X = make_paths(rng, n_sample, L, d)
+    C = np.ones((n_sample, n_sample))
+    threads = os.cpu_count() or 1
+    pairs = n_sample * (n_sample + 1) // 2
+    cells = pairs * ((L - 1) << lam) ** 2
+    for _ in range(args.warmup):
+        orc.gram_backward(X[:4], None, C[:4, :4], lam, lam, threads=threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        orc.gram_backward(X, None, C, lam, lam, threads=threads)
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    value = cells / t
+    sample = (f"symmetric sub-Gram {n_sample}x{n_sample} of the {desc} workload per step "
+              f"(cells/s is size-independent per pair; full config extrapolates linearly)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "cells/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference _make_paths, seed 0)",
+        "config": {"workload": desc, "n": n, "L": L, "d": d, "dyadic_order": lam},
+        "gram_entries_per_s": n_sample * n_sample / t,
+        "cpu_baseline": {"value": value, "unit": "cells/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2509_10613_b200 as sk
+    from paper_2509_10613_b200 import gram_dist, ops
+
+    n, L, d, lam, desc = CONFIGS[args.config]
+    rng = np.random.default_rng(0)
+    Xh = make_paths(rng, n, L, d)
+    X = torch.as_tensor(Xh, device=dev)
+    C = torch.ones((n, n), dtype=torch.float64, device=dev)
+    ranges = gram_dist.row_blocks(n, world, rank, True)
+    my_pairs = gram_dist.pair_count(ranges, n, True)
+    total_pairs = n * (n + 1) // 2
+    cells_pair = ((L - 1) << lam) ** 2
+    i_fwd, i_bwd = dp_instr_per_cell(d, lam, lam)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step_device(ev=None):
+        """Device-resident step; optionally records (fwd_start, bwd_start, end) events."""
+        if ev is not None:
+            ev[0].record()
+        parts = [ops.forward_gram(X, None, lam, lam, 0, 1.0, rows=rg) for rg in ranges]
+        if ev is not None:
+            ev[1].record()
+        gx = torch.zeros_like(X)
+        for rg in ranges:
+            ops.backward_gram(X, None, lam, lam, 0, 1.0, C, rows=rg, grad_x=gx)
+        if ev is not None:
+            ev[2].record()
+        if world > 1:
+            local_rows = torch.cat(parts, 0)
+            ranges_all = [gram_dist.row_blocks(n, world, r, True) for r in range(world)]
+            G = gram_dist._gather_rows(local_rows, ranges_all, n, n, group)
+            ops.mirror_upper(G)
+            gx = gram_dist._gather_sum(gx, group)
+        return parts, gx
+
+    # warmup (also sizes workspaces / JIT-free: kernels are precompiled)
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+
+    peak_fma = ops.dfma_peak()  # live FP64 roofline denominator on this GPU
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    fwd_ms, bwd_ms, step_ms = [], [], []
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush between timed steps (256 MiB > 126 MB L2)
+        barrier()
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        e_end = torch.cuda.Event(enable_timing=True)
+        step_device(ev)
+        e_end.record()
+        torch.cuda.synchronize()
+        barrier()
+        fwd_ms.append(ev[0].elapsed_time(ev[1]))
+        bwd_ms.append(ev[1].elapsed_time(ev[2]))
+        step_ms.append(ev[0].elapsed_time(e_end))
+    clocks = sampler.stop()
+
+    t_step = sum(step_ms) / len(step_ms) / 1e3
+    t_bwd = sum(bwd_ms) / len(bwd_ms) / 1e3
+    t_fwd = sum(fwd_ms) / len(fwd_ms) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_step, t_bwd, t_fwd], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step, t_bwd, t_fwd = tt.tolist()
+
+    total_cells = total_pairs * cells_pair
+    value = total_cells / t_step
+    my_cells = my_pairs * cells_pair
+    achieved = my_cells * i_bwd * 2 / t_bwd / 1e12  # FMA-equivalent TFLOP/s
+    peak = 2 * peak_fma / 1e12
+
+    # ---- e2e through the public API, host buffers, copies inside the region
+    e2e = None
+    if not args.no_e2e:
+        Xpin = torch.from_numpy(Xh).pin_memory()
+        Gh = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        gh = torch.empty_like(Xpin).pin_memory()
+
+        def step_e2e():
+            Xd = Xpin.to(dev, non_blocking=True).requires_grad_(True)
+            if world > 1:
+                G = gram_dist.sig_kernel_gram_sharded(Xd, dyadic_order=lam)
+            else:
+                G = sk.sig_kernel_gram(Xd, dyadic_order=lam)
+            G.sum().backward()  # cotangent ones
+            Gh.copy_(G.detach(), non_blocking=True)
+            gh.copy_(Xd.grad, non_blocking=True)
+
+        for _ in range(2):
+            step_e2e()
+        torch.cuda.synchronize()
+        e2e_ms = []
+        for _ in range(max(1, min(args.steps, 3))):
+            flush.fill_(1.0)
+            barrier()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            step_e2e()
+            b.record()
+            torch.cuda.synchronize()
+            barrier()
+            e2e_ms.append(a.elapsed_time(b))
+        t_e2e = sum(e2e_ms) / len(e2e_ms) / 1e3
+        if world > 1:
+            tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e2e = tt.item()
+        e2e = {"value": total_cells / t_e2e, "unit": "cells/s",
+               "h2d_bytes_per_step": int(Xh.nbytes),
+               "d2h_bytes_per_step": int(Gh.numel() * 8 + gh.numel() * 8),
+               "ms_per_step": t_e2e * 1e3,
+               "api": "paper_2509_10613_b200.sig_kernel_gram + torch autograd"
+                      + (" (gram_dist sharded)" if world > 1 else "")}
+
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.config)
+        except (OSError, ValueError):
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(24 if args.config == "c3" else 8, L, d, lam)
+
+    if rank == 0:
+        launches_per_step = (2 * len(ranges)) + (2 * len(ranges))  # prep+kernel, fwd and bwd
+        launches_per_step += 1 if world > 1 else 0  # mirror after gather
+        out = {
+            "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic Brownian paths (reference _make_paths generator, seed 0)",
+            "config": {"workload": desc, "n": n, "L": L, "d": d, "dyadic_order": lam,
+                       "static_kernel": "linear", "cotangent": "ones", "symmetric": True,
+                       "parallelism": f"gram row blocks x{world}",
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "gram_entries_per_s": n * n / t_step,
+            "fwd_ms": t_fwd * 1e3, "bwd_ms": t_bwd * 1e3,
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
+                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "bwd_kernel (reverse wavefront incl. checkpointed re-forward)",
+                         "work": f"{i_bwd:g} DP instr/cell (SURVEY 8d I_bwd) x {my_cells} cells "
+                                 f"per launch; FMA-equivalent flops = 2 x DP instr",
+                         "peak_source": "live DFMA probe on this GPU (MEASURED_PEAKS.json "
+                                        "has no FP64 figure)",
+                         "step_frac": total_cells * (i_fwd + i_bwd) * 2 / world / t_step / 1e12
+                         / peak},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches_per_step * args.steps,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -64,6 +64,12 @@ const char *sk_last_error(void);
 /* number of SMs of the current device (the persistent-grid size basis) */
 int sk_device_sms(void);
 
+/* FP64 roofline probe: enqueues independent DFMA chains on all SMs; the
+ * caller times it with CUDA events and divides *fma_count by the duration
+ * (bench.py's roofline denominator).  scratch: sk_dfma_probe_scratch_bytes(). */
+size_t sk_dfma_probe_scratch_bytes(void);
+int sk_dfma_probe(double *scratch, int iters, double *fma_count, void *stream);
+
 /* ---- forward ----------------------------------------------------------- */
 
 size_t sk_forward_batch_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d,
@@ -94,6 +100,10 @@ int sk_solve_delta(const double *delta, int64_t B, int64_t r1, int64_t r2, int l
 int sk_solve_delta_grid(const double *delta, int64_t r1, int64_t r2, int lam1, int lam2,
                         double *grid, void *stream);
 
+/* mirror the upper triangle of an (n, n) row-major matrix (leading dim ld)
+ * into the lower one; used to assemble a sharded symmetric Gram. */
+int sk_mirror_upper(double *g, int64_t n, int64_t ld, void *stream);
+
 /* ---- backward ---------------------------------------------------------- */
 
 size_t sk_backward_batch_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d,
@@ -108,9 +118,14 @@ int sk_backward_batch(const double *x, const double *y, int64_t B, int64_t L1, i
 size_t sk_backward_gram_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
                                         int64_t d, int lam1, int lam2, int static_kernel,
                                         int symmetric);
-/* F = sum_{a in rows, b} cot[a - row_begin, b] G[a, b];  grad_x += dF/dx,
- * grad_y += dF/dy (grad_y unused when y == NULL: both sides land in grad_x).
- * Gradients ACCUMULATE into the caller's buffers (zero them first). */
+/* F = sum_{a, b} cot[a, b] G[a, b] restricted to the pairs this call solves
+ * (rows a in [row_begin, row_end); symmetric: pairs a <= b, weighted by
+ * cot[a,b] + cot[b,a] because G mirrors the upper triangle).  cot is the FULL
+ * (n1, n2) cotangent.  grad_x += dF/dx, grad_y += dF/dy (grad_y unused when
+ * y == NULL: both sides land in grad_x).  Gradients ACCUMULATE into the
+ * caller's buffers with device atomics (zero them first); values are
+ * deterministic to rounding, not bitwise, across runs.  The batch backward
+ * (no shared paths) is bitwise deterministic. */
 int sk_backward_gram(const double *x, const double *y, int64_t n1, int64_t n2, int64_t L1,
                      int64_t L2, int64_t d, int lam1, int lam2, int static_kernel,
                      double sigma, int64_t row_begin, int64_t row_end, const double *cot,

@@ -25,6 +25,8 @@ SIGNATURES = {
     "sk_abi_version": ([], _ci),
     "sk_last_error": ([], ctypes.c_char_p),
     "sk_device_sms": ([], _ci),
+    "sk_dfma_probe_scratch_bytes": ([], _sz),
+    "sk_dfma_probe": ([_dp, _ci, ctypes.POINTER(ctypes.c_double), _vp], _ci),
     "sk_forward_batch_workspace_bytes": ([_i64, _i64, _i64, _i64, _ci, _ci, _ci], _sz),
     "sk_forward_batch": ([_dp, _dp, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd, _dp, _vp, _sz,
                           _vp], _ci),
@@ -34,6 +36,7 @@ SIGNATURES = {
     "sk_solve_delta_workspace_bytes": ([_i64, _i64, _i64, _ci, _ci], _sz),
     "sk_solve_delta": ([_dp, _i64, _i64, _i64, _ci, _ci, _dp, _vp, _sz, _vp], _ci),
     "sk_solve_delta_grid": ([_dp, _i64, _i64, _ci, _ci, _dp, _vp], _ci),
+    "sk_mirror_upper": ([_dp, _i64, _i64, _vp], _ci),
     "sk_backward_batch_workspace_bytes": ([_i64, _i64, _i64, _i64, _ci, _ci, _ci], _sz),
     "sk_backward_batch": ([_dp, _dp, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd, _dp, _dp, _dp,
                            _dp, _vp, _sz, _vp], _ci),

@@ -620,3 +620,45 @@ int sk_backward_gram(const double* x, const double* y, int64_t n1, int64_t n2, i
 }
 
 }  // extern "C"
+
+// ================================================================ peak probe
+// Independent DFMA chains (8 per thread, 8 warps per CTA, 8 CTAs per SM):
+// the FP64 FMA-pipe issue rate that bench.py divides by (the roofline of
+// this path).  Timed by the caller with CUDA events.
+namespace sk {
+__global__ void dfma_probe_kernel(double* out, double a, double b, int iters) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5,
+         x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+}  // namespace sk
+
+extern "C" size_t sk_dfma_probe_scratch_bytes(void) {
+  return (size_t)device_sms() * 8 * 256 * sizeof(double);
+}
+
+extern "C" int sk_dfma_probe(double* scratch, int iters, double* fma_count, void* stream) {
+  const int blocks = device_sms() * 8, threads = 256;
+  dfma_probe_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(scratch, 0.999, 1e-3, iters);
+  SK_CUDA(cudaGetLastError());
+  if (fma_count) *fma_count = (double)blocks * threads * (double)iters * 32.0;
+  return SK_OK;
+}
+
+// Mirror the upper triangle of an (n x n) matrix into its lower triangle
+// (kernel.py:177-179); used after the sharded Gram all-gather.
+extern "C" int sk_mirror_upper(double* g, int64_t n, int64_t ld, void* stream) {
+  if (n < 0 || ld < n) return fail(SK_INVALID_ARGUMENT, "bad matrix shape");
+  if (n < 2) return SK_OK;
+  int blocks = (int)std::min<int64_t>((n * n + 255) / 256, 4096);
+  mirror_upper<<<blocks, 256, 0, (cudaStream_t)stream>>>(g, ld, 0, (int)n);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}

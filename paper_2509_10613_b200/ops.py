@@ -166,3 +166,32 @@ def backward_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, grad_x=None, gr
                                     _ptr(grad_y) if not sym else None, _ptr(ws), ws.numel(),
                                     _stream()))
     return grad_x, grad_y
+
+
+def mirror_upper(G: torch.Tensor) -> torch.Tensor:
+    """In place: lower triangle := upper triangle (kernel.py:177-179)."""
+    lib = _lib.load()
+    n = G.shape[0]
+    _lib.check(lib.sk_mirror_upper(_ptr(G), n, G.stride(0), _stream()))
+    return G
+
+
+def dfma_peak(iters: int = 4096, reps: int = 3) -> float:
+    """Measured FP64 FMA rate (FMA/s) of this device: the roofline denominator."""
+    lib = _lib.load()
+    import ctypes
+    dev = torch.device("cuda", torch.cuda.current_device())
+    scratch = torch.empty(lib.sk_dfma_probe_scratch_bytes() // 8 + 1, dtype=torch.float64,
+                          device=dev)
+    cnt = ctypes.c_double(0.0)
+    _lib.check(lib.sk_dfma_probe(_ptr(scratch), 64, ctypes.byref(cnt), _stream()))  # warm
+    best = 0.0
+    for _ in range(reps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _lib.check(lib.sk_dfma_probe(_ptr(scratch), iters, ctypes.byref(cnt), _stream()))
+        e1.record()
+        e1.synchronize()
+        best = max(best, cnt.value / (e0.elapsed_time(e1) * 1e-3))
+    return best
