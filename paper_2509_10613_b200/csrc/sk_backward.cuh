@@ -184,6 +184,12 @@ bwd_kernel(Problem pb, BwdArgs ba) {
     if constexpr (MAP == DBUF) {
       for (int64_t e = u; e < (int64_t)pb.M1c * pb.M2c; e += 32) dbuf[e] = 0.0;
     }
+    // increment-gradient scratch of this pair: rows [M1c][DP], cols [M2c][DP]
+    double* __restrict__ gxs = ba.gscr + slot * ba.gscr_stride;
+    double* __restrict__ gcs = gxs + (int64_t)pb.M1c * DP;
+    if constexpr (MAP == FUSED) {
+      for (int64_t e = u; e < (int64_t)(pb.M1c + pb.M2c) * DP; e += 32) gxs[e] = 0.0;
+    }
     __syncwarp();
     double* __restrict__ gR = ba.gradR + pr * ba.gR_path;
     double* __restrict__ gC = ba.gradC + pc * ba.gC_path;
@@ -365,11 +371,14 @@ bwd_kernel(Problem pb, BwdArgs ba) {
               gys[k] = g;
             }
             if (u == 0 && colv) {
-              // telescope dF/d(dy_j) to points j, j+1 (kernel_grad.py:58-60)
-              double* q = gC + (int64_t)jc * dR;
-              for (int k = 0; k < dR; ++k) {
-                grad_add(q + k, -gys[k], atomic);
-                grad_add(q + dR + k, gys[k], atomic);
+              // lane 0 holds the strip's column sum: accumulate dF/d(dy_j)
+              double2* q = reinterpret_cast<double2*>(gcs + (int64_t)jc * DP);
+#pragma unroll
+              for (int k = 0; k < DP / 2; ++k) {
+                double2 v = q[k];
+                v.x += gys[2 * k];
+                v.y += gys[2 * k + 1];
+                q[k] = v;
               }
             }
           } else {
@@ -387,27 +396,55 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         }
       }
       if constexpr (MAP == FUSED) {
-        // row-side point gradients, lanes in a fixed order (telescoping
-        // touches the neighbour lane's first point)
-        for (int ln = 31; ln >= 0; --ln) {
-          if (u == ln) {
+        // row-side dF/d(dx_i) into the pair's scratch.  A coarse row owned by
+        // one lane is stored once; when 2^lam1 > R a coarse row spans lanes
+        // (and possibly strips) and the lanes add in a fixed order.
+        if (ba.rows_exclusive) {
 #pragma unroll
-            for (int c = 0; c < RC; ++c) {
-              const int i = i0 + c;
-              if (i < pb.M1c) {
-                double* q = gR + (int64_t)i * dR;
+          for (int c = 0; c < RC; ++c) {
+            const int i = i0 + c;
+            if (i < pb.M1c) {
+              double2* q = reinterpret_cast<double2*>(gxs + (int64_t)i * DP);
 #pragma unroll
-                for (int k = 0; k < DP; ++k) {
-                  if (k < dR) {
-                    grad_add(q + k, -gxr[c][k], atomic);
-                    grad_add(q + dR + k, gxr[c][k], atomic);
-                  }
+              for (int k = 0; k < DP / 2; ++k) q[k] = make_double2(gxr[c][2 * k], gxr[c][2 * k + 1]);
+            }
+          }
+        } else {
+          for (int ln = 31; ln >= 0; --ln) {
+            if (u == ln) {
+#pragma unroll
+              for (int c = 0; c < RC; ++c) {
+                const int i = i0 + c;
+                if (i < pb.M1c) {
+#pragma unroll
+                  for (int k = 0; k < DP; ++k) gxs[(int64_t)i * DP + k] += gxr[c][k];
                 }
               }
             }
+            __syncwarp();
           }
-          __syncwarp();
         }
+      }
+      __syncwarp();
+    }
+
+    if constexpr (MAP == FUSED) {
+      // telescope increment gradients to point gradients (kernel_grad.py:55-60)
+      // and flush once per pair, coalesced across the warp
+      __syncwarp();
+      for (int64_t e = u; e < (int64_t)(pb.M1c + 1) * dR; e += 32) {
+        const int p = (int)(e / dR), k = (int)(e % dR);
+        double v = 0.0;
+        if (p >= 1) v += gxs[(int64_t)(p - 1) * DP + k];
+        if (p < pb.M1c) v -= gxs[(int64_t)p * DP + k];
+        grad_add(gR + e, v, atomic);
+      }
+      for (int64_t e = u; e < (int64_t)(pb.M2c + 1) * dR; e += 32) {
+        const int p = (int)(e / dR), k = (int)(e % dR);
+        double v = 0.0;
+        if (p >= 1) v += gcs[(int64_t)(p - 1) * DP + k];
+        if (p < pb.M2c) v -= gcs[(int64_t)p * DP + k];
+        grad_add(gC + e, v, atomic);
       }
       __syncwarp();
     }

@@ -430,7 +430,7 @@ struct BwdPlan {
   int smem_bytes = 0;
   int threads = 128;
   int64_t blocks = 0, slots = 0, nitems = 0;
-  int64_t rowck_stride = 0, colck_stride = 0, row_stride = 0, dbuf_stride = 0;
+  int64_t rowck_stride = 0, colck_stride = 0, row_stride = 0, dbuf_stride = 0, gscr_stride = 0;
 };
 
 static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, int64_t M1c,
@@ -475,11 +475,12 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   pl.colck_stride = (int64_t)align_up((size_t)(nstrips * NB * s.R * 32), 32);
   pl.row_stride = (int64_t)align_up((size_t)(M2 + 1), 32);
   pl.dbuf_stride = kind == RBF ? (int64_t)align_up((size_t)(M1c * M2c), 32) : 0;
+  pl.gscr_stride = kind == LINEAR ? (int64_t)align_up((size_t)((M1c + M2c) * s.DP), 32) : 0;
   return SK_OK;
 }
 
 struct BwdLayout {
-  size_t prepR = 0, prepC = 0, rowck = 0, colck = 0, rows = 0, dbuf = 0, total = 0;
+  size_t prepR = 0, prepC = 0, rowck = 0, colck = 0, rows = 0, dbuf = 0, gscr = 0, total = 0;
 };
 
 static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n2, int64_t L1,
@@ -511,7 +512,8 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   lo.colck = align_up((size_t)pl.slots * pl.colck_stride * sizeof(double), 256);
   lo.rows = align_up((size_t)pl.slots * pl.row_stride * 2 * sizeof(double), 256);
   lo.dbuf = align_up((size_t)pl.slots * pl.dbuf_stride * sizeof(double), 256);
-  lo.total = lo.prepR + lo.prepC + lo.rowck + lo.colck + lo.rows + lo.dbuf;
+  lo.gscr = align_up((size_t)pl.slots * pl.gscr_stride * sizeof(double), 256);
+  lo.total = lo.prepR + lo.prepC + lo.rowck + lo.colck + lo.rows + lo.dbuf + lo.gscr;
   if (query) {
     *query = lo.total;
     return SK_OK;
@@ -543,6 +545,10 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   p += lo.rows;
   ba.dbuf = reinterpret_cast<double*>(p);
   ba.dbuf_stride = pl.dbuf_stride;
+  p += lo.dbuf;
+  ba.gscr = reinterpret_cast<double*>(p);
+  ba.gscr_stride = pl.gscr_stride;
+  ba.rows_exclusive = (1 << g.lamR) <= pl.shape.R ? 1 : 0;
   const double* xr = g.swap ? y : x;
   const double* xc = g.swap ? x : y;
   launch_prep(kind, xr, g.nR, g.LR, d, pb.dpad, prepR, st);

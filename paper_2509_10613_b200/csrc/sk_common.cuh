@@ -66,6 +66,9 @@ struct BwdArgs {
   int64_t row_stride;
   double* dbuf;  // DBUF: per-slot coarse adjoint [M1c][M2c]
   int64_t dbuf_stride;
+  double* gscr;  // FUSED: per-slot increment gradients [M1c + M2c][DP]
+  int64_t gscr_stride;
+  int rows_exclusive;  // 2^lam1 <= R: every coarse row belongs to one lane
   // outputs (point gradients, real dimension d)
   double* gradR;  // gradient of the grid-row path set
   double* gradC;  // gradient of the grid-column path set
