@@ -1,0 +1,215 @@
+"""Drop-in facade with the reference's kernel API (sigcore 0.1.0).
+
+Same names, signatures, exceptions and dtype rules as
+/root/reference/pkg/src/sigcore/kernel.py and kernel_grad.py, so code (and
+the reference's own kernel tests) written against sigcore can switch to the
+B200 path by importing this module instead:
+
+    from paper_2509_10613_b200 import sigcore_compat as sc
+    sc.kernel_batch(x, y, sc.KernelConfig(1, 1))
+
+numpy arrays in, new numpy arrays out (the caller owns them), exactly like the
+reference; every solve runs on the GPU (current CUDA device) through the C ABI.
+`threads` is accepted for signature compatibility and ignored (results never
+depended on it); `strip_width` likewise has no GPU meaning.
+
+Divergence (documented): integer-dtype paths are cast to float64 instead of
+reproducing the reference's integer-buffer bug.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import ops
+from .errors import InvalidArgument, InvalidState
+
+__all__ = ["KernelConfig", "SolveResult", "InvalidArgument", "InvalidState", "increment_gram",
+           "fine_cells", "solve_workspace_elements", "solve_goursat", "kernel_batch",
+           "kernel_gram", "kernel_backward", "kernel_batch_backward"]
+
+
+@dataclass(frozen=True)
+class KernelConfig:
+    """Per-axis dyadic refinement orders, strip width, grid retention (kernel.py:21-38)."""
+
+    dyadic_x: int = 0
+    dyadic_y: int = 0
+    strip_width: int = 32
+    store_grid: bool = False
+
+    def __post_init__(self):
+        if self.dyadic_x < 0 or self.dyadic_y < 0:
+            raise InvalidArgument("dyadic orders must be >= 0")
+        if self.strip_width < 1:
+            raise InvalidArgument("strip width must be >= 1")
+
+    @property
+    def scale(self) -> float:
+        return 2.0 ** -(self.dyadic_x + self.dyadic_y)
+
+
+@dataclass
+class SolveResult:
+    """Kernel value, plus the full fine-resolution grid when retained (kernel.py:41-46)."""
+
+    value: float
+    grid: np.ndarray | None = None
+
+
+def _device():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _dtype_of(*arrays):
+    dt = np.result_type(*[a.dtype for a in arrays])
+    return dt if np.issubdtype(dt, np.floating) else np.dtype(np.float64)
+
+
+def _as_paths(x, name):
+    x = np.ascontiguousarray(x)
+    if x.ndim == 2:
+        x = x[None]
+    if x.ndim != 3:
+        raise InvalidArgument(f"{name} must be (L, d) or (B, L, d), got shape {x.shape}")
+    if x.shape[1] < 2:
+        raise InvalidArgument(f"{name} needs at least 2 points per path")
+    return x
+
+
+def _cuda(a):
+    return torch.as_tensor(np.asarray(a, dtype=np.float64), device=_device())
+
+
+def increment_gram(x, y) -> np.ndarray:
+    """Materialised increment products (kernel.py:60-77).  The B200 solvers never
+    form this matrix; it is provided for API compatibility (one batched DGEMM)."""
+    x = np.asarray(x)
+    squeeze = x.ndim == 2
+    x = _as_paths(x, "x")
+    y = _as_paths(y, "y")
+    if x.shape[0] != y.shape[0]:
+        raise InvalidArgument(f"batch sizes differ: {x.shape[0]} vs {y.shape[0]}")
+    if x.shape[2] != y.shape[2]:
+        raise InvalidArgument(f"path dimensions differ: {x.shape[2]} vs {y.shape[2]}")
+    dt = _dtype_of(x, y)
+    dx = torch.diff(_cuda(x), dim=1)
+    dy = torch.diff(_cuda(y), dim=1)
+    delta = torch.matmul(dx, dy.transpose(1, 2)).cpu().numpy().astype(dt, copy=False)
+    return delta[0] if squeeze else delta
+
+
+def fine_cells(delta_shape, cfg: KernelConfig) -> tuple[int, int]:
+    """kernel.py:80-82."""
+    return (delta_shape[0] << cfg.dyadic_x, delta_shape[1] << cfg.dyadic_y)
+
+
+def solve_workspace_elements(delta_shape, cfg: KernelConfig) -> int:
+    """kernel.py:85-91 (the reference's gridless CPU march; reported for API
+    compatibility -- the GPU solve keeps its wavefront in registers)."""
+    m1, m2 = fine_cells(delta_shape, cfg)
+    if m2 > m1:
+        m1, m2 = m2, m1
+    return 3 * (min(cfg.strip_width, m1) + 1) + (m2 + 1)
+
+
+def solve_goursat(delta, cfg: KernelConfig) -> SolveResult:
+    """One PDE solve over a given coarse increment matrix (kernel.py:94-122)."""
+    delta = np.asarray(delta)
+    if delta.ndim != 2 or delta.shape[0] < 1 or delta.shape[1] < 1:
+        raise InvalidArgument(f"increment matrix must be 2-d and non-empty, "
+                              f"got shape {delta.shape}")
+    dt = _dtype_of(delta)
+    d = _cuda(delta)
+    if cfg.store_grid:
+        grid = ops.solve_delta_grid(d, cfg.dyadic_x, cfg.dyadic_y).cpu().numpy()
+        return SolveResult(float(grid[-1, -1]), grid.astype(dt, copy=False))
+    v = ops.solve_delta(d[None], cfg.dyadic_x, cfg.dyadic_y)
+    return SolveResult(float(v.item()))
+
+
+def kernel_batch(x, y, cfg: KernelConfig = KernelConfig(), threads: int | None = None):
+    """Pairwise k(x_b, y_b) for aligned batches (kernel.py:125-148)."""
+    x = _as_paths(x, "x")
+    y = _as_paths(y, "y")
+    if x.shape[0] != y.shape[0]:
+        raise InvalidArgument(f"batch sizes differ: {x.shape[0]} vs {y.shape[0]}")
+    if x.shape[2] != y.shape[2]:
+        raise InvalidArgument(f"path dimensions differ: {x.shape[2]} vs {y.shape[2]}")
+    dt = _dtype_of(x, y)
+    out = ops.forward_batch(_cuda(x), _cuda(y), cfg.dyadic_x, cfg.dyadic_y, 0, 1.0)
+    return out.cpu().numpy().astype(dt, copy=False)
+
+
+def kernel_gram(x, y=None, cfg: KernelConfig = KernelConfig(), threads: int | None = None):
+    """Gram matrix G[a, b] = k(x_a, y_b) (kernel.py:151-180); exactly symmetric
+    when y is x (or omitted)."""
+    symmetric = y is None or y is x
+    x = _as_paths(x, "x")
+    yy = x if symmetric else _as_paths(y, "y")
+    if x.shape[2] != yy.shape[2]:
+        raise InvalidArgument(f"path dimensions differ: {x.shape[2]} vs {yy.shape[2]}")
+    dt = _dtype_of(x, yy)
+    G = ops.forward_gram(_cuda(x), None if symmetric else _cuda(yy), cfg.dyadic_x,
+                         cfg.dyadic_y, 0, 1.0)
+    return G.cpu().numpy().astype(dt, copy=False)
+
+
+def _one_pair(x, name):
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if x.ndim != 2 or x.shape[0] < 2:
+        raise InvalidArgument(f"{name} must be a single (L, d) path with L >= 2, "
+                              f"got shape {x.shape}")
+    return x
+
+
+def kernel_backward(x, y, cfg: KernelConfig, forward: SolveResult, cot: float = 1.0):
+    """Gradients of cot * k(x, y) w.r.t. both paths (kernel_grad.py:27-61).
+
+    The reference differentiates through a stored forward grid; the B200
+    backward recomputes the forward values it needs from checkpoints, so the
+    grid is only validated (presence and shape, same errors as the reference)."""
+    x = _one_pair(x, "x")
+    y = _one_pair(y, "y")
+    if x.shape[1] != y.shape[1]:
+        raise InvalidArgument(f"path dimensions differ: {x.shape[1]} vs {y.shape[1]}")
+    if forward.grid is None:
+        raise InvalidState("kernel_backward needs a forward solve with store_grid=True")
+    m1, m2 = fine_cells((x.shape[0] - 1, y.shape[0] - 1), cfg)
+    if forward.grid.shape != (m1 + 1, m2 + 1):
+        raise InvalidArgument(
+            f"forward grid shape {forward.grid.shape} does not match "
+            f"({m1 + 1}, {m2 + 1}) for this config")
+    _, gx, gy = ops.backward_batch(_cuda(x[None]), _cuda(y[None]), cfg.dyadic_x, cfg.dyadic_y,
+                                   0, 1.0, _cuda(np.array([float(cot)])))
+    return gx[0].cpu().numpy(), gy[0].cpu().numpy()
+
+
+def kernel_batch_backward(x, y, cfg: KernelConfig, cot=None, threads: int | None = None):
+    """Values and gradients for aligned batches (kernel_grad.py:64-98)."""
+    x = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    y = np.ascontiguousarray(np.asarray(y, dtype=np.float64))
+    squeeze = x.ndim == 2
+    if x.ndim == 2:
+        x = x[None]
+    if y.ndim == 2:
+        y = y[None]
+    if x.shape[0] != y.shape[0]:
+        raise InvalidArgument(f"batch sizes differ: {x.shape[0]} vs {y.shape[0]}")
+    if cot is None:
+        cot = np.ones(x.shape[0])
+    cot = np.atleast_1d(np.asarray(cot, dtype=np.float64))
+    if cot.shape != (x.shape[0],):
+        raise InvalidArgument(f"cotangent has shape {cot.shape}, "
+                              f"expected ({x.shape[0]},)")
+    x = _as_paths(x, "x")
+    y = _as_paths(y, "y")
+    vals, gx, gy = ops.backward_batch(_cuda(x), _cuda(y), cfg.dyadic_x, cfg.dyadic_y, 0, 1.0,
+                                      _cuda(cot), want_values=True)
+    vals, gx, gy = vals.cpu().numpy(), gx.cpu().numpy(), gy.cpu().numpy()
+    if squeeze:
+        return vals[0], gx[0], gy[0]
+    return vals, gx, gy

@@ -138,6 +138,24 @@ def main():
     gx, gy = sc.kernel_backward(x, y, cfg, res, 1.0)
     save("c5_pair_grad", x=x, y=y, value=np.array(res.value), gx=gx, gy=gy)
 
+    # dyadic-convergence oracle: depth-12 truncated signature inner products of
+    # low-variation paths (reference tests/conftest.py:40-52, 93-100)
+    rng = np.random.default_rng(4)
+    xs, ys, oracles = [], [], []
+    for _ in range(5):
+        steps = rng.uniform(0.2, 1.0, size=(4, 2))
+        steps *= 1.0 / steps.sum()
+        x = np.zeros((5, 2)); x[1:] = np.cumsum(steps, axis=0)
+        steps = rng.uniform(0.2, 1.0, size=(5, 2))
+        steps *= 1.0 / steps.sum()
+        y = np.zeros((6, 2)); y[1:] = np.cumsum(steps, axis=0)
+        shape = sc.tensor_shape(2, 12)
+        opts = sc.SigOptions(12)
+        sx = sc.TruncatedSig(shape, sc.signature(x, opts))
+        sy = sc.TruncatedSig(shape, sc.signature(y, opts))
+        xs.append(x); ys.append(y); oracles.append(sc.dot(sx, sy))
+    save("dyadic_convergence", x=np.array(xs), y=np.array(ys), oracle=np.array(oracles))
+
     print("reference:", sc.__file__, "numba", __import__("numba").__version__,
           "numpy", np.__version__, file=sys.stderr)
 
