@@ -128,6 +128,7 @@ struct FwdPlan {
   int64_t hand_stride = 0;
   int64_t nitems = 0;
   int P = 1;
+  int smem_bytes = 0;
 };
 
 // Chooses lanes-per-pair and the persistent grid.  `gram` marks tiles whose
@@ -148,8 +149,11 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
   const int64_t lanes_per_pair = (M1 + s.R - 1) / s.R;
   s.XW = false;
   s.W = 1;
-  if (gram || npairs * 4 >= target_lanes || lanes_per_pair <= 8) {
-    s.G = 4;
+  // G = 4 packs 8 pairs per warp and needs them to share the column path
+  // (Gram tiles); batches use one pair per warp, or per CTA when long pairs
+  // are too few to fill the GPU.
+  if (gram) {
+    s.G = (npairs * 4 >= target_lanes || lanes_per_pair <= 8) ? 4 : 32;
   } else if (npairs * 32 >= target_lanes || lanes_per_pair <= 64 || kind != LINEAR) {
     s.G = 32;
   } else {
@@ -159,21 +163,30 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
     s.W = W;
     s.G = 32 * W;
   }
-  FwdFn fn = kind == LINEAR ? select_fwd_linear(s) : kind == RBF ? select_fwd_rbf(s)
-                                                                 : select_fwd_delta(s);
+  int smem = 0;
+  FwdFn fn = kind == LINEAR ? select_fwd_linear(s, smem)
+             : kind == RBF  ? select_fwd_rbf(s, smem)
+                            : select_fwd_delta(s, smem);
   if (!fn) return fail(SK_INVALID_ARGUMENT, "no forward kernel instance for this shape");
   pl.shape = s;
   pl.fn = fn;
+  pl.smem_bytes = smem;
   pl.threads = s.XW ? 32 * s.W : 128;
   pl.P = s.XW ? 1 : 32 / s.G;
   const int warps = pl.threads / 32;
   if (mode == BATCH) pl.nitems = (npairs + pl.P - 1) / pl.P;
   else pl.nitems = gram_items(mode, n2, r0, r1, pl.P);
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+          cudaSuccess)
+    (void)cudaGetLastError();
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, pl.threads, 0) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, pl.threads, smem) !=
           cudaSuccess ||
-      occ < 1)
+      occ < 1) {
+    (void)cudaGetLastError();
     occ = 1;
+  }
   int64_t want = s.XW ? pl.nitems : (pl.nitems + warps - 1) / warps;
   pl.blocks = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)occ * sms));
   pl.slots = s.XW ? pl.blocks : pl.blocks * warps * pl.P;
@@ -302,7 +315,7 @@ static int forward_impl(const double* x, const double* y, int64_t n1, int64_t n2
   pb.C.path_stride = (kind == RBF ? g.LC : g.LC - 1) * pb.dpad;
   pb.nitems = pl.nitems;
   pb.out = out;
-  pl.fn<<<(unsigned)pl.blocks, pl.threads, 0, st>>>(pb, hand, pl.hand_stride);
+  pl.fn<<<(unsigned)pl.blocks, pl.threads, pl.smem_bytes, st>>>(pb, hand, pl.hand_stride);
   SK_CUDA(cudaGetLastError());
   if (sym) {
     int64_t span = r1 - r0;
@@ -388,8 +401,8 @@ static int solve_delta_impl(const double* delta, int64_t B, int64_t r1, int64_t 
   if (ws_bytes < need) return fail(SK_INVALID_ARGUMENT, "workspace too small");
   pb.nitems = pl.nitems;
   pb.out = out;
-  pl.fn<<<(unsigned)pl.blocks, pl.threads, 0, st>>>(pb, static_cast<double*>(ws),
-                                                     pl.hand_stride);
+  pl.fn<<<(unsigned)pl.blocks, pl.threads, pl.smem_bytes, st>>>(
+      pb, static_cast<double*>(ws), pl.hand_stride);
   SK_CUDA(cudaGetLastError());
   return SK_OK;
 }

@@ -9,160 +9,59 @@
 //     "step" (F fine columns) at a time, lagging lane u-1 by one step.  The
 //     three rotating anti-diagonals of the reference become registers: k_left
 //     per owned row, the top-row value from lane u-1 arrives by __shfl_up_sync.
-//   * G <= 32: 32/G pairs per warp (Gram tiles share the column path, so the
-//     per-step column loads are warp broadcasts).  XW: one pair per CTA and
-//     G = blockDim.x lanes; lane 31 -> lane 0 of the next warp goes through a
-//     double-buffered shared-memory slot with one CTA barrier per step (long
-//     pairs, BASELINE config 4).
+//   * G = 4: 8 pairs per warp sharing the column path (Gram tiles); G = 32: one
+//     pair per warp; XW: one pair per CTA, G = blockDim.x lanes, lane 31 ->
+//     lane 0 of the next warp through a double-buffered shared-memory slot and
+//     one CTA barrier per step (long pairs, BASELINE config 4).
+//   * column data (increments dy_j or RBF nodes y_{j+1}) and the strip's
+//     handoff row stream through a shared-memory ring filled by cp.async PF
+//     steps ahead, so no global latency sits on the recurrence;
 //   * the increment product delta (kernel.py:60-77) is never materialised: the
-//     lane keeps its rows' (pre-scaled) increments in registers and forms
-//     <dx_i, dy_j> on the fly per coarse cell; dyadic refinement is on the fly
-//     (fine cell (s,t) reads coarse (s-1)>>lam1, (t-1)>>lam2, _kernels.py:325).
+//     lane keeps its rows' increments in registers and forms <dx_i, dy_j> for
+//     step tau+1 while the recurrence of step tau runs (software pipeline);
+//     dyadic refinement is on the fly (fine cell (s,t) reads coarse
+//     (s-1)>>lam1, (t-1)>>lam2, _kernels.py:325);
 //   * the strip's bottom row is handed to the next strip through a per-group
-//     row in global memory (L2 resident), in place, exactly like the
-//     reference's handoff row.
+//     row in global memory (L2 resident), in place, like the reference's
+//     handoff row.
 #pragma once
-#include "sk_common.cuh"
+#include "sk_cell.cuh"
 
 namespace sk {
 
-// _kernels.py:286-290: k = (k_up + k_left) * A(p) - k_diag * B(p),
-// A = 1 + p/2 + p^2/12, B = 1 - p^2/12 (A, B hoisted per coarse cell).
-struct Coef {
-  double A, B;
-};
-__device__ __forceinline__ Coef coef(double p) {
-  double q = p * p;
-  Coef c;
-  c.A = fma(q, 1.0 / 12.0, fma(p, 0.5, 1.0));
-  c.B = fma(-q, 1.0 / 12.0, 1.0);
-  return c;
-}
-__device__ __forceinline__ double cell(double up, double left, double diag, const Coef& c) {
-  return fma(up + left, c.A, -diag * c.B);
-}
-
-template <int DP>
-__device__ __forceinline__ void load_vec(double (&v)[DP], const double* __restrict__ src) {
-  if constexpr (DP % 2 == 0) {
-    const double2* s2 = reinterpret_cast<const double2*>(src);
-#pragma unroll
-    for (int k = 0; k < DP / 2; ++k) {
-      double2 t = __ldg(s2 + k);
-      v[2 * k] = t.x;
-      v[2 * k + 1] = t.y;
-    }
-  } else {
-#pragma unroll
-    for (int k = 0; k < DP; ++k) v[k] = __ldg(src + k);
-  }
-}
-
-template <int DP>
-__device__ __forceinline__ double dot(const double (&a)[DP], const double (&b)[DP]) {
-  double s = a[0] * b[0];
-#pragma unroll
-  for (int k = 1; k < DP; ++k) s = fma(a[k], b[k], s);
-  return s;
-}
-
-template <int DP>
-__device__ __forceinline__ double sqdist(const double (&a)[DP], const double (&b)[DP]) {
-  double t = a[0] - b[0];
-  double s = t * t;
-#pragma unroll
-  for (int k = 1; k < DP; ++k) {
-    t = a[k] - b[k];
-    s = fma(t, t, s);
-  }
-  return s;
-}
-
-// Row-path registers of one lane for one strip.
-template <int KIND, int DP, int RC>
-struct RowRegs {
-  static constexpr int NR = (KIND == RBF) ? RC + 1 : RC;
-  double v[NR][DP];
+template <int KIND, int DP, int F, int P>
+struct FwdRec {
+  static constexpr int CD = (KIND == DELTA) ? 0 : DP;  // column data doubles
+  static constexpr int RAW = CD + P * F;               // + handoff values per group
+  static constexpr int REC = (RAW + 1) & ~1;           // 16-byte aligned records
 };
 
-template <int KIND, int DP, int RC>
-__device__ __forceinline__ void load_rows(RowRegs<KIND, DP, RC>& rr, const Problem& pb,
-                                          int64_t pr, int i0, int ch) {
-  constexpr int NR = RowRegs<KIND, DP, RC>::NR;
-  const int lim = (KIND == RBF) ? pb.M1c + 1 : pb.M1c;
-#pragma unroll
-  for (int c = 0; c < NR; ++c) {
-    if (i0 + c < lim) {
-      load_vec<DP>(rr.v[c], pb.R.p + pr * pb.R.path_stride + (int64_t)(i0 + c) * pb.dpad + ch * DP);
-    } else {
-#pragma unroll
-      for (int k = 0; k < DP; ++k) rr.v[c][k] = 0.0;
-    }
-  }
-}
-
-// p for the lane's RC coarse rows at coarse column jc (LINEAR / DELTA), or the
-// RBF second difference using the K values carried between steps.
-template <int KIND, int DP, int RC>
-struct ColState {
-  double Kold[RC + 1];
-  double Knew[RC + 1];
-  int have;  // coarse column whose Kold/Knew are held (-1: none)
+template <bool XW, int G>
+struct FwdRing {
+  static constexpr int PF = 4;
+  static constexpr int SLOTS = XW ? 1024 : (G >= 32 ? 64 : 16);
 };
 
-template <int KIND, int DP, int RC>
-__device__ __forceinline__ void rbf_column(double (&K)[RC + 1], const RowRegs<KIND, DP, RC>& rr,
-                                           const Problem& pb, int64_t pc, int node) {
-  double yv[DP];
-  load_vec<DP>(yv, pb.C.p + pc * pb.C.path_stride + (int64_t)node * pb.dpad);
-#pragma unroll
-  for (int c = 0; c <= RC; ++c) K[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
-}
-
-template <int KIND, int DP, int RC>
-__device__ __forceinline__ void coarse_p(double (&p)[RC], RowRegs<KIND, DP, RC>& rr,
-                                         ColState<KIND, DP, RC>& cs, const Problem& pb,
-                                         int64_t pr, int64_t pc, int64_t pidx, int i0, int jc) {
-  if constexpr (KIND == LINEAR) {
-    if (pb.nch == 1) {
-      double dy[DP];
-      load_vec<DP>(dy, pb.C.p + pc * pb.C.path_stride + (int64_t)jc * pb.dpad);
-#pragma unroll
-      for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy);
-    } else {
-#pragma unroll
-      for (int c = 0; c < RC; ++c) p[c] = 0.0;
-      for (int ch = 0; ch < pb.nch; ++ch) {
-        double dy[DP];
-        load_vec<DP>(dy, pb.C.p + pc * pb.C.path_stride + (int64_t)jc * pb.dpad + ch * DP);
-        load_rows<KIND, DP, RC>(rr, pb, pr, i0, ch);
-#pragma unroll
-        for (int c = 0; c < RC; ++c) p[c] += dot<DP>(rr.v[c], dy);
-      }
-    }
-  } else if constexpr (KIND == RBF) {
-    if (cs.have != jc) {
-      if (cs.have == jc - 1) {
-#pragma unroll
-        for (int c = 0; c <= RC; ++c) cs.Kold[c] = cs.Knew[c];
-      } else {
-        rbf_column<KIND, DP, RC>(cs.Kold, rr, pb, pc, jc);
-      }
-      rbf_column<KIND, DP, RC>(cs.Knew, rr, pb, pc, jc + 1);
-      cs.have = jc;
-    }
-#pragma unroll
-    for (int c = 0; c < RC; ++c)
-      p[c] = ((cs.Knew[c + 1] - cs.Kold[c + 1]) - (cs.Knew[c] - cs.Kold[c])) * pb.scale;
-  } else {  // DELTA
-#pragma unroll
-    for (int c = 0; c < RC; ++c) {
-      int i = i0 + c;
-      p[c] = (i < pb.M1c) ? __ldg(pb.delta + pidx * (int64_t)pb.M1c * pb.M2c +
-                                  (int64_t)i * pb.M2c + jc) * pb.scale
-                          : 0.0;
-    }
+// Issue the ring record of step jj: column data of coarse column jc(jj) and
+// the handoff values of every group (strip > 0).  Executed by one warp.
+template <int KIND, int DP, int F, int P>
+__device__ __forceinline__ void fwd_issue(double* ring_slot, const Problem& pb, int64_t pc,
+                                          const double* hrow0, int64_t hand_stride, int jj,
+                                          int NS, int strip, int lane) {
+  using RC_ = FwdRec<KIND, DP, F, P>;
+  const bool valid = (jj >= 0) && (jj < NS);
+  const int jc = valid ? ((jj * F) >> pb.lam2) : 0;
+  if constexpr (RC_::CD > 0) {
+    const int node = (KIND == RBF) ? jc + 1 : jc;
+    const double* src = pb.C.p + pc * pb.C.path_stride + (int64_t)node * pb.dpad;
+    for (int c = lane; c < RC_::CD / 2; c += 32) cp_async16(ring_slot + 2 * c, src + 2 * c, valid);
   }
+  for (int e = lane; e < P * F; e += 32) {
+    const int g = e / F, f = e % F;
+    const double* src = hrow0 + g * hand_stride + (valid ? jj * F + f + 1 : 0);
+    cp_async8(ring_slot + RC_::CD + e, src, valid && strip > 0);
+  }
+  cp_async_commit();
 }
 
 // Forward kernel.  Template parameters:
@@ -171,13 +70,20 @@ __device__ __forceinline__ void coarse_p(double (&p)[RC], RowRegs<KIND, DP, RC>&
 //   R     fine rows per lane;  FR = fine rows per coarse row inside a lane
 //         (= min(2^lam1, R)), so RC = R / FR coarse rows per lane
 //   F     fine columns per step (= min(2^lam2, 4))
-//   G     lanes per pair (<= 32); ignored when XW (G = blockDim.x)
+//   G     lanes per pair (4 or 32); ignored when XW (G = blockDim.x)
 //   XW    cross-warp lane groups (one pair per CTA)
+// Every group of a warp must share the column path (Gram tiles / one pair).
 template <int KIND, int DP, int R, int FR, int F, int G, bool XW>
-__global__ void __launch_bounds__(XW ? 1024 : 128)
+__global__ void __launch_bounds__(XW ? 512 : 128)
 fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
   constexpr int RC = R / FR;
   constexpr int P = XW ? 1 : 32 / G;
+  using Rec = FwdRec<KIND, DP, F, P>;
+  using Rg = FwdRing<XW, G>;
+  constexpr int REC = Rec::REC;
+  constexpr int SLOTS = Rg::SLOTS;
+  constexpr int PF = Rg::PF;
+  extern __shared__ double smem_fwd[];
   __shared__ double xbuf[XW ? 2 : 1][XW ? 32 : 1][F];
 
   const int lane = threadIdx.x & 31;
@@ -186,6 +92,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
   const int Grt = XW ? (int)blockDim.x : G;
   const int g = XW ? 0 : lane / G;
   const int u = XW ? (int)threadIdx.x : lane % G;
+  double* ring = XW ? smem_fwd : smem_fwd + (size_t)warp * SLOTS * REC;
 
   const int M1 = pb.M1c << pb.lam1;
   const int M2 = pb.M2c << pb.lam2;
@@ -196,8 +103,10 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
   const int u_star = ((M1 - 1) % H) / R;
   const int r_star = (M1 - 1) % R;
 
-  const int64_t slot = XW ? (int64_t)blockIdx.x : ((int64_t)blockIdx.x * nw + warp) * P + g;
-  double* __restrict__ hrow = hand + slot * hand_stride;
+  const int64_t slot0 = XW ? (int64_t)blockIdx.x : ((int64_t)blockIdx.x * nw + warp) * P;
+  const double* hrow0 = hand + slot0 * hand_stride;  // group g's row: + g * hand_stride
+  double* __restrict__ hrow = hand + (slot0 + g) * hand_stride;
+  const bool issuer = !XW || warp == 0;
 
   const int64_t item0 = XW ? blockIdx.x : (int64_t)blockIdx.x * nw + warp;
   const int64_t istep = XW ? gridDim.x : (int64_t)gridDim.x * nw;
@@ -205,7 +114,13 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
   for (int64_t item = item0; item < pb.nitems; item += istep) {
     int64_t pr = 0, pc = 0, oidx = 0, pidx = 0;
     const bool valid = resolve_pair(pb, item, P, g, pr, pc, oidx, pidx);
-    if (!valid) { pr = 0; pc = 0; pidx = 0; }
+    if (!valid) pidx = 0;
+    {
+      // the warp's column path (all groups share it; group 0 always resolves)
+      int64_t pr0, oi0, pi0;
+      resolve_pair(pb, item, P, 0, pr0, pc, oi0, pi0);
+      if (!valid) pr = pr0;
+    }
 
     for (int t = u; t <= M2; t += Grt) hrow[t] = 1.0;
     if (XW) __syncthreads(); else __syncwarp();
@@ -215,8 +130,99 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
       const int i0 = rbase >> pb.lam1;
       RowRegs<KIND, DP, RC> rr;
       if constexpr (KIND != DELTA) load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
-      ColState<KIND, DP, RC> cs;
-      cs.have = -2;
+      double Kl[RC + 1], Kr[RC + 1];  // RBF: K at node columns jc, jc+1 of the pending step
+      int jcur = -1;
+      if constexpr (KIND == RBF) {
+        double y0[DP];
+        load_vec<DP>(y0, pb.C.p + pc * pb.C.path_stride);
+#pragma unroll
+        for (int c = 0; c <= RC; ++c) Kr[c] = exp(-sqdist<DP>(rr.v[c], y0) * pb.inv2s2);
+#pragma unroll
+        for (int c = 0; c <= RC; ++c) Kl[c] = Kr[c];
+      }
+      // prologue: PF records in flight
+      if (issuer) {
+        for (int q = 0; q < PF; ++q)
+          fwd_issue<KIND, DP, F, P>(ring + (q & (SLOTS - 1)) * REC, pb, pc, hrow0, hand_stride, q, NS, strip,
+                                    lane);
+      }
+
+      // coefficients of the next step (software pipeline)
+      auto coefs_for = [&](int jj, Coef (&cf)[RC]) {
+        const double* rec = ring + (jj & (SLOTS - 1)) * REC;
+        const int jc = (jj * F) >> pb.lam2;
+        double p[RC];
+        if constexpr (KIND == LINEAR) {
+          double dy[DP];
+#pragma unroll
+          for (int k = 0; k < DP; k += 2) {
+            const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+            dy[k] = t2.x;
+            dy[k + 1] = t2.y;
+          }
+          if (DP < 32 || pb.nch == 1) {  // d > 32 only ever selects DP = 32
+#pragma unroll
+            for (int c = 0; c < RC; ++c) {
+              // two partial sums halve the dependent FMA chain
+              double s0 = rr.v[c][0] * dy[0], s1 = rr.v[c][1] * dy[1];
+#pragma unroll
+              for (int k = 2; k < DP; k += 2) {
+                s0 = fma(rr.v[c][k], dy[k], s0);
+                s1 = fma(rr.v[c][k + 1], dy[k + 1], s1);
+              }
+              p[c] = (s0 + s1) * pb.scale;
+            }
+          } else {
+            // d > 32: chunked dot products (second chunk onwards from L1)
+#pragma unroll
+            for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy);
+            for (int ch = 1; ch < pb.nch; ++ch) {
+              double dyc[DP], xc[DP];
+              load_vec<DP>(dyc, pb.C.p + pc * pb.C.path_stride + (int64_t)jc * pb.dpad + ch * DP);
+#pragma unroll
+              for (int c = 0; c < RC; ++c) {
+                const int i = i0 + c;
+                if (i < pb.M1c) {
+                  load_vec<DP>(xc, pb.R.p + pr * pb.R.path_stride + (int64_t)i * pb.dpad + ch * DP);
+                  p[c] += dot<DP>(xc, dyc);
+                }
+              }
+            }
+#pragma unroll
+            for (int c = 0; c < RC; ++c) p[c] *= pb.scale;
+          }
+        } else if constexpr (KIND == RBF) {
+          if (jj >= 0 && jc != jcur) {
+            double yv[DP];
+#pragma unroll
+            for (int k = 0; k < DP; k += 2) {
+              const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+              yv[k] = t2.x;
+              yv[k + 1] = t2.y;
+            }
+#pragma unroll
+            for (int c = 0; c <= RC; ++c) {
+              Kl[c] = Kr[c];
+              Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
+            }
+            jcur = jc;
+          }
+#pragma unroll
+          for (int c = 0; c < RC; ++c) p[c] = ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale;
+        } else {  // DELTA: per-row coarse values straight from global
+#pragma unroll
+          for (int c = 0; c < RC; ++c) {
+            const int i = i0 + c;
+            p[c] = (i < pb.M1c && jj >= 0 && jj < NS)
+                       ? __ldg(pb.delta + pidx * (int64_t)pb.M1c * pb.M2c + (int64_t)i * pb.M2c + jc) *
+                             pb.scale
+                       : 0.0;
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < RC; ++c) cf[c] = coef(p[c]);
+      };
+
       double kl[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) kl[r] = 1.0;
@@ -224,11 +230,24 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
       double bot[F];
 #pragma unroll
       for (int f = 0; f < F; ++f) bot[f] = 1.0;
+      Coef cf[RC];
+      if (issuer) cp_async_wait<PF - 1>();
+      if (XW) __syncthreads(); else __syncwarp();
+      coefs_for(-u, cf);
 
       const int nsteps = NS + Grt - 1;
       for (int tau = 0; tau < nsteps; ++tau) {
+        if (issuer) {
+          fwd_issue<KIND, DP, F, P>(ring + ((tau + PF) & (SLOTS - 1)) * REC, pb, pc, hrow0,
+                                    hand_stride, tau + PF, NS, strip, lane);
+          cp_async_wait<PF - 1>();  // records <= tau + 1 landed
+        }
+        if (XW) __syncthreads(); else __syncwarp();
         const int jj = tau - u;
         const bool active = (jj >= 0) && (jj < NS);
+        Coef cfn[RC];
+        coefs_for(jj + 1, cfn);  // independent of this step's recurrence
+
         double tv[F];
         if constexpr (XW) {
 #pragma unroll
@@ -241,36 +260,25 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
 #pragma unroll
           for (int f = 0; f < F; ++f) tv[f] = __shfl_up_sync(0xffffffffu, bot[f], 1, G);
         }
-        if (u == 0 && active) {
+        if (u == 0) {
+          const double* rec = ring + (jj & (SLOTS - 1)) * REC + Rec::CD + g * F;
 #pragma unroll
-          for (int f = 0; f < F; ++f) tv[f] = (strip == 0) ? 1.0 : hrow[jj * F + f + 1];
+          for (int f = 0; f < F; ++f) tv[f] = (strip == 0) ? 1.0 : rec[f];
+        }
+#pragma unroll
+        for (int f = 0; f < F; ++f) {
+          double up = tv[f];
+          double dg = (f == 0) ? topc : tv[f - 1];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const double nk = cell(up, kl[r], dg, cf[r / FR]);
+            dg = kl[r];
+            kl[r] = active ? nk : kl[r];
+            up = nk;
+          }
+          bot[f] = up;
         }
         if (active) {
-          const int jc = (jj * F) >> pb.lam2;
-          double p[RC];
-          coarse_p<KIND, DP, RC>(p, rr, cs, pb, pr, pc, pidx, i0, jc);
-          if constexpr (KIND == LINEAR) {
-            if (pb.scale != 1.0) {
-#pragma unroll
-              for (int c = 0; c < RC; ++c) p[c] *= pb.scale;  // exact: power of two
-            }
-          }
-          Coef cf[RC];
-#pragma unroll
-          for (int c = 0; c < RC; ++c) cf[c] = coef(p[c]);
-#pragma unroll
-          for (int f = 0; f < F; ++f) {
-            double up = tv[f];
-            double dg = (f == 0) ? topc : tv[f - 1];
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              const double nk = cell(up, kl[r], dg, cf[r / FR]);
-              dg = kl[r];
-              kl[r] = nk;
-              up = nk;
-            }
-            bot[f] = up;
-          }
           topc = tv[F - 1];
           if (u == Grt - 1) {
 #pragma unroll
@@ -284,17 +292,26 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
             pb.out[oidx] = v;
           }
         }
+#pragma unroll
+        for (int c = 0; c < RC; ++c) cf[c] = cfn[c];
         if constexpr (XW) {
           if (lane == 31) {
 #pragma unroll
             for (int f = 0; f < F; ++f) xbuf[tau & 1][warp][f] = bot[f];
           }
-          __syncthreads();
         }
       }
+      if (issuer) cp_async_wait<0>();
       if (XW) __syncthreads(); else __syncwarp();
     }
   }
+}
+
+// Dynamic shared memory of one fwd_kernel CTA (bytes).
+template <int KIND, int DP, int F, int G, bool XW>
+constexpr int fwd_smem_bytes(int warps) {
+  using Rec = FwdRec<KIND, DP, F, XW ? 1 : 32 / G>;
+  return (XW ? 1 : warps) * FwdRing<XW, G>::SLOTS * Rec::REC * (int)sizeof(double);
 }
 
 }  // namespace sk

@@ -1,5 +1,5 @@
 // Forward kernel instances for static kernel kind LINEAR (split for parallel builds).
 #include "sk_fwd_tables.cuh"
 namespace sk {
-FwdFn select_fwd_linear(const FwdShape& s) { return sk_fwd_select<LINEAR>(s); }
+FwdFn select_fwd_linear(const FwdShape& s, int& smem) { return sk_fwd_select<LINEAR>(s, smem); }
 }  // namespace sk

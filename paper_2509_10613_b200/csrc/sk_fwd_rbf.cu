@@ -1,5 +1,5 @@
 // Forward kernel instances for static kernel kind RBF (split for parallel builds).
 #include "sk_fwd_tables.cuh"
 namespace sk {
-FwdFn select_fwd_rbf(const FwdShape& s) { return sk_fwd_select<RBF>(s); }
+FwdFn select_fwd_rbf(const FwdShape& s, int& smem) { return sk_fwd_select<RBF>(s, smem); }
 }  // namespace sk

@@ -29,9 +29,9 @@ BwdFn select_bwd_linear(const BwdShape& s, int& smem_doubles);
 BwdFn select_bwd_rbf(const BwdShape& s, int& smem_doubles);
 
 // Per-kind instance tables (one translation unit each, compiled in parallel).
-FwdFn select_fwd_linear(const FwdShape& s);
-FwdFn select_fwd_rbf(const FwdShape& s);
-FwdFn select_fwd_delta(const FwdShape& s);
+FwdFn select_fwd_linear(const FwdShape& s, int& smem);
+FwdFn select_fwd_rbf(const FwdShape& s, int& smem);
+FwdFn select_fwd_delta(const FwdShape& s, int& smem);
 
 inline int rows_per_lane(int DP) {
   switch (DP) {
