@@ -176,7 +176,7 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
   const int warps = pl.threads / 32;
   if (mode == BATCH) pl.nitems = (npairs + pl.P - 1) / pl.P;
   else pl.nitems = gram_items(mode, n2, r0, r1, pl.P);
-  if (smem > 48 * 1024 &&
+  if (smem > 0 &&
       cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
           cudaSuccess)
     (void)cudaGetLastError();
@@ -288,7 +288,7 @@ static int forward_impl(const double* x, const double* y, int64_t n1, int64_t n2
   FwdPlan pl;
   const int64_t npairs = mode == BATCH ? n1 : (r1 - r0) * n2;
   if (int rc = plan_forward(pl, kind, d, g.lamR, g.lamC, pb.M1c, pb.M2c, npairs,
-                            mode != BATCH, mode, (int)n2, (int)r0, (int)r1))
+                            mode != BATCH && !(mode == GRAM_CROSS && g.swap), mode, (int)n2, (int)r0, (int)r1))
     return rc;
   FwdLayout lo = fwd_layout(pl, kind, g.nR, g.LR, g.nC, g.LC, pb.dpad, sym);
   if (query) {
