@@ -139,9 +139,9 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           double p[RC];
           coarse_p<KIND, DP, RC>(p, rr, cs, pb, pr, pc, pidx, i0, jc);
           if constexpr (KIND == LINEAR) {
-            if (pb.scale != 1.0) {
+            if (pb.pscale != 1.0) {
 #pragma unroll
-              for (int c = 0; c < RC; ++c) p[c] *= pb.scale;
+              for (int c = 0; c < RC; ++c) p[c] *= pb.pscale;
             }
           }
           Coef cf[RC];
@@ -253,9 +253,9 @@ bwd_kernel(Problem pb, BwdArgs ba) {
               const int jc = (jj * F) >> pb.lam2;
               coarse_p<KIND, DP, RC>(p, rr, cs, pb, pr, pc, pidx, i0, jc);
               if constexpr (KIND == LINEAR) {
-                if (pb.scale != 1.0) {
+                if (pb.pscale != 1.0) {
 #pragma unroll
-                  for (int c = 0; c < RC; ++c) p[c] *= pb.scale;
+                  for (int c = 0; c < RC; ++c) p[c] *= pb.pscale;
                 }
               }
             } else {

@@ -46,12 +46,12 @@ static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // ---------------------------------------------------------------- prep kernels
 // Increments (kernel.py:74-75 np.diff) into a zero-padded [n][L-1][dpad] array.
 __global__ void prep_increments(const double* __restrict__ x, int64_t n, int64_t L, int64_t d,
-                                int dpad, double* __restrict__ out) {
+                                int dpad, double scale, double* __restrict__ out) {
   int64_t total = n * (L - 1) * dpad;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     int64_t k = e % dpad, i = (e / dpad) % (L - 1), p = e / (dpad * (L - 1));
-    out[e] = (k < d) ? x[(p * L + i + 1) * d + k] - x[(p * L + i) * d + k] : 0.0;
+    out[e] = (k < d) ? (x[(p * L + i + 1) * d + k] - x[(p * L + i) * d + k]) * scale : 0.0;
   }
 }
 
@@ -200,12 +200,12 @@ static size_t prep_elems(int kind, int64_t n, int64_t L, int dpad) {
 }
 
 static void launch_prep(int kind, const double* x, int64_t n, int64_t L, int64_t d, int dpad,
-                        double* out, cudaStream_t st) {
+                        double* out, cudaStream_t st, double scale = 1.0) {
   size_t total = prep_elems(kind, n, L, dpad);
   if (total == 0) return;
   int blocks = (int)std::min<size_t>((total + 255) / 256, 4096);
   if (kind == RBF) prep_nodes<<<blocks, 256, 0, st>>>(x, n, L, d, dpad, out);
-  else prep_increments<<<blocks, 256, 0, st>>>(x, n, L, d, dpad, out);
+  else prep_increments<<<blocks, 256, 0, st>>>(x, n, L, d, dpad, scale, out);
 }
 
 static int validate(int64_t L1, int64_t L2, int64_t d, int lam1, int lam2, int kind,
@@ -236,6 +236,7 @@ static Problem base_problem(int kind, int64_t d, int lamR, int lamC, int64_t LR,
   pb.lam1 = lamR;
   pb.lam2 = lamC;
   pb.scale = std::ldexp(1.0, -(lamR + lamC));
+  pb.pscale = pb.scale;
   pb.inv2s2 = kind == RBF ? 1.0 / (2.0 * sigma * sigma) : 0.0;
   pb.invs2 = kind == RBF ? 1.0 / (sigma * sigma) : 0.0;
   return pb;
@@ -290,7 +291,12 @@ static int forward_impl(const double* x, const double* y, int64_t n1, int64_t n2
   if (int rc = plan_forward(pl, kind, d, g.lamR, g.lamC, pb.M1c, pb.M2c, npairs,
                             mode != BATCH && !(mode == GRAM_CROSS && g.swap), mode, (int)n2, (int)r0, (int)r1))
     return rc;
-  FwdLayout lo = fwd_layout(pl, kind, g.nR, g.LR, g.nC, g.LC, pb.dpad, sym);
+  // LINEAR: the exact dyadic factor 2^-(lamR+lamC) is folded into the row
+  // increments, so the kernel forms p without a multiply; a symmetric Gram then
+  // needs a separate (unscaled) column copy when the factor is not 1.
+  const bool fold = kind == LINEAR;
+  const bool share = sym && !(fold && pb.scale != 1.0);
+  FwdLayout lo = fwd_layout(pl, kind, g.nR, g.LR, g.nC, g.LC, pb.dpad, share);
   if (query) {
     *query = lo.total;
     return SK_OK;
@@ -301,12 +307,13 @@ static int forward_impl(const double* x, const double* y, int64_t n1, int64_t n2
                                          " bytes, got " + std::to_string(ws_bytes));
   char* base = static_cast<char*>(ws);
   double* prepR = reinterpret_cast<double*>(base);
-  double* prepC = sym ? prepR : reinterpret_cast<double*>(base + lo.prepR);
+  double* prepC = share ? prepR : reinterpret_cast<double*>(base + lo.prepR);
   double* hand = reinterpret_cast<double*>(base + lo.prepR + lo.prepC);
   const double* xr = g.swap ? y : x;
   const double* xc = g.swap ? x : y;
-  launch_prep(kind, xr, g.nR, g.LR, d, pb.dpad, prepR, st);
-  if (!sym) launch_prep(kind, xc, g.nC, g.LC, d, pb.dpad, prepC, st);
+  launch_prep(kind, xr, g.nR, g.LR, d, pb.dpad, prepR, st, fold ? pb.scale : 1.0);
+  if (!share) launch_prep(kind, xc, g.nC, g.LC, d, pb.dpad, prepC, st);
+  if (fold) pb.pscale = 1.0;
   pb.R.p = prepR;
   pb.R.rows = (int)(g.LR - 1);
   pb.R.path_stride = (kind == RBF ? g.LR : g.LR - 1) * pb.dpad;

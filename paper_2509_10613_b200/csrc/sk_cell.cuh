@@ -39,10 +39,15 @@ __device__ __forceinline__ void load_vec(double (&v)[DP], const double* __restri
 
 template <int DP>
 __device__ __forceinline__ double dot(const double (&a)[DP], const double (&b)[DP]) {
-  double s = a[0] * b[0];
+  // two interleaved partial sums halve the dependent FMA chain; every kernel
+  // forms <dx_i, dy_j> with this exact order, so forward and backward agree bitwise
+  double s0 = a[0] * b[0], s1 = a[1] * b[1];
 #pragma unroll
-  for (int k = 1; k < DP; ++k) s = fma(a[k], b[k], s);
-  return s;
+  for (int k = 2; k < DP; k += 2) {
+    s0 = fma(a[k], b[k], s0);
+    s1 = fma(a[k + 1], b[k + 1], s1);
+  }
+  return s0 + s1;
 }
 
 template <int DP>

@@ -39,7 +39,8 @@ struct Problem {
   int nch;       // number of DP-chunks of the dimension
   int M1c, M2c;  // coarse rows / cols of every pair
   int lam1, lam2;
-  double scale;   // 2^-(lam1+lam2), applied to every coarse p (exact: power of two)
+  double scale;   // 2^-(lam1+lam2): dyadic factor of every coarse p (exact: power of two)
+  double pscale;  // factor still to apply to LINEAR p (1 when folded into the row data)
   double inv2s2;  // RBF: 1/(2 sigma^2)
   double invs2;   // RBF: 1/sigma^2
   // pair mapping

@@ -5,10 +5,10 @@
 //
 // Mapping (B200-first):
 //   * a lane group of G lanes solves one pair; lane u owns R consecutive fine
-//     rows of a strip of G*R rows and sweeps the columns left->right, one
-//     "step" (F fine columns) at a time, lagging lane u-1 by one step.  The
+//     rows of a strip of G*R rows and sweeps the columns left->right, S
+//     columns (S*F fine columns) per step, lagging lane u-1 by one step.  The
 //     three rotating anti-diagonals of the reference become registers: k_left
-//     per owned row, the top-row value from lane u-1 arrives by __shfl_up_sync.
+//     per owned row, the top-row values from lane u-1 arrive by __shfl_up_sync.
 //   * G = 4: 8 pairs per warp sharing the column path (Gram tiles); G = 32: one
 //     pair per warp; XW: one pair per CTA, G = blockDim.x lanes, lane 31 ->
 //     lane 0 of the next warp through a double-buffered shared-memory slot and
@@ -17,8 +17,8 @@
 //     handoff row stream through a shared-memory ring filled by cp.async PF
 //     steps ahead, so no global latency sits on the recurrence;
 //   * the increment product delta (kernel.py:60-77) is never materialised: the
-//     lane keeps its rows' increments in registers and forms <dx_i, dy_j> for
-//     step tau+1 while the recurrence of step tau runs (software pipeline);
+//     lane keeps its rows' increments in registers (pre-scaled by the exact
+//     dyadic factor 2^-(lam1+lam2)) and forms <dx_i, dy_j> per coarse cell;
 //     dyadic refinement is on the fly (fine cell (s,t) reads coarse
 //     (s-1)>>lam1, (t-1)>>lam2, _kernels.py:325);
 //   * the strip's bottom row is handed to the next strip through a per-group
@@ -36,30 +36,42 @@ struct FwdRec {
   static constexpr int REC = (RAW + 1) & ~1;           // 16-byte aligned records
 };
 
-template <bool XW, int G>
+template <bool XW, int G, int S>
 struct FwdRing {
-  static constexpr int PF = 4;
-  static constexpr int SLOTS = XW ? 1024 : (G >= 32 ? 64 : 16);
+  static constexpr int PF = 2;  // steps in flight
+  static constexpr int NEED = ((XW ? 512 : G) + PF + 1) * S;
+  static constexpr int SLOTS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128
+                               : NEED <= 256 ? 256 : NEED <= 512 ? 512 : NEED <= 1024 ? 1024
+                                                                                      : 2048;
 };
 
-// Issue the ring record of step jj: column data of coarse column jc(jj) and
-// the handoff values of every group (strip > 0).  Executed by one warp.
-template <int KIND, int DP, int F, int P>
-__device__ __forceinline__ void fwd_issue(double* ring_slot, const Problem& pb, int64_t pc,
-                                          const double* hrow0, int64_t hand_stride, int jj,
-                                          int NS, int strip, int lane) {
-  using RC_ = FwdRec<KIND, DP, F, P>;
-  const bool valid = (jj >= 0) && (jj < NS);
-  const int jc = valid ? ((jj * F) >> pb.lam2) : 0;
-  if constexpr (RC_::CD > 0) {
+// Issue the ring records of columns [col0, col0 + S): column data of coarse
+// column jc(col) and the handoff values of every group (strip > 0).  One warp
+// issues; a single commit group per step.
+template <int KIND, int DP, int F, int P, int S, int SLOTS>
+__device__ __forceinline__ void fwd_issue(double* ring, const Problem& pb, int64_t pc,
+                                          const double* hrow0, int64_t hand_stride, int col0,
+                                          int NC, int strip, int lane) {
+  using Rc = FwdRec<KIND, DP, F, P>;
+  constexpr int CH = Rc::CD / 2;  // 16-byte chunks of column data
+  for (int e = lane; e < S * CH; e += 32) {
+    const int s = e / CH, c = e % CH;
+    const int col = col0 + s;
+    const bool valid = (col >= 0) && (col < NC);
+    const int jc = valid ? ((col * F) >> pb.lam2) : 0;
     const int node = (KIND == RBF) ? jc + 1 : jc;
-    const double* src = pb.C.p + pc * pb.C.path_stride + (int64_t)node * pb.dpad;
-    for (int c = lane; c < RC_::CD / 2; c += 32) cp_async16(ring_slot + 2 * c, src + 2 * c, valid);
+    const double* src = pb.C.p + pc * pb.C.path_stride + (int64_t)node * pb.dpad + 2 * c;
+    cp_async16(ring + ((col & (SLOTS - 1)) * Rc::REC) + 2 * c, src, valid);
   }
-  for (int e = lane; e < P * F; e += 32) {
-    const int g = e / F, f = e % F;
-    const double* src = hrow0 + g * hand_stride + (valid ? jj * F + f + 1 : 0);
-    cp_async8(ring_slot + RC_::CD + e, src, valid && strip > 0);
+  if (strip > 0) {
+    for (int e = lane; e < S * P * F; e += 32) {
+      const int s = e / (P * F), q = e % (P * F);
+      const int g = q / F, f = q % F;
+      const int col = col0 + s;
+      const bool valid = (col >= 0) && (col < NC);
+      const double* src = hrow0 + g * hand_stride + (valid ? col * F + f + 1 : 0);
+      cp_async8(ring + ((col & (SLOTS - 1)) * Rc::REC) + Rc::CD + q, src, valid);
+    }
   }
   cp_async_commit();
 }
@@ -69,22 +81,24 @@ __device__ __forceinline__ void fwd_issue(double* ring_slot, const Problem& pb, 
 //   DP    padded path dimension held in registers per chunk
 //   R     fine rows per lane;  FR = fine rows per coarse row inside a lane
 //         (= min(2^lam1, R)), so RC = R / FR coarse rows per lane
-//   F     fine columns per step (= min(2^lam2, 4))
+//   F     fine columns per column record (= min(2^lam2, 4))
 //   G     lanes per pair (4 or 32); ignored when XW (G = blockDim.x)
 //   XW    cross-warp lane groups (one pair per CTA)
+//   S     columns per step
 // Every group of a warp must share the column path (Gram tiles / one pair).
-template <int KIND, int DP, int R, int FR, int F, int G, bool XW>
+template <int KIND, int DP, int R, int FR, int F, int G, bool XW, int S>
 __global__ void __launch_bounds__(XW ? 512 : 128)
 fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
   constexpr int RC = R / FR;
   constexpr int P = XW ? 1 : 32 / G;
+  constexpr int SF = S * F;
   using Rec = FwdRec<KIND, DP, F, P>;
-  using Rg = FwdRing<XW, G>;
+  using Rg = FwdRing<XW, G, S>;
   constexpr int REC = Rec::REC;
   constexpr int SLOTS = Rg::SLOTS;
   constexpr int PF = Rg::PF;
   extern __shared__ double smem_fwd[];
-  __shared__ double xbuf[XW ? 2 : 1][XW ? 32 : 1][F];
+  __shared__ double xbuf[XW ? 2 : 1][XW ? 16 : 1][SF];
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -96,12 +110,14 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
 
   const int M1 = pb.M1c << pb.lam1;
   const int M2 = pb.M2c << pb.lam2;
-  const int NS = M2 / F;  // steps per strip
-  const int H = Grt * R;  // strip height
+  const int NC = M2 / F;                 // column records per strip row
+  const int NSTEP = (NC + S - 1) / S;    // steps per strip
+  const int H = Grt * R;                 // strip height
   const int nstrips = (M1 + H - 1) / H;
   const int last_strip = (M1 - 1) / H;
   const int u_star = ((M1 - 1) % H) / R;
   const int r_star = (M1 - 1) % R;
+  const int s_star = (NC - 1) % S;       // sub-step of the last column
 
   const int64_t slot0 = XW ? (int64_t)blockIdx.x : ((int64_t)blockIdx.x * nw + warp) * P;
   const double* hrow0 = hand + slot0 * hand_stride;  // group g's row: + g * hand_stride
@@ -121,6 +137,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
       resolve_pair(pb, item, P, 0, pr0, pc, oi0, pi0);
       if (!valid) pr = pr0;
     }
+    double outv = 0.0;
 
     for (int t = u; t <= M2; t += Grt) hrow[t] = 1.0;
     if (XW) __syncthreads(); else __syncwarp();
@@ -130,7 +147,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
       const int i0 = rbase >> pb.lam1;
       RowRegs<KIND, DP, RC> rr;
       if constexpr (KIND != DELTA) load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
-      double Kl[RC + 1], Kr[RC + 1];  // RBF: K at node columns jc, jc+1 of the pending step
+      double Kl[RC + 1], Kr[RC + 1];  // RBF: K at node columns jc, jc+1
       int jcur = -1;
       if constexpr (KIND == RBF) {
         double y0[DP];
@@ -140,178 +157,181 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
 #pragma unroll
         for (int c = 0; c <= RC; ++c) Kl[c] = Kr[c];
       }
-      // prologue: PF records in flight
       if (issuer) {
         for (int q = 0; q < PF; ++q)
-          fwd_issue<KIND, DP, F, P>(ring + (q & (SLOTS - 1)) * REC, pb, pc, hrow0, hand_stride, q, NS, strip,
-                                    lane);
+          fwd_issue<KIND, DP, F, P, S, SLOTS>(ring, pb, pc, hrow0, hand_stride, q * S, NC, strip,
+                                              lane);
       }
-
-      // coefficients of the next step (software pipeline)
-      auto coefs_for = [&](int jj, Coef (&cf)[RC]) {
-        const double* rec = ring + (jj & (SLOTS - 1)) * REC;
-        const int jc = (jj * F) >> pb.lam2;
-        double p[RC];
-        if constexpr (KIND == LINEAR) {
-          double dy[DP];
-#pragma unroll
-          for (int k = 0; k < DP; k += 2) {
-            const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-            dy[k] = t2.x;
-            dy[k + 1] = t2.y;
-          }
-          if (DP < 32 || pb.nch == 1) {  // d > 32 only ever selects DP = 32
-#pragma unroll
-            for (int c = 0; c < RC; ++c) {
-              // two partial sums halve the dependent FMA chain
-              double s0 = rr.v[c][0] * dy[0], s1 = rr.v[c][1] * dy[1];
-#pragma unroll
-              for (int k = 2; k < DP; k += 2) {
-                s0 = fma(rr.v[c][k], dy[k], s0);
-                s1 = fma(rr.v[c][k + 1], dy[k + 1], s1);
-              }
-              p[c] = (s0 + s1) * pb.scale;
-            }
-          } else {
-            // d > 32: chunked dot products (second chunk onwards from L1)
-#pragma unroll
-            for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy);
-            for (int ch = 1; ch < pb.nch; ++ch) {
-              double dyc[DP], xc[DP];
-              load_vec<DP>(dyc, pb.C.p + pc * pb.C.path_stride + (int64_t)jc * pb.dpad + ch * DP);
-#pragma unroll
-              for (int c = 0; c < RC; ++c) {
-                const int i = i0 + c;
-                if (i < pb.M1c) {
-                  load_vec<DP>(xc, pb.R.p + pr * pb.R.path_stride + (int64_t)i * pb.dpad + ch * DP);
-                  p[c] += dot<DP>(xc, dyc);
-                }
-              }
-            }
-#pragma unroll
-            for (int c = 0; c < RC; ++c) p[c] *= pb.scale;
-          }
-        } else if constexpr (KIND == RBF) {
-          if (jj >= 0 && jc != jcur) {
-            double yv[DP];
-#pragma unroll
-            for (int k = 0; k < DP; k += 2) {
-              const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-              yv[k] = t2.x;
-              yv[k + 1] = t2.y;
-            }
-#pragma unroll
-            for (int c = 0; c <= RC; ++c) {
-              Kl[c] = Kr[c];
-              Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
-            }
-            jcur = jc;
-          }
-#pragma unroll
-          for (int c = 0; c < RC; ++c) p[c] = ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale;
-        } else {  // DELTA: per-row coarse values straight from global
-#pragma unroll
-          for (int c = 0; c < RC; ++c) {
-            const int i = i0 + c;
-            p[c] = (i < pb.M1c && jj >= 0 && jj < NS)
-                       ? __ldg(pb.delta + pidx * (int64_t)pb.M1c * pb.M2c + (int64_t)i * pb.M2c + jc) *
-                             pb.scale
-                       : 0.0;
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < RC; ++c) cf[c] = coef(p[c]);
-      };
 
       double kl[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) kl[r] = 1.0;
       double topc = 1.0;
-      double bot[F];
+      double bot[SF];
 #pragma unroll
-      for (int f = 0; f < F; ++f) bot[f] = 1.0;
-      Coef cf[RC];
-      if (issuer) cp_async_wait<PF - 1>();
-      if (XW) __syncthreads(); else __syncwarp();
-      coefs_for(-u, cf);
+      for (int q = 0; q < SF; ++q) bot[q] = 1.0;
 
-      const int nsteps = NS + Grt - 1;
+      const int nsteps = NSTEP + Grt - 1;
       for (int tau = 0; tau < nsteps; ++tau) {
         if (issuer) {
-          fwd_issue<KIND, DP, F, P>(ring + ((tau + PF) & (SLOTS - 1)) * REC, pb, pc, hrow0,
-                                    hand_stride, tau + PF, NS, strip, lane);
-          cp_async_wait<PF - 1>();  // records <= tau + 1 landed
+          fwd_issue<KIND, DP, F, P, S, SLOTS>(ring, pb, pc, hrow0, hand_stride, (tau + PF) * S, NC,
+                                              strip, lane);
+          cp_async_wait<PF>();  // this step's records landed
         }
         if (XW) __syncthreads(); else __syncwarp();
-        const int jj = tau - u;
-        const bool active = (jj >= 0) && (jj < NS);
-        Coef cfn[RC];
-        coefs_for(jj + 1, cfn);  // independent of this step's recurrence
+        const int js = tau - u;
+        const bool active = (js >= 0) && (js < NSTEP);
 
-        double tv[F];
+        double tv[SF];
         if constexpr (XW) {
 #pragma unroll
-          for (int f = 0; f < F; ++f) tv[f] = __shfl_up_sync(0xffffffffu, bot[f], 1);
+          for (int q = 0; q < SF; ++q) tv[q] = __shfl_up_sync(0xffffffffu, bot[q], 1);
           if (lane == 0 && warp > 0) {
 #pragma unroll
-            for (int f = 0; f < F; ++f) tv[f] = xbuf[(tau + 1) & 1][warp - 1][f];
+            for (int q = 0; q < SF; ++q) tv[q] = xbuf[(tau + 1) & 1][warp - 1][q];
           }
         } else {
 #pragma unroll
-          for (int f = 0; f < F; ++f) tv[f] = __shfl_up_sync(0xffffffffu, bot[f], 1, G);
-        }
-        if (u == 0) {
-          const double* rec = ring + (jj & (SLOTS - 1)) * REC + Rec::CD + g * F;
-#pragma unroll
-          for (int f = 0; f < F; ++f) tv[f] = (strip == 0) ? 1.0 : rec[f];
-        }
-#pragma unroll
-        for (int f = 0; f < F; ++f) {
-          double up = tv[f];
-          double dg = (f == 0) ? topc : tv[f - 1];
-#pragma unroll
-          for (int r = 0; r < R; ++r) {
-            const double nk = cell(up, kl[r], dg, cf[r / FR]);
-            dg = kl[r];
-            kl[r] = active ? nk : kl[r];
-            up = nk;
-          }
-          bot[f] = up;
+          for (int q = 0; q < SF; ++q) tv[q] = __shfl_up_sync(0xffffffffu, bot[q], 1, G);
         }
         if (active) {
-          topc = tv[F - 1];
+          const int col0 = js * S;
+          if (u == 0) {
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+              const double* rec = ring + ((col0 + s) & (SLOTS - 1)) * REC + Rec::CD + g * F;
+#pragma unroll
+              for (int f = 0; f < F; ++f) tv[s * F + f] = (strip == 0) ? 1.0 : rec[f];
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            const int col = col0 + s;
+            const double* rec = ring + (col & (SLOTS - 1)) * REC;
+            double p[RC];
+            if constexpr (KIND == LINEAR) {
+              double dy[DP];
+#pragma unroll
+              for (int k = 0; k < DP; k += 2) {
+                const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+                dy[k] = t2.x;
+                dy[k + 1] = t2.y;
+              }
+              if (DP < 32 || pb.nch == 1) {  // d > 32 only ever selects DP = 32
+#pragma unroll
+                for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy);
+              } else {
+#pragma unroll
+                for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy);
+                const int jc = (col * F) >> pb.lam2;
+                for (int ch = 1; ch < pb.nch; ++ch) {
+                  double dyc[DP], xc[DP];
+                  if (col < NC) {
+                    load_vec<DP>(dyc, pb.C.p + pc * pb.C.path_stride + (int64_t)jc * pb.dpad +
+                                          ch * DP);
+                  } else {
+#pragma unroll
+                    for (int k = 0; k < DP; ++k) dyc[k] = 0.0;
+                  }
+#pragma unroll
+                  for (int c = 0; c < RC; ++c) {
+                    const int i = i0 + c;
+                    if (i < pb.M1c) {
+                      load_vec<DP>(xc, pb.R.p + pr * pb.R.path_stride + (int64_t)i * pb.dpad +
+                                           ch * DP);
+                      p[c] += dot<DP>(xc, dyc);
+                    }
+                  }
+                }
+              }
+              if (pb.pscale != 1.0) {
+#pragma unroll
+                for (int c = 0; c < RC; ++c) p[c] *= pb.pscale;
+              }
+            } else if constexpr (KIND == RBF) {
+              const int jc = (col * F) >> pb.lam2;
+              if (col < NC && jc != jcur) {
+                double yv[DP];
+#pragma unroll
+                for (int k = 0; k < DP; k += 2) {
+                  const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+                  yv[k] = t2.x;
+                  yv[k + 1] = t2.y;
+                }
+#pragma unroll
+                for (int c = 0; c <= RC; ++c) {
+                  Kl[c] = Kr[c];
+                  Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
+                }
+                jcur = jc;
+              }
+#pragma unroll
+              for (int c = 0; c < RC; ++c)
+                p[c] = ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale;
+            } else {  // DELTA: per-row coarse values straight from global
+              const int jc = (col * F) >> pb.lam2;
+#pragma unroll
+              for (int c = 0; c < RC; ++c) {
+                const int i = i0 + c;
+                p[c] = (i < pb.M1c && col < NC)
+                           ? __ldg(pb.delta + pidx * (int64_t)pb.M1c * pb.M2c +
+                                   (int64_t)i * pb.M2c + jc) * pb.scale
+                           : 0.0;
+              }
+            }
+            Coef cf[RC];
+#pragma unroll
+            for (int c = 0; c < RC; ++c) cf[c] = coef(p[c]);
+#pragma unroll
+            for (int f = 0; f < F; ++f) {
+              const int q = s * F + f;
+              double up = tv[q];
+              double dg = (q == 0) ? topc : tv[q - 1];
+#pragma unroll
+              for (int r = 0; r < R; ++r) {
+                const double nk = cell(up, kl[r], dg, cf[r / FR]);
+                dg = kl[r];
+                kl[r] = nk;
+                up = nk;
+              }
+              bot[q] = up;
+            }
+            if (s == s_star && col == NC - 1) {
+#pragma unroll
+              for (int r = 0; r < R; ++r)
+                if (r == r_star) outv = kl[r];
+            }
+          }
+          topc = tv[SF - 1];
           if (u == Grt - 1) {
 #pragma unroll
-            for (int f = 0; f < F; ++f) hrow[jj * F + f + 1] = bot[f];
-          }
-          if (strip == last_strip && u == u_star && jj == NS - 1 && valid) {
-            double v = kl[0];
+            for (int s = 0; s < S; ++s) {
+              if (col0 + s < NC) {
 #pragma unroll
-            for (int r = 1; r < R; ++r)
-              if (r == r_star) v = kl[r];
-            pb.out[oidx] = v;
+                for (int f = 0; f < F; ++f) hrow[(col0 + s) * F + f + 1] = bot[s * F + f];
+              }
+            }
           }
         }
-#pragma unroll
-        for (int c = 0; c < RC; ++c) cf[c] = cfn[c];
         if constexpr (XW) {
           if (lane == 31) {
 #pragma unroll
-            for (int f = 0; f < F; ++f) xbuf[tau & 1][warp][f] = bot[f];
+            for (int q = 0; q < SF; ++q) xbuf[tau & 1][warp][q] = bot[q];
           }
         }
       }
       if (issuer) cp_async_wait<0>();
       if (XW) __syncthreads(); else __syncwarp();
     }
+    if (u == u_star && valid) pb.out[oidx] = outv;
   }
 }
 
 // Dynamic shared memory of one fwd_kernel CTA (bytes).
-template <int KIND, int DP, int F, int G, bool XW>
+template <int KIND, int DP, int F, int G, bool XW, int S>
 constexpr int fwd_smem_bytes(int warps) {
   using Rec = FwdRec<KIND, DP, F, XW ? 1 : 32 / G>;
-  return (XW ? 1 : warps) * FwdRing<XW, G>::SLOTS * Rec::REC * (int)sizeof(double);
+  return (XW ? 1 : warps) * FwdRing<XW, G, S>::SLOTS * Rec::REC * (int)sizeof(double);
 }
 
 }  // namespace sk

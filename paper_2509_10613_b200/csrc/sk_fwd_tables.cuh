@@ -9,17 +9,17 @@ template <int KIND, int DP, int R, int FR, int F>
 inline void sk_fwd_leaf(const FwdShape& s, FwdFn& fn, int& smem) {
   if (s.XW) {
     if constexpr (KIND == LINEAR) {
-      fn = fwd_kernel<KIND, DP, R, FR, F, 32, true>;
-      smem = fwd_smem_bytes<KIND, DP, F, 32, true>(s.W);
+      fn = fwd_kernel<KIND, DP, R, FR, F, 32, true, 2>;
+      smem = fwd_smem_bytes<KIND, DP, F, 32, true, 2>(s.W);
     }
     return;
   }
   if (s.G == 4) {
-    fn = fwd_kernel<KIND, DP, R, FR, F, 4, false>;
-    smem = fwd_smem_bytes<KIND, DP, F, 4, false>(4);
+    fn = fwd_kernel<KIND, DP, R, FR, F, 4, false, 4>;
+    smem = fwd_smem_bytes<KIND, DP, F, 4, false, 4>(4);
   } else if (s.G == 32) {
-    fn = fwd_kernel<KIND, DP, R, FR, F, 32, false>;
-    smem = fwd_smem_bytes<KIND, DP, F, 32, false>(4);
+    fn = fwd_kernel<KIND, DP, R, FR, F, 32, false, 2>;
+    smem = fwd_smem_bytes<KIND, DP, F, 32, false, 2>(4);
   }
 }
 
