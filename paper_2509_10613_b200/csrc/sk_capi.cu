@@ -154,7 +154,7 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
   // are too few to fill the GPU.
   if (gram) {
     s.G = (npairs * 4 >= target_lanes || lanes_per_pair <= 8) ? 4 : 32;
-  } else if (npairs * 32 >= target_lanes || lanes_per_pair <= 64 || kind != LINEAR) {
+  } else if (npairs * 32 >= target_lanes || lanes_per_pair <= 64 || kind != LINEAR || s.DP > 8) {
     s.G = 32;
   } else {
     int W = 2;

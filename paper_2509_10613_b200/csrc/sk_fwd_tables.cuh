@@ -15,8 +15,10 @@ inline void sk_fwd_leaf(const FwdShape& s, FwdFn& fn, int& smem) {
     return;
   }
   if (s.G == 4) {
-    fn = fwd_kernel<KIND, DP, R, FR, F, 4, false, 4>;
-    smem = fwd_smem_bytes<KIND, DP, F, 4, false, 4>(4);
+    // columns per step: amortise per-step overhead without crowding registers
+    constexpr int S4 = DP >= 16 ? 2 : 4;
+    fn = fwd_kernel<KIND, DP, R, FR, F, 4, false, S4>;
+    smem = fwd_smem_bytes<KIND, DP, F, 4, false, S4>(4);
   } else if (s.G == 32) {
     fn = fwd_kernel<KIND, DP, R, FR, F, 32, false, 2>;
     smem = fwd_smem_bytes<KIND, DP, F, 32, false, 2>(4);
