@@ -10,19 +10,23 @@
 //
 // B200 mapping:
 //   * one warp per pair, lane u owns R fine rows of a 32R-row strip;
-//   * phase A: the forward wavefront of sk_forward.cuh, which additionally
+//   * phase A: the forward wavefront (as sk_forward.cuh), which additionally
 //     saves every lane's bottom row (row checkpoint, coalesced "diagonal"
-//     layout [strip][step][f][lane]) and every lane's R values at staggered
-//     block boundaries (column checkpoint);
-//   * phase B: strips bottom-up; per block of CB steps every lane recomputes its
-//     R x CB*F forward values from its own checkpoints into shared memory (no
-//     inter-lane dependency, so all lanes do it at the same time), then sweeps
-//     the block right-to-left one step behind lane u+1, receiving lane u+1's
-//     top-row messages by __shfl_down_sync;
+//     layout [strip][col + lane][f][lane]) and every lane's R values at
+//     staggered block boundaries (column checkpoint, [strip][blk][r][lane]);
+//   * phase B: strips bottom-up; per block of CB columns every lane recomputes
+//     its R x CB*F forward values from its own checkpoints into shared memory
+//     (no inter-lane dependency, so all lanes do it at the same time), then
+//     sweeps the block right-to-left one column behind lane u+1, receiving lane
+//     u+1's top-row messages by __shfl_down_sync;
+//   * column data (dy_j / RBF nodes), the adjoint handoff row from the strip
+//     below and the checkpoints of the next block stream into shared memory by
+//     cp.async one block ahead, so no global latency sits on the sweep;
 //   * the coarse adjoint dF/d(delta) is mapped to path space on the fly
-//     (FUSED: gx = D dy in registers, gy = D^T dx accumulated down the warp as a
-//     shuffle chain) or through a per-pair coarse buffer (DBUF: RBF and large
-//     dyadic orders), then telescoped to point gradients (kernel_grad.py:51-60).
+//     (FUSED: gx = D dy in registers, gy = D^T dx accumulated down the warp as
+//     a shuffle chain and handed from strip to strip through a per-pair column
+//     buffer) or through a per-pair coarse buffer (DBUF: RBF), then telescoped
+//     to point gradients (kernel_grad.py:51-60).
 //   * nothing proportional to the fine grid is stored per pair beyond the
 //     checkpoints (1/R + 1/(CB*F) of the grid).
 #pragma once
@@ -32,44 +36,50 @@ namespace sk {
 
 enum MapMode : int { FUSED = 0, DBUF = 1 };
 
-
 __device__ __forceinline__ void grad_add(double* p, double v, bool atomic) {
   if (atomic) atomicAdd(p, v);
   else *p += v;
 }
 
-// Per-warp shared-memory block store, lane-minor ([idx][32]) for conflict-free access.
-template <int R, int RC, int F, int CB>
-struct BlockSmem {
-  static constexpr int NK = CB * F * R;     // recomputed k values
-  static constexpr int NP = CB * RC;        // coarse p values
-  static constexpr int NT = CB * F + 1;     // top row (incl. left node)
-  static constexpr int NL = R;              // left column
-  static constexpr int TOTAL = NK + NP + NT + NL;
+// Per-warp shared-memory layout (doubles).
+template <int DP, int R, int RC, int F, int CB>
+struct BwdSmem {
+  static constexpr int SLOTS = 64;                   // column ring (>= 2*CB + 31)
+  static constexpr int REC = ((DP + F) + 1) & ~1;    // column data | handoff/adjoint (F)
+  static constexpr int NK = CB * F * R;              // recomputed k values (x32 lanes)
+  static constexpr int NP = CB * RC;                 // coarse p (then D) values (x32 lanes)
+  static constexpr int TS = (CB + 1) * F * 32;       // top-row checkpoints of the block
+  static constexpr int T0 = ((CB * F + 1) + 1) & ~1; // lane 0's top row (strip above)
+  static constexpr int LS = R * 32;                  // left-column checkpoint
+  static constexpr int GS = CB * DP;                 // lane 31's incoming column gradients
+  static constexpr int STG = TS + T0 + LS + GS;
+  static constexpr int TOTAL = SLOTS * REC + (NK + NP) * 32 + 2 * STG;
 };
 
 template <int KIND, int DP, int R, int FR, int F, int CB, int MAP>
 __global__ void __launch_bounds__(128)
 bwd_kernel(Problem pb, BwdArgs ba) {
   constexpr int RC = R / FR;
-  using SM = BlockSmem<R, RC, F, CB>;
+  using SM = BwdSmem<DP, R, RC, F, CB>;
+  constexpr int SLOTS = SM::SLOTS;
+  constexpr int REC = SM::REC;
+  constexpr int PF = 2;
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  double* sK = smem + (size_t)warp * SM::TOTAL * 32;
+  double* ring = smem + (size_t)warp * SM::TOTAL;
+  double* sK = ring + SLOTS * REC;
   double* sP = sK + SM::NK * 32;
-  double* sT = sP + SM::NP * 32;
-  double* sL = sT + SM::NT * 32;
+  double* stg0 = sP + SM::NP * 32;
 #define SK_KB(kap, f, r) sK[(((kap) * F + (f)) * R + (r)) * 32 + lane]
 #define SK_PB(kap, c) sP[((kap) * RC + (c)) * 32 + lane]
-#define SK_TB(q) sT[(q) * 32 + lane]
-#define SK_LB(r) sL[(r) * 32 + lane]
+#define SK_REC(col) (ring + ((col) & (SLOTS - 1)) * REC)
 
   const int u = lane;
   const int M1 = pb.M1c << pb.lam1;
   const int M2 = pb.M2c << pb.lam2;
-  const int NS = M2 / F;          // steps per strip
+  const int NS = M2 / F;          // columns per strip row
   const int NT = NS + 31;         // skewed steps per strip
   const int NB = (NT + CB - 1) / CB;
   const int H = 32 * R;
@@ -78,6 +88,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   const int u_star = ((M1 - 1) % H) / R;
   const int r_star = (M1 - 1) % R;
   const int dR = ba.d;
+  const int K2m = (1 << pb.lam2) / F - 1;  // columns per coarse column - 1 (power of 2)
 
   const int64_t slot = (int64_t)blockIdx.x * nw + warp;
   double* __restrict__ rowck = ba.rowck + slot * ba.rowck_stride;
@@ -85,8 +96,9 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   double* __restrict__ hrow = ba.hand + slot * ba.row_stride;
   double* __restrict__ arow = ba.adj + slot * ba.row_stride;
   double* __restrict__ dbuf = (MAP == DBUF) ? ba.dbuf + slot * ba.dbuf_stride : nullptr;
-#define SK_ROWCK(strip, tau, f, ln) rowck[(((int64_t)(strip) * NT + (tau)) * F + (f)) * 32 + (ln)]
-#define SK_COLCK(strip, blk, r) colck[(((int64_t)(strip) * NB + (blk)) * R + (r)) * 32 + lane]
+  double* __restrict__ gxs = ba.gscr + slot * ba.gscr_stride;  // [M1c][DP]
+  double* __restrict__ gcs = gxs + (int64_t)pb.M1c * DP;       // [M2c][DP]
+#define SK_ROWCK(strip, d, f, ln) rowck[(((int64_t)(strip) * NT + (d)) * F + (f)) * 32 + (ln)]
 
   for (int64_t item = slot; item < pb.nitems; item += (int64_t)gridDim.x * nw) {
     // ---------------------------------------------------------- resolve pair
@@ -101,6 +113,26 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       wcot = ba.cot[(int64_t)a * pb.n2 + b];
       if (pb.mode == GRAM_SYM && a != b) wcot += ba.cot[(int64_t)b * pb.n2 + a];
     }
+    const double* cbase = pb.C.p + pc * pb.C.path_stride;  // this pair's column path
+
+    // issue the ring records of columns [c0, c0 + n) (one warp, no commit)
+    auto issue_cols = [&](int c0, int n, const double* hsrc, bool hvalid) {
+      constexpr int PER = DP / 2 + F;
+      for (int e = lane; e < n * PER; e += 32) {
+        const int q = e / PER, w = e % PER;
+        const int col = c0 + q;
+        const bool cv = (col >= 0) && (col < NS);
+        double* dst = SK_REC(col);
+        if (w < DP / 2) {
+          const int jc = cv ? ((col * F) >> pb.lam2) : 0;
+          const int node = (KIND == RBF) ? jc + 1 : jc;
+          cp_async16(dst + 2 * w, cbase + (int64_t)node * pb.dpad + 2 * w, cv);
+        } else {
+          const int f = w - DP / 2;
+          cp_async8(dst + DP + f, hsrc + (cv ? col * F + f + 1 : 0), cv && hvalid);
+        }
+      }
+    };
 
     // ------------------------------------------- phase A: forward + checkpoints
     for (int t = u; t <= M2; t += 32) hrow[t] = 1.0;
@@ -110,9 +142,21 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       const int rbase = strip * H + u * R;
       const int i0 = rbase >> pb.lam1;
       RowRegs<KIND, DP, RC> rr;
-      if constexpr (KIND != DELTA) load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
-      ColState<KIND, DP, RC> cs;
-      cs.have = -2;
+      load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
+      double Kl[RC + 1], Kr[RC + 1];
+      int jcur = -1;
+      if constexpr (KIND == RBF) {
+        double y0[DP];
+        load_vec<DP>(y0, cbase);
+#pragma unroll
+        for (int c = 0; c <= RC; ++c) Kr[c] = exp(-sqdist<DP>(rr.v[c], y0) * pb.inv2s2);
+#pragma unroll
+        for (int c = 0; c <= RC; ++c) Kl[c] = Kr[c];
+      }
+      for (int q = 0; q < PF; ++q) {
+        issue_cols(q, 1, hrow, strip > 0);
+        cp_async_commit();
+      }
       double kl[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) kl[r] = 1.0;
@@ -121,28 +165,58 @@ bwd_kernel(Problem pb, BwdArgs ba) {
 #pragma unroll
       for (int f = 0; f < F; ++f) bot[f] = 1.0;
       for (int tau = 0; tau < NT; ++tau) {
+        issue_cols(tau + PF, 1, hrow, strip > 0);
+        cp_async_commit();
+        cp_async_wait<PF>();
+        __syncwarp();
         if (tau % CB == 0) {
+          // column checkpoint: values at node column (tau - u) * F
 #pragma unroll
-          for (int r = 0; r < R; ++r) SK_COLCK(strip, tau / CB, r) = kl[r];
+          for (int r = 0; r < R; ++r)
+            colck[(((int64_t)strip * NB + tau / CB) * R + r) * 32 + lane] = kl[r];
         }
         const int jj = tau - u;
         const bool active = (jj >= 0) && (jj < NS);
         double tv[F];
 #pragma unroll
         for (int f = 0; f < F; ++f) tv[f] = __shfl_up_sync(0xffffffffu, bot[f], 1);
-        if (u == 0 && active) {
-#pragma unroll
-          for (int f = 0; f < F; ++f) tv[f] = (strip == 0) ? 1.0 : hrow[jj * F + f + 1];
-        }
         if (active) {
-          const int jc = (jj * F) >> pb.lam2;
-          double p[RC];
-          coarse_p<KIND, DP, RC>(p, rr, cs, pb, pr, pc, pidx, i0, jc);
-          if constexpr (KIND == LINEAR) {
-            if (pb.pscale != 1.0) {
+          const double* rec = SK_REC(jj);
+          if (u == 0) {
 #pragma unroll
-              for (int c = 0; c < RC; ++c) p[c] *= pb.pscale;
+            for (int f = 0; f < F; ++f) tv[f] = (strip == 0) ? 1.0 : rec[DP + f];
+          }
+          double p[RC];
+          if constexpr (KIND == LINEAR) {
+            double dy[DP];
+#pragma unroll
+            for (int k = 0; k < DP; k += 2) {
+              const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+              dy[k] = t2.x;
+              dy[k + 1] = t2.y;
             }
+#pragma unroll
+            for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy) * pb.pscale;
+          } else {
+            const int jc = (jj * F) >> pb.lam2;
+            if (jc != jcur) {
+              double yv[DP];
+#pragma unroll
+              for (int k = 0; k < DP; k += 2) {
+                const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+                yv[k] = t2.x;
+                yv[k + 1] = t2.y;
+              }
+#pragma unroll
+              for (int c = 0; c <= RC; ++c) {
+                Kl[c] = Kr[c];
+                Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
+              }
+              jcur = jc;
+            }
+#pragma unroll
+            for (int c = 0; c < RC; ++c)
+              p[c] = ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale;
           }
           Coef cf[RC];
 #pragma unroll
@@ -159,7 +233,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
               up = nk;
             }
             bot[f] = up;
-            SK_ROWCK(strip, tau, f, lane) = up;
+            SK_ROWCK(strip, jj + u, f, lane) = up;  // diagonal index = column + writer lane
           }
           topc = tv[F - 1];
           if (u == 31) {
@@ -167,14 +241,13 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             for (int f = 0; f < F; ++f) hrow[jj * F + f + 1] = bot[f];
           }
           if (strip == last_strip && u == u_star && jj == NS - 1) {
-            double v = kl[0];
 #pragma unroll
-            for (int r = 1; r < R; ++r)
-              if (r == r_star) v = kl[r];
-            kval = v;
+            for (int r = 0; r < R; ++r)
+              if (r == r_star) kval = kl[r];
           }
         }
       }
+      cp_async_wait<0>();
       __syncwarp();
     }
     if (ba.values && u == u_star) ba.values[oidx] = kval;
@@ -183,11 +256,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
     for (int t = u; t <= M2; t += 32) arow[t] = 0.0;
     if constexpr (MAP == DBUF) {
       for (int64_t e = u; e < (int64_t)pb.M1c * pb.M2c; e += 32) dbuf[e] = 0.0;
-    }
-    // increment-gradient scratch of this pair: rows [M1c][DP], cols [M2c][DP]
-    double* __restrict__ gxs = ba.gscr + slot * ba.gscr_stride;
-    double* __restrict__ gcs = gxs + (int64_t)pb.M1c * DP;
-    if constexpr (MAP == FUSED) {
+    } else {
       for (int64_t e = u; e < (int64_t)(pb.M1c + pb.M2c) * DP; e += 32) gxs[e] = 0.0;
     }
     __syncwarp();
@@ -199,9 +268,52 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       const int rbase = strip * H + u * R;
       const int i0 = rbase >> pb.lam1;
       RowRegs<KIND, DP, RC> rr;
-      if constexpr (KIND != DELTA) load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
-      ColState<KIND, DP, RC> cs;
-      cs.have = -2;
+      load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
+
+      // staging of block blk: top-row checkpoints, lane 0's top row, left
+      // checkpoint, lane 31's incoming column gradients
+      auto issue_stage = [&](int blk) {
+        double* st = stg0 + (blk & 1) * SM::STG;
+        // TS: rowck[strip][d][f][*] for d in [blk*CB - 2, blk*CB + CB - 2]
+        {
+          const int dlo = blk * CB - 2;
+          constexpr int NCH = SM::TS / 2;
+          for (int e = lane; e < NCH; e += 32) {
+            const int row = e / (F * 16);  // (CB+1) rows of F*32 doubles
+            const int d = dlo + row;
+            const bool v = (d >= 0) && (d < NT);
+            cp_async16(st + 2 * e,
+                       rowck + (((int64_t)strip * NT + (v ? d : 0)) * F) * 32 + 2 * (e % (F * 16)),
+                       v);
+          }
+        }
+        // T0: lane 0's top row: nodes t = blk*CB*F + q, q = 0..CB*F, written by
+        // strip-1's lane 31 at diagonal (t-1)/F + 31
+        if (strip > 0) {
+          for (int q = lane; q <= CB * F; q += 32) {
+            const int t = blk * CB * F + q;
+            const bool v = (t >= 1) && (t <= M2);
+            const int js = v ? (t - 1) / F : 0, fs = v ? (t - 1) % F : 0;
+            cp_async8(st + SM::TS + q, &SK_ROWCK(strip - 1, js + 31, fs, 31), v);
+          }
+        }
+        // LS: colck[strip][blk][r][*]
+        for (int e = lane; e < SM::LS / 2; e += 32)
+          cp_async16(st + SM::TS + SM::T0 + 2 * e,
+                     colck + (((int64_t)strip * NB + blk) * R) * 32 + 2 * e, true);
+        // GS: gcs[jc(col)] for lane 31's columns col = blk*CB - 31 + kap
+        if constexpr (MAP == FUSED) {
+          for (int e = lane; e < CB * (DP / 2); e += 32) {
+            const int kap = e / (DP / 2), w = e % (DP / 2);
+            const int col = blk * CB - 31 + kap;
+            const bool v = (col >= 0) && (col < NS) && (strip < nstrips - 1);
+            const int jc = v ? ((col * F) >> pb.lam2) : 0;
+            cp_async16(st + SM::TS + SM::T0 + SM::LS + kap * DP + 2 * w, gcs + (int64_t)jc * DP + 2 * w,
+                       v);
+          }
+        }
+      };
+
       double aR[R], bR[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) { aR[r] = 0.0; bR[r] = 0.0; }
@@ -210,55 +322,104 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       for (int f = 0; f < F; ++f) sendm[f] = 0.0;
       double gxr[(MAP == FUSED) ? RC : 1][DP];
       double gys[DP];
+      double gacc[DP];  // lane 0: column sums of the current coarse column
 #pragma unroll
       for (int k = 0; k < DP; ++k) {
         gys[k] = 0.0;
+        gacc[k] = 0.0;
 #pragma unroll
         for (int c = 0; c < ((MAP == FUSED) ? RC : 1); ++c) gxr[c][k] = 0.0;
       }
+      double Kl[RC + 1], Kr[RC + 1];  // RBF recompute state
+      int jcur = -1000;
+
+      // prologue: records of the first block's columns + its staging
+      issue_cols((NB - 1) * CB - 31, CB + 31, arow, true);
+      issue_stage(NB - 1);
+      cp_async_commit();
 
       for (int blk = NB - 1; blk >= 0; --blk) {
-        const int jj0 = blk * CB - u;  // lane's first step in this block
+        if (blk > 0) {
+          issue_cols((blk - 1) * CB - 31, CB, arow, true);
+          issue_stage(blk - 1);
+        }
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncwarp();
+        const double* st = stg0 + (blk & 1) * SM::STG;
+        const double* sTS = st;
+        const double* sT0 = st + SM::TS;
+        const double* sLS = st + SM::TS + SM::T0;
+        const double* sGS = st + SM::TS + SM::T0 + SM::LS;
+        const int jj0 = blk * CB - u;  // lane's first column in this block
+        // top-row value at node t = jj0*F + q (q = 0..CB*F) of this lane's rows
+        auto topv = [&](int q) -> double {
+          const int t = jj0 * F + q;
+          if (t <= 0 || (strip == 0 && u == 0)) return 1.0;
+          if (t > M2) return 0.0;  // dead columns: keep values finite
+          if (u == 0) return sT0[q];
+          // writer lane u-1 at diagonal (t-1)/F + u - 1 = blk*CB - 2 + (q-1+F)/F ...
+          const int d = (t - 1) / F + u - 1 - (blk * CB - 2);
+          return sTS[(d * F + (t - 1) % F) * 32 + (u - 1)];
+        };
+
         // ---- recompute the block's forward values into shared memory
         {
           double kl[R];
 #pragma unroll
-          for (int r = 0; r < R; ++r) {
-            kl[r] = SK_COLCK(strip, blk, r);
-            SK_LB(r) = kl[r];
-          }
-          // top row: node columns t = jj0*F + q, q = 0..CB*F
+          for (int r = 0; r < R; ++r) kl[r] = sLS[r * 32 + lane];
+          if constexpr (KIND == RBF) {
+            // K at node columns jc(jj0), jc(jj0)+1 for the first column of the block
+            const int col0 = jj0 < 0 ? 0 : (jj0 >= NS ? NS - 1 : jj0);
+            const int jc0 = (col0 * F) >> pb.lam2;
+            double yv[DP];
+            load_vec<DP>(yv, cbase + (int64_t)jc0 * pb.dpad);
 #pragma unroll
-          for (int q = 0; q <= CB * F; ++q) {
-            const int t = jj0 * F + q;
-            double v;
-            if (t <= 0 || (strip == 0 && u == 0)) {
-              v = 1.0;
-            } else if (t > M2) {
-              v = 0.0;  // dead columns: keep values finite
-            } else {
-              const int js = (t - 1) / F, fs = (t - 1) % F;
-              v = (u > 0) ? SK_ROWCK(strip, js + u - 1, fs, u - 1)
-                          : SK_ROWCK(strip - 1, js + 31, fs, 31);
-            }
-            SK_TB(q) = v;
+            for (int c = 0; c <= RC; ++c) Kl[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
+            load_vec<DP>(yv, cbase + (int64_t)(jc0 + 1) * pb.dpad);
+#pragma unroll
+            for (int c = 0; c <= RC; ++c) Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
+            jcur = jc0;
           }
-          double topc = SK_TB(0);
+          double topc = topv(0);
 #pragma unroll
           for (int kap = 0; kap < CB; ++kap) {
             const int jj = jj0 + kap;
             const bool colv = (jj >= 0) && (jj < NS);
+            const double* rec = SK_REC(jj);
             double p[RC];
-            if (colv) {
-              const int jc = (jj * F) >> pb.lam2;
-              coarse_p<KIND, DP, RC>(p, rr, cs, pb, pr, pc, pidx, i0, jc);
-              if constexpr (KIND == LINEAR) {
-                if (pb.pscale != 1.0) {
+            if constexpr (KIND == LINEAR) {
+              double dy[DP];
 #pragma unroll
-                  for (int c = 0; c < RC; ++c) p[c] *= pb.pscale;
-                }
+              for (int k = 0; k < DP; k += 2) {
+                const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+                dy[k] = t2.x;
+                dy[k + 1] = t2.y;
               }
+#pragma unroll
+              for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy) * pb.pscale;
             } else {
+              const int jc = (jj * F) >> pb.lam2;
+              if (colv && jc != jcur) {
+                double yv[DP];
+#pragma unroll
+                for (int k = 0; k < DP; k += 2) {
+                  const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+                  yv[k] = t2.x;
+                  yv[k + 1] = t2.y;
+                }
+#pragma unroll
+                for (int c = 0; c <= RC; ++c) {
+                  Kl[c] = Kr[c];
+                  Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
+                }
+                jcur = jc;
+              }
+#pragma unroll
+              for (int c = 0; c < RC; ++c)
+                p[c] = colv ? ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale : 0.0;
+            }
+            if (!colv) {
 #pragma unroll
               for (int c = 0; c < RC; ++c) p[c] = 0.0;
             }
@@ -270,8 +431,8 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             }
 #pragma unroll
             for (int f = 0; f < F; ++f) {
-              double up = SK_TB(kap * F + f + 1);
-              double dg = (f == 0) ? topc : SK_TB(kap * F + f);
+              double up = topv(kap * F + f + 1);
+              double dg = (f == 0) ? topc : topv(kap * F + f);
 #pragma unroll
               for (int r = 0; r < R; ++r) {
                 const double nk = cell(up, kl[r], dg, cf[r / FR]);
@@ -281,14 +442,16 @@ bwd_kernel(Problem pb, BwdArgs ba) {
                 SK_KB(kap, f, r) = nk;
               }
             }
-            topc = SK_TB(kap * F + F);
+            topc = topv(kap * F + F);
           }
         }
-        // ---- reverse sweep over the block, one step per kap
+
+        // ---- reverse sweep over the block, one column per kap
 #pragma unroll 1
         for (int kap = CB - 1; kap >= 0; --kap) {
           const int jj = jj0 + kap;
           const bool colv = (jj >= 0) && (jj < NS);
+          const double* rec = SK_REC(jj);
           double recv[F];
 #pragma unroll
           for (int f = 0; f < F; ++f) recv[f] = __shfl_down_sync(0xffffffffu, sendm[f], 1);
@@ -299,9 +462,13 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           }
           if (u == 31) {
 #pragma unroll
-            for (int f = 0; f < F; ++f) recv[f] = colv ? arow[jj * F + f + 1] : 0.0;
+            for (int f = 0; f < F; ++f) recv[f] = colv ? rec[DP + f] : 0.0;
+            if constexpr (MAP == FUSED) {
+              // column gradient accumulated by the strips below, once per coarse column
+              const bool first = ((jj + 1) & K2m) == 0;
 #pragma unroll
-            for (int k = 0; k < DP; ++k) grecv[k] = 0.0;
+              for (int k = 0; k < DP; ++k) grecv[k] = (colv && first) ? sGS[kap * DP + k] : 0.0;
+            }
           }
           double Dp[RC];
 #pragma unroll
@@ -329,12 +496,12 @@ bwd_kernel(Problem pb, BwdArgs ba) {
               const double b = cf[c].B * lam;
               // forward values around the cell (s,t): left, up, up-left
               const double kL = (f > 0) ? SK_KB(kap, f - 1, r)
-                                        : (kap > 0 ? SK_KB(kap - 1, F - 1, r) : SK_LB(r));
-              const double kU = (r > 0) ? SK_KB(kap, f, r - 1) : SK_TB(kap * F + f + 1);
+                                        : (kap > 0 ? SK_KB(kap - 1, F - 1, r) : sLS[r * 32 + lane]);
+              const double kU = (r > 0) ? SK_KB(kap, f, r - 1) : topv(kap * F + f + 1);
               const double kD = (r > 0) ? ((f > 0) ? SK_KB(kap, f - 1, r - 1)
                                                    : (kap > 0 ? SK_KB(kap - 1, F - 1, r - 1)
-                                                              : SK_LB(r - 1)))
-                                        : SK_TB(kap * F + f);
+                                                              : sLS[(r - 1) * 32 + lane]))
+                                        : topv(kap * F + f);
               const double p6 = pk[c] * (1.0 / 6.0);
               const double wv = fma(kL + kU, 0.5 + p6, kD * p6);
               if (live) Dp[c] = fma(lam, wv, Dp[c]);
@@ -354,47 +521,64 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           if constexpr (MAP == FUSED) {
             // gx_i += D_ij dy_j (row-local);  gy_j += D_ij dx_i (down the warp)
             double dy[DP];
-            if (colv) {
-              load_vec<DP>(dy, pb.C.p + pc * pb.C.path_stride + (int64_t)jc * pb.dpad);
-            } else {
 #pragma unroll
-              for (int k = 0; k < DP; ++k) dy[k] = 0.0;
+            for (int k = 0; k < DP; k += 2) {
+              const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+              dy[k] = t2.x;
+              dy[k + 1] = t2.y;
             }
 #pragma unroll
             for (int k = 0; k < DP; ++k) {
-              double g = grecv[k];
+              double gsum = grecv[k];
 #pragma unroll
               for (int c = 0; c < RC; ++c) {
                 gxr[c][k] = fma(Dp[c], dy[k], gxr[c][k]);
-                g = fma(Dp[c], rr.v[c][k], g);
+                gsum = fma(Dp[c], rr.v[c][k], gsum);
               }
-              gys[k] = g;
+              gys[k] = gsum;
             }
             if (u == 0 && colv) {
-              // lane 0 holds the strip's column sum: accumulate dF/d(dy_j)
-              double2* q = reinterpret_cast<double2*>(gcs + (int64_t)jc * DP);
+              // lane 0 holds the column sum over this strip and all strips below
 #pragma unroll
-              for (int k = 0; k < DP / 2; ++k) {
-                double2 v = q[k];
-                v.x += gys[2 * k];
-                v.y += gys[2 * k + 1];
-                q[k] = v;
+              for (int k = 0; k < DP; ++k) gacc[k] += gys[k];
+              if ((jj & K2m) == 0) {  // last column of the coarse column (reverse order)
+                double2* q = reinterpret_cast<double2*>(gcs + (int64_t)jc * DP);
+#pragma unroll
+                for (int k = 0; k < DP / 2; ++k) q[k] = make_double2(gacc[2 * k], gacc[2 * k + 1]);
+#pragma unroll
+                for (int k = 0; k < DP; ++k) gacc[k] = 0.0;
               }
             }
           } else {
-            // coarse adjoint buffer; lanes sharing a coarse cell write in
-            // a fixed order (lane u+1 one step before lane u)
-            if (colv) {
+            // RBF: coarse adjoint, kept per block in shared memory (p is dead)
 #pragma unroll
-              for (int c = 0; c < RC; ++c) {
-                const int i = i0 + c;
-                if (i < pb.M1c) dbuf[(int64_t)i * pb.M2c + jc] += Dp[c];
-              }
-            }
-            __syncwarp();
+            for (int c = 0; c < RC; ++c) SK_PB(kap, c) = colv ? Dp[c] : 0.0;
           }
         }
+        if constexpr (MAP == DBUF) {
+          // flush the block's coarse adjoint; lanes sharing coarse rows go in order
+          const bool excl = ba.rows_exclusive != 0;
+          for (int ln = excl ? 0 : 31; ln >= 0; --ln) {
+            if (excl || u == ln) {
+#pragma unroll
+              for (int kap = CB - 1; kap >= 0; --kap) {
+                const int jj = jj0 + kap;
+                if (jj >= 0 && jj < NS) {
+                  const int jc = (jj * F) >> pb.lam2;
+#pragma unroll
+                  for (int c = 0; c < RC; ++c) {
+                    const int i = i0 + c;
+                    if (i < pb.M1c) dbuf[(int64_t)i * pb.M2c + jc] += SK_PB(kap, c);
+                  }
+                }
+              }
+            }
+            if (!excl) __syncwarp();
+          }
+        }
+        __syncwarp();
       }
+      cp_async_wait<0>();
       if constexpr (MAP == FUSED) {
         // row-side dF/d(dx_i) into the pair's scratch.  A coarse row owned by
         // one lane is stored once; when 2^lam1 > R a coarse row spans lanes
@@ -447,86 +631,49 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         grad_add(gC + e, v, atomic);
       }
       __syncwarp();
-    }
-
-    if constexpr (MAP == DBUF) {
+    } else {
+      // RBF node adjoint G_ij = D[i-1,j-1] - D[i-1,j] - D[i,j-1] + D[i,j] (zero
+      // padded); dF/dx_i = sum_j G_ij K_ij (y_j - x_i)/sigma^2, dF/dy_j = -sum_i (same)
       __syncwarp();
       const double* D = dbuf;
-      if constexpr (KIND == LINEAR) {
-        // gx_i = sum_j D_ij dy_j, gy_j = sum_i D_ij dx_i, then telescope
-        const double* dxp = pb.R.p + pr * pb.R.path_stride;
-        const double* dyp = pb.C.p + pc * pb.C.path_stride;
-        // serialised telescoping (deterministic): one lane at a time
-        for (int ln = 0; ln < 32; ++ln) {
-          if (u == ln) {
-            for (int i = u; i < pb.M1c; i += 32) {
-              for (int k = 0; k < dR; ++k) {
-                double g = 0.0;
-                for (int j = 0; j < pb.M2c; ++j)
-                  g = fma(D[(int64_t)i * pb.M2c + j], dyp[(int64_t)j * pb.dpad + k], g);
-                grad_add(gR + (int64_t)i * dR + k, -g, atomic);
-                grad_add(gR + (int64_t)(i + 1) * dR + k, g, atomic);
-              }
+      const double* xp = pb.R.p + pr * pb.R.path_stride;
+      const double* yp = cbase;
+      const int L1n = pb.M1c + 1, L2n = pb.M2c + 1;
+      auto Dat = [&](int i, int j) -> double {
+        return (i >= 0 && j >= 0 && i < pb.M1c && j < pb.M2c) ? D[(int64_t)i * pb.M2c + j] : 0.0;
+      };
+      for (int i = u; i < L1n; i += 32) {
+        for (int k = 0; k < dR; ++k) {
+          double acc = 0.0;
+          for (int j = 0; j < L2n; ++j) {
+            const double G = Dat(i - 1, j - 1) - Dat(i - 1, j) - Dat(i, j - 1) + Dat(i, j);
+            if (G == 0.0) continue;
+            double s2 = 0.0;
+            for (int kk = 0; kk < dR; ++kk) {
+              const double t = xp[(int64_t)i * pb.dpad + kk] - yp[(int64_t)j * pb.dpad + kk];
+              s2 = fma(t, t, s2);
             }
+            const double K = exp(-s2 * pb.inv2s2);
+            acc = fma(G * K * pb.invs2, yp[(int64_t)j * pb.dpad + k] - xp[(int64_t)i * pb.dpad + k], acc);
           }
-          __syncwarp();
+          grad_add(gR + (int64_t)i * dR + k, acc, atomic);
         }
-        for (int ln = 0; ln < 32; ++ln) {
-          if (u == ln) {
-            for (int j = u; j < pb.M2c; j += 32) {
-              for (int k = 0; k < dR; ++k) {
-                double g = 0.0;
-                for (int i = 0; i < pb.M1c; ++i)
-                  g = fma(D[(int64_t)i * pb.M2c + j], dxp[(int64_t)i * pb.dpad + k], g);
-                grad_add(gC + (int64_t)j * dR + k, -g, atomic);
-                grad_add(gC + (int64_t)(j + 1) * dR + k, g, atomic);
-              }
+      }
+      for (int j = u; j < L2n; j += 32) {
+        for (int k = 0; k < dR; ++k) {
+          double acc = 0.0;
+          for (int i = 0; i < L1n; ++i) {
+            const double G = Dat(i - 1, j - 1) - Dat(i - 1, j) - Dat(i, j - 1) + Dat(i, j);
+            if (G == 0.0) continue;
+            double s2 = 0.0;
+            for (int kk = 0; kk < dR; ++kk) {
+              const double t = xp[(int64_t)i * pb.dpad + kk] - yp[(int64_t)j * pb.dpad + kk];
+              s2 = fma(t, t, s2);
             }
+            const double K = exp(-s2 * pb.inv2s2);
+            acc = fma(G * K * pb.invs2, xp[(int64_t)i * pb.dpad + k] - yp[(int64_t)j * pb.dpad + k], acc);
           }
-          __syncwarp();
-        }
-      } else if constexpr (KIND == RBF) {
-        // node adjoint G_ij = D[i-1,j-1] - D[i-1,j] - D[i,j-1] + D[i,j] (zero padded);
-        // dF/dx_i = sum_j G_ij K_ij (y_j - x_i)/sigma^2,  dF/dy_j = -sum_i (same)
-        const double* xp = pb.R.p + pr * pb.R.path_stride;
-        const double* yp = pb.C.p + pc * pb.C.path_stride;
-        const int L1n = pb.M1c + 1, L2n = pb.M2c + 1;
-        auto Dat = [&](int i, int j) -> double {
-          return (i >= 0 && j >= 0 && i < pb.M1c && j < pb.M2c) ? D[(int64_t)i * pb.M2c + j] : 0.0;
-        };
-        for (int i = u; i < L1n; i += 32) {
-          for (int k = 0; k < dR; ++k) {
-            double acc = 0.0;
-            for (int j = 0; j < L2n; ++j) {
-              const double G = Dat(i - 1, j - 1) - Dat(i - 1, j) - Dat(i, j - 1) + Dat(i, j);
-              if (G == 0.0) continue;
-              double s2 = 0.0;
-              for (int kk = 0; kk < dR; ++kk) {
-                const double t = xp[(int64_t)i * pb.dpad + kk] - yp[(int64_t)j * pb.dpad + kk];
-                s2 = fma(t, t, s2);
-              }
-              const double K = exp(-s2 * pb.inv2s2);
-              acc = fma(G * K * pb.invs2, yp[(int64_t)j * pb.dpad + k] - xp[(int64_t)i * pb.dpad + k], acc);
-            }
-            grad_add(gR + (int64_t)i * dR + k, acc, atomic);
-          }
-        }
-        for (int j = u; j < L2n; j += 32) {
-          for (int k = 0; k < dR; ++k) {
-            double acc = 0.0;
-            for (int i = 0; i < L1n; ++i) {
-              const double G = Dat(i - 1, j - 1) - Dat(i - 1, j) - Dat(i, j - 1) + Dat(i, j);
-              if (G == 0.0) continue;
-              double s2 = 0.0;
-              for (int kk = 0; kk < dR; ++kk) {
-                const double t = xp[(int64_t)i * pb.dpad + kk] - yp[(int64_t)j * pb.dpad + kk];
-                s2 = fma(t, t, s2);
-              }
-              const double K = exp(-s2 * pb.inv2s2);
-              acc = fma(G * K * pb.invs2, xp[(int64_t)i * pb.dpad + k] - yp[(int64_t)j * pb.dpad + k], acc);
-            }
-            grad_add(gC + (int64_t)j * dR + k, acc, atomic);
-          }
+          grad_add(gC + (int64_t)j * dR + k, acc, atomic);
         }
       }
       __syncwarp();
@@ -534,10 +681,8 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   }
 #undef SK_KB
 #undef SK_PB
-#undef SK_TB
-#undef SK_LB
+#undef SK_REC
 #undef SK_ROWCK
-#undef SK_COLCK
 }
 
 }  // namespace sk

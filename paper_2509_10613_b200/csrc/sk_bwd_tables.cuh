@@ -5,12 +5,18 @@
 
 namespace sk {
 
+// Block width (columns): ~16 recomputed values per lane, within [2, 8].
+template <int R, int F>
+constexpr int bwd_cb() {
+  return (16 / (F * R)) < 2 ? 2 : (16 / (F * R)) > 8 ? 8 : 16 / (F * R);
+}
+
 template <int KIND, int DP, int R, int FR, int F>
 inline void sk_bwd_leaf(BwdFn& fn, int& smem_doubles) {
-  constexpr int CB = 8 / F;
+  constexpr int CB = bwd_cb<R, F>();
   constexpr int MAP = (KIND == LINEAR) ? FUSED : DBUF;
   fn = bwd_kernel<KIND, DP, R, FR, F, CB, MAP>;
-  smem_doubles = BlockSmem<R, R / FR, F, CB>::TOTAL * 32;
+  smem_doubles = BwdSmem<DP, R, R / FR, F, CB>::TOTAL;  // per warp
 }
 
 template <int KIND, int DP, int R, int FR>

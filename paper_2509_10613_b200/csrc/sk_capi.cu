@@ -489,7 +489,7 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
                                                      (int64_t)occ * sms));
   pl.slots = pl.blocks * warps;
   const int64_t M1 = M1c << lamR, M2 = M2c << lamC;
-  const int64_t NS = M2 / s.F, NT = NS + 31, CB = 8 / s.F, NB = (NT + CB - 1) / CB;
+  const int64_t NS = M2 / s.F, NT = NS + 31, CB = std::min(8, std::max(2, 16 / (s.F * s.R))), NB = (NT + CB - 1) / CB;
   const int64_t nstrips = (M1 + 32 * s.R - 1) / (32 * s.R);
   pl.rowck_stride = (int64_t)align_up((size_t)(nstrips * NT * s.F * 32), 32);
   pl.colck_stride = (int64_t)align_up((size_t)(nstrips * NB * s.R * 32), 32);
