@@ -53,7 +53,9 @@ struct BwdSmem {
   static constexpr int LS = R * 32;                  // left-column checkpoint
   static constexpr int GS = CB * DP;                 // lane 31's incoming column gradients
   static constexpr int STG = TS + T0 + LS + GS;
-  static constexpr int TOTAL = SLOTS * REC + (NK + NP) * 32 + 2 * STG;
+  static constexpr int NTR = CB * F + 1;            // top row of the block (x32 lanes)
+  static constexpr int GA = DP;                      // lane 0's coarse-column gradient sums
+  static constexpr int TOTAL = SLOTS * REC + (NK + NP + NTR) * 32 + 2 * STG + GA;
 };
 
 template <int KIND, int DP, int R, int FR, int F, int CB, int MAP>
@@ -71,7 +73,10 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   double* ring = smem + (size_t)warp * SM::TOTAL;
   double* sK = ring + SLOTS * REC;
   double* sP = sK + SM::NK * 32;
-  double* stg0 = sP + SM::NP * 32;
+  double* sTR = sP + SM::NP * 32;
+  double* stg0 = sTR + SM::NTR * 32;
+  double* sGA = stg0 + 2 * SM::STG;
+#define SK_TR(q) sTR[(q) * 32 + lane]
 #define SK_KB(kap, f, r) sK[(((kap) * F + (f)) * R + (r)) * 32 + lane]
 #define SK_PB(kap, c) sP[((kap) * RC + (c)) * 32 + lane]
 #define SK_REC(col) (ring + ((col) & (SLOTS - 1)) * REC)
@@ -134,6 +139,20 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       }
     };
 
+    // one column record, one cp.async per lane (lanes < DP/2 + F)
+    auto issue_one = [&](int col, const double* hsrc, bool hvalid) {
+      const bool cv = (col >= 0) && (col < NS);
+      double* dst = SK_REC(col);
+      if (lane < DP / 2) {
+        const int jc = cv ? ((col * F) >> pb.lam2) : 0;
+        const int node = (KIND == RBF) ? jc + 1 : jc;
+        cp_async16(dst + 2 * lane, cbase + (int64_t)node * pb.dpad + 2 * lane, cv);
+      } else if (lane < DP / 2 + F) {
+        const int f = lane - DP / 2;
+        cp_async8(dst + DP + f, hsrc + (cv ? col * F + f + 1 : 0), cv && hvalid);
+      }
+    };
+
     // ------------------------------------------- phase A: forward + checkpoints
     for (int t = u; t <= M2; t += 32) hrow[t] = 1.0;
     __syncwarp();
@@ -145,6 +164,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
       double Kl[RC + 1], Kr[RC + 1];
       int jcur = -1;
+      double* __restrict__ rowck_s = rowck + (int64_t)strip * NT * F * 32 + lane;
       if constexpr (KIND == RBF) {
         double y0[DP];
         load_vec<DP>(y0, cbase);
@@ -154,7 +174,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         for (int c = 0; c <= RC; ++c) Kl[c] = Kr[c];
       }
       for (int q = 0; q < PF; ++q) {
-        issue_cols(q, 1, hrow, strip > 0);
+        issue_one(q, hrow, strip > 0);
         cp_async_commit();
       }
       double kl[R];
@@ -165,7 +185,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
 #pragma unroll
       for (int f = 0; f < F; ++f) bot[f] = 1.0;
       for (int tau = 0; tau < NT; ++tau) {
-        issue_cols(tau + PF, 1, hrow, strip > 0);
+        issue_one(tau + PF, hrow, strip > 0);
         cp_async_commit();
         cp_async_wait<PF>();
         __syncwarp();
@@ -233,7 +253,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
               up = nk;
             }
             bot[f] = up;
-            SK_ROWCK(strip, jj + u, f, lane) = up;  // diagonal index = column + writer lane
+            rowck_s[(tau * F + f) * 32] = up;  // diagonal index = column + writer lane = tau
           }
           topc = tv[F - 1];
           if (u == 31) {
@@ -322,11 +342,10 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       for (int f = 0; f < F; ++f) sendm[f] = 0.0;
       double gxr[(MAP == FUSED) ? RC : 1][DP];
       double gys[DP];
-      double gacc[DP];  // lane 0: column sums of the current coarse column
+      for (int k = lane; k < DP; k += 32) sGA[k] = 0.0;  // lane 0's coarse-column sums
 #pragma unroll
       for (int k = 0; k < DP; ++k) {
         gys[k] = 0.0;
-        gacc[k] = 0.0;
 #pragma unroll
         for (int c = 0; c < ((MAP == FUSED) ? RC : 1); ++c) gxr[c][k] = 0.0;
       }
@@ -381,7 +400,9 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             for (int c = 0; c <= RC; ++c) Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
             jcur = jc0;
           }
-          double topc = topv(0);
+#pragma unroll
+          for (int q = 0; q <= CB * F; ++q) SK_TR(q) = topv(q);
+          double topc = SK_TR(0);
 #pragma unroll
           for (int kap = 0; kap < CB; ++kap) {
             const int jj = jj0 + kap;
@@ -431,8 +452,8 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             }
 #pragma unroll
             for (int f = 0; f < F; ++f) {
-              double up = topv(kap * F + f + 1);
-              double dg = (f == 0) ? topc : topv(kap * F + f);
+              double up = SK_TR(kap * F + f + 1);
+              double dg = (f == 0) ? topc : SK_TR(kap * F + f);
 #pragma unroll
               for (int r = 0; r < R; ++r) {
                 const double nk = cell(up, kl[r], dg, cf[r / FR]);
@@ -442,12 +463,12 @@ bwd_kernel(Problem pb, BwdArgs ba) {
                 SK_KB(kap, f, r) = nk;
               }
             }
-            topc = topv(kap * F + F);
+            topc = SK_TR(kap * F + F);
           }
         }
 
         // ---- reverse sweep over the block, one column per kap
-#pragma unroll 1
+#pragma unroll
         for (int kap = CB - 1; kap >= 0; --kap) {
           const int jj = jj0 + kap;
           const bool colv = (jj >= 0) && (jj < NS);
@@ -455,20 +476,9 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           double recv[F];
 #pragma unroll
           for (int f = 0; f < F; ++f) recv[f] = __shfl_down_sync(0xffffffffu, sendm[f], 1);
-          double grecv[DP];
-          if constexpr (MAP == FUSED) {
-#pragma unroll
-            for (int k = 0; k < DP; ++k) grecv[k] = __shfl_down_sync(0xffffffffu, gys[k], 1);
-          }
           if (u == 31) {
 #pragma unroll
             for (int f = 0; f < F; ++f) recv[f] = colv ? rec[DP + f] : 0.0;
-            if constexpr (MAP == FUSED) {
-              // column gradient accumulated by the strips below, once per coarse column
-              const bool first = ((jj + 1) & K2m) == 0;
-#pragma unroll
-              for (int k = 0; k < DP; ++k) grecv[k] = (colv && first) ? sGS[kap * DP + k] : 0.0;
-            }
           }
           double Dp[RC];
 #pragma unroll
@@ -497,11 +507,11 @@ bwd_kernel(Problem pb, BwdArgs ba) {
               // forward values around the cell (s,t): left, up, up-left
               const double kL = (f > 0) ? SK_KB(kap, f - 1, r)
                                         : (kap > 0 ? SK_KB(kap - 1, F - 1, r) : sLS[r * 32 + lane]);
-              const double kU = (r > 0) ? SK_KB(kap, f, r - 1) : topv(kap * F + f + 1);
+              const double kU = (r > 0) ? SK_KB(kap, f, r - 1) : SK_TR(kap * F + f + 1);
               const double kD = (r > 0) ? ((f > 0) ? SK_KB(kap, f - 1, r - 1)
                                                    : (kap > 0 ? SK_KB(kap - 1, F - 1, r - 1)
                                                               : sLS[(r - 1) * 32 + lane]))
-                                        : topv(kap * F + f);
+                                        : SK_TR(kap * F + f);
               const double p6 = pk[c] * (1.0 / 6.0);
               const double wv = fma(kL + kU, 0.5 + p6, kD * p6);
               if (live) Dp[c] = fma(lam, wv, Dp[c]);
@@ -520,33 +530,33 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           for (int c = 0; c < RC; ++c) Dp[c] *= pb.scale;
           if constexpr (MAP == FUSED) {
             // gx_i += D_ij dy_j (row-local);  gy_j += D_ij dx_i (down the warp)
-            double dy[DP];
-#pragma unroll
-            for (int k = 0; k < DP; k += 2) {
-              const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-              dy[k] = t2.x;
-              dy[k + 1] = t2.y;
-            }
+            // lane 31 starts the chain with the column gradient accumulated by
+            // the strips below, once per coarse column
+            const bool in31 = colv && (((jj + 1) & K2m) == 0);
 #pragma unroll
             for (int k = 0; k < DP; ++k) {
-              double gsum = grecv[k];
+              double g = __shfl_down_sync(0xffffffffu, gys[k], 1);
+              if (u == 31) g = in31 ? sGS[kap * DP + k] : 0.0;
+              const double dyk = rec[k];
 #pragma unroll
               for (int c = 0; c < RC; ++c) {
-                gxr[c][k] = fma(Dp[c], dy[k], gxr[c][k]);
-                gsum = fma(Dp[c], rr.v[c][k], gsum);
+                gxr[c][k] = fma(Dp[c], dyk, gxr[c][k]);
+                g = fma(Dp[c], rr.v[c][k], g);
               }
-              gys[k] = gsum;
+              gys[k] = g;
             }
             if (u == 0 && colv) {
               // lane 0 holds the column sum over this strip and all strips below
 #pragma unroll
-              for (int k = 0; k < DP; ++k) gacc[k] += gys[k];
+              for (int k = 0; k < DP; ++k) sGA[k] += gys[k];
               if ((jj & K2m) == 0) {  // last column of the coarse column (reverse order)
                 double2* q = reinterpret_cast<double2*>(gcs + (int64_t)jc * DP);
 #pragma unroll
-                for (int k = 0; k < DP / 2; ++k) q[k] = make_double2(gacc[2 * k], gacc[2 * k + 1]);
-#pragma unroll
-                for (int k = 0; k < DP; ++k) gacc[k] = 0.0;
+                for (int k = 0; k < DP / 2; ++k) {
+                  q[k] = make_double2(sGA[2 * k], sGA[2 * k + 1]);
+                  sGA[2 * k] = 0.0;
+                  sGA[2 * k + 1] = 0.0;
+                }
               }
             }
           } else {
@@ -682,6 +692,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
 #undef SK_KB
 #undef SK_PB
 #undef SK_REC
+#undef SK_TR
 #undef SK_ROWCK
 }
 
