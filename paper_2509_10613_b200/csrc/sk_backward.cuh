@@ -59,7 +59,10 @@ struct BwdSmem {
 };
 
 template <int KIND, int DP, int R, int FR, int F, int CB, int MAP>
-__global__ void __launch_bounds__(128)
+#ifndef SK_BWD_MINB
+#define SK_BWD_MINB 1
+#endif
+__global__ void __launch_bounds__(128, SK_BWD_MINB)
 bwd_kernel(Problem pb, BwdArgs ba) {
   constexpr int RC = R / FR;
   using SM = BwdSmem<DP, R, RC, F, CB>;
