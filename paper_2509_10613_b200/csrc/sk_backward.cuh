@@ -59,10 +59,9 @@ struct BwdSmem {
 };
 
 template <int KIND, int DP, int R, int FR, int F, int CB, int MAP>
-#ifndef SK_BWD_MINB
-#define SK_BWD_MINB 1
-#endif
-__global__ void __launch_bounds__(128, SK_BWD_MINB)
+// 3 CTAs (12 warps) per SM when the sweep's live state (dx, gx: RC x DP each,
+// gy chain: DP doubles) is small, else 2.
+__global__ void __launch_bounds__(128, ((R / FR) * DP * 2 + DP <= 48) ? 3 : 2)
 bwd_kernel(Problem pb, BwdArgs ba) {
   constexpr int RC = R / FR;
   using SM = BwdSmem<DP, R, RC, F, CB>;

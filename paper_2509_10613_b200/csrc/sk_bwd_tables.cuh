@@ -46,7 +46,10 @@ inline BwdFn sk_bwd_select(const BwdShape& s, int& smem_doubles) {
   switch (s.DP) {
     case 4: sk_bwd_table<KIND, 4, 8>(s, fn, smem_doubles); break;
     case 8: sk_bwd_table<KIND, 8, 4>(s, fn, smem_doubles); break;
-    case 16: sk_bwd_table<KIND, 16, 2>(s, fn, smem_doubles); break;
+    case 16:
+      if (s.R == 1) sk_bwd_table<KIND, 16, 1>(s, fn, smem_doubles);
+      else sk_bwd_table<KIND, 16, 2>(s, fn, smem_doubles);
+      break;
     case 32: sk_bwd_table<KIND, 32, 1>(s, fn, smem_doubles); break;
     default: break;
   }

@@ -460,7 +460,7 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   s.kind = kind;
   s.DP = pick_dp(d, nch);
   if (nch > 1) return fail(SK_INVALID_ARGUMENT, "backward supports d <= 32");
-  s.R = rows_per_lane(s.DP);
+  s.R = bwd_rows_per_lane(s.DP);
   s.FR = std::min(1 << std::min(lamR, 3), s.R);
   s.F = std::min(1 << std::min(lamC, 2), 4);
   int smd = 0;

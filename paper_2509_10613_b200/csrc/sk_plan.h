@@ -1,5 +1,7 @@
 // sk_plan.h -- host-side kernel selection (template instance tables).
 #pragma once
+#include <cstdlib>
+
 #include "sk_common.cuh"
 
 namespace sk {
@@ -40,6 +42,14 @@ inline int rows_per_lane(int DP) {
     case 16: return 2;
     default: return 1;
   }
+}
+
+// Backward: the reverse sweep keeps dx, gx (RC x DP each) and the gy chain
+// (DP) live, so wide paths trade rows per lane for occupancy.
+inline int bwd_rows_per_lane(int DP) {
+  if (DP != 16) return rows_per_lane(DP);
+  const char* e = std::getenv("SK_BWD_R16");  // tuning override (1 or 2)
+  return (e && e[0] == '2') ? 2 : 1;
 }
 
 }  // namespace sk
