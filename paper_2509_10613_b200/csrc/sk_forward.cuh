@@ -163,6 +163,79 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
                                               lane);
       }
 
+      // coefficients of the S columns of step js (reads the ring; no recurrence)
+      auto col_coefs = [&](int col, Coef (&cfo)[RC]) {
+        {
+          const double* rec = ring + (col & (SLOTS - 1)) * REC;
+          double p[RC];
+          if constexpr (KIND == LINEAR) {
+            double dy[DP];
+#pragma unroll
+            for (int k = 0; k < DP; k += 2) {
+              const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+              dy[k] = t2.x;
+              dy[k + 1] = t2.y;
+            }
+#pragma unroll
+            for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy);
+            if (DP == 32 && pb.nch > 1 && col >= 0 && col < NC) {  // d > 32: further chunks
+              const int jc = (col * F) >> pb.lam2;
+              for (int ch = 1; ch < pb.nch; ++ch) {
+                double dyc[DP], xc[DP];
+                load_vec<DP>(dyc, pb.C.p + pc * pb.C.path_stride + (int64_t)jc * pb.dpad + ch * DP);
+#pragma unroll
+                for (int c = 0; c < RC; ++c) {
+                  const int i = i0 + c;
+                  if (i < pb.M1c) {
+                    load_vec<DP>(xc, pb.R.p + pr * pb.R.path_stride + (int64_t)i * pb.dpad + ch * DP);
+                    p[c] += dot<DP>(xc, dyc);
+                  }
+                }
+              }
+            }
+            if (pb.pscale != 1.0) {
+#pragma unroll
+              for (int c = 0; c < RC; ++c) p[c] *= pb.pscale;
+            }
+          } else if constexpr (KIND == RBF) {
+            const int jc = (col * F) >> pb.lam2;
+            if (col >= 0 && col < NC && jc != jcur) {
+              double yv[DP];
+#pragma unroll
+              for (int k = 0; k < DP; k += 2) {
+                const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+                yv[k] = t2.x;
+                yv[k + 1] = t2.y;
+              }
+#pragma unroll
+              for (int c = 0; c <= RC; ++c) {
+                Kl[c] = Kr[c];
+                Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
+              }
+              jcur = jc;
+            }
+#pragma unroll
+            for (int c = 0; c < RC; ++c) p[c] = ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale;
+          } else {  // DELTA: per-row coarse values straight from global
+            const int jc = (col * F) >> pb.lam2;
+#pragma unroll
+            for (int c = 0; c < RC; ++c) {
+              const int i = i0 + c;
+              p[c] = (i < pb.M1c && col >= 0 && col < NC)
+                         ? __ldg(pb.delta + pidx * (int64_t)pb.M1c * pb.M2c + (int64_t)i * pb.M2c +
+                                 jc) * pb.scale
+                         : 0.0;
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < RC; ++c) cfo[c] = coef(p[c]);
+        }
+      };
+      auto step_coefs = [&](int js, Coef (&cfo)[S][RC]) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) col_coefs(js * S + s, cfo[s]);
+      };
+
       double kl[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) kl[r] = 1.0;
@@ -170,17 +243,30 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
       double bot[SF];
 #pragma unroll
       for (int q = 0; q < SF; ++q) bot[q] = 1.0;
+      // wide paths (DP >= 16) pipeline the next step's coefficients behind the
+      // recurrence; narrow ones keep the registers for S columns per step
+      constexpr bool PIPE = DP >= 16;
+      Coef cf[S][RC];
+      if constexpr (PIPE) {
+        if (issuer) cp_async_wait<PF - 1>();  // step 0 landed
+        if (XW) __syncthreads(); else __syncwarp();
+        step_coefs(-u, cf);
+      }
 
       const int nsteps = NSTEP + Grt - 1;
       for (int tau = 0; tau < nsteps; ++tau) {
         if (issuer) {
           fwd_issue<KIND, DP, F, P, S, SLOTS>(ring, pb, pc, hrow0, hand_stride, (tau + PF) * S, NC,
                                               strip, lane);
-          cp_async_wait<PF>();  // this step's records landed
+          if constexpr (PIPE) cp_async_wait<PF - 1>();  // steps <= tau + 1 landed
+          else cp_async_wait<PF>();                     // step tau landed
         }
         if (XW) __syncthreads(); else __syncwarp();
         const int js = tau - u;
         const bool active = (js >= 0) && (js < NSTEP);
+        // software pipeline: next step's coefficients overlap this step's recurrence
+        Coef cfn[PIPE ? S : 1][RC];
+        if constexpr (PIPE) step_coefs(js + 1, cfn);
 
         double tv[SF];
         if constexpr (XW) {
@@ -207,81 +293,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
 #pragma unroll
           for (int s = 0; s < S; ++s) {
             const int col = col0 + s;
-            const double* rec = ring + (col & (SLOTS - 1)) * REC;
-            double p[RC];
-            if constexpr (KIND == LINEAR) {
-              double dy[DP];
-#pragma unroll
-              for (int k = 0; k < DP; k += 2) {
-                const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-                dy[k] = t2.x;
-                dy[k + 1] = t2.y;
-              }
-              if (DP < 32 || pb.nch == 1) {  // d > 32 only ever selects DP = 32
-#pragma unroll
-                for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy);
-              } else {
-#pragma unroll
-                for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy);
-                const int jc = (col * F) >> pb.lam2;
-                for (int ch = 1; ch < pb.nch; ++ch) {
-                  double dyc[DP], xc[DP];
-                  if (col < NC) {
-                    load_vec<DP>(dyc, pb.C.p + pc * pb.C.path_stride + (int64_t)jc * pb.dpad +
-                                          ch * DP);
-                  } else {
-#pragma unroll
-                    for (int k = 0; k < DP; ++k) dyc[k] = 0.0;
-                  }
-#pragma unroll
-                  for (int c = 0; c < RC; ++c) {
-                    const int i = i0 + c;
-                    if (i < pb.M1c) {
-                      load_vec<DP>(xc, pb.R.p + pr * pb.R.path_stride + (int64_t)i * pb.dpad +
-                                           ch * DP);
-                      p[c] += dot<DP>(xc, dyc);
-                    }
-                  }
-                }
-              }
-              if (pb.pscale != 1.0) {
-#pragma unroll
-                for (int c = 0; c < RC; ++c) p[c] *= pb.pscale;
-              }
-            } else if constexpr (KIND == RBF) {
-              const int jc = (col * F) >> pb.lam2;
-              if (col < NC && jc != jcur) {
-                double yv[DP];
-#pragma unroll
-                for (int k = 0; k < DP; k += 2) {
-                  const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-                  yv[k] = t2.x;
-                  yv[k + 1] = t2.y;
-                }
-#pragma unroll
-                for (int c = 0; c <= RC; ++c) {
-                  Kl[c] = Kr[c];
-                  Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
-                }
-                jcur = jc;
-              }
-#pragma unroll
-              for (int c = 0; c < RC; ++c)
-                p[c] = ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale;
-            } else {  // DELTA: per-row coarse values straight from global
-              const int jc = (col * F) >> pb.lam2;
-#pragma unroll
-              for (int c = 0; c < RC; ++c) {
-                const int i = i0 + c;
-                p[c] = (i < pb.M1c && col < NC)
-                           ? __ldg(pb.delta + pidx * (int64_t)pb.M1c * pb.M2c +
-                                   (int64_t)i * pb.M2c + jc) * pb.scale
-                           : 0.0;
-              }
-            }
-            Coef cf[RC];
-#pragma unroll
-            for (int c = 0; c < RC; ++c) cf[c] = coef(p[c]);
+            if constexpr (!PIPE) col_coefs(col, cf[s]);
 #pragma unroll
             for (int f = 0; f < F; ++f) {
               const int q = s * F + f;
@@ -289,7 +301,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
               double dg = (q == 0) ? topc : tv[q - 1];
 #pragma unroll
               for (int r = 0; r < R; ++r) {
-                const double nk = cell(up, kl[r], dg, cf[r / FR]);
+                const double nk = cell(up, kl[r], dg, cf[s][r / FR]);
                 dg = kl[r];
                 kl[r] = nk;
                 up = nk;
@@ -312,6 +324,12 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
               }
             }
           }
+        }
+        if constexpr (PIPE) {
+#pragma unroll
+          for (int s = 0; s < S; ++s)
+#pragma unroll
+            for (int c = 0; c < RC; ++c) cf[s][c] = cfn[s][(PIPE ? c : 0)];
         }
         if constexpr (XW) {
           if (lane == 31) {
