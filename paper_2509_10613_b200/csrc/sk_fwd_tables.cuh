@@ -16,7 +16,7 @@ inline void sk_fwd_leaf(const FwdShape& s, FwdFn& fn, int& smem) {
   }
   if (s.G == 4) {
     // columns per step: amortise per-step overhead without crowding registers
-    constexpr int S4 = DP >= 16 ? 2 : 4;
+    constexpr int S4 = DP >= 16 ? 1 : 4;
     fn = fwd_kernel<KIND, DP, R, FR, F, 4, false, S4>;
     smem = fwd_smem_bytes<KIND, DP, F, 4, false, S4>(4);
   } else if (s.G == 32) {
