@@ -186,10 +186,51 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       double bot[F];
 #pragma unroll
       for (int f = 0; f < F; ++f) bot[f] = 1.0;
+      // coefficients of column jj (reads the ring; independent of the recurrence)
+      auto colcoef = [&](int jj, Coef (&cfo)[RC]) {
+        const double* rec = SK_REC(jj);
+        double p[RC];
+        if constexpr (KIND == LINEAR) {
+          double dy[DP];
+#pragma unroll
+          for (int k = 0; k < DP; k += 2) {
+            const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+            dy[k] = t2.x;
+            dy[k + 1] = t2.y;
+          }
+#pragma unroll
+          for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy) * pb.pscale;
+        } else {
+          const int jc = (jj * F) >> pb.lam2;
+          if (jj >= 0 && jj < NS && jc != jcur) {
+            double yv[DP];
+#pragma unroll
+            for (int k = 0; k < DP; k += 2) {
+              const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+              yv[k] = t2.x;
+              yv[k + 1] = t2.y;
+            }
+#pragma unroll
+            for (int c = 0; c <= RC; ++c) {
+              Kl[c] = Kr[c];
+              Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
+            }
+            jcur = jc;
+          }
+#pragma unroll
+          for (int c = 0; c < RC; ++c) p[c] = ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale;
+        }
+#pragma unroll
+        for (int c = 0; c < RC; ++c) cfo[c] = coef(p[c]);
+      };
+      Coef cf[RC];
+      cp_async_wait<PF - 1>();  // column 0 landed
+      __syncwarp();
+      colcoef(-u, cf);
       for (int tau = 0; tau < NT; ++tau) {
         issue_one(tau + PF, hrow, strip > 0);
         cp_async_commit();
-        cp_async_wait<PF>();
+        cp_async_wait<PF - 1>();  // columns <= tau + 1 landed
         __syncwarp();
         if (tau % CB == 0) {
           // column checkpoint: values at node column (tau - u) * F
@@ -202,47 +243,14 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         double tv[F];
 #pragma unroll
         for (int f = 0; f < F; ++f) tv[f] = __shfl_up_sync(0xffffffffu, bot[f], 1);
+        Coef cfn[RC];
+        colcoef(jj + 1, cfn);  // software pipeline: next column's coefficients
         if (active) {
           const double* rec = SK_REC(jj);
           if (u == 0) {
 #pragma unroll
             for (int f = 0; f < F; ++f) tv[f] = (strip == 0) ? 1.0 : rec[DP + f];
           }
-          double p[RC];
-          if constexpr (KIND == LINEAR) {
-            double dy[DP];
-#pragma unroll
-            for (int k = 0; k < DP; k += 2) {
-              const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-              dy[k] = t2.x;
-              dy[k + 1] = t2.y;
-            }
-#pragma unroll
-            for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy) * pb.pscale;
-          } else {
-            const int jc = (jj * F) >> pb.lam2;
-            if (jc != jcur) {
-              double yv[DP];
-#pragma unroll
-              for (int k = 0; k < DP; k += 2) {
-                const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-                yv[k] = t2.x;
-                yv[k + 1] = t2.y;
-              }
-#pragma unroll
-              for (int c = 0; c <= RC; ++c) {
-                Kl[c] = Kr[c];
-                Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
-              }
-              jcur = jc;
-            }
-#pragma unroll
-            for (int c = 0; c < RC; ++c)
-              p[c] = ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale;
-          }
-          Coef cf[RC];
-#pragma unroll
-          for (int c = 0; c < RC; ++c) cf[c] = coef(p[c]);
 #pragma unroll
           for (int f = 0; f < F; ++f) {
             double up = tv[f];
@@ -268,6 +276,8 @@ bwd_kernel(Problem pb, BwdArgs ba) {
               if (r == r_star) kval = kl[r];
           }
         }
+#pragma unroll
+        for (int c = 0; c < RC; ++c) cf[c] = cfn[c];
       }
       cp_async_wait<0>();
       __syncwarp();
