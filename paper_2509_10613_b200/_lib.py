@@ -13,7 +13,7 @@ import os
 from .errors import InvalidArgument, InvalidState, NativeUnavailable
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "_native", "libsigkernel.so")
+SO_PATH = os.environ.get("SK_LIBSIGKERNEL") or os.path.join(HERE, "_native", "libsigkernel.so")
 
 SK_OK, SK_INVALID_ARGUMENT, SK_INVALID_STATE, SK_CUDA_ERROR = 0, 1, 2, 3
 STATIC_LINEAR, STATIC_RBF = 0, 1

@@ -36,6 +36,12 @@ namespace sk {
 
 enum MapMode : int { FUSED = 0, DBUF = 1 };
 
+// Profiling experiments only (default 0): 1 skips the gradient map, 2 the
+// reverse sweep, 4 the block recompute.  Results are wrong when set.
+#ifndef SK_EXP
+#define SK_EXP 0
+#endif
+
 __device__ __forceinline__ void grad_add(double* p, double v, bool atomic) {
   if (atomic) atomicAdd(p, v);
   else *p += v;
@@ -395,7 +401,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         };
 
         // ---- recompute the block's forward values into shared memory
-        {
+        if (!(SK_EXP & 4)) {
           double kl[R];
 #pragma unroll
           for (int r = 0; r < R; ++r) kl[r] = sLS[r * 32 + lane];
@@ -481,7 +487,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
 
         // ---- reverse sweep over the block, one column per kap
 #pragma unroll
-        for (int kap = CB - 1; kap >= 0; --kap) {
+        for (int kap = CB - 1; kap >= 0 && !(SK_EXP & 2); --kap) {
           const int jj = jj0 + kap;
           const bool colv = (jj >= 0) && (jj < NS);
           const double* rec = SK_REC(jj);
@@ -540,7 +546,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           const int jc = colv ? ((jj * F) >> pb.lam2) : 0;
 #pragma unroll
           for (int c = 0; c < RC; ++c) Dp[c] *= pb.scale;
-          if constexpr (MAP == FUSED) {
+          if constexpr (MAP == FUSED && !(SK_EXP & 1)) {
             // gx_i += D_ij dy_j (row-local);  gy_j += D_ij dx_i (down the warp)
             // lane 31 starts the chain with the column gradient accumulated by
             // the strips below, once per coarse column
