@@ -10,23 +10,26 @@
 //
 // B200 mapping:
 //   * one warp per pair, lane u owns R fine rows of a 32R-row strip;
-//   * phase A: the forward wavefront (as sk_forward.cuh), which additionally
-//     saves every lane's bottom row (row checkpoint, coalesced "diagonal"
-//     layout [strip][col + lane][f][lane]) and every lane's R values at
-//     staggered block boundaries (column checkpoint, [strip][blk][r][lane]);
+//   * phase A: the forward wavefront (as sk_forward.cuh, coefficients
+//     software-pipelined one column ahead), which additionally saves every
+//     lane's bottom row (row checkpoint, coalesced "diagonal" layout
+//     [strip][column + lane][f][lane]) and every lane's R values at staggered
+//     block boundaries (column checkpoint, [strip][blk][r][lane]);
 //   * phase B: strips bottom-up; per block of CB columns every lane recomputes
 //     its R x CB*F forward values from its own checkpoints into shared memory
 //     (no inter-lane dependency, so all lanes do it at the same time), then
 //     sweeps the block right-to-left one column behind lane u+1, receiving lane
 //     u+1's top-row messages by __shfl_down_sync;
 //   * column data (dy_j / RBF nodes), the adjoint handoff row from the strip
-//     below and the checkpoints of the next block stream into shared memory by
-//     cp.async one block ahead, so no global latency sits on the sweep;
+//     below and the next block's checkpoints stream into shared memory by
+//     cp.async while the current block is swept;
 //   * the coarse adjoint dF/d(delta) is mapped to path space on the fly
-//     (FUSED: gx = D dy in registers, gy = D^T dx accumulated down the warp as
-//     a shuffle chain and handed from strip to strip through a per-pair column
-//     buffer) or through a per-pair coarse buffer (DBUF: RBF), then telescoped
-//     to point gradients (kernel_grad.py:51-60).
+//     (FUSED): gx_i += D_ij dy_j stays in the lane's registers; gy_j += D_ij dx_i
+//     is accumulated in a per-warp shared-memory row per coarse column (lanes
+//     touch a row one step apart, in a fixed order, so no shuffles and no
+//     atomics), seeded by the strips below and finished by lane 0; RBF uses a
+//     per-pair coarse buffer (DBUF).  Increment gradients are telescoped to
+//     point gradients once per pair (kernel_grad.py:51-60).
 //   * nothing proportional to the fine grid is stored per pair beyond the
 //     checkpoints (1/R + 1/(CB*F) of the grid).
 #pragma once
@@ -50,24 +53,23 @@ __device__ __forceinline__ void grad_add(double* p, double v, bool atomic) {
 // Per-warp shared-memory layout (doubles).
 template <int DP, int R, int RC, int F, int CB>
 struct BwdSmem {
-  static constexpr int SLOTS = 64;                   // column ring (>= 2*CB + 31)
+  static constexpr int SLOTS = 48;                   // column ring (>= 2*CB + 31)
   static constexpr int REC = ((DP + F) + 1) & ~1;    // column data | handoff/adjoint (F)
   static constexpr int NK = CB * F * R;              // recomputed k values (x32 lanes)
   static constexpr int NP = CB * RC;                 // coarse p (then D) values (x32 lanes)
-  static constexpr int TS = (CB + 1) * F * 32;       // top-row checkpoints of the block
+  static constexpr int NTR = CB * F + 1;             // top row of the block (x32 lanes)
+  static constexpr int TS = (CB + 1) * F * 32;       // top-row checkpoints of the next block
   static constexpr int T0 = ((CB * F + 1) + 1) & ~1; // lane 0's top row (strip above)
   static constexpr int LS = R * 32;                  // left-column checkpoint
-  static constexpr int GS = CB * DP;                 // lane 31's incoming column gradients
-  static constexpr int STG = TS + T0 + LS + GS;
-  static constexpr int NTR = CB * F + 1;            // top row of the block (x32 lanes)
-  static constexpr int GA = DP;                      // lane 0's coarse-column gradient sums
-  static constexpr int TOTAL = SLOTS * REC + (NK + NP + NTR) * 32 + 2 * STG + GA;
+  static constexpr int GS = CB * DP;                 // lane 31's incoming column gradients (x2)
+  static constexpr int GROWS = 40;                   // gy accumulator rows (>= CB + 32)
+  static constexpr int GSTR = DP + 2;                // row stride: conflict-free 16-B accesses
+  static constexpr int TOTAL =
+      SLOTS * REC + (NK + NP + NTR) * 32 + TS + T0 + LS + 2 * GS + GROWS * GSTR + 2 * DP;
 };
 
 template <int KIND, int DP, int R, int FR, int F, int CB, int MAP>
-// 3 CTAs (12 warps) per SM when the sweep's live state (dx, gx: RC x DP each,
-// gy chain: DP doubles) is small, else 2.
-__global__ void __launch_bounds__(128, ((R / FR) * DP * 2 + DP <= 48) ? 3 : 2)
+__global__ void __launch_bounds__(128, 2)
 bwd_kernel(Problem pb, BwdArgs ba) {
   constexpr int RC = R / FR;
   using SM = BwdSmem<DP, R, RC, F, CB>;
@@ -82,12 +84,19 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   double* sK = ring + SLOTS * REC;
   double* sP = sK + SM::NK * 32;
   double* sTR = sP + SM::NP * 32;
-  double* stg0 = sTR + SM::NTR * 32;
-  double* sGA = stg0 + 2 * SM::STG;
+  double* sTS = sTR + SM::NTR * 32;
+  double* sT0 = sTS + SM::TS;
+  double* sLS = sT0 + SM::T0;
+  double* sGS0 = sLS + SM::LS;
+  double* sGW = sGS0 + 2 * SM::GS;
+  double* sZero = sGW + SM::GROWS * SM::GSTR;  // DP zeros (lane 31's unseeded rows)
+  double* sGA = sZero + DP;                    // lane 0's coarse-column sums (2^lam2 > F)
+  for (int k = lane; k < DP; k += 32) sZero[k] = 0.0;
+  __syncwarp();
 #define SK_TR(q) sTR[(q) * 32 + lane]
 #define SK_KB(kap, f, r) sK[(((kap) * F + (f)) * R + (r)) * 32 + lane]
 #define SK_PB(kap, c) sP[((kap) * RC + (c)) * 32 + lane]
-#define SK_REC(col) (ring + ((col) & (SLOTS - 1)) * REC)
+#define SK_REC(col) (ring + (((col) + 2 * SLOTS) % SLOTS) * REC)
 
   const int u = lane;
   const int M1 = pb.M1c << pb.lam1;
@@ -128,7 +137,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
     }
     const double* cbase = pb.C.p + pc * pb.C.path_stride;  // this pair's column path
 
-    // issue the ring records of columns [c0, c0 + n) (one warp, no commit)
+    // ring records of columns [c0, c0 + n): column data + F handoff values (no commit)
     auto issue_cols = [&](int c0, int n, const double* hsrc, bool hvalid) {
       constexpr int PER = DP / 2 + F;
       for (int e = lane; e < n * PER; e += 32) {
@@ -146,7 +155,6 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         }
       }
     };
-
     // one column record, one cp.async per lane (lanes < DP/2 + F)
     auto issue_one = [&](int col, const double* hsrc, bool hvalid) {
       const bool cv = (col >= 0) && (col < NS);
@@ -295,7 +303,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
     if constexpr (MAP == DBUF) {
       for (int64_t e = u; e < (int64_t)pb.M1c * pb.M2c; e += 32) dbuf[e] = 0.0;
     } else {
-      for (int64_t e = u; e < (int64_t)(pb.M1c + pb.M2c) * DP; e += 32) gxs[e] = 0.0;
+      for (int64_t e = u; e < (int64_t)pb.M1c * DP; e += 32) gxs[e] = 0.0;
     }
     __syncwarp();
     double* __restrict__ gR = ba.gradR + pr * ba.gR_path;
@@ -308,48 +316,46 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       RowRegs<KIND, DP, RC> rr;
       load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
 
-      // staging of block blk: top-row checkpoints, lane 0's top row, left
-      // checkpoint, lane 31's incoming column gradients
-      auto issue_stage = [&](int blk) {
-        double* st = stg0 + (blk & 1) * SM::STG;
-        // TS: rowck[strip][d][f][*] for d in [blk*CB - 2, blk*CB + CB - 2]
+      // records + staging of block blk: top-row checkpoints, lane 0's top row,
+      // left checkpoint (single buffers, consumed by the recompute) and lane
+      // 31's incoming column gradients (double buffered, used by the sweep)
+      auto issue_block = [&](int blk, bool first) {
+        if (first) issue_cols(blk * CB - 31, CB + 31, arow, true);
+        else issue_cols(blk * CB - 31, CB, arow, true);  // the new columns only
         {
-          const int dlo = blk * CB - 2;
+          const int dlo = blk * CB - 2;  // rowck[strip][d][f][*], d in [blk*CB-2, blk*CB+CB-2]
           constexpr int NCH = SM::TS / 2;
           for (int e = lane; e < NCH; e += 32) {
             const int row = e / (F * 16);  // (CB+1) rows of F*32 doubles
             const int d = dlo + row;
             const bool v = (d >= 0) && (d < NT);
-            cp_async16(st + 2 * e,
+            cp_async16(sTS + 2 * e,
                        rowck + (((int64_t)strip * NT + (v ? d : 0)) * F) * 32 + 2 * (e % (F * 16)),
                        v);
           }
         }
-        // T0: lane 0's top row: nodes t = blk*CB*F + q, q = 0..CB*F, written by
-        // strip-1's lane 31 at diagonal (t-1)/F + 31
         if (strip > 0) {
+          // lane 0's top row: nodes t = blk*CB*F + q, written by strip-1's lane 31
           for (int q = lane; q <= CB * F; q += 32) {
             const int t = blk * CB * F + q;
             const bool v = (t >= 1) && (t <= M2);
             const int js = v ? (t - 1) / F : 0, fs = v ? (t - 1) % F : 0;
-            cp_async8(st + SM::TS + q, &SK_ROWCK(strip - 1, js + 31, fs, 31), v);
+            cp_async8(sT0 + q, &SK_ROWCK(strip - 1, js + 31, fs, 31), v);
           }
         }
-        // LS: colck[strip][blk][r][*]
         for (int e = lane; e < SM::LS / 2; e += 32)
-          cp_async16(st + SM::TS + SM::T0 + 2 * e,
-                     colck + (((int64_t)strip * NB + blk) * R) * 32 + 2 * e, true);
-        // GS: gcs[jc(col)] for lane 31's columns col = blk*CB - 31 + kap
+          cp_async16(sLS + 2 * e, colck + (((int64_t)strip * NB + blk) * R) * 32 + 2 * e, true);
         if constexpr (MAP == FUSED) {
+          double* gs = sGS0 + (blk & 1) * SM::GS;
           for (int e = lane; e < CB * (DP / 2); e += 32) {
             const int kap = e / (DP / 2), w = e % (DP / 2);
-            const int col = blk * CB - 31 + kap;
+            const int col = blk * CB - 31 + kap;  // lane 31's columns
             const bool v = (col >= 0) && (col < NS) && (strip < nstrips - 1);
             const int jc = v ? ((col * F) >> pb.lam2) : 0;
-            cp_async16(st + SM::TS + SM::T0 + SM::LS + kap * DP + 2 * w, gcs + (int64_t)jc * DP + 2 * w,
-                       v);
+            cp_async16(gs + kap * DP + 2 * w, gcs + (int64_t)jc * DP + 2 * w, v);
           }
         }
+        cp_async_commit();
       };
 
       double aR[R], bR[R];
@@ -359,52 +365,45 @@ bwd_kernel(Problem pb, BwdArgs ba) {
 #pragma unroll
       for (int f = 0; f < F; ++f) sendm[f] = 0.0;
       double gxr[(MAP == FUSED) ? RC : 1][DP];
-      double gys[DP];
-      for (int k = lane; k < DP; k += 32) sGA[k] = 0.0;  // lane 0's coarse-column sums
 #pragma unroll
-      for (int k = 0; k < DP; ++k) {
-        gys[k] = 0.0;
+      for (int k = 0; k < DP; ++k)
 #pragma unroll
         for (int c = 0; c < ((MAP == FUSED) ? RC : 1); ++c) gxr[c][k] = 0.0;
-      }
       double Kl[RC + 1], Kr[RC + 1];  // RBF recompute state
       int jcur = -1000;
 
-      // prologue: records of the first block's columns + its staging
-      issue_cols((NB - 1) * CB - 31, CB + 31, arow, true);
-      issue_stage(NB - 1);
-      cp_async_commit();
-
+      issue_block(NB - 1, true);
       for (int blk = NB - 1; blk >= 0; --blk) {
-        if (blk > 0) {
-          issue_cols((blk - 1) * CB - 31, CB, arow, true);
-          issue_stage(blk - 1);
-        }
-        cp_async_commit();
-        cp_async_wait<1>();
+        cp_async_wait<0>();
         __syncwarp();
-        const double* st = stg0 + (blk & 1) * SM::STG;
-        const double* sTS = st;
-        const double* sT0 = st + SM::TS;
-        const double* sLS = st + SM::TS + SM::T0;
-        const double* sGS = st + SM::TS + SM::T0 + SM::LS;
+        const double* sGS = sGS0 + (blk & 1) * SM::GS;
         const int jj0 = blk * CB - u;  // lane's first column in this block
-        // top-row value at node t = jj0*F + q (q = 0..CB*F) of this lane's rows
-        auto topv = [&](int q) -> double {
-          const int t = jj0 * F + q;
-          if (t <= 0 || (strip == 0 && u == 0)) return 1.0;
-          if (t > M2) return 0.0;  // dead columns: keep values finite
-          if (u == 0) return sT0[q];
-          // writer lane u-1 at diagonal (t-1)/F + u - 1 = blk*CB - 2 + (q-1+F)/F ...
-          const int d = (t - 1) / F + u - 1 - (blk * CB - 2);
-          return sTS[(d * F + (t - 1) % F) * 32 + (u - 1)];
-        };
+        double kleft[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) kleft[r] = sLS[r * 32 + lane];
 
         // ---- recompute the block's forward values into shared memory
         if (!(SK_EXP & 4)) {
+          // top row at node t = jj0*F + q (q = 0..CB*F) of this lane's rows
+#pragma unroll
+          for (int q = 0; q <= CB * F; ++q) {
+            const int t = jj0 * F + q;
+            double v;
+            if (t <= 0 || (strip == 0 && u == 0)) {
+              v = 1.0;
+            } else if (t > M2) {
+              v = 0.0;  // dead columns: keep values finite
+            } else if (u == 0) {
+              v = sT0[q];
+            } else {
+              const int d = (t - 1) / F + u - 1 - (blk * CB - 2);
+              v = sTS[(d * F + (t - 1) % F) * 32 + (u - 1)];
+            }
+            SK_TR(q) = v;
+          }
           double kl[R];
 #pragma unroll
-          for (int r = 0; r < R; ++r) kl[r] = sLS[r * 32 + lane];
+          for (int r = 0; r < R; ++r) kl[r] = kleft[r];
           if constexpr (KIND == RBF) {
             // K at node columns jc(jj0), jc(jj0)+1 for the first column of the block
             const int col0 = jj0 < 0 ? 0 : (jj0 >= NS ? NS - 1 : jj0);
@@ -418,8 +417,6 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             for (int c = 0; c <= RC; ++c) Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
             jcur = jc0;
           }
-#pragma unroll
-          for (int q = 0; q <= CB * F; ++q) SK_TR(q) = topv(q);
           double topc = SK_TR(0);
 #pragma unroll
           for (int kap = 0; kap < CB; ++kap) {
@@ -436,7 +433,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
                 dy[k + 1] = t2.y;
               }
 #pragma unroll
-              for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy) * pb.pscale;
+              for (int c = 0; c < RC; ++c) p[c] = colv ? dot<DP>(rr.v[c], dy) * pb.pscale : 0.0;
             } else {
               const int jc = (jj * F) >> pb.lam2;
               if (colv && jc != jcur) {
@@ -457,10 +454,6 @@ bwd_kernel(Problem pb, BwdArgs ba) {
 #pragma unroll
               for (int c = 0; c < RC; ++c)
                 p[c] = colv ? ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale : 0.0;
-            }
-            if (!colv) {
-#pragma unroll
-              for (int c = 0; c < RC; ++c) p[c] = 0.0;
             }
             Coef cf[RC];
 #pragma unroll
@@ -484,6 +477,9 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             topc = SK_TR(kap * F + F);
           }
         }
+        __syncwarp();
+        // staging buffers are free again: prefetch the next block under the sweep
+        if (blk > 0) issue_block(blk - 1, false);
 
         // ---- reverse sweep over the block, one column per kap
 #pragma unroll
@@ -524,11 +520,11 @@ bwd_kernel(Problem pb, BwdArgs ba) {
               const double b = cf[c].B * lam;
               // forward values around the cell (s,t): left, up, up-left
               const double kL = (f > 0) ? SK_KB(kap, f - 1, r)
-                                        : (kap > 0 ? SK_KB(kap - 1, F - 1, r) : sLS[r * 32 + lane]);
+                                        : (kap > 0 ? SK_KB(kap - 1, F - 1, r) : kleft[r]);
               const double kU = (r > 0) ? SK_KB(kap, f, r - 1) : SK_TR(kap * F + f + 1);
               const double kD = (r > 0) ? ((f > 0) ? SK_KB(kap, f - 1, r - 1)
                                                    : (kap > 0 ? SK_KB(kap - 1, F - 1, r - 1)
-                                                              : sLS[(r - 1) * 32 + lane]))
+                                                              : kleft[r - 1]))
                                         : SK_TR(kap * F + f);
               const double p6 = pk[c] * (1.0 / 6.0);
               const double wv = fma(kL + kU, 0.5 + p6, kD * p6);
@@ -547,37 +543,52 @@ bwd_kernel(Problem pb, BwdArgs ba) {
 #pragma unroll
           for (int c = 0; c < RC; ++c) Dp[c] *= pb.scale;
           if constexpr (MAP == FUSED && !(SK_EXP & 1)) {
-            // gx_i += D_ij dy_j (row-local);  gy_j += D_ij dx_i (down the warp)
-            // lane 31 starts the chain with the column gradient accumulated by
-            // the strips below, once per coarse column
-            const bool in31 = colv && (((jj + 1) & K2m) == 0);
+            // gx_i += D_ij dy_j (row-local registers)
 #pragma unroll
-            for (int k = 0; k < DP; ++k) {
-              double g = __shfl_down_sync(0xffffffffu, gys[k], 1);
-              if (u == 31) g = in31 ? sGS[kap * DP + k] : 0.0;
-              const double dyk = rec[k];
+            for (int k = 0; k < DP; k += 2) {
+              const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
 #pragma unroll
               for (int c = 0; c < RC; ++c) {
-                gxr[c][k] = fma(Dp[c], dyk, gxr[c][k]);
-                g = fma(Dp[c], rr.v[c][k], g);
+                gxr[c][k] = fma(Dp[c], t2.x, gxr[c][k]);
+                gxr[c][k + 1] = fma(Dp[c], t2.y, gxr[c][k + 1]);
               }
-              gys[k] = g;
             }
-            if (u == 0 && colv) {
-              // lane 0 holds the column sum over this strip and all strips below
+            // gy_j += D_ij dx_i into the column's shared row.  Lanes touch a row one
+            // step apart (u+1 before u, fixed order); lane 31 starts it (seeded by
+            // the strips below at the coarse column's first column), lane 0
+            // finishes it and emits the coarse column's sum.
+            if (colv) {
+              double* row = sGW + (jj % SM::GROWS) * SM::GSTR;
+              const bool seed = ((jj + 1) & K2m) == 0;
+              const double* src = (u == 31) ? (seed ? (sGS + kap * DP) : sZero) : row;
 #pragma unroll
-              for (int k = 0; k < DP; ++k) sGA[k] += gys[k];
-              if ((jj & K2m) == 0) {  // last column of the coarse column (reverse order)
+              for (int k = 0; k < DP; k += 2) {
+                double2 v = *reinterpret_cast<const double2*>(src + k);
+#pragma unroll
+                for (int c = 0; c < RC; ++c) {
+                  v.x = fma(Dp[c], rr.v[c][k], v.x);
+                  v.y = fma(Dp[c], rr.v[c][k + 1], v.y);
+                }
+                *reinterpret_cast<double2*>(row + k) = v;
+              }
+              if (u == 0) {
                 double2* q = reinterpret_cast<double2*>(gcs + (int64_t)jc * DP);
+                if (K2m == 0) {  // one column per coarse column
 #pragma unroll
-                for (int k = 0; k < DP / 2; ++k) {
-                  q[k] = make_double2(sGA[2 * k], sGA[2 * k + 1]);
-                  sGA[2 * k] = 0.0;
-                  sGA[2 * k + 1] = 0.0;
+                  for (int k = 0; k < DP; k += 2) q[k / 2] = *reinterpret_cast<const double2*>(row + k);
+                } else {  // several: lane 0 sums them (reverse order), emits at the last
+                  const bool last = (jj & K2m) == 0;
+#pragma unroll
+                  for (int k = 0; k < DP; ++k) {
+                    const double a = (seed ? 0.0 : sGA[k]) + row[k];
+                    sGA[k] = a;
+                    if (last) gcs[(int64_t)jc * DP + k] = a;
+                  }
                 }
               }
             }
-          } else {
+            __syncwarp();
+          } else if constexpr (MAP == DBUF) {
             // RBF: coarse adjoint, kept per block in shared memory (p is dead)
 #pragma unroll
             for (int c = 0; c < RC; ++c) SK_PB(kap, c) = colv ? Dp[c] : 0.0;
