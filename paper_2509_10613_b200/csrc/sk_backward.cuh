@@ -53,7 +53,7 @@ __device__ __forceinline__ void grad_add(double* p, double v, bool atomic) {
 // Per-warp shared-memory layout (doubles).
 template <int DP, int R, int RC, int F, int CB>
 struct BwdSmem {
-  static constexpr int SLOTS = 48;                   // column ring (>= 2*CB + 31)
+  static constexpr int SLOTS = DP >= 16 ? 48 : 64;   // column ring (>= 2*CB + 31)
   static constexpr int REC = ((DP + F) + 1) & ~1;    // column data | handoff/adjoint (F)
   static constexpr int NK = CB * F * R;              // recomputed k values (x32 lanes)
   static constexpr int NP = CB * RC;                 // coarse p (then D) values (x32 lanes)
@@ -96,7 +96,8 @@ bwd_kernel(Problem pb, BwdArgs ba) {
 #define SK_TR(q) sTR[(q) * 32 + lane]
 #define SK_KB(kap, f, r) sK[(((kap) * F + (f)) * R + (r)) * 32 + lane]
 #define SK_PB(kap, c) sP[((kap) * RC + (c)) * 32 + lane]
-#define SK_REC(col) (ring + (((col) + 2 * SLOTS) % SLOTS) * REC)
+#define SK_REC(col)                                                                 \
+  (ring + ((SLOTS & (SLOTS - 1)) == 0 ? ((col) & (SLOTS - 1)) : (((col) + 2 * SLOTS) % SLOTS)) * REC)
 
   const int u = lane;
   const int M1 = pb.M1c << pb.lam1;
