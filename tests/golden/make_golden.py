@@ -156,6 +156,16 @@ def main():
         xs.append(x); ys.append(y); oracles.append(sc.dot(sx, sy))
     save("dyadic_convergence", x=np.array(xs), y=np.array(ys), oracle=np.array(oracles))
 
+    # SGT1 files written by the reference's io.write_array (io.py:27-39)
+    rng = np.random.default_rng(12)
+    a3 = rng.standard_normal((2, 5, 3))
+    a2 = rng.standard_normal((4, 2)).astype(np.float32)
+    a1 = np.arange(7, dtype=np.int64)  # integers are widened to float64
+    sc.write_array(a3, os.path.join(OUT, "ref_f64_3d.sgt"))
+    sc.write_array(a2, os.path.join(OUT, "ref_f32_2d.sgt"))
+    sc.write_array(a1, os.path.join(OUT, "ref_int_1d.sgt"))
+    save("sgt_contents", a3=a3, a2=a2, a1=a1)
+
     print("reference:", sc.__file__, "numba", __import__("numba").__version__,
           "numpy", np.__version__, file=sys.stderr)
 
