@@ -9,29 +9,29 @@
 // neighbours and -b = -B*lambda to its upper-left one.
 //
 // B200 mapping:
-//   * one warp per pair, lane u owns R fine rows of a 32R-row strip;
-//   * phase A: the forward wavefront (as sk_forward.cuh, coefficients
-//     software-pipelined one column ahead), which additionally saves every
-//     lane's bottom row (row checkpoint, coalesced "diagonal" layout
-//     [strip][column + lane][f][lane]) and every lane's R values at staggered
-//     block boundaries (column checkpoint, [strip][blk][r][lane]);
-//   * phase B: strips bottom-up; per block of CB columns every lane recomputes
-//     its R x CB*F forward values from its own checkpoints into shared memory
+//   * one warp per pair, lane u owns R fine rows of a 32R-row strip; a "step"
+//     is S columns (S*F fine columns) and lane u runs one step behind lane u-1;
+//   * phase A: the forward wavefront (as sk_forward.cuh), which additionally
+//     saves every lane's bottom row (row checkpoint, coalesced "diagonal"
+//     layout [strip][step + lane][fine column][lane]) and every lane's R values
+//     at staggered block boundaries (column checkpoint, [strip][blk][r][lane]);
+//   * phase B: strips bottom-up; per block of CB steps every lane recomputes
+//     its R x CB*S*F forward values from its own checkpoints into shared memory
 //     (no inter-lane dependency, so all lanes do it at the same time), then
-//     sweeps the block right-to-left one column behind lane u+1, receiving lane
+//     sweeps the block right-to-left one step behind lane u+1, receiving lane
 //     u+1's top-row messages by __shfl_down_sync;
 //   * column data (dy_j / RBF nodes), the adjoint handoff row from the strip
 //     below and the next block's checkpoints stream into shared memory by
 //     cp.async while the current block is swept;
 //   * the coarse adjoint dF/d(delta) is mapped to path space on the fly
 //     (FUSED): gx_i += D_ij dy_j stays in the lane's registers; gy_j += D_ij dx_i
-//     is accumulated in a per-warp shared-memory row per coarse column (lanes
-//     touch a row one step apart, in a fixed order, so no shuffles and no
-//     atomics), seeded by the strips below and finished by lane 0; RBF uses a
-//     per-pair coarse buffer (DBUF).  Increment gradients are telescoped to
-//     point gradients once per pair (kernel_grad.py:51-60).
+//     is accumulated in a per-warp shared-memory row per column (lanes touch a
+//     row one step apart, in a fixed order, so no shuffles and no atomics),
+//     seeded by the strips below and finished by lane 0; RBF uses a per-pair
+//     coarse buffer (DBUF).  Increment gradients are telescoped to point
+//     gradients once per pair (kernel_grad.py:51-60).
 //   * nothing proportional to the fine grid is stored per pair beyond the
-//     checkpoints (1/R + 1/(CB*F) of the grid).
+//     checkpoints (1/R + 1/(CB*S*F) of the grid).
 #pragma once
 #include "sk_forward.cuh"
 
@@ -50,32 +50,40 @@ __device__ __forceinline__ void grad_add(double* p, double v, bool atomic) {
   else *p += v;
 }
 
+constexpr int pow2_at_least(int n) {
+  return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256;
+}
+
 // Per-warp shared-memory layout (doubles).
-template <int DP, int R, int RC, int F, int CB>
+template <int DP, int R, int RC, int F, int CB, int S>
 struct BwdSmem {
-  static constexpr int SLOTS = DP >= 16 ? 48 : 64;   // column ring (>= 2*CB + 31)
+  static constexpr int SF = S * F;
+  // column ring: power of two when cheap, else the exact need (modulo indexing)
+  static constexpr int NEED = (2 * CB + 32) * S;
+  static constexpr int SLOTS = (DP >= 16) ? ((NEED + 15) / 16) * 16 : pow2_at_least(NEED);
   static constexpr int REC = ((DP + F) + 1) & ~1;    // column data | handoff/adjoint (F)
-  static constexpr int NK = CB * F * R;              // recomputed k values (x32 lanes)
-  static constexpr int NP = CB * RC;                 // coarse p (then D) values (x32 lanes)
-  static constexpr int NTR = CB * F + 1;             // top row of the block (x32 lanes)
-  static constexpr int TS = (CB + 1) * F * 32;       // top-row checkpoints of the next block
-  static constexpr int T0 = ((CB * F + 1) + 1) & ~1; // lane 0's top row (strip above)
+  static constexpr int NK = CB * SF * R;             // recomputed k values (x32 lanes)
+  static constexpr int NP = CB * S * RC;             // coarse p (then D) values (x32 lanes)
+  static constexpr int NTR = CB * SF + 1;            // top row of the block (x32 lanes)
+  static constexpr int TS = (CB + 1) * SF * 32;      // top-row checkpoints of the next block
+  static constexpr int T0 = ((CB * SF + 1) + 1) & ~1; // lane 0's top row (strip above)
   static constexpr int LS = R * 32;                  // left-column checkpoint
-  static constexpr int GS = CB * DP;                 // lane 31's incoming column gradients (x2)
-  static constexpr int GROWS = 40;                   // gy accumulator rows (>= CB + 32)
+  static constexpr int GS = CB * S * DP;             // lane 31's incoming column gradients (x2)
+  static constexpr int GROWS = (32 + CB) * S;        // gy accumulator rows (one per column)
   static constexpr int GSTR = DP + 2;                // row stride: conflict-free 16-B accesses
   static constexpr int TOTAL =
       SLOTS * REC + (NK + NP + NTR) * 32 + TS + T0 + LS + 2 * GS + GROWS * GSTR + 2 * DP;
 };
 
-template <int KIND, int DP, int R, int FR, int F, int CB, int MAP>
+template <int KIND, int DP, int R, int FR, int F, int CB, int MAP, int S>
 __global__ void __launch_bounds__(128, 2)
 bwd_kernel(Problem pb, BwdArgs ba) {
   constexpr int RC = R / FR;
-  using SM = BwdSmem<DP, R, RC, F, CB>;
+  constexpr int SF = S * F;
+  using SM = BwdSmem<DP, R, RC, F, CB, S>;
   constexpr int SLOTS = SM::SLOTS;
   constexpr int REC = SM::REC;
-  constexpr int PF = 2;
+  constexpr int PF = 2;  // steps in flight in phase A
   extern __shared__ double smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -94,16 +102,18 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   for (int k = lane; k < DP; k += 32) sZero[k] = 0.0;
   __syncwarp();
 #define SK_TR(q) sTR[(q) * 32 + lane]
-#define SK_KB(kap, f, r) sK[(((kap) * F + (f)) * R + (r)) * 32 + lane]
-#define SK_PB(kap, c) sP[((kap) * RC + (c)) * 32 + lane]
-#define SK_REC(col)                                                                 \
-  (ring + ((SLOTS & (SLOTS - 1)) == 0 ? ((col) & (SLOTS - 1)) : (((col) + 2 * SLOTS) % SLOTS)) * REC)
+#define SK_KB(kap, s, f, r) sK[((((kap) * S + (s)) * F + (f)) * R + (r)) * 32 + lane]
+#define SK_PB(kap, s, c) sP[(((kap) * S + (s)) * RC + (c)) * 32 + lane]
+#define SK_REC(col)                                                                     \
+  (ring + ((SLOTS & (SLOTS - 1)) == 0 ? ((col) & (SLOTS - 1))                              \
+                                      : (((col) + 4 * SLOTS) % SLOTS)) * REC)
 
   const int u = lane;
   const int M1 = pb.M1c << pb.lam1;
   const int M2 = pb.M2c << pb.lam2;
-  const int NS = M2 / F;          // columns per strip row
-  const int NT = NS + 31;         // skewed steps per strip
+  const int NC = M2 / F;                // columns per strip row
+  const int NSTEP = (NC + S - 1) / S;   // steps per strip row
+  const int NT = NSTEP + 31;            // skewed steps per strip
   const int NB = (NT + CB - 1) / CB;
   const int H = 32 * R;
   const int nstrips = (M1 + H - 1) / H;
@@ -112,6 +122,8 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   const int r_star = (M1 - 1) % R;
   const int dR = ba.d;
   const int K2m = (1 << pb.lam2) / F - 1;  // columns per coarse column - 1 (power of 2)
+  // LINEAR rows carry the exact dyadic factor: gx needs it on D, gy does not
+  const double gxs_scale = (KIND == LINEAR) ? pb.scale : 1.0;
 
   const int64_t slot = (int64_t)blockIdx.x * nw + warp;
   double* __restrict__ rowck = ba.rowck + slot * ba.rowck_stride;
@@ -121,7 +133,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   double* __restrict__ dbuf = (MAP == DBUF) ? ba.dbuf + slot * ba.dbuf_stride : nullptr;
   double* __restrict__ gxs = ba.gscr + slot * ba.gscr_stride;  // [M1c][DP]
   double* __restrict__ gcs = gxs + (int64_t)pb.M1c * DP;       // [M2c][DP]
-#define SK_ROWCK(strip, d, f, ln) rowck[(((int64_t)(strip) * NT + (d)) * F + (f)) * 32 + (ln)]
+#define SK_ROWCK(strip, d, q, ln) rowck[(((int64_t)(strip) * NT + (d)) * SF + (q)) * 32 + (ln)]
 
   for (int64_t item = slot; item < pb.nitems; item += (int64_t)gridDim.x * nw) {
     // ---------------------------------------------------------- resolve pair
@@ -144,7 +156,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       for (int e = lane; e < n * PER; e += 32) {
         const int q = e / PER, w = e % PER;
         const int col = c0 + q;
-        const bool cv = (col >= 0) && (col < NS);
+        const bool cv = (col >= 0) && (col < NC);
         double* dst = SK_REC(col);
         if (w < DP / 2) {
           const int jc = cv ? ((col * F) >> pb.lam2) : 0;
@@ -156,18 +168,47 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         }
       }
     };
-    // one column record, one cp.async per lane (lanes < DP/2 + F)
-    auto issue_one = [&](int col, const double* hsrc, bool hvalid) {
-      const bool cv = (col >= 0) && (col < NS);
-      double* dst = SK_REC(col);
-      if (lane < DP / 2) {
-        const int jc = cv ? ((col * F) >> pb.lam2) : 0;
-        const int node = (KIND == RBF) ? jc + 1 : jc;
-        cp_async16(dst + 2 * lane, cbase + (int64_t)node * pb.dpad + 2 * lane, cv);
-      } else if (lane < DP / 2 + F) {
-        const int f = lane - DP / 2;
-        cp_async8(dst + DP + f, hsrc + (cv ? col * F + f + 1 : 0), cv && hvalid);
+
+    // coefficients of column col from its ring record (RBF carries K across columns)
+    double Kl[RC + 1], Kr[RC + 1];
+    int jcur = -1;
+    auto colcoef = [&](const RowRegs<KIND, DP, RC>& rr, int col, Coef (&cfo)[RC]) {
+      const double* rec = SK_REC(col);
+      const bool cv = (col >= 0) && (col < NC);
+      double p[RC];
+      if constexpr (KIND == LINEAR) {
+        double dy[DP];
+#pragma unroll
+        for (int k = 0; k < DP; k += 2) {
+          const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+          dy[k] = t2.x;
+          dy[k + 1] = t2.y;
+        }
+#pragma unroll
+        for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy);
+      } else {
+        const int jc = (col * F) >> pb.lam2;
+        if (cv && jc != jcur) {
+          double yv[DP];
+#pragma unroll
+          for (int k = 0; k < DP; k += 2) {
+            const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+            yv[k] = t2.x;
+            yv[k + 1] = t2.y;
+          }
+#pragma unroll
+          for (int c = 0; c <= RC; ++c) {
+            Kl[c] = Kr[c];
+            Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
+          }
+          jcur = jc;
+        }
+#pragma unroll
+        for (int c = 0; c < RC; ++c)
+          p[c] = cv ? ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale : 0.0;
       }
+#pragma unroll
+      for (int c = 0; c < RC; ++c) cfo[c] = coef(p[c]);
     };
 
     // ------------------------------------------- phase A: forward + checkpoints
@@ -179,9 +220,8 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       const int i0 = rbase >> pb.lam1;
       RowRegs<KIND, DP, RC> rr;
       load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
-      double Kl[RC + 1], Kr[RC + 1];
-      int jcur = -1;
-      double* __restrict__ rowck_s = rowck + (int64_t)strip * NT * F * 32 + lane;
+      jcur = -1;
+      double* __restrict__ rowck_s = rowck + (int64_t)strip * NT * SF * 32 + lane;
       if constexpr (KIND == RBF) {
         double y0[DP];
         load_vec<DP>(y0, cbase);
@@ -191,108 +231,79 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         for (int c = 0; c <= RC; ++c) Kl[c] = Kr[c];
       }
       for (int q = 0; q < PF; ++q) {
-        issue_one(q, hrow, strip > 0);
+        issue_cols(q * S, S, hrow, strip > 0);
         cp_async_commit();
       }
       double kl[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) kl[r] = 1.0;
       double topc = 1.0;
-      double bot[F];
+      double bot[SF];
 #pragma unroll
-      for (int f = 0; f < F; ++f) bot[f] = 1.0;
-      // coefficients of column jj (reads the ring; independent of the recurrence)
-      auto colcoef = [&](int jj, Coef (&cfo)[RC]) {
-        const double* rec = SK_REC(jj);
-        double p[RC];
-        if constexpr (KIND == LINEAR) {
-          double dy[DP];
-#pragma unroll
-          for (int k = 0; k < DP; k += 2) {
-            const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-            dy[k] = t2.x;
-            dy[k + 1] = t2.y;
-          }
-#pragma unroll
-          for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy) * pb.pscale;
-        } else {
-          const int jc = (jj * F) >> pb.lam2;
-          if (jj >= 0 && jj < NS && jc != jcur) {
-            double yv[DP];
-#pragma unroll
-            for (int k = 0; k < DP; k += 2) {
-              const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-              yv[k] = t2.x;
-              yv[k + 1] = t2.y;
-            }
-#pragma unroll
-            for (int c = 0; c <= RC; ++c) {
-              Kl[c] = Kr[c];
-              Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
-            }
-            jcur = jc;
-          }
-#pragma unroll
-          for (int c = 0; c < RC; ++c) p[c] = ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale;
-        }
-#pragma unroll
-        for (int c = 0; c < RC; ++c) cfo[c] = coef(p[c]);
-      };
-      Coef cf[RC];
-      cp_async_wait<PF - 1>();  // column 0 landed
-      __syncwarp();
-      colcoef(-u, cf);
+      for (int q = 0; q < SF; ++q) bot[q] = 1.0;
       for (int tau = 0; tau < NT; ++tau) {
-        issue_one(tau + PF, hrow, strip > 0);
+        issue_cols((tau + PF) * S, S, hrow, strip > 0);
         cp_async_commit();
-        cp_async_wait<PF - 1>();  // columns <= tau + 1 landed
+        cp_async_wait<PF>();  // step tau landed
         __syncwarp();
         if (tau % CB == 0) {
-          // column checkpoint: values at node column (tau - u) * F
+          // column checkpoint: values at node column (tau - u) * S * F
 #pragma unroll
           for (int r = 0; r < R; ++r)
             colck[(((int64_t)strip * NB + tau / CB) * R + r) * 32 + lane] = kl[r];
         }
-        const int jj = tau - u;
-        const bool active = (jj >= 0) && (jj < NS);
-        double tv[F];
+        const int js = tau - u;
+        const bool active = (js >= 0) && (js < NSTEP);
+        double tv[SF];
 #pragma unroll
-        for (int f = 0; f < F; ++f) tv[f] = __shfl_up_sync(0xffffffffu, bot[f], 1);
-        Coef cfn[RC];
-        colcoef(jj + 1, cfn);  // software pipeline: next column's coefficients
+        for (int q = 0; q < SF; ++q) tv[q] = __shfl_up_sync(0xffffffffu, bot[q], 1);
         if (active) {
-          const double* rec = SK_REC(jj);
           if (u == 0) {
 #pragma unroll
-            for (int f = 0; f < F; ++f) tv[f] = (strip == 0) ? 1.0 : rec[DP + f];
-          }
+            for (int s = 0; s < S; ++s) {
+              const double* rec = SK_REC(js * S + s);
 #pragma unroll
-          for (int f = 0; f < F; ++f) {
-            double up = tv[f];
-            double dg = (f == 0) ? topc : tv[f - 1];
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-              const double nk = cell(up, kl[r], dg, cf[r / FR]);
-              dg = kl[r];
-              kl[r] = nk;
-              up = nk;
+              for (int f = 0; f < F; ++f) tv[s * F + f] = (strip == 0) ? 1.0 : rec[DP + f];
             }
-            bot[f] = up;
-            rowck_s[(tau * F + f) * 32] = up;  // diagonal index = column + writer lane = tau
           }
-          topc = tv[F - 1];
+#pragma unroll
+          for (int s = 0; s < S; ++s) {
+            const int col = js * S + s;
+            Coef cf[RC];
+            colcoef(rr, col, cf);
+#pragma unroll
+            for (int f = 0; f < F; ++f) {
+              const int q = s * F + f;
+              double up = tv[q];
+              double dg = (q == 0) ? topc : tv[q - 1];
+#pragma unroll
+              for (int r = 0; r < R; ++r) {
+                const double nk = cell(up, kl[r], dg, cf[r / FR]);
+                dg = kl[r];
+                kl[r] = nk;
+                up = nk;
+              }
+              bot[q] = up;
+              rowck_s[(tau * SF + q) * 32] = up;  // diagonal index = step + writer lane = tau
+            }
+            if (strip == last_strip && u == u_star && col == NC - 1) {
+#pragma unroll
+              for (int r = 0; r < R; ++r)
+                if (r == r_star) kval = kl[r];
+            }
+          }
+          topc = tv[SF - 1];
           if (u == 31) {
 #pragma unroll
-            for (int f = 0; f < F; ++f) hrow[jj * F + f + 1] = bot[f];
-          }
-          if (strip == last_strip && u == u_star && jj == NS - 1) {
+            for (int s = 0; s < S; ++s) {
+              const int col = js * S + s;
+              if (col < NC) {
 #pragma unroll
-            for (int r = 0; r < R; ++r)
-              if (r == r_star) kval = kl[r];
+                for (int f = 0; f < F; ++f) hrow[col * F + f + 1] = bot[s * F + f];
+              }
+            }
           }
         }
-#pragma unroll
-        for (int c = 0; c < RC; ++c) cf[c] = cfn[c];
       }
       cp_async_wait<0>();
       __syncwarp();
@@ -321,39 +332,39 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       // left checkpoint (single buffers, consumed by the recompute) and lane
       // 31's incoming column gradients (double buffered, used by the sweep)
       auto issue_block = [&](int blk, bool first) {
-        if (first) issue_cols(blk * CB - 31, CB + 31, arow, true);
-        else issue_cols(blk * CB - 31, CB, arow, true);  // the new columns only
+        if (first) issue_cols((blk * CB - 31) * S, (CB + 31) * S, arow, true);
+        else issue_cols((blk * CB - 31) * S, CB * S, arow, true);  // the new columns only
         {
-          const int dlo = blk * CB - 2;  // rowck[strip][d][f][*], d in [blk*CB-2, blk*CB+CB-2]
+          const int dlo = blk * CB - 2;  // rowck[strip][d][q][*], d in [blk*CB-2, blk*CB+CB-2]
           constexpr int NCH = SM::TS / 2;
           for (int e = lane; e < NCH; e += 32) {
-            const int row = e / (F * 16);  // (CB+1) rows of F*32 doubles
+            const int row = e / (SF * 16);  // (CB+1) rows of SF*32 doubles
             const int d = dlo + row;
             const bool v = (d >= 0) && (d < NT);
             cp_async16(sTS + 2 * e,
-                       rowck + (((int64_t)strip * NT + (v ? d : 0)) * F) * 32 + 2 * (e % (F * 16)),
+                       rowck + (((int64_t)strip * NT + (v ? d : 0)) * SF) * 32 + 2 * (e % (SF * 16)),
                        v);
           }
         }
         if (strip > 0) {
-          // lane 0's top row: nodes t = blk*CB*F + q, written by strip-1's lane 31
-          for (int q = lane; q <= CB * F; q += 32) {
-            const int t = blk * CB * F + q;
+          // lane 0's top row: nodes t = blk*CB*SF + q, written by strip-1's lane 31
+          for (int q = lane; q <= CB * SF; q += 32) {
+            const int t = blk * CB * SF + q;
             const bool v = (t >= 1) && (t <= M2);
-            const int js = v ? (t - 1) / F : 0, fs = v ? (t - 1) % F : 0;
-            cp_async8(sT0 + q, &SK_ROWCK(strip - 1, js + 31, fs, 31), v);
+            const int js = v ? (t - 1) / SF : 0, qs = v ? (t - 1) % SF : 0;
+            cp_async8(sT0 + q, &SK_ROWCK(strip - 1, js + 31, qs, 31), v);
           }
         }
         for (int e = lane; e < SM::LS / 2; e += 32)
           cp_async16(sLS + 2 * e, colck + (((int64_t)strip * NB + blk) * R) * 32 + 2 * e, true);
         if constexpr (MAP == FUSED) {
           double* gs = sGS0 + (blk & 1) * SM::GS;
-          for (int e = lane; e < CB * (DP / 2); e += 32) {
-            const int kap = e / (DP / 2), w = e % (DP / 2);
-            const int col = blk * CB - 31 + kap;  // lane 31's columns
-            const bool v = (col >= 0) && (col < NS) && (strip < nstrips - 1);
+          for (int e = lane; e < CB * S * (DP / 2); e += 32) {
+            const int ks = e / (DP / 2), w = e % (DP / 2);
+            const int col = (blk * CB - 31) * S + ks;  // lane 31's columns
+            const bool v = (col >= 0) && (col < NC) && (strip < nstrips - 1);
             const int jc = v ? ((col * F) >> pb.lam2) : 0;
-            cp_async16(gs + kap * DP + 2 * w, gcs + (int64_t)jc * DP + 2 * w, v);
+            cp_async16(gs + ks * DP + 2 * w, gcs + (int64_t)jc * DP + 2 * w, v);
           }
         }
         cp_async_commit();
@@ -362,33 +373,31 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       double aR[R], bR[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) { aR[r] = 0.0; bR[r] = 0.0; }
-      double sendm[F];
+      double sendm[SF];
 #pragma unroll
-      for (int f = 0; f < F; ++f) sendm[f] = 0.0;
+      for (int q = 0; q < SF; ++q) sendm[q] = 0.0;
       double gxr[(MAP == FUSED) ? RC : 1][DP];
 #pragma unroll
       for (int k = 0; k < DP; ++k)
 #pragma unroll
         for (int c = 0; c < ((MAP == FUSED) ? RC : 1); ++c) gxr[c][k] = 0.0;
-      double Kl[RC + 1], Kr[RC + 1];  // RBF recompute state
-      int jcur = -1000;
 
       issue_block(NB - 1, true);
       for (int blk = NB - 1; blk >= 0; --blk) {
         cp_async_wait<0>();
         __syncwarp();
         const double* sGS = sGS0 + (blk & 1) * SM::GS;
-        const int jj0 = blk * CB - u;  // lane's first column in this block
+        const int js0 = blk * CB - u;  // lane's first step in this block
         double kleft[R];
 #pragma unroll
         for (int r = 0; r < R; ++r) kleft[r] = sLS[r * 32 + lane];
 
         // ---- recompute the block's forward values into shared memory
         if (!(SK_EXP & 4)) {
-          // top row at node t = jj0*F + q (q = 0..CB*F) of this lane's rows
+          // top row at node t = js0*SF + q (q = 0..CB*SF) of this lane's rows
 #pragma unroll
-          for (int q = 0; q <= CB * F; ++q) {
-            const int t = jj0 * F + q;
+          for (int q = 0; q <= CB * SF; ++q) {
+            const int t = js0 * SF + q;
             double v;
             if (t <= 0 || (strip == 0 && u == 0)) {
               v = 1.0;
@@ -397,8 +406,8 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             } else if (u == 0) {
               v = sT0[q];
             } else {
-              const int d = (t - 1) / F + u - 1 - (blk * CB - 2);
-              v = sTS[(d * F + (t - 1) % F) * 32 + (u - 1)];
+              const int d = (t - 1) / SF + u - 1 - (blk * CB - 2);
+              v = sTS[(d * SF + (t - 1) % SF) * 32 + (u - 1)];
             }
             SK_TR(q) = v;
           }
@@ -406,8 +415,8 @@ bwd_kernel(Problem pb, BwdArgs ba) {
 #pragma unroll
           for (int r = 0; r < R; ++r) kl[r] = kleft[r];
           if constexpr (KIND == RBF) {
-            // K at node columns jc(jj0), jc(jj0)+1 for the first column of the block
-            const int col0 = jj0 < 0 ? 0 : (jj0 >= NS ? NS - 1 : jj0);
+            // K at node columns jc, jc+1 of the block's first column
+            const int col0 = js0 * S < 0 ? 0 : (js0 * S >= NC ? NC - 1 : js0 * S);
             const int jc0 = (col0 * F) >> pb.lam2;
             double yv[DP];
             load_vec<DP>(yv, cbase + (int64_t)jc0 * pb.dpad);
@@ -421,179 +430,195 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           double topc = SK_TR(0);
 #pragma unroll
           for (int kap = 0; kap < CB; ++kap) {
-            const int jj = jj0 + kap;
-            const bool colv = (jj >= 0) && (jj < NS);
-            const double* rec = SK_REC(jj);
-            double p[RC];
-            if constexpr (KIND == LINEAR) {
-              double dy[DP];
 #pragma unroll
-              for (int k = 0; k < DP; k += 2) {
-                const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-                dy[k] = t2.x;
-                dy[k + 1] = t2.y;
-              }
+            for (int s = 0; s < S; ++s) {
+              const int col = (js0 + kap) * S + s;
+              Coef cf[RC];
+              {
+                const bool cv = (col >= 0) && (col < NC);
+                double p[RC];
+                const double* rec = SK_REC(col);
+                if constexpr (KIND == LINEAR) {
+                  double dy[DP];
 #pragma unroll
-              for (int c = 0; c < RC; ++c) p[c] = colv ? dot<DP>(rr.v[c], dy) * pb.pscale : 0.0;
-            } else {
-              const int jc = (jj * F) >> pb.lam2;
-              if (colv && jc != jcur) {
-                double yv[DP];
+                  for (int k = 0; k < DP; k += 2) {
+                    const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+                    dy[k] = t2.x;
+                    dy[k + 1] = t2.y;
+                  }
 #pragma unroll
-                for (int k = 0; k < DP; k += 2) {
-                  const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-                  yv[k] = t2.x;
-                  yv[k + 1] = t2.y;
+                  for (int c = 0; c < RC; ++c) p[c] = cv ? dot<DP>(rr.v[c], dy) : 0.0;
+                } else {
+                  const int jc = (col * F) >> pb.lam2;
+                  if (cv && jc != jcur) {
+                    double yv[DP];
+#pragma unroll
+                    for (int k = 0; k < DP; k += 2) {
+                      const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+                      yv[k] = t2.x;
+                      yv[k + 1] = t2.y;
+                    }
+#pragma unroll
+                    for (int c = 0; c <= RC; ++c) {
+                      Kl[c] = Kr[c];
+                      Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
+                    }
+                    jcur = jc;
+                  }
+#pragma unroll
+                  for (int c = 0; c < RC; ++c)
+                    p[c] = cv ? ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale : 0.0;
                 }
 #pragma unroll
-                for (int c = 0; c <= RC; ++c) {
-                  Kl[c] = Kr[c];
-                  Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
+                for (int c = 0; c < RC; ++c) {
+                  SK_PB(kap, s, c) = p[c];
+                  cf[c] = coef(p[c]);
                 }
-                jcur = jc;
               }
 #pragma unroll
-              for (int c = 0; c < RC; ++c)
-                p[c] = colv ? ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale : 0.0;
-            }
-            Coef cf[RC];
+              for (int f = 0; f < F; ++f) {
+                const int q = (kap * S + s) * F + f;
+                double up = SK_TR(q + 1);
+                double dg = (q == 0) ? topc : SK_TR(q);
 #pragma unroll
-            for (int c = 0; c < RC; ++c) {
-              SK_PB(kap, c) = p[c];
-              cf[c] = coef(p[c]);
-            }
-#pragma unroll
-            for (int f = 0; f < F; ++f) {
-              double up = SK_TR(kap * F + f + 1);
-              double dg = (f == 0) ? topc : SK_TR(kap * F + f);
-#pragma unroll
-              for (int r = 0; r < R; ++r) {
-                const double nk = cell(up, kl[r], dg, cf[r / FR]);
-                dg = kl[r];
-                kl[r] = nk;
-                up = nk;
-                SK_KB(kap, f, r) = nk;
+                for (int r = 0; r < R; ++r) {
+                  const double nk = cell(up, kl[r], dg, cf[r / FR]);
+                  dg = kl[r];
+                  kl[r] = nk;
+                  up = nk;
+                  SK_KB(kap, s, f, r) = nk;
+                }
               }
             }
-            topc = SK_TR(kap * F + F);
           }
         }
         __syncwarp();
         // staging buffers are free again: prefetch the next block under the sweep
         if (blk > 0) issue_block(blk - 1, false);
 
-        // ---- reverse sweep over the block, one column per kap
+        // ---- reverse sweep over the block, one step per kap
 #pragma unroll
         for (int kap = CB - 1; kap >= 0 && !(SK_EXP & 2); --kap) {
-          const int jj = jj0 + kap;
-          const bool colv = (jj >= 0) && (jj < NS);
-          const double* rec = SK_REC(jj);
-          double recv[F];
+          const int js = js0 + kap;
+          double recv[SF];
 #pragma unroll
-          for (int f = 0; f < F; ++f) recv[f] = __shfl_down_sync(0xffffffffu, sendm[f], 1);
+          for (int q = 0; q < SF; ++q) recv[q] = __shfl_down_sync(0xffffffffu, sendm[q], 1);
           if (u == 31) {
 #pragma unroll
-            for (int f = 0; f < F; ++f) recv[f] = colv ? rec[DP + f] : 0.0;
-          }
-          double Dp[RC];
+            for (int s = 0; s < S; ++s) {
+              const int col = js * S + s;
+              const bool cv = (col >= 0) && (col < NC);
+              const double* rec = SK_REC(col);
 #pragma unroll
-          for (int c = 0; c < RC; ++c) Dp[c] = 0.0;
-          double pk[RC];
-          Coef cf[RC];
-#pragma unroll
-          for (int c = 0; c < RC; ++c) {
-            pk[c] = SK_PB(kap, c);
-            cf[c] = coef(pk[c]);
-          }
-#pragma unroll
-          for (int f = F - 1; f >= 0; --f) {
-            const int t = jj * F + f + 1;
-            double m = recv[f];
-#pragma unroll
-            for (int r = R - 1; r >= 0; --r) {
-              const int s = rbase + r + 1;
-              const bool live = colv && (s <= M1);
-              double lam = aR[r] + m;
-              if (s == M1 && t == M2) lam += wcot;
-              lam = live ? lam : 0.0;
-              const int c = r / FR;
-              const double a = cf[c].A * lam;
-              const double b = cf[c].B * lam;
-              // forward values around the cell (s,t): left, up, up-left
-              const double kL = (f > 0) ? SK_KB(kap, f - 1, r)
-                                        : (kap > 0 ? SK_KB(kap - 1, F - 1, r) : kleft[r]);
-              const double kU = (r > 0) ? SK_KB(kap, f, r - 1) : SK_TR(kap * F + f + 1);
-              const double kD = (r > 0) ? ((f > 0) ? SK_KB(kap, f - 1, r - 1)
-                                                   : (kap > 0 ? SK_KB(kap - 1, F - 1, r - 1)
-                                                              : kleft[r - 1]))
-                                        : SK_TR(kap * F + f);
-              const double p6 = pk[c] * (1.0 / 6.0);
-              const double wv = fma(kL + kU, 0.5 + p6, kD * p6);
-              if (live) Dp[c] = fma(lam, wv, Dp[c]);
-              m = a - bR[r];
-              aR[r] = a;
-              bR[r] = b;
+              for (int f = 0; f < F; ++f) recv[s * F + f] = cv ? rec[DP + f] : 0.0;
             }
-            sendm[f] = m;
           }
-          if (u == 0 && colv) {
 #pragma unroll
-            for (int f = 0; f < F; ++f) arow[jj * F + f + 1] = sendm[f];
-          }
-          const int jc = colv ? ((jj * F) >> pb.lam2) : 0;
+          for (int s = S - 1; s >= 0; --s) {
+            const int jj = js * S + s;  // column
+            const bool colv = (jj >= 0) && (jj < NC);
+            const double* rec = SK_REC(jj);
+            double Dp[RC];
 #pragma unroll
-          for (int c = 0; c < RC; ++c) Dp[c] *= pb.scale;
-          if constexpr (MAP == FUSED && !(SK_EXP & 1)) {
-            // gx_i += D_ij dy_j (row-local registers)
+            for (int c = 0; c < RC; ++c) Dp[c] = 0.0;
+            double pk[RC];
+            Coef cf[RC];
 #pragma unroll
-            for (int k = 0; k < DP; k += 2) {
-              const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+            for (int c = 0; c < RC; ++c) {
+              pk[c] = SK_PB(kap, s, c);
+              cf[c] = coef(pk[c]);
+            }
 #pragma unroll
-              for (int c = 0; c < RC; ++c) {
-                gxr[c][k] = fma(Dp[c], t2.x, gxr[c][k]);
-                gxr[c][k + 1] = fma(Dp[c], t2.y, gxr[c][k + 1]);
+            for (int f = F - 1; f >= 0; --f) {
+              const int q = s * F + f;                 // fine column within the step
+              const int qb = (kap * S + s) * F + f;    // fine column within the block
+              const int t = jj * F + f + 1;
+              double m = recv[q];
+#pragma unroll
+              for (int r = R - 1; r >= 0; --r) {
+                const int srow = rbase + r + 1;
+                const bool live = colv && (srow <= M1);
+                double lam = aR[r] + m;
+                if (srow == M1 && t == M2) lam += wcot;
+                lam = live ? lam : 0.0;
+                const int c = r / FR;
+                const double a = cf[c].A * lam;
+                const double b = cf[c].B * lam;
+                // forward values around the cell: left, up, up-left
+                const double kL = (qb > 0) ? sK[((qb - 1) * R + r) * 32 + lane] : kleft[r];
+                const double kU = (r > 0) ? sK[(qb * R + r - 1) * 32 + lane] : SK_TR(qb + 1);
+                const double kD = (r > 0) ? ((qb > 0) ? sK[((qb - 1) * R + r - 1) * 32 + lane]
+                                                      : kleft[r - 1])
+                                          : SK_TR(qb);
+                const double p6 = pk[c] * (1.0 / 6.0);
+                const double wv = fma(kL + kU, 0.5 + p6, kD * p6);
+                if (live) Dp[c] = fma(lam, wv, Dp[c]);
+                m = a - bR[r];
+                aR[r] = a;
+                bR[r] = b;
               }
+              sendm[q] = m;
             }
-            // gy_j += D_ij dx_i into the column's shared row.  Lanes touch a row one
-            // step apart (u+1 before u, fixed order); lane 31 starts it (seeded by
-            // the strips below at the coarse column's first column), lane 0
-            // finishes it and emits the coarse column's sum.
-            if (colv) {
-              double* row = sGW + (jj % SM::GROWS) * SM::GSTR;
-              const bool seed = ((jj + 1) & K2m) == 0;
-              const double* src = (u == 31) ? (seed ? (sGS + kap * DP) : sZero) : row;
+            if (u == 0 && colv) {
+#pragma unroll
+              for (int f = 0; f < F; ++f) arow[jj * F + f + 1] = sendm[s * F + f];
+            }
+            const int jc = colv ? ((jj * F) >> pb.lam2) : 0;
+            if constexpr (MAP == FUSED && !(SK_EXP & 1)) {
+              // gx_i += D_ij dy_j (row-local registers; D carries the dyadic factor)
+              double Dg[RC];
+#pragma unroll
+              for (int c = 0; c < RC; ++c) Dg[c] = Dp[c] * gxs_scale;
 #pragma unroll
               for (int k = 0; k < DP; k += 2) {
-                double2 v = *reinterpret_cast<const double2*>(src + k);
+                const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
 #pragma unroll
                 for (int c = 0; c < RC; ++c) {
-                  v.x = fma(Dp[c], rr.v[c][k], v.x);
-                  v.y = fma(Dp[c], rr.v[c][k + 1], v.y);
+                  gxr[c][k] = fma(Dg[c], t2.x, gxr[c][k]);
+                  gxr[c][k + 1] = fma(Dg[c], t2.y, gxr[c][k + 1]);
                 }
-                *reinterpret_cast<double2*>(row + k) = v;
               }
-              if (u == 0) {
-                double2* q = reinterpret_cast<double2*>(gcs + (int64_t)jc * DP);
-                if (K2m == 0) {  // one column per coarse column
+              // gy_j += D_ij dx_i into the column's shared row (rows carry the
+              // dyadic factor already).  Lanes touch a row one step apart (u+1
+              // before u); lane 31 starts it (seeded by the strips below at the
+              // coarse column's first column), lane 0 finishes it.
+              if (colv) {
+                double* row = sGW + (jj % SM::GROWS) * SM::GSTR;
+                const bool seed = ((jj + 1) & K2m) == 0;
+                const double* src = (u == 31) ? (seed ? (sGS + ((kap * S + s) * DP)) : sZero) : row;
 #pragma unroll
-                  for (int k = 0; k < DP; k += 2) q[k / 2] = *reinterpret_cast<const double2*>(row + k);
-                } else {  // several: lane 0 sums them (reverse order), emits at the last
-                  const bool last = (jj & K2m) == 0;
+                for (int k = 0; k < DP; k += 2) {
+                  double2 v = *reinterpret_cast<const double2*>(src + k);
 #pragma unroll
-                  for (int k = 0; k < DP; ++k) {
-                    const double a = (seed ? 0.0 : sGA[k]) + row[k];
-                    sGA[k] = a;
-                    if (last) gcs[(int64_t)jc * DP + k] = a;
+                  for (int c = 0; c < RC; ++c) {
+                    v.x = fma(Dp[c], rr.v[c][k], v.x);
+                    v.y = fma(Dp[c], rr.v[c][k + 1], v.y);
+                  }
+                  *reinterpret_cast<double2*>(row + k) = v;
+                }
+                if (u == 0) {
+                  double2* dst = reinterpret_cast<double2*>(gcs + (int64_t)jc * DP);
+                  if (K2m == 0) {  // one column per coarse column
+#pragma unroll
+                    for (int k = 0; k < DP; k += 2) dst[k / 2] = *reinterpret_cast<const double2*>(row + k);
+                  } else {  // several: lane 0 sums them (reverse order), emits at the last
+                    const bool last = (jj & K2m) == 0;
+#pragma unroll
+                    for (int k = 0; k < DP; ++k) {
+                      const double a = (seed ? 0.0 : sGA[k]) + row[k];
+                      sGA[k] = a;
+                      if (last) gcs[(int64_t)jc * DP + k] = a;
+                    }
                   }
                 }
               }
-            }
-            __syncwarp();
-          } else if constexpr (MAP == DBUF) {
-            // RBF: coarse adjoint, kept per block in shared memory (p is dead)
+            } else if constexpr (MAP == DBUF) {
+              // RBF: coarse adjoint, kept per block in shared memory (p is dead)
 #pragma unroll
-            for (int c = 0; c < RC; ++c) SK_PB(kap, c) = colv ? Dp[c] : 0.0;
+              for (int c = 0; c < RC; ++c) SK_PB(kap, s, c) = colv ? Dp[c] * pb.scale : 0.0;
+            }
           }
+          __syncwarp();
         }
         if constexpr (MAP == DBUF) {
           // flush the block's coarse adjoint; lanes sharing coarse rows go in order
@@ -602,13 +627,16 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             if (excl || u == ln) {
 #pragma unroll
               for (int kap = CB - 1; kap >= 0; --kap) {
-                const int jj = jj0 + kap;
-                if (jj >= 0 && jj < NS) {
-                  const int jc = (jj * F) >> pb.lam2;
 #pragma unroll
-                  for (int c = 0; c < RC; ++c) {
-                    const int i = i0 + c;
-                    if (i < pb.M1c) dbuf[(int64_t)i * pb.M2c + jc] += SK_PB(kap, c);
+                for (int s = S - 1; s >= 0; --s) {
+                  const int jj = (js0 + kap) * S + s;
+                  if (jj >= 0 && jj < NC) {
+                    const int jc = (jj * F) >> pb.lam2;
+#pragma unroll
+                    for (int c = 0; c < RC; ++c) {
+                      const int i = i0 + c;
+                      if (i < pb.M1c) dbuf[(int64_t)i * pb.M2c + jc] += SK_PB(kap, s, c);
+                    }
                   }
                 }
               }

@@ -5,18 +5,13 @@
 
 namespace sk {
 
-// Block width (columns): ~16 recomputed values per lane, within [2, 8].
-template <int R, int F>
-constexpr int bwd_cb() {
-  return (16 / (F * R)) < 2 ? 2 : (16 / (F * R)) > 8 ? 8 : 16 / (F * R);
-}
-
 template <int KIND, int DP, int R, int FR, int F>
 inline void sk_bwd_leaf(BwdFn& fn, int& smem_doubles) {
-  constexpr int CB = bwd_cb<R, F>();
+  constexpr int S = bwd_steps_cols(DP, F);
+  constexpr int CB = bwd_block_steps(R, F, S);
   constexpr int MAP = (KIND == LINEAR) ? FUSED : DBUF;
-  fn = bwd_kernel<KIND, DP, R, FR, F, CB, MAP>;
-  smem_doubles = BwdSmem<DP, R, R / FR, F, CB>::TOTAL;  // per warp
+  fn = bwd_kernel<KIND, DP, R, FR, F, CB, MAP, S>;
+  smem_doubles = BwdSmem<DP, R, R / FR, F, CB, S>::TOTAL;  // per warp
 }
 
 template <int KIND, int DP, int R, int FR>

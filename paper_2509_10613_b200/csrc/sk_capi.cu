@@ -489,9 +489,10 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
                                                      (int64_t)occ * sms));
   pl.slots = pl.blocks * warps;
   const int64_t M1 = M1c << lamR, M2 = M2c << lamC;
-  const int64_t NS = M2 / s.F, NT = NS + 31, CB = std::min(8, std::max(2, 16 / (s.F * s.R))), NB = (NT + CB - 1) / CB;
+  const int64_t Sc = bwd_steps_cols(s.DP, s.F), NC = M2 / s.F, NSTEP = (NC + Sc - 1) / Sc,
+                NT = NSTEP + 31, CB = bwd_block_steps(s.R, s.F, (int)Sc), NB = (NT + CB - 1) / CB;
   const int64_t nstrips = (M1 + 32 * s.R - 1) / (32 * s.R);
-  pl.rowck_stride = (int64_t)align_up((size_t)(nstrips * NT * s.F * 32), 32);
+  pl.rowck_stride = (int64_t)align_up((size_t)(nstrips * NT * Sc * s.F * 32), 32);
   pl.colck_stride = (int64_t)align_up((size_t)(nstrips * NB * s.R * 32), 32);
   pl.row_stride = (int64_t)align_up((size_t)(M2 + 1), 32);
   pl.dbuf_stride = kind == RBF ? (int64_t)align_up((size_t)(M1c * M2c), 32) : 0;
@@ -527,7 +528,11 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
     return rc;
   BwdLayout lo;
   lo.prepR = align_up(prep_elems(kind, g.nR, g.LR, pb.dpad) * sizeof(double), 256);
-  lo.prepC = sym ? 0 : align_up(prep_elems(kind, g.nC, g.LC, pb.dpad) * sizeof(double), 256);
+  // LINEAR rows carry the exact dyadic factor (as in the forward); a symmetric
+  // Gram then needs an unscaled column copy when the factor is not 1
+  const bool fold = kind == LINEAR;
+  const bool share = sym && !(fold && pb.scale != 1.0);
+  lo.prepC = share ? 0 : align_up(prep_elems(kind, g.nC, g.LC, pb.dpad) * sizeof(double), 256);
   lo.rowck = align_up((size_t)pl.slots * pl.rowck_stride * sizeof(double), 256);
   lo.colck = align_up((size_t)pl.slots * pl.colck_stride * sizeof(double), 256);
   lo.rows = align_up((size_t)pl.slots * pl.row_stride * 2 * sizeof(double), 256);
@@ -550,7 +555,7 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   if (!grad_x || (!sym && !grad_y)) return fail(SK_INVALID_ARGUMENT, "gradient buffers missing");
   char* base = static_cast<char*>(ws);
   double* prepR = reinterpret_cast<double*>(base);
-  double* prepC = sym ? prepR : reinterpret_cast<double*>(base + lo.prepR);
+  double* prepC = share ? prepR : reinterpret_cast<double*>(base + lo.prepR);
   char* p = base + lo.prepR + lo.prepC;
   BwdArgs ba{};
   ba.rowck = reinterpret_cast<double*>(p);
@@ -571,8 +576,9 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   ba.rows_exclusive = (1 << g.lamR) <= pl.shape.R ? 1 : 0;
   const double* xr = g.swap ? y : x;
   const double* xc = g.swap ? x : y;
-  launch_prep(kind, xr, g.nR, g.LR, d, pb.dpad, prepR, st);
-  if (!sym) launch_prep(kind, xc, g.nC, g.LC, d, pb.dpad, prepC, st);
+  launch_prep(kind, xr, g.nR, g.LR, d, pb.dpad, prepR, st, fold ? pb.scale : 1.0);
+  if (!share) launch_prep(kind, xc, g.nC, g.LC, d, pb.dpad, prepC, st);
+  if (fold) pb.pscale = 1.0;
   pb.R.p = prepR;
   pb.R.rows = (int)(g.LR - 1);
   pb.R.path_stride = (kind == RBF ? g.LR : g.LR - 1) * pb.dpad;

@@ -46,6 +46,13 @@ inline int rows_per_lane(int DP) {
 
 // Backward: the reverse sweep keeps dx, gx (RC x DP each) and the gy chain
 // (DP) live, so wide paths trade rows per lane for occupancy.
+// Backward columns per step (narrow paths amortise per-step overhead) and
+// block width in steps (~16 recomputed values per lane, at least one step).
+constexpr int bwd_steps_cols(int DP, int F) { return (DP <= 8 && F == 1) ? 2 : 1; }
+constexpr int bwd_block_steps(int R, int F, int S) {
+  return (16 / (F * R * S)) < 1 ? 1 : (16 / (F * R * S)) > 8 ? 8 : 16 / (F * R * S);
+}
+
 inline int bwd_rows_per_lane(int DP) {
   if (DP != 16) return rows_per_lane(DP);
   const char* e = std::getenv("SK_BWD_R16");  // tuning override (1 or 2)
