@@ -48,7 +48,9 @@ inline int rows_per_lane(int DP) {
 // (DP) live, so wide paths trade rows per lane for occupancy.
 // Backward columns per step (narrow paths amortise per-step overhead) and
 // block width in steps (~16 recomputed values per lane, at least one step).
-constexpr int bwd_steps_cols(int DP, int F) { return (DP <= 8 && F == 1) ? 2 : 1; }
+// (measured: S = 2 for d = 8 was slower, 426 vs 366 ms on a 256^2 C5-shaped Gram,
+// register pressure; kept as a knob)
+constexpr int bwd_steps_cols(int DP, int F) { return (DP <= 8 && F == 1 && false) ? 2 : 1; }
 constexpr int bwd_block_steps(int R, int F, int S) {
   return (16 / (F * R * S)) < 1 ? 1 : (16 / (F * R * S)) > 8 ? 8 : 16 / (F * R * S);
 }
