@@ -71,8 +71,9 @@ struct BwdSmem {
   static constexpr int GS = CB * S * DP;             // lane 31's incoming column gradients (x2)
   static constexpr int GROWS = (32 + CB) * S;        // gy accumulator rows (one per column)
   static constexpr int GSTR = DP + 2;                // row stride: conflict-free 16-B accesses
+  static constexpr int PS = CB * S * RC * 32;        // coarse p checkpoints of the next block
   static constexpr int TOTAL =
-      SLOTS * REC + (NK + NP + NTR) * 32 + TS + T0 + LS + 2 * GS + GROWS * GSTR + 2 * DP;
+      SLOTS * REC + (NK + NP + NTR) * 32 + TS + T0 + LS + 2 * GS + GROWS * GSTR + 2 * DP + PS;
 };
 
 template <int KIND, int DP, int R, int FR, int F, int CB, int MAP, int S>
@@ -99,6 +100,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   double* sGW = sGS0 + 2 * SM::GS;
   double* sZero = sGW + SM::GROWS * SM::GSTR;  // DP zeros (lane 31's unseeded rows)
   double* sGA = sZero + DP;                    // lane 0's coarse-column sums (2^lam2 > F)
+  double* sPS = sGA + DP;                      // staged coarse p of the next block
   for (int k = lane; k < DP; k += 32) sZero[k] = 0.0;
   __syncwarp();
 #define SK_TR(q) sTR[(q) * 32 + lane]
@@ -128,6 +130,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   const int64_t slot = (int64_t)blockIdx.x * nw + warp;
   double* __restrict__ rowck = ba.rowck + slot * ba.rowck_stride;
   double* __restrict__ colck = ba.colck + slot * ba.colck_stride;
+  double* __restrict__ pck = ba.pck + slot * ba.pck_stride;
   double* __restrict__ hrow = ba.hand + slot * ba.row_stride;
   double* __restrict__ arow = ba.adj + slot * ba.row_stride;
   double* __restrict__ dbuf = (MAP == DBUF) ? ba.dbuf + slot * ba.dbuf_stride : nullptr;
@@ -172,7 +175,8 @@ bwd_kernel(Problem pb, BwdArgs ba) {
     // coefficients of column col from its ring record (RBF carries K across columns)
     double Kl[RC + 1], Kr[RC + 1];
     int jcur = -1;
-    auto colcoef = [&](const RowRegs<KIND, DP, RC>& rr, int col, Coef (&cfo)[RC]) {
+    auto colcoef = [&](const RowRegs<KIND, DP, RC>& rr, int col, Coef (&cfo)[RC],
+                       double (&po)[RC]) {
       const double* rec = SK_REC(col);
       const bool cv = (col >= 0) && (col < NC);
       double p[RC];
@@ -208,7 +212,10 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           p[c] = cv ? ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale : 0.0;
       }
 #pragma unroll
-      for (int c = 0; c < RC; ++c) cfo[c] = coef(p[c]);
+      for (int c = 0; c < RC; ++c) {
+        cfo[c] = coef(p[c]);
+        po[c] = p[c];
+      }
     };
 
     // ------------------------------------------- phase A: forward + checkpoints
@@ -222,6 +229,9 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
       jcur = -1;
       double* __restrict__ rowck_s = rowck + (int64_t)strip * NT * SF * 32 + lane;
+      // coarse p of every column this lane solves: the block recompute reads
+      // it back instead of re-forming <dx_i, dy_j> (or the RBF exps)
+      double* __restrict__ pck_s = pck + (int64_t)strip * NT * S * RC * 32 + lane;
       if constexpr (KIND == RBF) {
         double y0[DP];
         load_vec<DP>(y0, cbase);
@@ -270,7 +280,10 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           for (int s = 0; s < S; ++s) {
             const int col = js * S + s;
             Coef cf[RC];
-            colcoef(rr, col, cf);
+            double pv[RC];
+            colcoef(rr, col, cf, pv);
+#pragma unroll
+            for (int c = 0; c < RC; ++c) pck_s[((tau * S + s) * RC + c) * 32] = pv[c];
 #pragma unroll
             for (int f = 0; f < F; ++f) {
               const int q = s * F + f;
@@ -357,6 +370,16 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         }
         for (int e = lane; e < SM::LS / 2; e += 32)
           cp_async16(sLS + 2 * e, colck + (((int64_t)strip * NB + blk) * R) * 32 + 2 * e, true);
+        {
+          // coarse p: lane u's step js0 + kap sits at diagonal index blk*CB + kap
+          constexpr int ROWC = S * RC * 16;  // 16-byte chunks per diagonal row
+          for (int e = lane; e < CB * ROWC; e += 32) {
+            const int d = blk * CB + e / ROWC;
+            const bool v = d < NT;
+            cp_async16(sPS + 2 * e,
+                       pck + ((int64_t)strip * NT + (v ? d : 0)) * S * RC * 32 + 2 * (e % ROWC), v);
+          }
+        }
         if constexpr (MAP == FUSED) {
           double* gs = sGS0 + (blk & 1) * SM::GS;
           for (int e = lane; e < CB * S * (DP / 2); e += 32) {
@@ -414,19 +437,6 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           double kl[R];
 #pragma unroll
           for (int r = 0; r < R; ++r) kl[r] = kleft[r];
-          if constexpr (KIND == RBF) {
-            // K at node columns jc, jc+1 of the block's first column
-            const int col0 = js0 * S < 0 ? 0 : (js0 * S >= NC ? NC - 1 : js0 * S);
-            const int jc0 = (col0 * F) >> pb.lam2;
-            double yv[DP];
-            load_vec<DP>(yv, cbase + (int64_t)jc0 * pb.dpad);
-#pragma unroll
-            for (int c = 0; c <= RC; ++c) Kl[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
-            load_vec<DP>(yv, cbase + (int64_t)(jc0 + 1) * pb.dpad);
-#pragma unroll
-            for (int c = 0; c <= RC; ++c) Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
-            jcur = jc0;
-          }
           double topc = SK_TR(0);
 #pragma unroll
           for (int kap = 0; kap < CB; ++kap) {
@@ -436,43 +446,11 @@ bwd_kernel(Problem pb, BwdArgs ba) {
               Coef cf[RC];
               {
                 const bool cv = (col >= 0) && (col < NC);
-                double p[RC];
-                const double* rec = SK_REC(col);
-                if constexpr (KIND == LINEAR) {
-                  double dy[DP];
-#pragma unroll
-                  for (int k = 0; k < DP; k += 2) {
-                    const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-                    dy[k] = t2.x;
-                    dy[k + 1] = t2.y;
-                  }
-#pragma unroll
-                  for (int c = 0; c < RC; ++c) p[c] = cv ? dot<DP>(rr.v[c], dy) : 0.0;
-                } else {
-                  const int jc = (col * F) >> pb.lam2;
-                  if (cv && jc != jcur) {
-                    double yv[DP];
-#pragma unroll
-                    for (int k = 0; k < DP; k += 2) {
-                      const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-                      yv[k] = t2.x;
-                      yv[k + 1] = t2.y;
-                    }
-#pragma unroll
-                    for (int c = 0; c <= RC; ++c) {
-                      Kl[c] = Kr[c];
-                      Kr[c] = exp(-sqdist<DP>(rr.v[c], yv) * pb.inv2s2);
-                    }
-                    jcur = jc;
-                  }
-#pragma unroll
-                  for (int c = 0; c < RC; ++c)
-                    p[c] = cv ? ((Kr[c + 1] - Kl[c + 1]) - (Kr[c] - Kl[c])) * pb.scale : 0.0;
-                }
 #pragma unroll
                 for (int c = 0; c < RC; ++c) {
-                  SK_PB(kap, s, c) = p[c];
-                  cf[c] = coef(p[c]);
+                  const double p = cv ? sPS[((kap * S + s) * RC + c) * 32 + lane] : 0.0;
+                  SK_PB(kap, s, c) = p;
+                  cf[c] = coef(p);
                 }
               }
 #pragma unroll

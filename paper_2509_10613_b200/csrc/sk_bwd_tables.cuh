@@ -8,7 +8,7 @@ namespace sk {
 template <int KIND, int DP, int R, int FR, int F>
 inline void sk_bwd_leaf(BwdFn& fn, int& smem_doubles) {
   constexpr int S = bwd_steps_cols(DP, F);
-  constexpr int CB = bwd_block_steps(R, F, S);
+  constexpr int CB = bwd_block_steps(DP, R, F, S);
   constexpr int MAP = (KIND == LINEAR) ? FUSED : DBUF;
   fn = bwd_kernel<KIND, DP, R, FR, F, CB, MAP, S>;
   smem_doubles = BwdSmem<DP, R, R / FR, F, CB, S>::TOTAL;  // per warp

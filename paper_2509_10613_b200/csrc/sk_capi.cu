@@ -450,7 +450,7 @@ struct BwdPlan {
   int smem_bytes = 0;
   int threads = 128;
   int64_t blocks = 0, slots = 0, nitems = 0;
-  int64_t rowck_stride = 0, colck_stride = 0, row_stride = 0, dbuf_stride = 0, gscr_stride = 0;
+  int64_t rowck_stride = 0, colck_stride = 0, pck_stride = 0, row_stride = 0, dbuf_stride = 0, gscr_stride = 0;
 };
 
 static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, int64_t M1c,
@@ -490,10 +490,11 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   pl.slots = pl.blocks * warps;
   const int64_t M1 = M1c << lamR, M2 = M2c << lamC;
   const int64_t Sc = bwd_steps_cols(s.DP, s.F), NC = M2 / s.F, NSTEP = (NC + Sc - 1) / Sc,
-                NT = NSTEP + 31, CB = bwd_block_steps(s.R, s.F, (int)Sc), NB = (NT + CB - 1) / CB;
+                NT = NSTEP + 31, CB = bwd_block_steps(s.DP, s.R, s.F, (int)Sc), NB = (NT + CB - 1) / CB;
   const int64_t nstrips = (M1 + 32 * s.R - 1) / (32 * s.R);
   pl.rowck_stride = (int64_t)align_up((size_t)(nstrips * NT * Sc * s.F * 32), 32);
   pl.colck_stride = (int64_t)align_up((size_t)(nstrips * NB * s.R * 32), 32);
+  pl.pck_stride = (int64_t)align_up((size_t)(nstrips * NT * Sc * (s.R / s.FR) * 32), 32);
   pl.row_stride = (int64_t)align_up((size_t)(M2 + 1), 32);
   pl.dbuf_stride = kind == RBF ? (int64_t)align_up((size_t)(M1c * M2c), 32) : 0;
   pl.gscr_stride = kind == LINEAR ? (int64_t)align_up((size_t)((M1c + M2c) * s.DP), 32) : 0;
@@ -501,7 +502,8 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
 }
 
 struct BwdLayout {
-  size_t prepR = 0, prepC = 0, rowck = 0, colck = 0, rows = 0, dbuf = 0, gscr = 0, total = 0;
+  size_t prepR = 0, prepC = 0, rowck = 0, colck = 0, pck = 0, rows = 0, dbuf = 0, gscr = 0,
+         total = 0;
 };
 
 static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n2, int64_t L1,
@@ -535,10 +537,11 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   lo.prepC = share ? 0 : align_up(prep_elems(kind, g.nC, g.LC, pb.dpad) * sizeof(double), 256);
   lo.rowck = align_up((size_t)pl.slots * pl.rowck_stride * sizeof(double), 256);
   lo.colck = align_up((size_t)pl.slots * pl.colck_stride * sizeof(double), 256);
+  lo.pck = align_up((size_t)pl.slots * pl.pck_stride * sizeof(double), 256);
   lo.rows = align_up((size_t)pl.slots * pl.row_stride * 2 * sizeof(double), 256);
   lo.dbuf = align_up((size_t)pl.slots * pl.dbuf_stride * sizeof(double), 256);
   lo.gscr = align_up((size_t)pl.slots * pl.gscr_stride * sizeof(double), 256);
-  lo.total = lo.prepR + lo.prepC + lo.rowck + lo.colck + lo.rows + lo.dbuf + lo.gscr;
+  lo.total = lo.prepR + lo.prepC + lo.rowck + lo.colck + lo.pck + lo.rows + lo.dbuf + lo.gscr;
   if (query) {
     *query = lo.total;
     return SK_OK;
@@ -564,6 +567,9 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   ba.colck = reinterpret_cast<double*>(p);
   ba.colck_stride = pl.colck_stride;
   p += lo.colck;
+  ba.pck = reinterpret_cast<double*>(p);
+  ba.pck_stride = pl.pck_stride;
+  p += lo.pck;
   ba.hand = reinterpret_cast<double*>(p);
   ba.adj = ba.hand + pl.slots * pl.row_stride;
   ba.row_stride = pl.row_stride;

@@ -62,6 +62,8 @@ struct BwdArgs {
   int64_t rowck_stride;
   double* colck;
   int64_t colck_stride;
+  double* pck;  // coarse p per solved column ([strip][step + lane][s][c][lane])
+  int64_t pck_stride;
   double* hand;  // forward handoff rows
   double* adj;   // reverse handoff rows (messages between strips)
   int64_t row_stride;

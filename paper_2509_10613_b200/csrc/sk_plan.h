@@ -51,8 +51,11 @@ inline int rows_per_lane(int DP) {
 // (measured: S = 2 for d = 8 was slower, 426 vs 366 ms on a 256^2 C5-shaped Gram,
 // register pressure; kept as a knob)
 constexpr int bwd_steps_cols(int DP, int F) { return (DP <= 8 && F == 1 && false) ? 2 : 1; }
-constexpr int bwd_block_steps(int R, int F, int S) {
-  return (16 / (F * R * S)) < 1 ? 1 : (16 / (F * R * S)) > 8 ? 8 : 16 / (F * R * S);
+constexpr int bwd_block_steps(int DP, int R, int F, int S) {
+  // wide paths: ~8 values per lane so two CTAs of four warps fit in shared memory
+  return ((DP >= 16 ? 8 : 16) / (F * R * S)) < 1 ? 1
+         : ((DP >= 16 ? 8 : 16) / (F * R * S)) > 8 ? 8
+                                                   : (DP >= 16 ? 8 : 16) / (F * R * S);
 }
 
 inline int bwd_rows_per_lane(int DP) {
