@@ -1,0 +1,54 @@
+"""One full BASELINE config 5 step on one GPU: symmetric sig_kernel_gram of
+8192 Brownian paths (L=1024, d=8, lambda=0), fp64 forward + backward
+(cotangent ones), device-timed, with a sub-block parity check against the C
+oracle.  Writes a JSON summary (evidence run; bench.py's default is C3)."""
+import json
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = __file__.rsplit("/tools/", 1)[0]
+sys.path.insert(0, ROOT)
+from paper_2509_10613_b200 import ops  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
+L, d = 1024, 8
+rng = np.random.default_rng(0)
+X = np.cumsum(rng.standard_normal((n, L, d)) / np.sqrt(L), axis=1)
+Xd = torch.as_tensor(X, device="cuda")
+C = torch.ones((n, n), dtype=torch.float64, device="cuda")
+peak = ops.dfma_peak()
+torch.cuda.synchronize()
+e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+t0 = time.time()
+e[0].record()
+G = ops.forward_gram(Xd, None, 0, 0, 0, 1.0)
+e[1].record()
+gx, _ = ops.backward_gram(Xd, None, 0, 0, 0, 1.0, C)
+e[2].record()
+torch.cuda.synchronize()
+wall = time.time() - t0
+fwd_s = e[0].elapsed_time(e[1]) / 1e3
+bwd_s = e[1].elapsed_time(e[2]) / 1e3
+pairs = n * (n + 1) // 2
+cells = pairs * (L - 1) ** 2
+out = {"config": f"C5 sym Gram n={n} L={L} d={d} lambda=0 fp64 fwd+bwd, cotangent ones, 1 GPU",
+       "fwd_s": fwd_s, "bwd_s": bwd_s, "step_s": fwd_s + bwd_s, "wall_s": wall,
+       "cells": cells, "cells_per_s": cells / (fwd_s + bwd_s),
+       "gram_entries_per_s": n * n / (fwd_s + bwd_s),
+       "fwd_frac_of_dfma": cells * 15 / fwd_s / peak,
+       "bwd_frac_of_dfma_algorithmic": cells * 25 / bwd_s / peak,
+       "step_frac_of_dfma_algorithmic": cells * 40 / (fwd_s + bwd_s) / peak,
+       "dfma_peak_fma_per_s": peak}
+# parity of a sub-block (first 6 paths) and symmetry
+sys.path.insert(0, ROOT)
+from oracle import oracle as orc  # noqa: E402  (checker only)
+Gs = G[:6, :6].cpu().numpy()
+want = orc.kernel_gram(X[:6])
+out["subblock_rel_err"] = float(np.abs(Gs - want).max() / np.abs(want).max())
+out["symmetric_exact"] = bool(torch.equal(G, G.T))
+out["grad_finite"] = bool(torch.isfinite(gx).all().item())
+out["grad_abs_max"] = float(gx.abs().max().item())
+print(json.dumps(out, indent=1))
