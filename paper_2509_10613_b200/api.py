@@ -112,12 +112,39 @@ def _prep(t, name):
     return t
 
 
-def sig_kernel(x, y, dyadic_order=0, static_kernel=None):
+TRANSFORMS = (None, "time_augment", "lead_lag")
+
+
+def path_transform(x: torch.Tensor, kind):
+    """Time augmentation / lead-lag of a (B, L, d) batch (reference transforms.py:37-66).
+
+    time_augment: (B, L, d) -> (B, L, d+1), last coordinate the uniform time grid
+    on [0, 1]; lead_lag: (B, L, d) -> (B, 2L-1, 2d) with Z[2k] = (X[k], X[k]),
+    Z[2k+1] = (X[k+1], X[k]).  Linear in x, so autograd supplies the reference's
+    transform_adjoint (transforms.py:69-90)."""
+    if kind is None:
+        return x
+    if kind == "time_augment":
+        B, L, _ = x.shape
+        t = torch.linspace(0.0, 1.0, L, dtype=x.dtype, device=x.device) if L > 1 else \
+            torch.zeros(1, dtype=x.dtype, device=x.device)
+        return torch.cat([x, t.view(1, L, 1).expand(B, L, 1)], dim=2)
+    if kind == "lead_lag":
+        B, L, d = x.shape
+        lead = torch.stack([x, torch.cat([x[:, 1:], x[:, -1:]], 1)], 2).reshape(B, 2 * L, d)
+        lag = torch.stack([x, x], 2).reshape(B, 2 * L, d)
+        return torch.cat([lead, lag], dim=2)[:, : 2 * L - 1]
+    raise InvalidArgument(f"unknown transform {kind!r}, expected one of {TRANSFORMS}")
+
+
+def sig_kernel(x, y, dyadic_order=0, static_kernel=None, transform=None):
     """k(x_b, y_b) for aligned batches (B, L1, d), (B, L2, d) -> (B,).
 
-    A pair of (L, d) paths returns a 0-d tensor."""
+    A pair of (L, d) paths returns a 0-d tensor.  `transform` ("time_augment" or
+    "lead_lag") is applied to both paths first (pySigLib's path transforms)."""
     x, sq = _batched(_prep(x, "x"), "x")
     y, _ = _batched(_prep(y, "y"), "y")
+    x, y = path_transform(x, transform), path_transform(y, transform)
     l1, l2 = _orders(dyadic_order)
     kind, sigma = ops.static_kind(static_kernel)
     out_dtype = torch.promote_types(x.dtype, y.dtype)
@@ -126,19 +153,21 @@ def sig_kernel(x, y, dyadic_order=0, static_kernel=None):
     return k[0] if sq else k
 
 
-def sig_kernel_gram(x, y=None, dyadic_order=0, static_kernel=None):
+def sig_kernel_gram(x, y=None, dyadic_order=0, static_kernel=None, transform=None):
     """Gram matrix G[a, b] = k(x_a, y_b) -> (n1, n2).
 
     y None (or y is x) -> symmetric: only a <= b is solved and the result is
     mirrored, hence exactly symmetric (reference kernel.py:151-180)."""
     sym = y is None or y is x
     x, _ = _batched(_prep(x, "x"), "x")
+    x = path_transform(x, transform)
     l1, l2 = _orders(dyadic_order)
     kind, sigma = ops.static_kind(static_kernel)
     if sym:
         G = _SigKernelGramFn.apply(x.to(torch.float64), None, l1, l2, kind, sigma)
         return G.to(x.dtype)
     y, _ = _batched(_prep(y, "y"), "y")
+    y = path_transform(y, transform)
     out_dtype = torch.promote_types(x.dtype, y.dtype)
     G = _SigKernelGramFn.apply(x.to(torch.float64), y.to(torch.float64), l1, l2, kind, sigma)
     return G.to(out_dtype)

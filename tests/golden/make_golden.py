@@ -166,6 +166,16 @@ def main():
     sc.write_array(a1, os.path.join(OUT, "ref_int_1d.sgt"))
     save("sgt_contents", a3=a3, a2=a2, a1=a1)
 
+    # path transforms (transforms.py:37-66) and their adjoints (69-90)
+    rng = np.random.default_rng(13)
+    xt = rng.standard_normal((3, 6, 2))
+    gt_ta = rng.standard_normal((3, 6, 3))
+    gt_ll = rng.standard_normal((3, 11, 4))
+    save("transforms", x=xt, time_augment=sc.transform(xt, "time_augment"),
+         lead_lag=sc.transform(xt, "lead_lag"), g_ta=gt_ta, g_ll=gt_ll,
+         adj_ta=sc.transform_adjoint(gt_ta, "time_augment"),
+         adj_ll=sc.transform_adjoint(gt_ll, "lead_lag"))
+
     print("reference:", sc.__file__, "numba", __import__("numba").__version__,
           "numpy", np.__version__, file=sys.stderr)
 
