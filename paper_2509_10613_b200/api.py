@@ -126,8 +126,12 @@ def path_transform(x: torch.Tensor, kind):
         return x
     if kind == "time_augment":
         B, L, _ = x.shape
-        t = torch.linspace(0.0, 1.0, L, dtype=x.dtype, device=x.device) if L > 1 else \
-            torch.zeros(1, dtype=x.dtype, device=x.device)
+        # numpy.linspace's arithmetic (i * (1/(L-1)), last point exactly 1), as the reference
+        t = torch.arange(L, dtype=torch.float64, device=x.device)
+        if L > 1:
+            t = t * (1.0 / (L - 1))
+            t[-1] = 1.0
+        t = t.to(x.dtype)
         return torch.cat([x, t.view(1, L, 1).expand(B, L, 1)], dim=2)
     if kind == "lead_lag":
         B, L, d = x.shape
