@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -162,6 +163,35 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
     s.XW = true;
     s.W = W;
     s.G = 32 * W;
+  }
+  // Gram tiles of the linear kernel at dyadic order 0: increment products on
+  // the FP64 tensor cores (sk_mma_fwd.cuh).  SK_NO_MMA=1 keeps the r01 kernels.
+  s.MMA = gram && kind == LINEAR && lamR == 0 && lamC == 0 && nch == 1 && s.DP <= 16 &&
+          !(std::getenv("SK_NO_MMA") && std::getenv("SK_NO_MMA")[0] == '1');
+  if (s.MMA) {
+    int per_warp = 0;
+    FwdFn fn = select_fwd_mma(s.DP, per_warp);
+    if (!fn) return fail(SK_INVALID_ARGUMENT, "no DMMA forward instance for this shape");
+    pl.shape = s;
+    pl.fn = fn;
+    pl.threads = 128;
+    pl.P = 8;
+    pl.smem_bytes = per_warp * 4;
+    pl.nitems = gram_items(mode, n2, r0, r1, pl.P);
+    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             pl.smem_bytes) != cudaSuccess)
+      (void)cudaGetLastError();
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, pl.threads,
+                                                      pl.smem_bytes) != cudaSuccess || occ < 1) {
+      (void)cudaGetLastError();
+      occ = 1;
+    }
+    pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + 3) / 4, (int64_t)occ * sms));
+    pl.slots = pl.blocks * 4 * pl.P;
+    // lane u = 0 prefetches the handoff row 8 columns ahead of an 8-step tile loop
+    pl.hand_stride = 8 * ((M2c + 10) / 8 + 2);
+    return SK_OK;
   }
   int smem = 0;
   FwdFn fn = kind == LINEAR ? select_fwd_linear(s, smem)

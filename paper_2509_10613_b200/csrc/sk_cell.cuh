@@ -39,15 +39,14 @@ __device__ __forceinline__ void load_vec(double (&v)[DP], const double* __restri
 
 template <int DP>
 __device__ __forceinline__ double dot(const double (&a)[DP], const double (&b)[DP]) {
-  // two interleaved partial sums halve the dependent FMA chain; every kernel
-  // forms <dx_i, dy_j> with this exact order, so forward and backward agree bitwise
-  double s0 = a[0] * b[0], s1 = a[1] * b[1];
+  // one sequential FMA chain, k = 0..DP-1, starting from 0: exactly what the
+  // FP64 tensor-core path computes (mma.m8n8k4.f64 is a sequential fma chain
+  // over its k, measured bitwise by tools/dmma_probe.cu), so the DMMA Gram
+  // kernels, the batch kernels and the backward recompute agree bitwise
+  double s = a[0] * b[0];
 #pragma unroll
-  for (int k = 2; k < DP; k += 2) {
-    s0 = fma(a[k], b[k], s0);
-    s1 = fma(a[k + 1], b[k + 1], s1);
-  }
-  return s0 + s1;
+  for (int k = 1; k < DP; ++k) s = fma(a[k], b[k], s);
+  return s;
 }
 
 template <int DP>

@@ -18,6 +18,7 @@ struct FwdShape {
   int G;    // lanes per pair (4 or 32), ignored if XW
   bool XW;  // cross-warp groups: one pair per CTA of W warps
   int W;    // warps per CTA when XW
+  bool MMA; // DMMA Gram tile kernel (sk_mma_fwd.cuh): LINEAR, dyadic order 0, DP <= 16
 };
 
 using BwdFn = void (*)(Problem, BwdArgs);
@@ -34,6 +35,7 @@ BwdFn select_bwd_rbf(const BwdShape& s, int& smem_doubles);
 FwdFn select_fwd_linear(const FwdShape& s, int& smem);
 FwdFn select_fwd_rbf(const FwdShape& s, int& smem);
 FwdFn select_fwd_delta(const FwdShape& s, int& smem);
+FwdFn select_fwd_mma(int DP, int& smem_per_warp);
 
 inline int rows_per_lane(int DP) {
   switch (DP) {

@@ -1,0 +1,81 @@
+"""GPU parity of the DMMA (FP64 tensor-core) Gram kernels.
+
+The DMMA kernels serve linear-kernel Gram tiles at dyadic order 0 (BASELINE
+configs C3 / C5).  They must agree with the C oracle (rel 1e-10)
+and bitwise with the r01 FMA-pipe kernels (SK_NO_MMA=1), which form <dx, dy>
+in the same sequential FMA order (tools/dmma_probe.cu)."""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import random_paths, rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def mods():
+    from oracle import oracle as orc
+    from paper_2509_10613_b200 import ops
+    return ops, orc
+
+
+def cu(a):
+    return torch.as_tensor(np.asarray(a, dtype=np.float64), device="cuda")
+
+
+class _NoMMA:
+    def __enter__(self):
+        os.environ["SK_NO_MMA"] = "1"
+
+    def __exit__(self, *a):
+        os.environ.pop("SK_NO_MMA", None)
+
+
+SHAPES = [  # (n1, n2, L, d)
+    (1, 1, 2, 1), (3, 3, 3, 2), (9, 9, 9, 4), (8, 8, 17, 5), (17, 17, 33, 8),
+    (5, 12, 64, 3), (16, 16, 70, 16), (11, 11, 130, 13), (24, 24, 41, 7), (4, 4, 300, 16),
+]
+
+
+@pytest.mark.parametrize("n1,n2,L,d", SHAPES)
+def test_gram_forward_mma(mods, n1, n2, L, d):
+    ops, orc = mods
+    rng = np.random.default_rng(n1 * 1000 + L * 10 + d)
+    X = random_paths(rng, n1, L, d)
+    Y = random_paths(rng, n2, L, d) if n1 != n2 else None
+    want = orc.kernel_gram(X, Y, 0, 0)
+    got = ops.forward_gram(cu(X), None if Y is None else cu(Y), 0, 0, 0, 1.0).cpu().numpy()
+    assert rel_err(got, want) < TOL
+    with _NoMMA():
+        old = ops.forward_gram(cu(X), None if Y is None else cu(Y), 0, 0, 0, 1.0).cpu().numpy()
+    np.testing.assert_array_equal(got, old)
+    if Y is None:
+        np.testing.assert_array_equal(got, got.T)
+
+
+def test_gram_forward_mma_cross_lengths(mods):
+    ops, orc = mods
+    rng = np.random.default_rng(3)
+    X = random_paths(rng, 6, 40, 6)
+    Y = random_paths(rng, 5, 23, 6)  # shorter columns: no orientation swap
+    got = ops.forward_gram(cu(X), cu(Y), 0, 0, 0, 1.0).cpu().numpy()
+    assert rel_err(got, orc.kernel_gram(X, Y, 0, 0)) < TOL
+    got2 = ops.forward_gram(cu(Y), cu(X), 0, 0, 0, 1.0).cpu().numpy()  # swapped orientation
+    np.testing.assert_array_equal(got2, got.T)
+
+
+def test_gram_forward_mma_row_range(mods):
+    ops, orc = mods
+    rng = np.random.default_rng(4)
+    X = random_paths(rng, 20, 33, 8)
+    full = orc.kernel_gram(X, None, 0, 0)
+    got = ops.forward_gram(cu(X), None, 0, 0, 0, 1.0, rows=(5, 13)).cpu().numpy()
+    # a symmetric row block holds the upper triangle (b >= a); the rest is the
+    # all-gather's job (gram_dist.py)
+    for i, a in enumerate(range(5, 13)):
+        assert rel_err(got[i, a:], full[a, a:]) < TOL
