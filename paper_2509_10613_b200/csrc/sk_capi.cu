@@ -484,12 +484,50 @@ struct BwdPlan {
 };
 
 static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, int64_t M1c,
-                         int64_t M2c, int mode, int64_t npairs, int n2, int r0, int r1) {
+                         int64_t M2c, int mode, int64_t npairs, int n2, int r0, int r1,
+                         bool shared_cols) {
   int nch = 1;
   BwdShape s{};
   s.kind = kind;
   s.DP = pick_dp(d, nch);
   if (nch > 1) return fail(SK_INVALID_ARGUMENT, "backward supports d <= 32");
+  // Gram tiles of the linear kernel at dyadic order 0: DMMA backward
+  // (sk_mma_bwd.cuh).  SK_NO_MMA=1 keeps the r01 kernels.
+  s.MMA = shared_cols && kind == LINEAR && lamR == 0 && lamC == 0 && (s.DP == 8 || s.DP == 16) &&
+          !(std::getenv("SK_NO_MMA") && std::getenv("SK_NO_MMA")[0] == '1');
+  if (s.MMA) {
+    const char* w = std::getenv("SK_BWD_WPC");
+    s.WPC = (w && (w[0] == '2' || w[0] == '4')) ? w[0] - '0' : 3;
+    int per_warp = 0;
+    BwdFn fn = select_bwd_mma(s.DP, s.WPC, per_warp);
+    if (!fn) return fail(SK_INVALID_ARGUMENT, "no DMMA backward instance for this shape");
+    pl.shape = s;
+    pl.fn = fn;
+    pl.threads = 32 * s.WPC;
+    pl.smem_bytes = per_warp * (int)sizeof(double) * s.WPC;
+    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             pl.smem_bytes) != cudaSuccess)
+      (void)cudaGetLastError();
+    pl.nitems = gram_items(mode, n2, r0, r1, 8);
+    const int sms = device_sms();
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, pl.threads,
+                                                      pl.smem_bytes) != cudaSuccess || occ < 1) {
+      (void)cudaGetLastError();
+      occ = 1;
+    }
+    pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + s.WPC - 1) / s.WPC,
+                                                       (int64_t)occ * sms));
+    pl.slots = pl.blocks * s.WPC;
+    const int64_t nstrips = (M1c + 7) / 8, NT8 = (M2c + 10) / 8, NTS = 8 * (NT8 + 2);
+    pl.rowck_stride = nstrips * NTS * 32;
+    pl.colck_stride = nstrips * NT8 * 32 * 2;
+    pl.pck_stride = 0;
+    pl.row_stride = 8 * (NT8 + 2);  // per pair; 8 pairs per slot
+    pl.dbuf_stride = 0;
+    pl.gscr_stride = 8 * nstrips * 8 * s.DP + 8 * NT8 * s.DP;
+    return SK_OK;
+  }
   s.R = bwd_rows_per_lane(s.DP);
   s.FR = std::min(1 << std::min(lamR, 3), s.R);
   s.F = std::min(1 << std::min(lamC, 2), 4);
@@ -556,7 +594,8 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   BwdPlan pl;
   const int64_t npairs = mode == BATCH ? n1 : (r1 - r0) * n2;
   if (int rc = plan_backward(pl, kind, d, g.lamR, g.lamC, pb.M1c, pb.M2c, mode, npairs,
-                             (int)n2, (int)r0, (int)r1))
+                             (int)n2, (int)r0, (int)r1,
+                             mode != BATCH && !(mode == GRAM_CROSS && g.swap)))
     return rc;
   BwdLayout lo;
   lo.prepR = align_up(prep_elems(kind, g.nR, g.LR, pb.dpad) * sizeof(double), 256);
@@ -568,7 +607,8 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   lo.rowck = align_up((size_t)pl.slots * pl.rowck_stride * sizeof(double), 256);
   lo.colck = align_up((size_t)pl.slots * pl.colck_stride * sizeof(double), 256);
   lo.pck = align_up((size_t)pl.slots * pl.pck_stride * sizeof(double), 256);
-  lo.rows = align_up((size_t)pl.slots * pl.row_stride * 2 * sizeof(double), 256);
+  const int64_t row_slots = pl.slots * (pl.shape.MMA ? 8 : 1);  // DMMA: one row per pair of a tile
+  lo.rows = align_up((size_t)row_slots * pl.row_stride * 2 * sizeof(double), 256);
   lo.dbuf = align_up((size_t)pl.slots * pl.dbuf_stride * sizeof(double), 256);
   lo.gscr = align_up((size_t)pl.slots * pl.gscr_stride * sizeof(double), 256);
   lo.total = lo.prepR + lo.prepC + lo.rowck + lo.colck + lo.pck + lo.rows + lo.dbuf + lo.gscr;
@@ -601,7 +641,7 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   ba.pck_stride = pl.pck_stride;
   p += lo.pck;
   ba.hand = reinterpret_cast<double*>(p);
-  ba.adj = ba.hand + pl.slots * pl.row_stride;
+  ba.adj = ba.hand + row_slots * pl.row_stride;
   ba.row_stride = pl.row_stride;
   p += lo.rows;
   ba.dbuf = reinterpret_cast<double*>(p);

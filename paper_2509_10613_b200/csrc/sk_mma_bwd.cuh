@@ -1,0 +1,408 @@
+// sk_mma_bwd.cuh -- Gram backward (paper Alg. 4, the exact adjoint of the
+// solver) with every dense contraction on the FP64 tensor cores (DMMA).
+//
+// Replaces goursat_grid + goursat_backward + the gradient map of
+// kernel_backward (/root/reference/pkg/src/sigcore/_kernels.py:381-396,
+// 436-466; kernel_grad.py:27-61) for linear-kernel Gram tiles at dyadic
+// order 0 (BASELINE configs C3, C5).  The adjoint recursion is the
+// reference's, in push form (see sk_backward.cuh):
+//    d1[s,t] = d1[s+1,t] A(p[s+1,t]) + d1[s,t+1] A(p[s,t+1]) - d1[s+1,t+1] B(p[s+1,t+1])
+//    D[s,t]  = d1[s,t] ((k[s,t-1] + k[s-1,t]) (1/2 + p/6) + k[s-1,t-1] p/6)
+//    gx_i = sum_j D_ij dy_j,  gy_j = sum_i D_ij dx_i          (kernel_grad.py:53-54)
+//
+// Work per fine cell: p = <dx_i, dy_j> twice (forward checkpoint pass and the
+// block recompute), gx and gy: 4d FMAs, all on DMMA; the recurrences (forward
+// 7 DP ops, adjoint 10, recompute 7) on the FMA pipe.  In r01 the FMA-pipe-only
+// backward was issue/latency bound at ~10 % of the FP64 roofline.
+//
+// Mapping (one warp = one Gram tile of 8 pairs (a0+g, b), lane = 4g + u):
+//   phase A  forward wavefront exactly as sk_mma_fwd.cuh (lane u owns rows
+//            2u, 2u+1 of each 8-row strip, skew 1 column per lane), plus
+//            checkpoints: every lane's bottom row, diagonal layout
+//            rowck[strip][step][lane] (one coalesced 256-B store per step), and
+//            every lane's two values at its block boundaries colck[strip][blk][lane];
+//   phase B  strips bottom-up, blocks of 8 lane-relative columns right-to-left
+//            (lane u's block blk = columns 8blk-u .. 8blk-u+7):
+//            1. p tiles blk, blk-1 (DMMA, computed two blocks ahead into a 2-slot
+//               shared ring) -> each lane recomputes its 2 x 8 forward values in
+//               registers from its own checkpoints (no inter-lane dependency);
+//            2. reverse sweep of the block, lane u one column behind lane u+1,
+//               adjoint messages by __shfl_down_sync; D per cell into a 2-tile
+//               shared ring [column][row];
+//            3. tile blk's D is now complete for all 64 rows: gx += D dY (DMMA,
+//               accumulators in registers for the strip) and gy = D^T dX (DMMA
+//               over the 64 rows of the tile, dX staged in shared memory),
+//               added to the column path's scratch.
+//   Increment gradients are telescoped to point gradients once per tile and
+//   flushed with fp64 atomics (several tiles share a path), kernel_grad.py:55-60.
+#pragma once
+#include "sk_mma_fwd.cuh"
+
+namespace sk {
+
+template <int DP>
+struct MmaBwdCfg {
+  static constexpr int KS = DP / 4;            // k-steps of a p tile
+  static constexpr int NN = DP / 8;            // 8-wide component tiles (gx, gy)
+  static constexpr int PSTR = 36;              // double2 per p-tile column (conflict-free)
+  static constexpr int PTILE = 8 * PSTR;       // double2 per p tile
+  static constexpr int DSTR = 68;              // doubles per D column: 64 rows + 4
+  static constexpr int DTILE = 8 * DSTR;
+  static constexpr int XSTR = DP + 4;          // doubles per staged dX row
+  // block-input staging (cp.async, lane-private): 9 top-row values + 2 left
+  // values per lane, 8 strip-below messages per lane group, double buffered
+  static constexpr int STG = 11 * 32 + 8 * 8;
+  static constexpr int WARP_DOUBLES = 2 * PTILE * 2 + 2 * DTILE + 64 * XSTR + 2 * STG;
+};
+
+template <int DP, int WPC>
+__global__ void __launch_bounds__(32 * WPC, 1)
+gram_bwd_mma(Problem pb, BwdArgs ba) {
+  using Cf = MmaBwdCfg<DP>;
+  constexpr int KS = Cf::KS, NN = Cf::NN, PSTR = Cf::PSTR, DSTR = Cf::DSTR, XSTR = Cf::XSTR;
+  extern __shared__ double smem_mb[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, u = lane & 3;
+  double* wsm = smem_mb + (size_t)warp * Cf::WARP_DOUBLES;
+  double2* __restrict__ sP = reinterpret_cast<double2*>(wsm);  // 2 p tiles
+  double* __restrict__ sD = wsm + 2 * Cf::PTILE * 2;            // 2 D tiles
+  double* __restrict__ sX = sD + 2 * Cf::DTILE;                  // [64][XSTR]
+  double* __restrict__ sS = sX + 64 * XSTR;                      // [2][STG] staging
+  for (int e = lane; e < Cf::WARP_DOUBLES; e += 32) wsm[e] = 0.0;
+  __syncwarp();
+
+  const int M1 = pb.M1c, NC = pb.M2c;
+  const int nstrips = (M1 + 7) >> 3;
+  const int NT8 = (NC + 3 + 7) >> 3;
+  const int NTS = 8 * (NT8 + 2);  // diagonal rows per strip in rowck
+  const int u_star = ((M1 - 1) & 7) >> 1, r_star = (M1 - 1) & 1;
+  const int64_t slot = (int64_t)blockIdx.x * WPC + warp;
+  double* __restrict__ rowck = ba.rowck + slot * ba.rowck_stride;
+  double2* __restrict__ colck = reinterpret_cast<double2*>(ba.colck + slot * ba.colck_stride);
+  double* __restrict__ hrow = ba.hand + (slot * 8 + g) * ba.row_stride;
+  double* __restrict__ arow = ba.adj + (slot * 8 + g) * ba.row_stride;
+  double* __restrict__ gxs = ba.gscr + slot * ba.gscr_stride;  // [8][nstrips*8][DP]
+  double* __restrict__ gcs = gxs + (int64_t)8 * nstrips * 8 * DP;  // [8*NT8][DP]
+
+  for (int64_t item = slot; item < pb.nitems; item += (int64_t)gridDim.x * WPC) {
+    int a0, b;
+    gram_item(pb, item, 8, a0, b);
+    const int a = a0 + g;
+    const bool valid = a < pb.r1 && !(pb.mode == GRAM_SYM && a > b);
+    double wcot = 0.0;
+    if (valid) {
+      wcot = ba.cot[(int64_t)a * pb.n2 + b];
+      if (pb.mode == GRAM_SYM && a != b) wcot += ba.cot[(int64_t)b * pb.n2 + a];
+    }
+    const double* __restrict__ cpath = pb.C.p + (int64_t)b * pb.C.path_stride;
+
+    // p-tile B fragments: dX of pair h at strip row 8s + lane/4, component 4kk + lane%4
+    double bf[8][KS];
+    auto load_bf = [&](int strip) {
+      const int row = strip * 8 + g;
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const int ah = min(a0 + h, pb.r1 - 1);
+        const double* rp = pb.R.p + (int64_t)ah * pb.R.path_stride + (int64_t)row * DP + u;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) bf[h][kk] = (row < M1) ? __ldg(rp + 4 * kk) : 0.0;
+      }
+    };
+    auto loadA = [&](int T, double (&af)[KS]) {  // dY[col 8T + lane/4][4kk + lane%4]
+      const int col = 8 * T + g;
+      const double* cp = cpath + (int64_t)col * DP + u;
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) af[kk] = (col >= 0 && col < NC) ? __ldg(cp + 4 * kk) : 0.0;
+    };
+    auto ptile = [&](double2* ring, int slotT, int h, const double (&af)[KS]) {
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) dmma(c0, c1, af[kk], bf[h][kk]);
+      ring[(slotT * 8 + g) * PSTR + 4 * h + u] = make_double2(c0, c1);
+    };
+
+    // ------------------------------------------------ phase A: forward + checkpoints
+    for (int strip = 0; strip < nstrips; ++strip) {
+      __syncwarp();
+      load_bf(strip);
+      double af[KS];
+      loadA(0, af);
+#pragma unroll
+      for (int h = 0; h < 8; ++h) ptile(sP, 0, h, af);
+      double hcur[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) hcur[m] = 1.0;
+      if (strip > 0 && u == 0) {
+#pragma unroll
+        for (int m = 0; m < 8; m += 2) {
+          const double2 t = *reinterpret_cast<const double2*>(hrow + m);
+          hcur[m] = t.x;
+          hcur[m + 1] = t.y;
+        }
+      }
+      double* __restrict__ rck = rowck + (int64_t)strip * NTS * 32 + lane;
+      double2* __restrict__ cck = colck + (int64_t)strip * NT8 * 32 + lane;
+      double kl0 = 1.0, kl1 = 1.0, topc = 1.0, bot = 1.0;
+      const bool last = strip == nstrips - 1;
+      __syncwarp();
+      for (int T = 0; T < NT8; ++T) {
+        loadA(T + 1, af);  // consumed after the 8 steps
+        double hnxt[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) hnxt[m] = 1.0;
+        if (strip > 0 && u == 0) {
+#pragma unroll
+          for (int m = 0; m < 8; m += 2) {
+            const double2 t = *reinterpret_cast<const double2*>(hrow + 8 * (T + 1) + m);
+            hnxt[m] = t.x;
+            hnxt[m + 1] = t.y;
+          }
+        }
+        cck[(int64_t)T * 32] = make_double2(kl0, kl1);  // values at node column 8T - u
+        const int s0 = T & 1, s1 = (T - 1) & 1;          // slots of tiles T and T-1
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const int c = 8 * T + m - u;
+          const int sl = (m - u < 0) ? s1 : s0;
+          const double2 pv = sP[(sl * 8 + ((m - u) & 7)) * PSTR + lane];
+          double tv = __shfl_up_sync(0xffffffffu, bot, 1, 4);
+          if (u == 0) tv = hcur[m];
+          if (c >= 0 && c < NC) {
+            const Coef c0 = coef(pv.x), c1 = coef(pv.y);
+            const double k0 = cell(tv, kl0, topc, c0);
+            const double k1 = cell(k0, kl1, kl0, c1);
+            topc = tv;
+            kl0 = k0;
+            kl1 = k1;
+            bot = k1;
+            if (u == 3 && !last) hrow[c] = k1;
+          }
+          rck[(int64_t)(8 * T + m) * 32] = bot;  // diagonal index = column + lane
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m) hcur[m] = hnxt[m];
+        __syncwarp();  // tile T-1 is dead
+#pragma unroll
+        for (int h = 0; h < 8; ++h) ptile(sP, (T + 1) & 1, h, af);
+        __syncwarp();
+      }
+      // rows read by the phase-B recompute past the last step: keep them finite
+      for (int e = 8 * NT8; e < NTS; ++e) rck[(int64_t)e * 32] = bot;
+    }
+
+    // ------------------------------------------------ phase B: reverse sweep
+    for (int e = lane; e < 8 * NT8 * DP; e += 32) gcs[e] = 0.0;
+    for (int strip = nstrips - 1; strip >= 0; --strip) {
+      __syncwarp();
+      load_bf(strip);
+      // dX of the strip's 64 rows (8 pairs x 8 rows) for the gy B operand
+      for (int e = lane; e < 64 * (DP / 2); e += 32) {
+        const int R = e / (DP / 2), k2 = e % (DP / 2);
+        const int h = R >> 3, row = strip * 8 + (R & 7);
+        const int ah = min(a0 + h, pb.r1 - 1);
+        double2 v = make_double2(0.0, 0.0);
+        if (row < M1)
+          v = __ldg(reinterpret_cast<const double2*>(pb.R.p + (int64_t)ah * pb.R.path_stride +
+                                                     (int64_t)row * DP) + k2);
+        *reinterpret_cast<double2*>(sX + R * XSTR + 2 * k2) = v;
+      }
+      const int rb = strip * 8 + 2 * u;  // lane's first fine row (0-based)
+      const bool live0r = rb < M1, live1r = rb + 1 < M1;
+      const bool fin0 = (rb == M1 - 1), fin1 = (rb + 1 == M1 - 1);
+      const double* __restrict__ rck_own = rowck + (int64_t)strip * NTS * 32;
+      const double* __restrict__ rck_up = rowck + (int64_t)max(strip - 1, 0) * NTS * 32;
+      const double2* __restrict__ cck = colck + (int64_t)strip * NT8 * 32 + lane;
+      const bool below = strip < nstrips - 1;
+
+      // block inputs staged by cp.async one block ahead (lane-private records):
+      // top row tv[i] = node column 8blk-u+i of the row above the lane (i = 0..8),
+      // the lane's two values at node column 8blk-u, and (lane u = 3) the
+      // adjoint messages of the strip below at columns 8blk-3 .. 8blk+4
+      auto stage_block = [&](int blk) {
+        double* st = sS + (blk & 1) * Cf::STG;
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+          const double* src;
+          if (u > 0) src = rck_own + (int64_t)max(8 * blk - 2 + i, 0) * 32 + lane - 1;
+          else src = rck_up + (int64_t)(8 * blk + 2 + i) * 32 + 4 * g + 3;
+          cp_async8(st + i * 32 + lane, src, u > 0 || strip > 0);
+        }
+        cp_async16(st + 9 * 32 + 2 * lane, cck + (int64_t)blk * 32, true);
+        if (u == 3) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int c = 8 * blk - 3 + i;
+            const bool v = below && c >= 0 && c < NC;
+            cp_async8(st + 11 * 32 + i * 8 + g, arow + (v ? c : 0), v);
+          }
+        }
+        cp_async_commit();
+      };
+      auto loadGX = [&](int T, double (&gb)[2][NN]) {  // dY[col 8T + 4kk + lane%4][8n + lane/4]
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          const int col = 8 * T + 4 * kk + u;
+#pragma unroll
+          for (int n = 0; n < NN; ++n)
+            gb[kk][n] = (col >= 0 && col < NC) ? __ldg(cpath + (int64_t)col * DP + 8 * n + g) : 0.0;
+        }
+      };
+
+      double gx[8][NN][2];
+#pragma unroll
+      for (int h = 0; h < 8; ++h)
+#pragma unroll
+        for (int n = 0; n < NN; ++n) gx[h][n][0] = gx[h][n][1] = 0.0;
+      {
+        double af[KS];
+        loadA(NT8 - 1, af);
+#pragma unroll
+        for (int h = 0; h < 8; ++h) ptile(sP, (NT8 - 1) & 1, h, af);
+        loadA(NT8 - 2, af);
+#pragma unroll
+        for (int h = 0; h < 8; ++h) ptile(sP, (NT8 - 2) & 1, h, af);
+      }
+      stage_block(NT8 - 1);
+      double aR0 = 0.0, aR1 = 0.0, bR0 = 0.0, bR1 = 0.0, sendm = 0.0;
+
+      for (int blk = NT8 - 1; blk >= 0; --blk) {
+        double af[KS], gb[2][NN];
+        loadA(blk - 2, af);   // p tile blk-2, computed after the sweep
+        loadGX(blk, gb);      // gx B operand of tile blk
+        cp_async_wait<0>();
+        __syncwarp();         // staged inputs, p tiles blk and blk-1 visible
+        const double* st = sS + (blk & 1) * Cf::STG;
+        if (blk > 0) stage_block(blk - 1);
+        double tv[9];
+#pragma unroll
+        for (int i = 0; i < 9; ++i) {
+          const int cc = 8 * blk - u + i;
+          const double v = (u == 0 && strip == 0) ? 1.0 : st[i * 32 + lane];
+          tv[i] = (cc <= 0) ? 1.0 : (cc > NC ? 0.0 : v);
+        }
+        const double2 kleft = *reinterpret_cast<const double2*>(st + 9 * 32 + 2 * lane);
+
+        // ---- 1. recompute the lane's 2 x 8 forward values (registers)
+        double K0[8], K1[8];
+        {
+          double k0 = kleft.x, k1 = kleft.y;
+#pragma unroll
+          for (int kap = 0; kap < 8; ++kap) {
+            const int c = 8 * blk - u + kap;
+            double2 pv = sP[((((c >> 3) & 1) * 8) + (c & 7)) * PSTR + lane];
+            if (c < 0 || c >= NC) pv = make_double2(0.0, 0.0);
+            const Coef c0 = coef(pv.x), c1 = coef(pv.y);
+            const double n0 = cell(tv[kap + 1], k0, tv[kap], c0);
+            const double n1 = cell(n0, k1, k0, c1);
+            k0 = n0;
+            k1 = n1;
+            K0[kap] = n0;
+            K1[kap] = n1;
+          }
+        }
+
+        // ---- 2. reverse sweep, lane u one column behind lane u+1
+#pragma unroll
+        for (int kap = 7; kap >= 0; --kap) {
+          const int c = 8 * blk - u + kap;
+          const bool colv = (c >= 0) && (c < NC);
+          double recv = __shfl_down_sync(0xffffffffu, sendm, 1, 4);
+          if (u == 3) recv = st[11 * 32 + kap * 8 + g];
+          double2 pv = sP[((((c >> 3) & 1) * 8) + (c & 7)) * PSTR + lane];
+          if (!colv) pv = make_double2(0.0, 0.0);
+          const Coef c0 = coef(pv.x), c1 = coef(pv.y);
+          const bool fin = colv && (c == NC - 1);
+          // row 1 (bottom)
+          double lam1 = aR1 + recv;
+          if (fin && fin1) lam1 += wcot;
+          lam1 = (colv && live1r) ? lam1 : 0.0;
+          const double a1 = c1.A * lam1, b1 = c1.B * lam1;
+          const double kL1 = kap > 0 ? K1[kap - 1] : kleft.y;
+          const double kD1 = kap > 0 ? K0[kap - 1] : kleft.x;
+          const double p61 = pv.y * (1.0 / 6.0);
+          const double D1 = lam1 * fma(kL1 + K0[kap], 0.5 + p61, kD1 * p61);
+          const double m1 = a1 - bR1;
+          aR1 = a1;
+          bR1 = b1;
+          // row 0 (top)
+          double lam0 = aR0 + m1;
+          if (fin && fin0) lam0 += wcot;
+          lam0 = (colv && live0r) ? lam0 : 0.0;
+          const double a0v = c0.A * lam0, b0v = c0.B * lam0;
+          const double kL0 = kap > 0 ? K0[kap - 1] : kleft.x;
+          const double p60 = pv.x * (1.0 / 6.0);
+          const double D0 = lam0 * fma(kL0 + tv[kap + 1], 0.5 + p60, tv[kap] * p60);
+          sendm = a0v - bR0;
+          aR0 = a0v;
+          bR0 = b0v;
+          *reinterpret_cast<double2*>(sD + ((c >> 3) & 1) * Cf::DTILE + (c & 7) * DSTR + 2 * lane) =
+              make_double2(D0, D1);
+          if (u == 0 && colv) arow[c] = sendm;
+        }
+        __syncwarp();  // tile blk's D complete; p tile blk dead
+
+        // ---- 3. gradient maps on tile blk, then p tile blk-2 into tile blk's slot
+        const double* __restrict__ Dt = sD + (blk & 1) * Cf::DTILE;
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+#pragma unroll
+          for (int h = 0; h < 8; ++h) {
+            const double av_ = Dt[(4 * kk + u) * DSTR + 8 * h + g];
+#pragma unroll
+            for (int n = 0; n < NN; ++n) dmma(gx[h][n][0], gx[h][n][1], av_, gb[kk][n]);
+          }
+        }
+#pragma unroll
+        for (int n = 0; n < NN; ++n) {
+          double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 16; ++kk)
+            dmma(c0, c1, Dt[g * DSTR + 4 * kk + u], sX[(4 * kk + u) * XSTR + 8 * n + g]);
+          double2* q = reinterpret_cast<double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u);
+          const double2 o = *q;
+          *q = make_double2(o.x + c0, o.y + c1);
+        }
+#pragma unroll
+        for (int h = 0; h < 8; ++h) ptile(sP, blk & 1, h, af);
+        __syncwarp();
+      }
+      // strip rows' dF/d(dx): plain stores (every row belongs to one strip)
+#pragma unroll
+      for (int h = 0; h < 8; ++h)
+#pragma unroll
+        for (int n = 0; n < NN; ++n)
+          *reinterpret_cast<double2*>(gxs + ((int64_t)h * nstrips * 8 + strip * 8 + g) * DP + 8 * n +
+                                      2 * u) = make_double2(gx[h][n][0], gx[h][n][1]);
+    }
+    __syncwarp();
+
+    // ------------------------------------------------ flush (kernel_grad.py:55-60)
+    const int dR = ba.d;
+    for (int h = 0; h < 8; ++h) {
+      const int ah = a0 + h;
+      if (ah >= pb.r1 || (pb.mode == GRAM_SYM && ah > b)) continue;  // warp-uniform
+      double* gR = ba.gradR + (int64_t)ah * ba.gR_path;
+      const double* gh = gxs + (int64_t)h * nstrips * 8 * DP;
+      for (int e = lane; e < (M1 + 1) * dR; e += 32) {
+        const int p = e / dR, k = e % dR;
+        double v = 0.0;
+        if (p >= 1) v += gh[(int64_t)(p - 1) * DP + k];
+        if (p < M1) v -= gh[(int64_t)p * DP + k];
+        atomicAdd(gR + e, v);
+      }
+    }
+    {
+      double* gC = ba.gradC + (int64_t)b * ba.gC_path;
+      for (int e = lane; e < (NC + 1) * dR; e += 32) {
+        const int p = e / dR, k = e % dR;
+        double v = 0.0;
+        if (p >= 1) v += gcs[(int64_t)(p - 1) * DP + k];
+        if (p < NC) v -= gcs[(int64_t)p * DP + k];
+        atomicAdd(gC + e, v);
+      }
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace sk

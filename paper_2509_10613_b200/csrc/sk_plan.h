@@ -26,10 +26,13 @@ using BwdFn = void (*)(Problem, BwdArgs);
 struct BwdShape {
   int kind;
   int DP, R, FR, F;  // as FwdShape; lanes per pair fixed at 32, CB = 8 / F
+  bool MMA;          // DMMA Gram tile kernel (sk_mma_bwd.cuh): LINEAR, order 0, DP 8/16
+  int WPC;           // warps per CTA of the DMMA kernel
 };
 
 BwdFn select_bwd_linear(const BwdShape& s, int& smem_doubles);
 BwdFn select_bwd_rbf(const BwdShape& s, int& smem_doubles);
+BwdFn select_bwd_mma(int DP, int WPC, int& smem_doubles_per_warp);
 
 // Per-kind instance tables (one translation unit each, compiled in parallel).
 FwdFn select_fwd_linear(const FwdShape& s, int& smem);

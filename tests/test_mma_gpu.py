@@ -79,3 +79,42 @@ def test_gram_forward_mma_row_range(mods):
     # all-gather's job (gram_dist.py)
     for i, a in enumerate(range(5, 13)):
         assert rel_err(got[i, a:], full[a, a:]) < TOL
+
+
+BWD_SHAPES = [  # (n1, n2, L, d) -- DMMA backward serves 4 < d <= 16
+    (1, 1, 2, 5), (3, 3, 3, 6), (9, 9, 9, 8), (8, 8, 17, 5), (17, 17, 33, 8),
+    (5, 12, 64, 7), (16, 16, 70, 16), (11, 11, 130, 13), (10, 10, 41, 12),
+]
+
+
+@pytest.mark.parametrize("n1,n2,L,d", BWD_SHAPES)
+def test_gram_backward_mma(mods, n1, n2, L, d):
+    ops, orc = mods
+    rng = np.random.default_rng(n1 * 7 + L * 3 + d)
+    X = random_paths(rng, n1, L, d)
+    Y = random_paths(rng, n2, L, d) if n1 != n2 else None
+    C = rng.standard_normal((n1, n2))
+    want = orc.gram_backward(X, Y, C, 0, 0)
+    gx, gy = ops.backward_gram(cu(X), None if Y is None else cu(Y), 0, 0, 0, 1.0, cu(C))
+    if Y is None:
+        assert rel_err(gx.cpu().numpy(), want) < TOL
+    else:
+        assert rel_err(gx.cpu().numpy(), want[0]) < TOL
+        assert rel_err(gy.cpu().numpy(), want[1]) < TOL
+    with _NoMMA():
+        ox, oy = ops.backward_gram(cu(X), None if Y is None else cu(Y), 0, 0, 0, 1.0, cu(C))
+    assert rel_err(gx.cpu().numpy(), ox.cpu().numpy()) < 1e-13
+
+
+def test_gram_backward_mma_row_blocks_sum(mods):
+    """Row blocks (the multi-GPU split, gram_dist.py) add up to the full gradient."""
+    ops, orc = mods
+    rng = np.random.default_rng(11)
+    X = random_paths(rng, 21, 37, 8)
+    C = rng.standard_normal((21, 21))
+    full, _ = ops.backward_gram(cu(X), None, 0, 0, 0, 1.0, cu(C))
+    acc = torch.zeros_like(full)
+    for r in ((0, 4), (4, 13), (13, 21)):
+        ops.backward_gram(cu(X), None, 0, 0, 0, 1.0, cu(C), rows=r, grad_x=acc)
+    assert rel_err(acc.cpu().numpy(), full.cpu().numpy()) < 1e-13
+    assert rel_err(full.cpu().numpy(), orc.gram_backward(X, None, C, 0, 0)) < TOL
