@@ -523,9 +523,9 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
     pl.rowck_stride = nstrips * NTS * 32;
     pl.colck_stride = nstrips * NT8 * 32 * 2;
     pl.pck_stride = 0;
-    pl.row_stride = 8 * (NT8 + 2);  // per pair; 8 pairs per slot
+    pl.row_stride = 8 * (NT8 + 3);  // per pair; 8 pairs per slot (adjoint row at column + 3)
     pl.dbuf_stride = 0;
-    pl.gscr_stride = 8 * nstrips * 8 * s.DP + 8 * NT8 * s.DP;
+    pl.gscr_stride = 8 * NT8 * s.DP;
     return SK_OK;
   }
   s.R = bwd_rows_per_lane(s.DP);

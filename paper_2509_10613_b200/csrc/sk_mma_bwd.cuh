@@ -36,6 +36,8 @@
 //   Increment gradients are telescoped to point gradients once per tile and
 //   flushed with fp64 atomics (several tiles share a path), kernel_grad.py:55-60.
 #pragma once
+#include <type_traits>
+
 #include "sk_mma_fwd.cuh"
 
 namespace sk {
@@ -75,14 +77,12 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
   const int nstrips = (M1 + 7) >> 3;
   const int NT8 = (NC + 3 + 7) >> 3;
   const int NTS = 8 * (NT8 + 2);  // diagonal rows per strip in rowck
-  const int u_star = ((M1 - 1) & 7) >> 1, r_star = (M1 - 1) & 1;
   const int64_t slot = (int64_t)blockIdx.x * WPC + warp;
   double* __restrict__ rowck = ba.rowck + slot * ba.rowck_stride;
   double2* __restrict__ colck = reinterpret_cast<double2*>(ba.colck + slot * ba.colck_stride);
   double* __restrict__ hrow = ba.hand + (slot * 8 + g) * ba.row_stride;
   double* __restrict__ arow = ba.adj + (slot * 8 + g) * ba.row_stride;
-  double* __restrict__ gxs = ba.gscr + slot * ba.gscr_stride;  // [8][nstrips*8][DP]
-  double* __restrict__ gcs = gxs + (int64_t)8 * nstrips * 8 * DP;  // [8*NT8][DP]
+  double* __restrict__ gcs = ba.gscr + slot * ba.gscr_stride;  // column gradients [8*NT8][DP]
 
   for (int64_t item = slot; item < pb.nitems; item += (int64_t)gridDim.x * WPC) {
     int a0, b;
@@ -145,7 +145,9 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       double kl0 = 1.0, kl1 = 1.0, topc = 1.0, bot = 1.0;
       const bool last = strip == nstrips - 1;
       __syncwarp();
-      for (int T = 0; T < NT8; ++T) {
+      // one 8-step iteration; EDGE iterations hold columns outside [0, NC)
+      auto iterA = [&](auto edge, int T) {
+        constexpr bool EDGE = decltype(edge)::value;
         loadA(T + 1, af);  // consumed after the 8 steps
         double hnxt[8];
 #pragma unroll
@@ -167,7 +169,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           const double2 pv = sP[(sl * 8 + ((m - u) & 7)) * PSTR + lane];
           double tv = __shfl_up_sync(0xffffffffu, bot, 1, 4);
           if (u == 0) tv = hcur[m];
-          if (c >= 0 && c < NC) {
+          if (!EDGE || (c >= 0 && c < NC)) {
             const Coef c0 = coef(pv.x), c1 = coef(pv.y);
             const double k0 = cell(tv, kl0, topc, c0);
             const double k1 = cell(k0, kl1, kl0, c1);
@@ -185,6 +187,10 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
 #pragma unroll
         for (int h = 0; h < 8; ++h) ptile(sP, (T + 1) & 1, h, af);
         __syncwarp();
+      };
+      for (int T = 0; T < NT8; ++T) {
+        if (T == 0 || 8 * T + 8 > NC) iterA(std::true_type{}, T);
+        else iterA(std::false_type{}, T);
       }
       // rows read by the phase-B recompute past the last step: keep them finite
       for (int e = 8 * NT8; e < NTS; ++e) rck[(int64_t)e * 32] = bot;
@@ -207,7 +213,6 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         *reinterpret_cast<double2*>(sX + R * XSTR + 2 * k2) = v;
       }
       const int rb = strip * 8 + 2 * u;  // lane's first fine row (0-based)
-      const bool live0r = rb < M1, live1r = rb + 1 < M1;
       const bool fin0 = (rb == M1 - 1), fin1 = (rb + 1 == M1 - 1);
       const double* __restrict__ rck_own = rowck + (int64_t)strip * NTS * 32;
       const double* __restrict__ rck_up = rowck + (int64_t)max(strip - 1, 0) * NTS * 32;
@@ -217,7 +222,8 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       // block inputs staged by cp.async one block ahead (lane-private records):
       // top row tv[i] = node column 8blk-u+i of the row above the lane (i = 0..8),
       // the lane's two values at node column 8blk-u, and (lane u = 3) the
-      // adjoint messages of the strip below at columns 8blk-3 .. 8blk+4
+      // adjoint messages of the strip below at columns 8blk-3 .. 8blk+4, which
+      // arow holds at index column + 3 (16-byte aligned per block)
       auto stage_block = [&](int blk) {
         double* st = sS + (blk & 1) * Cf::STG;
 #pragma unroll
@@ -230,11 +236,8 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         cp_async16(st + 9 * 32 + 2 * lane, cck + (int64_t)blk * 32, true);
         if (u == 3) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int c = 8 * blk - 3 + i;
-            const bool v = below && c >= 0 && c < NC;
-            cp_async8(st + 11 * 32 + i * 8 + g, arow + (v ? c : 0), v);
-          }
+          for (int i = 0; i < 8; i += 2)
+            cp_async16(st + 11 * 32 + g * 8 + i, arow + 8 * blk + i, below);
         }
         cp_async_commit();
       };
@@ -265,7 +268,9 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       stage_block(NT8 - 1);
       double aR0 = 0.0, aR1 = 0.0, bR0 = 0.0, bR1 = 0.0, sendm = 0.0;
 
-      for (int blk = NT8 - 1; blk >= 0; --blk) {
+      // one block; EDGE blocks hold columns outside [0, NC) or the final cell
+      auto blockB = [&](auto edge, int blk) {
+        constexpr bool EDGE = decltype(edge)::value;
         double af[KS], gb[2][NN];
         loadA(blk - 2, af);   // p tile blk-2, computed after the sweep
         loadGX(blk, gb);      // gx B operand of tile blk
@@ -276,9 +281,13 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         double tv[9];
 #pragma unroll
         for (int i = 0; i < 9; ++i) {
-          const int cc = 8 * blk - u + i;
           const double v = (u == 0 && strip == 0) ? 1.0 : st[i * 32 + lane];
-          tv[i] = (cc <= 0) ? 1.0 : (cc > NC ? 0.0 : v);
+          if constexpr (EDGE) {
+            const int cc = 8 * blk - u + i;
+            tv[i] = (cc <= 0) ? 1.0 : (cc > NC ? 0.0 : v);
+          } else {
+            tv[i] = v;
+          }
         }
         const double2 kleft = *reinterpret_cast<const double2*>(st + 9 * 32 + 2 * lane);
 
@@ -290,7 +299,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           for (int kap = 0; kap < 8; ++kap) {
             const int c = 8 * blk - u + kap;
             double2 pv = sP[((((c >> 3) & 1) * 8) + (c & 7)) * PSTR + lane];
-            if (c < 0 || c >= NC) pv = make_double2(0.0, 0.0);
+            if (EDGE && (c < 0 || c >= NC)) pv = make_double2(0.0, 0.0);
             const Coef c0 = coef(pv.x), c1 = coef(pv.y);
             const double n0 = cell(tv[kap + 1], k0, tv[kap], c0);
             const double n1 = cell(n0, k1, k0, c1);
@@ -301,21 +310,21 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           }
         }
 
-        // ---- 2. reverse sweep, lane u one column behind lane u+1
+        // ---- 2. reverse sweep, lane u one column behind lane u+1.  Dead rows
+        // (>= M1) and columns (>= NC) lie below / right of the seeded final
+        // cell, so their adjoint is exactly 0 without masking; columns < 0
+        // (block 0) only feed D slots that are never consumed.
 #pragma unroll
         for (int kap = 7; kap >= 0; --kap) {
           const int c = 8 * blk - u + kap;
-          const bool colv = (c >= 0) && (c < NC);
           double recv = __shfl_down_sync(0xffffffffu, sendm, 1, 4);
-          if (u == 3) recv = st[11 * 32 + kap * 8 + g];
+          if (u == 3) recv = st[11 * 32 + g * 8 + kap];
           double2 pv = sP[((((c >> 3) & 1) * 8) + (c & 7)) * PSTR + lane];
-          if (!colv) pv = make_double2(0.0, 0.0);
+          if (EDGE && (c < 0 || c >= NC)) pv = make_double2(0.0, 0.0);
           const Coef c0 = coef(pv.x), c1 = coef(pv.y);
-          const bool fin = colv && (c == NC - 1);
           // row 1 (bottom)
           double lam1 = aR1 + recv;
-          if (fin && fin1) lam1 += wcot;
-          lam1 = (colv && live1r) ? lam1 : 0.0;
+          if (EDGE && fin1 && c == NC - 1) lam1 += wcot;
           const double a1 = c1.A * lam1, b1 = c1.B * lam1;
           const double kL1 = kap > 0 ? K1[kap - 1] : kleft.y;
           const double kD1 = kap > 0 ? K0[kap - 1] : kleft.x;
@@ -326,8 +335,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           bR1 = b1;
           // row 0 (top)
           double lam0 = aR0 + m1;
-          if (fin && fin0) lam0 += wcot;
-          lam0 = (colv && live0r) ? lam0 : 0.0;
+          if (EDGE && fin0 && c == NC - 1) lam0 += wcot;
           const double a0v = c0.A * lam0, b0v = c0.B * lam0;
           const double kL0 = kap > 0 ? K0[kap - 1] : kleft.x;
           const double p60 = pv.x * (1.0 / 6.0);
@@ -337,7 +345,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           bR0 = b0v;
           *reinterpret_cast<double2*>(sD + ((c >> 3) & 1) * Cf::DTILE + (c & 7) * DSTR + 2 * lane) =
               make_double2(D0, D1);
-          if (u == 0 && colv) arow[c] = sendm;
+          if (u == 0 && (!EDGE || c >= 0)) arow[c + 3] = sendm;
         }
         __syncwarp();  // tile blk's D complete; p tile blk dead
 
@@ -352,46 +360,62 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
             for (int n = 0; n < NN; ++n) dmma(gx[h][n][0], gx[h][n][1], av_, gb[kk][n]);
           }
         }
+        // gy = D^T dX over the tile's 64 rows: four independent DMMA chains per
+        // component tile (fixed order, so results stay deterministic)
 #pragma unroll
         for (int n = 0; n < NN; ++n) {
-          double c0 = 0.0, c1 = 0.0;
+          double c[4][2];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) c[j][0] = c[j][1] = 0.0;
 #pragma unroll
           for (int kk = 0; kk < 16; ++kk)
-            dmma(c0, c1, Dt[g * DSTR + 4 * kk + u], sX[(4 * kk + u) * XSTR + 8 * n + g]);
+            dmma(c[kk & 3][0], c[kk & 3][1], Dt[g * DSTR + 4 * kk + u],
+                 sX[(4 * kk + u) * XSTR + 8 * n + g]);
           double2* q = reinterpret_cast<double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u);
           const double2 o = *q;
-          *q = make_double2(o.x + c0, o.y + c1);
+          *q = make_double2(o.x + ((c[0][0] + c[1][0]) + (c[2][0] + c[3][0])),
+                            o.y + ((c[0][1] + c[1][1]) + (c[2][1] + c[3][1])));
         }
 #pragma unroll
         for (int h = 0; h < 8; ++h) ptile(sP, blk & 1, h, af);
         __syncwarp();
+      };
+      for (int blk = NT8 - 1; blk >= 0; --blk) {
+        if (blk == 0 || 8 * blk + 8 >= NC) blockB(std::true_type{}, blk);
+        else blockB(std::false_type{}, blk);
       }
-      // strip rows' dF/d(dx): plain stores (every row belongs to one strip)
+
+      // row-side gradient of the strip, telescoped to points (kernel_grad.py:55-60):
+      // point r gets gx[r-1] - gx[r]; row r-1 sits 4 lanes up (same u)
+      const int dR = ba.d;
+      const int rho = strip * 8 + g;
 #pragma unroll
-      for (int h = 0; h < 8; ++h)
+      for (int h = 0; h < 8; ++h) {
+        const int ah = a0 + h;
+        const bool hv = ah < pb.r1 && !(pb.mode == GRAM_SYM && ah > b);  // warp-uniform
 #pragma unroll
-        for (int n = 0; n < NN; ++n)
-          *reinterpret_cast<double2*>(gxs + ((int64_t)h * nstrips * 8 + strip * 8 + g) * DP + 8 * n +
-                                      2 * u) = make_double2(gx[h][n][0], gx[h][n][1]);
+        for (int n = 0; n < NN; ++n) {
+          const double up0 = __shfl_up_sync(0xffffffffu, gx[h][n][0], 4);
+          const double up1 = __shfl_up_sync(0xffffffffu, gx[h][n][1], 4);
+          if (!hv || rho >= M1) continue;
+          double* gp = ba.gradR + (int64_t)ah * ba.gR_path;
+          const int k = 8 * n + 2 * u;
+          const double v0 = (g > 0 ? up0 : 0.0) - gx[h][n][0];
+          const double v1 = (g > 0 ? up1 : 0.0) - gx[h][n][1];
+          if (k < dR) atomicAdd(gp + (int64_t)rho * dR + k, v0);
+          if (k + 1 < dR) atomicAdd(gp + (int64_t)rho * dR + k + 1, v1);
+          if (g == 7 || rho == M1 - 1) {  // point rho + 1 (next strip's row 0 adds the rest)
+            if (k < dR) atomicAdd(gp + (int64_t)(rho + 1) * dR + k, gx[h][n][0]);
+            if (k + 1 < dR) atomicAdd(gp + (int64_t)(rho + 1) * dR + k + 1, gx[h][n][1]);
+          }
+        }
+      }
     }
     __syncwarp();
 
-    // ------------------------------------------------ flush (kernel_grad.py:55-60)
-    const int dR = ba.d;
-    for (int h = 0; h < 8; ++h) {
-      const int ah = a0 + h;
-      if (ah >= pb.r1 || (pb.mode == GRAM_SYM && ah > b)) continue;  // warp-uniform
-      double* gR = ba.gradR + (int64_t)ah * ba.gR_path;
-      const double* gh = gxs + (int64_t)h * nstrips * 8 * DP;
-      for (int e = lane; e < (M1 + 1) * dR; e += 32) {
-        const int p = e / dR, k = e % dR;
-        double v = 0.0;
-        if (p >= 1) v += gh[(int64_t)(p - 1) * DP + k];
-        if (p < M1) v -= gh[(int64_t)p * DP + k];
-        atomicAdd(gR + e, v);
-      }
-    }
+    // column-side gradient (summed over the tile's pairs and strips), telescoped
     {
+      const int dR = ba.d;
       double* gC = ba.gradC + (int64_t)b * ba.gC_path;
       for (int e = lane; e < (NC + 1) * dR; e += 32) {
         const int p = e / dR, k = e % dR;
