@@ -96,16 +96,19 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
     }
     const double* __restrict__ cpath = pb.C.p + (int64_t)b * pb.C.path_stride;
 
-    // p-tile B fragments: dX of pair h at strip row 8s + lane/4, component 4kk + lane%4
-    double bf[8][KS];
-    auto load_bf = [&](int strip) {
-      const int row = strip * 8 + g;
-#pragma unroll
-      for (int h = 0; h < 8; ++h) {
+    // the strip's dX (8 pairs x 8 rows) staged in shared memory: B operand of
+    // the p tiles (row 8h + lane/4, component 4kk + lane%4) and of gy
+    // (row 4kk + lane%4, component 8n + lane/4); both reads are conflict-free
+    auto stage_x = [&](int strip) {
+      for (int e = lane; e < 64 * (DP / 2); e += 32) {
+        const int R = e / (DP / 2), k2 = e % (DP / 2);
+        const int h = R >> 3, row = strip * 8 + (R & 7);
         const int ah = min(a0 + h, pb.r1 - 1);
-        const double* rp = pb.R.p + (int64_t)ah * pb.R.path_stride + (int64_t)row * DP + u;
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk) bf[h][kk] = (row < M1) ? __ldg(rp + 4 * kk) : 0.0;
+        double2 v = make_double2(0.0, 0.0);
+        if (row < M1)
+          v = __ldg(reinterpret_cast<const double2*>(pb.R.p + (int64_t)ah * pb.R.path_stride +
+                                                     (int64_t)row * DP) + k2);
+        *reinterpret_cast<double2*>(sX + R * XSTR + 2 * k2) = v;
       }
     };
     auto loadA = [&](int T, double (&af)[KS]) {  // dY[col 8T + lane/4][4kk + lane%4]
@@ -117,14 +120,15 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
     auto ptile = [&](double2* ring, int slotT, int h, const double (&af)[KS]) {
       double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-      for (int kk = 0; kk < KS; ++kk) dmma(c0, c1, af[kk], bf[h][kk]);
+      for (int kk = 0; kk < KS; ++kk) dmma(c0, c1, af[kk], sX[(8 * h + g) * XSTR + 4 * kk + u]);
       ring[(slotT * 8 + g) * PSTR + 4 * h + u] = make_double2(c0, c1);
     };
 
     // ------------------------------------------------ phase A: forward + checkpoints
     for (int strip = 0; strip < nstrips; ++strip) {
       __syncwarp();
-      load_bf(strip);
+      stage_x(strip);
+      __syncwarp();
       double af[KS];
       loadA(0, af);
 #pragma unroll
@@ -200,18 +204,8 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
     for (int e = lane; e < 8 * NT8 * DP; e += 32) gcs[e] = 0.0;
     for (int strip = nstrips - 1; strip >= 0; --strip) {
       __syncwarp();
-      load_bf(strip);
-      // dX of the strip's 64 rows (8 pairs x 8 rows) for the gy B operand
-      for (int e = lane; e < 64 * (DP / 2); e += 32) {
-        const int R = e / (DP / 2), k2 = e % (DP / 2);
-        const int h = R >> 3, row = strip * 8 + (R & 7);
-        const int ah = min(a0 + h, pb.r1 - 1);
-        double2 v = make_double2(0.0, 0.0);
-        if (row < M1)
-          v = __ldg(reinterpret_cast<const double2*>(pb.R.p + (int64_t)ah * pb.R.path_stride +
-                                                     (int64_t)row * DP) + k2);
-        *reinterpret_cast<double2*>(sX + R * XSTR + 2 * k2) = v;
-      }
+      stage_x(strip);
+      __syncwarp();
       const int rb = strip * 8 + 2 * u;  // lane's first fine row (0-based)
       const bool fin0 = (rb == M1 - 1), fin1 = (rb + 1 == M1 - 1);
       const double* __restrict__ rck_own = rowck + (int64_t)strip * NTS * 32;
