@@ -674,6 +674,7 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   ba.atomic = mode == BATCH ? 0 : 1;
   ba.cot = cot;
   ba.values = values;
+  ba.exp = std::getenv("SK_EXP") ? std::atoi(std::getenv("SK_EXP")) : 0;
   pl.fn<<<(unsigned)pl.blocks, pl.threads, pl.smem_bytes, st>>>(pb, ba);
   SK_CUDA(cudaGetLastError());
   return SK_OK;

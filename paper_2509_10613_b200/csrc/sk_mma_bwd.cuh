@@ -51,8 +51,8 @@ struct MmaBwdCfg {
   static constexpr int DSTR = 68;              // doubles per D column: 64 rows + 4
   static constexpr int DTILE = 8 * DSTR;
   static constexpr int XSTR = DP + 4;          // doubles per staged dX row
-  // block-input staging (cp.async, lane-private): 9 top-row values + 2 left
-  // values per lane, 8 strip-below messages per lane group, double buffered
+  // block-input staging (cp.async, lane-private, double buffered): 9 top-row
+  // values + 2 left values per lane, 8 strip-below messages per lane group
   static constexpr int STG = 11 * 32 + 8 * 8;
   static constexpr int WARP_DOUBLES = 2 * PTILE * 2 + 2 * DTILE + 64 * XSTR + 2 * STG;
 };
@@ -125,7 +125,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
     };
 
     // ------------------------------------------------ phase A: forward + checkpoints
-    for (int strip = 0; strip < nstrips; ++strip) {
+    for (int strip = 0; strip < ((ba.exp & 2) ? 0 : nstrips); ++strip) {
       __syncwarp();
       stage_x(strip);
       __syncwarp();
@@ -144,7 +144,9 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           hcur[m + 1] = t.y;
         }
       }
-      double* __restrict__ rck = rowck + (int64_t)strip * NTS * 32 + lane;
+      // checkpoint rows keep lane (g, u) at position 8u + g, so lane u = 3's
+      // values (the strip handoff) are one contiguous 64-B quarter row
+      double* __restrict__ rck = rowck + (int64_t)strip * NTS * 32 + 8 * u + g;
       double2* __restrict__ cck = colck + (int64_t)strip * NT8 * 32 + lane;
       double kl0 = 1.0, kl1 = 1.0, topc = 1.0, bot = 1.0;
       const bool last = strip == nstrips - 1;
@@ -168,6 +170,11 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         const int s0 = T & 1, s1 = (T - 1) & 1;          // slots of tiles T and T-1
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
+          if (m == 3) __syncwarp();  // lane 3 read tile T-1 last at step 2: its slot is free
+          if (m >= 3 && m <= 6) {    // tile T+1 (two pairs per step) under the recurrence
+            ptile(sP, s1, 2 * (m - 3), af);
+            ptile(sP, s1, 2 * (m - 3) + 1, af);
+          }
           const int c = 8 * T + m - u;
           const int sl = (m - u < 0) ? s1 : s0;
           const double2 pv = sP[(sl * 8 + ((m - u) & 7)) * PSTR + lane];
@@ -187,10 +194,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         }
 #pragma unroll
         for (int m = 0; m < 8; ++m) hcur[m] = hnxt[m];
-        __syncwarp();  // tile T-1 is dead
-#pragma unroll
-        for (int h = 0; h < 8; ++h) ptile(sP, (T + 1) & 1, h, af);
-        __syncwarp();
+        __syncwarp();  // tile T+1 visible
       };
       for (int T = 0; T < NT8; ++T) {
         if (T == 0 || 8 * T + 8 > NC) iterA(std::true_type{}, T);
@@ -202,7 +206,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
 
     // ------------------------------------------------ phase B: reverse sweep
     for (int e = lane; e < 8 * NT8 * DP; e += 32) gcs[e] = 0.0;
-    for (int strip = nstrips - 1; strip >= 0; --strip) {
+    for (int strip = nstrips - 1; strip >= ((ba.exp & 1) ? nstrips : 0); --strip) {
       __syncwarp();
       stage_x(strip);
       __syncwarp();
@@ -210,7 +214,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       const bool fin0 = (rb == M1 - 1), fin1 = (rb + 1 == M1 - 1);
       const double* __restrict__ rck_own = rowck + (int64_t)strip * NTS * 32;
       const double* __restrict__ rck_up = rowck + (int64_t)max(strip - 1, 0) * NTS * 32;
-      const double2* __restrict__ cck = colck + (int64_t)strip * NT8 * 32 + lane;
+      const double2* __restrict__ cck0 = colck + (int64_t)strip * NT8 * 32;
       const bool below = strip < nstrips - 1;
 
       // block inputs staged by cp.async one block ahead (lane-private records):
@@ -220,14 +224,14 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       // arow holds at index column + 3 (16-byte aligned per block)
       auto stage_block = [&](int blk) {
         double* st = sS + (blk & 1) * Cf::STG;
+        // lane-private: the 9 checkpoint values above the lane (lane u-1 of this
+        // strip, or lane 3 of the strip above: a contiguous 64-B quarter row)
+        const double* src0 = (u > 0) ? rck_own + 8 * (u - 1) + g : rck_up + 24 + g;
+        const int t0 = (u > 0) ? 8 * blk - 2 : 8 * blk + 2;
 #pragma unroll
-        for (int i = 0; i < 9; ++i) {
-          const double* src;
-          if (u > 0) src = rck_own + (int64_t)max(8 * blk - 2 + i, 0) * 32 + lane - 1;
-          else src = rck_up + (int64_t)(8 * blk + 2 + i) * 32 + 4 * g + 3;
-          cp_async8(st + i * 32 + lane, src, u > 0 || strip > 0);
-        }
-        cp_async16(st + 9 * 32 + 2 * lane, cck + (int64_t)blk * 32, true);
+        for (int i = 0; i < 9; ++i)
+          cp_async8(st + i * 32 + lane, src0 + (int64_t)max(t0 + i, 0) * 32, u > 0 || strip > 0);
+        cp_async16(st + 9 * 32 + 2 * lane, cck0 + (int64_t)blk * 32 + lane, true);
         if (u == 3) {
 #pragma unroll
           for (int i = 0; i < 8; i += 2)
@@ -272,6 +276,10 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         __syncwarp();         // staged inputs, p tiles blk and blk-1 visible
         const double* st = sS + (blk & 1) * Cf::STG;
         if (blk > 0) stage_block(blk - 1);
+        double2 gco[NN];  // column-gradient scratch of tile blk, read early
+#pragma unroll
+        for (int n = 0; n < NN; ++n)
+          gco[n] = *reinterpret_cast<const double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u);
         double tv[9];
 #pragma unroll
         for (int i = 0; i < 9; ++i) {
@@ -303,6 +311,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
             K1[kap] = n1;
           }
         }
+
 
         // ---- 2. reverse sweep, lane u one column behind lane u+1.  Dead rows
         // (>= M1) and columns (>= NC) lie below / right of the seeded final
@@ -341,9 +350,12 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
               make_double2(D0, D1);
           if (u == 0 && (!EDGE || c >= 0)) arow[c + 3] = sendm;
         }
-        __syncwarp();  // tile blk's D complete; p tile blk dead
+        __syncwarp();  // tile blk's D complete, p tile blk dead
 
-        // ---- 3. gradient maps on tile blk, then p tile blk-2 into tile blk's slot
+        // ---- 3. p tile blk-2 into tile blk's slot (its latency hides under the
+        // maps), then the gradient maps on tile blk
+#pragma unroll
+        for (int h = 0; h < 8; ++h) ptile(sP, blk & 1, h, af);
         const double* __restrict__ Dt = sD + (blk & 1) * Cf::DTILE;
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
@@ -365,13 +377,10 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           for (int kk = 0; kk < 16; ++kk)
             dmma(c[kk & 3][0], c[kk & 3][1], Dt[g * DSTR + 4 * kk + u],
                  sX[(4 * kk + u) * XSTR + 8 * n + g]);
-          double2* q = reinterpret_cast<double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u);
-          const double2 o = *q;
-          *q = make_double2(o.x + ((c[0][0] + c[1][0]) + (c[2][0] + c[3][0])),
-                            o.y + ((c[0][1] + c[1][1]) + (c[2][1] + c[3][1])));
+          *reinterpret_cast<double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u) =
+              make_double2(gco[n].x + ((c[0][0] + c[1][0]) + (c[2][0] + c[3][0])),
+                           gco[n].y + ((c[0][1] + c[1][1]) + (c[2][1] + c[3][1])));
         }
-#pragma unroll
-        for (int h = 0; h < 8; ++h) ptile(sP, blk & 1, h, af);
         __syncwarp();
       };
       for (int blk = NT8 - 1; blk >= 0; --blk) {
