@@ -349,7 +349,8 @@ def main():
         cpu = cpu_baseline(24 if args.config == "c3" else 8, L, d, lam)
 
     if rank == 0:
-        launches_per_step = (2 * len(ranges)) + (2 * len(ranges))  # prep+kernel, fwd and bwd
+        # per row range: forward = prep + DMMA Gram kernel + mirror, backward = prep + kernel
+        launches_per_step = 3 * len(ranges) + 2 * len(ranges)
         launches_per_step += 1 if world > 1 else 0  # mirror after gather
         out = {
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world,
@@ -363,9 +364,12 @@ def main():
                        "l2": "flushed between timed steps (256 MiB write)"},
             "gram_entries_per_s": n * n / t_step,
             "fwd_ms": t_fwd * 1e3, "bwd_ms": t_bwd * 1e3,
-            "roofline": {"bound": "fp64", "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "bwd_kernel (reverse wavefront incl. checkpointed re-forward)",
+                         "kernel": "gram_bwd_mma (FP64 tensor-core DMMA for <dx,dy>, gx, gy + "
+                                   "DFMA reverse wavefront, incl. checkpointed re-forward)",
+                         "pipe": "FP64: DMMA (mma.m8n8k4.f64) and DFMA share one pipe on B200 "
+                                 "(tools/dmma_probe.cu), so the FP64 peak bounds both",
                          "work": f"{i_bwd:g} DP instr/cell (SURVEY 8d I_bwd) x {my_cells} cells "
                                  f"per launch; FMA-equivalent flops = 2 x DP instr",
                          "peak_source": "live DFMA probe on this GPU (MEASURED_PEAKS.json "
