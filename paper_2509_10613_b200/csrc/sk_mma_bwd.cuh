@@ -46,15 +46,17 @@ template <int DP>
 struct MmaBwdCfg {
   static constexpr int KS = DP / 4;            // k-steps of a p tile
   static constexpr int NN = DP / 8;            // 8-wide component tiles (gx, gy)
-  static constexpr int PSTR = 36;              // double2 per p-tile column (conflict-free)
+  // shared-memory tiles are unpadded; XOR swizzles (psw / dsw / xsw below)
+  // keep every fragment store and load conflict-free
+  static constexpr int PSTR = 32;              // double2 per p-tile column
   static constexpr int PTILE = 8 * PSTR;       // double2 per p tile
-  static constexpr int DSTR = 68;              // doubles per D column: 64 rows + 4
+  static constexpr int DSTR = 64;              // doubles per D column (64 rows)
   static constexpr int DTILE = 8 * DSTR;
-  static constexpr int XSTR = DP + 4;          // doubles per staged dX row
+  static constexpr int XSTR = DP;              // doubles per staged dX row
   // block-input staging (cp.async, lane-private, double buffered): 9 top-row
   // values + 2 left values per lane, 8 strip-below messages per lane group
   static constexpr int STG = 11 * 32 + 8 * 8;
-  static constexpr int WARP_DOUBLES = 2 * PTILE * 2 + 2 * DTILE + 64 * XSTR + 2 * STG;
+  static constexpr int WARP_DOUBLES = 2 * PTILE * 2 + 2 * DTILE + 64 * XSTR + STG;
 };
 
 template <int DP, int WPC>
@@ -69,7 +71,12 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
   double2* __restrict__ sP = reinterpret_cast<double2*>(wsm);  // 2 p tiles
   double* __restrict__ sD = wsm + 2 * Cf::PTILE * 2;            // 2 D tiles
   double* __restrict__ sX = sD + 2 * Cf::DTILE;                  // [64][XSTR]
-  double* __restrict__ sS = sX + 64 * XSTR;                      // [2][STG] staging
+  double* __restrict__ sS = sX + 64 * XSTR;                      // [STG] staging
+  // swizzles: p tile slot of wavefront lane wl in column col; D row in column
+  // col; dX component k of staged row R
+  auto psw = [](int col, int wl) { return wl ^ (4 * (col & 1)); };
+  auto dsw = [](int col, int row) { return row ^ (4 * (col & 3)); };
+  auto xsw = [](int R, int k) { return k ^ (DP == 16 ? 4 * (R & 3) : 4 * ((R >> 1) & 1)); };
   for (int e = lane; e < Cf::WARP_DOUBLES; e += 32) wsm[e] = 0.0;
   __syncwarp();
 
@@ -108,7 +115,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         if (row < M1)
           v = __ldg(reinterpret_cast<const double2*>(pb.R.p + (int64_t)ah * pb.R.path_stride +
                                                      (int64_t)row * DP) + k2);
-        *reinterpret_cast<double2*>(sX + R * XSTR + 2 * k2) = v;
+        *reinterpret_cast<double2*>(sX + R * XSTR + xsw(R, 2 * k2)) = v;
       }
     };
     auto loadA = [&](int T, double (&af)[KS]) {  // dY[col 8T + lane/4][4kk + lane%4]
@@ -120,8 +127,9 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
     auto ptile = [&](double2* ring, int slotT, int h, const double (&af)[KS]) {
       double c0 = 0.0, c1 = 0.0;
 #pragma unroll
-      for (int kk = 0; kk < KS; ++kk) dmma(c0, c1, af[kk], sX[(8 * h + g) * XSTR + 4 * kk + u]);
-      ring[(slotT * 8 + g) * PSTR + 4 * h + u] = make_double2(c0, c1);
+      for (int kk = 0; kk < KS; ++kk)
+        dmma(c0, c1, af[kk], sX[(8 * h + g) * XSTR + xsw(8 * h + g, 4 * kk + u)]);
+      ring[(slotT * 8 + g) * PSTR + psw(g, 4 * h + u)] = make_double2(c0, c1);
     };
 
     // ------------------------------------------------ phase A: forward + checkpoints
@@ -177,7 +185,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           }
           const int c = 8 * T + m - u;
           const int sl = (m - u < 0) ? s1 : s0;
-          const double2 pv = sP[(sl * 8 + ((m - u) & 7)) * PSTR + lane];
+          const double2 pv = sP[(sl * 8 + ((m - u) & 7)) * PSTR + psw(m - u, lane)];
           double tv = __shfl_up_sync(0xffffffffu, bot, 1, 4);
           if (u == 0) tv = hcur[m];
           if (!EDGE || (c >= 0 && c < NC)) {
@@ -223,7 +231,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       // adjoint messages of the strip below at columns 8blk-3 .. 8blk+4, which
       // arow holds at index column + 3 (16-byte aligned per block)
       auto stage_block = [&](int blk) {
-        double* st = sS + (blk & 1) * Cf::STG;
+        double* st = sS;
         // lane-private: the 9 checkpoint values above the lane (lane u-1 of this
         // strip, or lane 3 of the strip above: a contiguous 64-B quarter row)
         const double* src0 = (u > 0) ? rck_own + 8 * (u - 1) + g : rck_up + 24 + g;
@@ -274,8 +282,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         loadGX(blk, gb);      // gx B operand of tile blk
         cp_async_wait<0>();
         __syncwarp();         // staged inputs, p tiles blk and blk-1 visible
-        const double* st = sS + (blk & 1) * Cf::STG;
-        if (blk > 0) stage_block(blk - 1);
+        const double* st = sS;
         double2 gco[NN];  // column-gradient scratch of tile blk, read early
 #pragma unroll
         for (int n = 0; n < NN; ++n)
@@ -292,6 +299,11 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           }
         }
         const double2 kleft = *reinterpret_cast<const double2*>(st + 9 * 32 + 2 * lane);
+        double av[8];  // lane u = 3: adjoint messages of the strip below
+#pragma unroll
+        for (int i = 0; i < 8; ++i) av[i] = st[11 * 32 + g * 8 + i];
+        // the staging records are lane-private: refill them for block blk-1
+        if (blk > 0) stage_block(blk - 1);
 
         // ---- 1. recompute the lane's 2 x 8 forward values (registers)
         double K0[8], K1[8];
@@ -300,7 +312,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
 #pragma unroll
           for (int kap = 0; kap < 8; ++kap) {
             const int c = 8 * blk - u + kap;
-            double2 pv = sP[((((c >> 3) & 1) * 8) + (c & 7)) * PSTR + lane];
+            double2 pv = sP[((((c >> 3) & 1) * 8) + (c & 7)) * PSTR + psw(c, lane)];
             if (EDGE && (c < 0 || c >= NC)) pv = make_double2(0.0, 0.0);
             const Coef c0 = coef(pv.x), c1 = coef(pv.y);
             const double n0 = cell(tv[kap + 1], k0, tv[kap], c0);
@@ -321,8 +333,8 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         for (int kap = 7; kap >= 0; --kap) {
           const int c = 8 * blk - u + kap;
           double recv = __shfl_down_sync(0xffffffffu, sendm, 1, 4);
-          if (u == 3) recv = st[11 * 32 + g * 8 + kap];
-          double2 pv = sP[((((c >> 3) & 1) * 8) + (c & 7)) * PSTR + lane];
+          if (u == 3) recv = av[kap];
+          double2 pv = sP[((((c >> 3) & 1) * 8) + (c & 7)) * PSTR + psw(c, lane)];
           if (EDGE && (c < 0 || c >= NC)) pv = make_double2(0.0, 0.0);
           const Coef c0 = coef(pv.x), c1 = coef(pv.y);
           // row 1 (bottom)
@@ -346,7 +358,8 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           sendm = a0v - bR0;
           aR0 = a0v;
           bR0 = b0v;
-          *reinterpret_cast<double2*>(sD + ((c >> 3) & 1) * Cf::DTILE + (c & 7) * DSTR + 2 * lane) =
+          *reinterpret_cast<double2*>(sD + ((c >> 3) & 1) * Cf::DTILE + (c & 7) * DSTR +
+                                      dsw(c, 2 * lane)) =
               make_double2(D0, D1);
           if (u == 0 && (!EDGE || c >= 0)) arow[c + 3] = sendm;
         }
@@ -361,7 +374,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         for (int kk = 0; kk < 2; ++kk) {
 #pragma unroll
           for (int h = 0; h < 8; ++h) {
-            const double av_ = Dt[(4 * kk + u) * DSTR + 8 * h + g];
+            const double av_ = Dt[(4 * kk + u) * DSTR + dsw(u, 8 * h + g)];
 #pragma unroll
             for (int n = 0; n < NN; ++n) dmma(gx[h][n][0], gx[h][n][1], av_, gb[kk][n]);
           }
@@ -375,8 +388,8 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           for (int j = 0; j < 4; ++j) c[j][0] = c[j][1] = 0.0;
 #pragma unroll
           for (int kk = 0; kk < 16; ++kk)
-            dmma(c[kk & 3][0], c[kk & 3][1], Dt[g * DSTR + 4 * kk + u],
-                 sX[(4 * kk + u) * XSTR + 8 * n + g]);
+            dmma(c[kk & 3][0], c[kk & 3][1], Dt[g * DSTR + dsw(g, 4 * kk + u)],
+                 sX[(4 * kk + u) * XSTR + xsw(4 * kk + u, 8 * n + g)]);
           *reinterpret_cast<double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u) =
               make_double2(gco[n].x + ((c[0][0] + c[1][0]) + (c[2][0] + c[3][0])),
                            gco[n].y + ((c[0][1] + c[1][1]) + (c[2][1] + c[3][1])));
