@@ -337,27 +337,34 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           double2 pv = sP[((((c >> 3) & 1) * 8) + (c & 7)) * PSTR + psw(c, lane)];
           if (EDGE && (c < 0 || c >= NC)) pv = make_double2(0.0, 0.0);
           const Coef c0 = coef(pv.x), c1 = coef(pv.y);
-          // row 1 (bottom)
-          double lam1 = aR1 + recv;
-          if (EDGE && fin1 && c == NC - 1) lam1 += wcot;
-          const double a1 = c1.A * lam1, b1 = c1.B * lam1;
+          double lam1, lam0;
+          if constexpr (EDGE) {
+            // rows 1 then 0, the message chain as written (final-cell seed here)
+            lam1 = aR1 + recv;
+            if (fin1 && c == NC - 1) lam1 += wcot;
+            lam0 = aR0 + (c1.A * lam1 - bR1);
+            if (fin0 && c == NC - 1) lam0 += wcot;
+            sendm = c0.A * lam0 - bR0;
+          } else {
+            // the message to lane u-1 is affine in recv: one FMA on the
+            // lane-to-lane critical path instead of six dependent operations
+            const double R0 = aR0 + fma(c1.A, aR1, -bR1);  // lam0 - A1 recv
+            const double P = c0.A * c1.A, Q = fma(c0.A, R0, -bR0);
+            sendm = fma(P, recv, Q);
+            lam1 = aR1 + recv;
+            lam0 = fma(c1.A, recv, R0);
+          }
           const double kL1 = kap > 0 ? K1[kap - 1] : kleft.y;
           const double kD1 = kap > 0 ? K0[kap - 1] : kleft.x;
           const double p61 = pv.y * (1.0 / 6.0);
           const double D1 = lam1 * fma(kL1 + K0[kap], 0.5 + p61, kD1 * p61);
-          const double m1 = a1 - bR1;
-          aR1 = a1;
-          bR1 = b1;
-          // row 0 (top)
-          double lam0 = aR0 + m1;
-          if (EDGE && fin0 && c == NC - 1) lam0 += wcot;
-          const double a0v = c0.A * lam0, b0v = c0.B * lam0;
           const double kL0 = kap > 0 ? K0[kap - 1] : kleft.x;
           const double p60 = pv.x * (1.0 / 6.0);
           const double D0 = lam0 * fma(kL0 + tv[kap + 1], 0.5 + p60, tv[kap] * p60);
-          sendm = a0v - bR0;
-          aR0 = a0v;
-          bR0 = b0v;
+          aR1 = c1.A * lam1;
+          bR1 = c1.B * lam1;
+          aR0 = c0.A * lam0;
+          bR0 = c0.B * lam0;
           *reinterpret_cast<double2*>(sD + ((c >> 3) & 1) * Cf::DTILE + (c & 7) * DSTR +
                                       dsw(c, 2 * lane)) =
               make_double2(D0, D1);
