@@ -137,10 +137,18 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       __syncwarp();
       stage_x(strip);
       __syncwarp();
-      double af[KS];
+      // phase A ring: 4 tiles, slots 0-1 in sP and 2-3 in the (idle) D region
+      auto aslot = [&](int t) -> double2* {
+        return ((t & 2) ? reinterpret_cast<double2*>(sD) : sP);
+      };
+      double af[KS], an[KS];
       loadA(0, af);
 #pragma unroll
-      for (int h = 0; h < 8; ++h) ptile(sP, 0, h, af);
+      for (int h = 0; h < 8; ++h) ptile(aslot(0), 0, h, af);
+      loadA(1, af);
+#pragma unroll
+      for (int h = 0; h < 8; ++h) ptile(aslot(1), 1, h, af);
+      loadA(2, af);
       double hcur[8];
 #pragma unroll
       for (int m = 0; m < 8; ++m) hcur[m] = 1.0;
@@ -162,7 +170,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       // one 8-step iteration; EDGE iterations hold columns outside [0, NC)
       auto iterA = [&](auto edge, int T) {
         constexpr bool EDGE = decltype(edge)::value;
-        loadA(T + 1, af);  // consumed after the 8 steps
+        loadA(T + 3, an);  // A operand one iteration ahead
         double hnxt[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) hnxt[m] = 1.0;
@@ -175,17 +183,15 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           }
         }
         cck[(int64_t)T * 32] = make_double2(kl0, kl1);  // values at node column 8T - u
-        const int s0 = T & 1, s1 = (T - 1) & 1;          // slots of tiles T and T-1
+        double2* __restrict__ r0 = aslot(T);
+        double2* __restrict__ r1 = aslot(T - 1);
+        const int s0 = T & 1, s1 = (T - 1) & 1;  // slot within the ring half
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
-          if (m == 3) __syncwarp();  // lane 3 read tile T-1 last at step 2: its slot is free
-          if (m >= 3 && m <= 6) {    // tile T+1 (two pairs per step) under the recurrence
-            ptile(sP, s1, 2 * (m - 3), af);
-            ptile(sP, s1, 2 * (m - 3) + 1, af);
-          }
+          ptile(aslot(T + 2), (T + 2) & 1, m, af);  // tile T+2, pair m, under the recurrence
           const int c = 8 * T + m - u;
           const int sl = (m - u < 0) ? s1 : s0;
-          const double2 pv = sP[(sl * 8 + ((m - u) & 7)) * PSTR + psw(m - u, lane)];
+          const double2 pv = ((m - u < 0) ? r1 : r0)[(sl * 8 + ((m - u) & 7)) * PSTR + psw(m - u, lane)];
           double tv = __shfl_up_sync(0xffffffffu, bot, 1, 4);
           if (u == 0) tv = hcur[m];
           if (!EDGE || (c >= 0 && c < NC)) {
@@ -202,7 +208,9 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         }
 #pragma unroll
         for (int m = 0; m < 8; ++m) hcur[m] = hnxt[m];
-        __syncwarp();  // tile T+1 visible
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) af[kk] = an[kk];
+        __syncwarp();  // tile T+2 visible, tile T-1 dead
       };
       for (int T = 0; T < NT8; ++T) {
         if (T == 0 || 8 * T + 8 > NC) iterA(std::true_type{}, T);
