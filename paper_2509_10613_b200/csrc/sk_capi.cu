@@ -497,7 +497,7 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
           !(std::getenv("SK_NO_MMA") && std::getenv("SK_NO_MMA")[0] == '1');
   if (s.MMA) {
     const char* w = std::getenv("SK_BWD_WPC");
-    s.WPC = (w && (w[0] == '2' || w[0] == '3')) ? w[0] - '0' : 4;
+    s.WPC = (w && (w[0] == '3' || w[0] == '4')) ? w[0] - '0' : 2;  // measured: 2 >= 4 > 3
     int per_warp = 0;
     BwdFn fn = select_bwd_mma(s.DP, s.WPC, per_warp);
     if (!fn) return fail(SK_INVALID_ARGUMENT, "no DMMA backward instance for this shape");
