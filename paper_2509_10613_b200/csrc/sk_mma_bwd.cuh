@@ -131,12 +131,30 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         dmma(c0, c1, af[kk], sX[(8 * h + g) * XSTR + xsw(8 * h + g, 4 * kk + u)]);
       ring[(slotT * 8 + g) * PSTR + psw(g, 4 * h + u)] = make_double2(c0, c1);
     };
+    // phase A keeps the B fragments in registers (phase B's state is not live
+    // then); phase B reads them from the staged strip
+    auto ptile_r = [&](double2* ring, int slotT, int h, const double (&af)[KS],
+                       const double (&bf)[8][KS]) {
+      double c0 = 0.0, c1 = 0.0;
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) dmma(c0, c1, af[kk], bf[h][kk]);
+      ring[(slotT * 8 + g) * PSTR + psw(g, 4 * h + u)] = make_double2(c0, c1);
+    };
 
     // ------------------------------------------------ phase A: forward + checkpoints
     for (int strip = 0; strip < ((ba.exp & 2) ? 0 : nstrips); ++strip) {
       __syncwarp();
-      stage_x(strip);
-      __syncwarp();
+      double bf[8][KS];  // dX of pair h, row 8 strip + lane/4, component 4kk + lane%4
+      {
+        const int row = strip * 8 + g;
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const int ah = min(a0 + h, pb.r1 - 1);
+          const double* rp = pb.R.p + (int64_t)ah * pb.R.path_stride + (int64_t)row * DP + u;
+#pragma unroll
+          for (int kk = 0; kk < KS; ++kk) bf[h][kk] = (row < M1) ? __ldg(rp + 4 * kk) : 0.0;
+        }
+      }
       // phase A ring: 4 tiles, slots 0-1 in sP and 2-3 in the (idle) D region
       auto aslot = [&](int t) -> double2* {
         return ((t & 2) ? reinterpret_cast<double2*>(sD) : sP);
@@ -144,10 +162,10 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       double af[KS], an[KS];
       loadA(0, af);
 #pragma unroll
-      for (int h = 0; h < 8; ++h) ptile(aslot(0), 0, h, af);
+      for (int h = 0; h < 8; ++h) ptile_r(aslot(0), 0, h, af, bf);
       loadA(1, af);
 #pragma unroll
-      for (int h = 0; h < 8; ++h) ptile(aslot(1), 1, h, af);
+      for (int h = 0; h < 8; ++h) ptile_r(aslot(1), 1, h, af, bf);
       loadA(2, af);
       double hcur[8];
 #pragma unroll
@@ -188,7 +206,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         const int s0 = T & 1, s1 = (T - 1) & 1;  // slot within the ring half
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
-          ptile(aslot(T + 2), (T + 2) & 1, m, af);  // tile T+2, pair m, under the recurrence
+          ptile_r(aslot(T + 2), (T + 2) & 1, m, af, bf);  // tile T+2, pair m, under the recurrence
           const int c = 8 * T + m - u;
           const int sl = (m - u < 0) ? s1 : s0;
           const double2 pv = ((m - u < 0) ? r1 : r0)[(sl * 8 + ((m - u) & 7)) * PSTR + psw(m - u, lane)];
