@@ -523,7 +523,9 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
     pl.rowck_stride = nstrips * NTS * 32;
     pl.colck_stride = nstrips * NT8 * 32 * 2;
     pl.pck_stride = 0;
-    pl.row_stride = 8 * (NT8 + 3);  // per pair; 8 pairs per slot (adjoint row at column + 3)
+    // per pair, 8 pairs per slot: the adjoint row sits at column + 3 and the
+    // handoff row is prefetched 4 iterations (32 columns) ahead
+    pl.row_stride = 8 * (NT8 + 5);
     pl.dbuf_stride = 0;
     pl.gscr_stride = 8 * NT8 * s.DP;
     return SK_OK;

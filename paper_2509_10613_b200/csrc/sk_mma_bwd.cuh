@@ -42,6 +42,11 @@
 
 namespace sk {
 
+template <int K>
+struct Frag {
+  double v[K];
+};
+
 template <int DP>
 struct MmaBwdCfg {
   static constexpr int KS = DP / 4;            // k-steps of a p tile
@@ -159,25 +164,30 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       auto aslot = [&](int t) -> double2* {
         return ((t & 2) ? reinterpret_cast<double2*>(sD) : sP);
       };
-      double af[KS], an[KS];
-      loadA(0, af);
+      Frag<KS> af, an;  // A operands, alternating between iterations (no copies)
+      loadA(0, af.v);
 #pragma unroll
-      for (int h = 0; h < 8; ++h) ptile_r(aslot(0), 0, h, af, bf);
-      loadA(1, af);
+      for (int h = 0; h < 8; ++h) ptile_r(aslot(0), 0, h, af.v, bf);
+      loadA(1, af.v);
 #pragma unroll
-      for (int h = 0; h < 8; ++h) ptile_r(aslot(1), 1, h, af, bf);
-      loadA(2, af);
-      double hcur[8];
+      for (int h = 0; h < 8; ++h) ptile_r(aslot(1), 1, h, af.v, bf);
+      loadA(2, af.v);
+      loadA(3, an.v);
+      // the strip's top row (lane u = 0's input, written by the strip above)
+      // streams through a shared ring (the idle dX staging area) HPD
+      // iterations ahead: the checkpoint stores push it out of L2
+      constexpr int HPD = 4;
+      double* __restrict__ sH = sX;  // [8 iterations][8 pairs][8 columns]
+      auto issue_h = [&](int T) {
+        if (strip > 0 && u == 0) {
 #pragma unroll
-      for (int m = 0; m < 8; ++m) hcur[m] = 1.0;
-      if (strip > 0 && u == 0) {
-#pragma unroll
-        for (int m = 0; m < 8; m += 2) {
-          const double2 t = *reinterpret_cast<const double2*>(hrow + m);
-          hcur[m] = t.x;
-          hcur[m + 1] = t.y;
+          for (int q = 0; q < 4; ++q)
+            cp_async16(sH + (T & 7) * 64 + g * 8 + 2 * q, hrow + 8 * T + 2 * q, true);
         }
-      }
+        cp_async_commit();
+      };
+#pragma unroll
+      for (int T = 0; T < HPD; ++T) issue_h(T);
       // checkpoint rows keep lane (g, u) at position 8u + g, so lane u = 3's
       // values (the strip handoff) are one contiguous 64-B quarter row
       double* __restrict__ rck = rowck + (int64_t)strip * NTS * 32 + 8 * u + g;
@@ -186,27 +196,22 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       const bool last = strip == nstrips - 1;
       __syncwarp();
       // one 8-step iteration; EDGE iterations hold columns outside [0, NC)
-      auto iterA = [&](auto edge, int T) {
+      // acur: A operand of tile T+2 (loaded two iterations ago); the buffer is
+      // refilled with tile T+4's after this iteration's DMMAs
+      auto iterA = [&](auto edge, int T, Frag<KS>& acur) {
         constexpr bool EDGE = decltype(edge)::value;
-        loadA(T + 3, an);  // A operand one iteration ahead
-        double hnxt[8];
+        issue_h(T + HPD);
+        cp_async_wait<HPD>();  // this iteration's top row landed (lane-private)
+        double hcur[8];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) hnxt[m] = 1.0;
-        if (strip > 0 && u == 0) {
-#pragma unroll
-          for (int m = 0; m < 8; m += 2) {
-            const double2 t = *reinterpret_cast<const double2*>(hrow + 8 * (T + 1) + m);
-            hnxt[m] = t.x;
-            hnxt[m + 1] = t.y;
-          }
-        }
+        for (int m = 0; m < 8; ++m) hcur[m] = (strip > 0) ? sH[(T & 7) * 64 + g * 8 + m] : 1.0;
         cck[(int64_t)T * 32] = make_double2(kl0, kl1);  // values at node column 8T - u
         double2* __restrict__ r0 = aslot(T);
         double2* __restrict__ r1 = aslot(T - 1);
         const int s0 = T & 1, s1 = (T - 1) & 1;  // slot within the ring half
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
-          ptile_r(aslot(T + 2), (T + 2) & 1, m, af, bf);  // tile T+2, pair m, under the recurrence
+          ptile_r(aslot(T + 2), (T + 2) & 1, m, acur.v, bf);  // tile T+2, pair m, under the recurrence
           const int c = 8 * T + m - u;
           const int sl = (m - u < 0) ? s1 : s0;
           const double2 pv = ((m - u < 0) ? r1 : r0)[(sl * 8 + ((m - u) & 7)) * PSTR + psw(m - u, lane)];
@@ -224,18 +229,20 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           }
           rck[(int64_t)(8 * T + m) * 32] = bot;  // diagonal index = column + lane
         }
-#pragma unroll
-        for (int m = 0; m < 8; ++m) hcur[m] = hnxt[m];
-#pragma unroll
-        for (int kk = 0; kk < KS; ++kk) af[kk] = an[kk];
+        loadA(T + 4, acur.v);
         __syncwarp();  // tile T+2 visible, tile T-1 dead
       };
-      for (int T = 0; T < NT8; ++T) {
-        if (T == 0 || 8 * T + 8 > NC) iterA(std::true_type{}, T);
-        else iterA(std::false_type{}, T);
+      for (int T = 0; T < NT8; T += 2) {
+        if (T == 0 || 8 * T + 8 > NC) iterA(std::true_type{}, T, af);
+        else iterA(std::false_type{}, T, af);
+        if (T + 1 < NT8) {
+          if (8 * T + 16 > NC) iterA(std::true_type{}, T + 1, an);
+          else iterA(std::false_type{}, T + 1, an);
+        }
       }
       // rows read by the phase-B recompute past the last step: keep them finite
       for (int e = 8 * NT8; e < NTS; ++e) rck[(int64_t)e * 32] = bot;
+      cp_async_wait<0>();
     }
 
     // ------------------------------------------------ phase B: reverse sweep
