@@ -374,6 +374,11 @@ def main():
                                  f"per launch; FMA-equivalent flops = 2 x DP instr",
                          "peak_source": "live DFMA probe on this GPU (MEASURED_PEAKS.json "
                                         "has no FP64 figure)",
+                         # what the kernel actually issues per cell (lambda = 0): forward
+                         # re-run with checkpoints (7 DFMA + d DMMA-FMA), block recompute
+                         # (7 + d), adjoint sweep (13), gx/gy maps (2d on DMMA)
+                         "executed_fma_per_cell": 27 + 4 * d,
+                         "executed_frac": my_cells * (27 + 4 * d) / t_bwd / peak_fma,
                          "step_frac": total_cells * (i_fwd + i_bwd) * 2 / world / t_step / 1e12
                          / peak},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,

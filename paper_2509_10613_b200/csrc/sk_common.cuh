@@ -81,7 +81,8 @@ struct BwdArgs {
   const double* cot;  // BATCH: [npairs] (nullptr = ones); GRAM: [n1][n2]
   double* values;     // BATCH: optional kernel values
   int exp;            // profiling experiments (env SK_EXP, default 0): 1 skips phase B,
-                      // 2 skips phase A of the DMMA backward -- results are wrong when set
+                      // 2 skips phase A, 4 the gradient maps, 8 the phase-B p tiles of
+                      // the DMMA backward -- results are wrong when set
 };
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }

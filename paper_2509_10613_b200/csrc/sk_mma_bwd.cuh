@@ -408,8 +408,9 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         // ---- 3. p tile blk-2 into tile blk's slot (its latency hides under the
         // maps), then the gradient maps on tile blk
 #pragma unroll
-        for (int h = 0; h < 8; ++h) ptile(sP, blk & 1, h, af);
+        for (int h = 0; h < 8 && !(ba.exp & 8); ++h) ptile(sP, blk & 1, h, af);
         const double* __restrict__ Dt = sD + (blk & 1) * Cf::DTILE;
+        if (!(ba.exp & 4)) {
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
 #pragma unroll
@@ -433,6 +434,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           *reinterpret_cast<double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u) =
               make_double2(gco[n].x + ((c[0][0] + c[1][0]) + (c[2][0] + c[3][0])),
                            gco[n].y + ((c[0][1] + c[1][1]) + (c[2][1] + c[3][1])));
+        }
         }
         __syncwarp();
       };
