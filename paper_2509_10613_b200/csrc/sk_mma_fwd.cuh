@@ -33,6 +33,8 @@
 // same as sk_cell.cuh dot(), so these values are bitwise those of the batch
 // kernels.
 #pragma once
+#include <type_traits>
+
 #include "sk_cell.cuh"
 
 namespace sk {
@@ -128,7 +130,10 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
       double kl0 = 1.0, kl1 = 1.0, topc = 1.0, bot = 1.0;
       const bool last = strip == nstrips - 1;
 
-      for (int T = 0; T < NT8; ++T) {
+      // one 8-step iteration; EDGE iterations hold columns outside [0, NC) or
+      // the final column (the only ones that need range checks)
+      auto iter = [&](auto edge, int T) {
+        constexpr bool EDGE = decltype(edge)::value;
         loadA(T + 3, an);
         double hnxt[8];
 #pragma unroll
@@ -152,7 +157,7 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
           }
           double tv = __shfl_up_sync(0xffffffffu, bot, 1, 4);
           if (u == 0) tv = hcur[m];
-          if (c >= 0 && c < NC) {
+          if (!EDGE || (c >= 0 && c < NC)) {
             const Coef c0 = coef(pv.x), c1 = coef(pv.y);
             const double k0 = cell(tv, kl0, topc, c0);
             const double k1 = cell(k0, kl1, kl0, c1);
@@ -161,7 +166,7 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
             kl1 = k1;
             bot = k1;
             if (u == 3 && !last) hrow[c] = k1;
-            if (last && u == u_star && c == NC - 1) kval = r_star ? k1 : k0;
+            if (EDGE && last && u == u_star && c == NC - 1) kval = r_star ? k1 : k0;
           }
         }
 #pragma unroll
@@ -169,6 +174,10 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
 #pragma unroll
         for (int m = 0; m < 8; ++m) hcur[m] = hnxt[m];
         __syncwarp();  // tile T+2 visible; tile T-2's slot free
+      };
+      for (int T = 0; T < NT8; ++T) {
+        if (T == 0 || 8 * T + 8 >= NC) iter(std::true_type{}, T);
+        else iter(std::false_type{}, T);
       }
     }
     if (valid && u == u_star) pb.out[(int64_t)(a - pb.r0) * pb.ldo + b] = kval;
