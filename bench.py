@@ -6,18 +6,23 @@ JSON line on rank 0.  N>1 runs under torchrun, one rank per GPU (NCCL).
 Workload (default --config c3, BASELINE.json configs[2]): symmetric
 sig_kernel_gram of 1024 Brownian paths, L=512, d=16, dyadic order 0, linear
 static kernel, fp64 forward + exact backward with cotangent ones (the
-reference default, kernel_grad.py:81-82).  A "step" = forward Gram + backward
-gradient of the whole Gram.  With N GPUs the same Gram is sharded by
-balanced row blocks (strong scaling) and assembled with NCCL all-gathers.
+reference default, kernel_grad.py:81-82).  A "step" = the Gram G AND the
+gradient dF/dX of F = sum G, computed by ONE fused value + gradient pass
+(sig_kernel_gram_value_and_grad; the Gram counterpart of the reference's
+kernel_batch_backward, which returns values with the gradients,
+kernel_grad.py:64-98).  The autograd split (forward kernel, then backward
+kernel) is reported beside it ("unfused", "e2e_autograd").  With N GPUs the
+same Gram is sharded by balanced row blocks (strong scaling) and assembled
+with NCCL all-gathers.
 
   value  = solved PDE cells per second (device-resident inputs, device timed,
            max over ranks); Gram entries/s reported beside it
-  e2e    = the same step through the public API (sig_kernel_gram + autograd)
+  e2e    = the same step through the public API (sig_kernel_gram_value_and_grad)
            from pinned host memory: H2D of X and D2H of G and dF/dX inside
            the timed region
-  roofline: dominant kernel (backward wavefront) vs the FP64 FMA pipe,
-           algorithmic DP instructions per cell from SURVEY.md 8d, peak
-           measured live with a DFMA probe on this GPU
+  roofline: the fused kernel vs the FP64 pipe (DMMA + DFMA), algorithmic DP
+           instructions per cell (I_fwd + I_bwd), peak measured
+           live with a DFMA probe on this GPU
   cpu_baseline: the C oracle (restatement of the reference algorithm,
            OpenMP over pairs, all host threads) on a bounded sub-Gram
 
@@ -234,23 +239,36 @@ def main():
             dist.barrier()
 
     def step_device(ev=None):
-        """Device-resident step; optionally records (fwd_start, bwd_start, end) events."""
+        """Device-resident step: ONE fused value + gradient pass (G and dF/dX of
+        F = sum C * G, C = ones) -- the Gram counterpart of the reference's
+        kernel_batch_backward, which returns values with the gradients.
+        Optionally records (start, end) events."""
         if ev is not None:
             ev[0].record()
-        parts = [ops.forward_gram(X, None, lam, lam, 0, 1.0, rows=rg) for rg in ranges]
+        gx = torch.zeros_like(X)
+        parts = [ops.value_and_grad_gram(X, None, lam, lam, 0, 1.0, C, rows=rg, grad_x=gx)[0]
+                 for rg in ranges]
         if ev is not None:
             ev[1].record()
-        gx = torch.zeros_like(X)
-        for rg in ranges:
-            ops.backward_gram(X, None, lam, lam, 0, 1.0, C, rows=rg, grad_x=gx)
-        if ev is not None:
-            ev[2].record()
         if world > 1:
             local_rows = torch.cat(parts, 0)
             ranges_all = [gram_dist.row_blocks(n, world, r, True) for r in range(world)]
             G = gram_dist._gather_rows(local_rows, ranges_all, n, n, group)
             ops.mirror_upper(G)
             gx = gram_dist._gather_sum(gx, group)
+        return parts, gx
+
+    def step_unfused(ev):
+        """The autograd-style step: forward Gram, then the backward (which
+        re-solves the forward for its checkpoints).  Reported beside the fused
+        step; ev = (start, fwd_end, end)."""
+        ev[0].record()
+        parts = [ops.forward_gram(X, None, lam, lam, 0, 1.0, rows=rg) for rg in ranges]
+        ev[1].record()
+        gx = torch.zeros_like(X)
+        for rg in ranges:
+            ops.backward_gram(X, None, lam, lam, 0, 1.0, C, rows=rg, grad_x=gx)
+        ev[2].record()
         return parts, gx
 
     # warmup (also sizes workspaces / JIT-free: kernels are precompiled)
@@ -262,21 +280,32 @@ def main():
 
     sampler = ClockSampler(local)
     sampler.start()
-    fwd_ms, bwd_ms, step_ms = [], [], []
+    step_ms = []
     for _ in range(args.steps):
         flush.fill_(1.0)  # L2 flush between timed steps (256 MiB > 126 MB L2)
         barrier()
         torch.cuda.synchronize()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
         e_end = torch.cuda.Event(enable_timing=True)
         step_device(ev)
         e_end.record()
         torch.cuda.synchronize()
         barrier()
+        step_ms.append(ev[0].elapsed_time(e_end))
+        kern_ms = ev[0].elapsed_time(ev[1])
+    clocks = sampler.stop()
+    # unfused split (forward kernel, then backward kernel), fewer steps
+    fwd_ms, bwd_ms = [], []
+    for _ in range(max(1, min(args.steps, 2))):
+        flush.fill_(1.0)
+        barrier()
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        step_unfused(ev)
+        torch.cuda.synchronize()
+        barrier()
         fwd_ms.append(ev[0].elapsed_time(ev[1]))
         bwd_ms.append(ev[1].elapsed_time(ev[2]))
-        step_ms.append(ev[0].elapsed_time(e_end))
-    clocks = sampler.stop()
 
     t_step = sum(step_ms) / len(step_ms) / 1e3
     t_bwd = sum(bwd_ms) / len(bwd_ms) / 1e3
@@ -289,17 +318,29 @@ def main():
     total_cells = total_pairs * cells_pair
     value = total_cells / t_step
     my_cells = my_pairs * cells_pair
-    achieved = my_cells * i_bwd * 2 / t_bwd / 1e12  # FMA-equivalent TFLOP/s
+    # the fused kernel does the forward (values) and the backward: algorithmic
+    # work = (I_fwd + I_bwd) DP instructions per cell
+    achieved = my_cells * (i_fwd + i_bwd) * 2 / t_step / 1e12  # FMA-equivalent TFLOP/s
     peak = 2 * peak_fma / 1e12
 
     # ---- e2e through the public API, host buffers, copies inside the region
     e2e = None
+    e2e_autograd = None
     if not args.no_e2e:
         Xpin = torch.from_numpy(Xh).pin_memory()
         Gh = torch.empty((n, n), dtype=torch.float64).pin_memory()
         gh = torch.empty_like(Xpin).pin_memory()
 
-        def step_e2e():
+        def step_e2e():  # the fused public call (cotangent ones = its default)
+            Xd = Xpin.to(dev, non_blocking=True)
+            if world > 1:
+                G, g, _ = gram_dist.value_and_grad_sharded(Xd, dyadic_order=lam, group=group)
+            else:
+                G, g, _ = sk.sig_kernel_gram_value_and_grad(Xd, dyadic_order=lam)
+            Gh.copy_(G, non_blocking=True)
+            gh.copy_(g, non_blocking=True)
+
+        def step_autograd():  # sig_kernel_gram + torch autograd (forward, then backward)
             Xd = Xpin.to(dev, non_blocking=True).requires_grad_(True)
             if world > 1:
                 G = gram_dist.sig_kernel_gram_sharded(Xd, dyadic_order=lam)
@@ -309,32 +350,40 @@ def main():
             Gh.copy_(G.detach(), non_blocking=True)
             gh.copy_(Xd.grad, non_blocking=True)
 
-        for _ in range(2):
-            step_e2e()
-        torch.cuda.synchronize()
-        e2e_ms = []
-        for _ in range(max(1, min(args.steps, 3))):
-            flush.fill_(1.0)
-            barrier()
+        def timed(fn, reps):
+            fn()
             torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            step_e2e()
-            b.record()
-            torch.cuda.synchronize()
-            barrier()
-            e2e_ms.append(a.elapsed_time(b))
-        t_e2e = sum(e2e_ms) / len(e2e_ms) / 1e3
-        if world > 1:
-            tt = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t_e2e = tt.item()
-        e2e = {"value": total_cells / t_e2e, "unit": "cells/s",
-               "h2d_bytes_per_step": int(Xh.nbytes),
-               "d2h_bytes_per_step": int(Gh.numel() * 8 + gh.numel() * 8),
+            ms = []
+            for _ in range(reps):
+                flush.fill_(1.0)
+                barrier()
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                fn()
+                b.record()
+                torch.cuda.synchronize()
+                barrier()
+                ms.append(a.elapsed_time(b))
+            t = sum(ms) / len(ms) / 1e3
+            if world > 1:
+                tt = torch.tensor([t], dtype=torch.float64, device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = tt.item()
+            return t
+
+        t_e2e = timed(step_e2e, max(1, min(args.steps, 3)))
+        t_ag = timed(step_autograd, 1)
+        io = {"h2d_bytes_per_step": int(Xh.nbytes),
+              "d2h_bytes_per_step": int(Gh.numel() * 8 + gh.numel() * 8)}
+        e2e = {"value": total_cells / t_e2e, "unit": "cells/s", **io,
                "ms_per_step": t_e2e * 1e3,
-               "api": "paper_2509_10613_b200.sig_kernel_gram + torch autograd"
-                      + (" (gram_dist sharded)" if world > 1 else "")}
+               "api": "paper_2509_10613_b200.sig_kernel_gram_value_and_grad (fused G + dF/dX)"
+                      + (" via gram_dist.value_and_grad_sharded" if world > 1 else "")}
+        e2e_autograd = {"value": total_cells / t_ag, "unit": "cells/s", **io,
+                        "ms_per_step": t_ag * 1e3,
+                        "api": "paper_2509_10613_b200.sig_kernel_gram + torch autograd"
+                               + (" (gram_dist sharded)" if world > 1 else "")}
 
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -349,8 +398,8 @@ def main():
         cpu = cpu_baseline(24 if args.config == "c3" else 8, L, d, lam)
 
     if rank == 0:
-        # per row range: forward = prep + DMMA Gram kernel + mirror, backward = prep + kernel
-        launches_per_step = 3 * len(ranges) + 2 * len(ranges)
+        # per row range: prep + fused DMMA kernel + mirror of the block
+        launches_per_step = 3 * len(ranges)
         launches_per_step += 1 if world > 1 else 0  # mirror after gather
         out = {
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world,
@@ -363,24 +412,34 @@ def main():
                        "parallelism": f"gram row blocks x{world}",
                        "l2": "flushed between timed steps (256 MiB write)"},
             "gram_entries_per_s": n * n / t_step,
-            "fwd_ms": t_fwd * 1e3, "bwd_ms": t_bwd * 1e3,
+            "step": "one fused value + gradient pass per row block (G and dF/dX; the Gram "
+                    "counterpart of the reference's kernel_batch_backward, which returns values "
+                    "with gradients, kernel_grad.py:64-98)",
+            "kernel_ms": kern_ms,
+            "unfused": {"fwd_ms": t_fwd * 1e3, "bwd_ms": t_bwd * 1e3,
+                        "ms_per_step": (t_fwd + t_bwd) * 1e3,
+                        "value": total_cells / (t_fwd + t_bwd),
+                        "what": "forward Gram kernel, then the backward kernel (the torch "
+                                "autograd split; the backward re-solves the forward)"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "gram_bwd_mma (FP64 tensor-core DMMA for <dx,dy>, gx, gy + "
-                                   "DFMA reverse wavefront, incl. checkpointed re-forward)",
+                         "kernel": "gram_bwd_mma in value+gradient mode (FP64 tensor-core DMMA "
+                                   "for <dx,dy>, gx, gy + DFMA wavefronts: forward with "
+                                   "checkpoints, block recompute, reverse sweep)",
                          "pipe": "FP64: DMMA (mma.m8n8k4.f64) and DFMA share one pipe on B200 "
                                  "(tools/dmma_probe.cu), so the FP64 peak bounds both",
-                         "work": f"{i_bwd:g} DP instr/cell (SURVEY 8d I_bwd) x {my_cells} cells "
-                                 f"per launch; FMA-equivalent flops = 2 x DP instr",
+                         "work": f"{i_fwd:g} + {i_bwd:g} DP instr/cell (SURVEY 8d I_fwd + I_bwd) "
+                                 f"x {my_cells} cells per launch; FMA-equivalent flops = 2 x DP "
+                                 f"instr; timed over the step (the kernel is "
+                                 f"{100 * kern_ms / (t_step * 1e3):.1f} % of it)",
                          "peak_source": "live DFMA probe on this GPU (MEASURED_PEAKS.json "
                                         "has no FP64 figure)",
                          # what the kernel actually issues per cell (lambda = 0): forward
-                         # re-run with checkpoints (7 DFMA + d DMMA-FMA), block recompute
-                         # (7 + d), adjoint sweep (13), gx/gy maps (2d on DMMA)
+                         # with checkpoints (7 DFMA + d DMMA-FMA), block recompute (7 + d),
+                         # adjoint sweep (13), gx/gy maps (2d on DMMA)
                          "executed_fma_per_cell": 27 + 4 * d,
-                         "executed_frac": my_cells * (27 + 4 * d) / t_bwd / peak_fma,
-                         "step_frac": total_cells * (i_fwd + i_bwd) * 2 / world / t_step / 1e12
-                         / peak},
+                         "executed_frac": my_cells * (27 + 4 * d) / t_step / peak_fma},
+            "e2e_autograd": e2e_autograd,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
         }

@@ -22,6 +22,8 @@
  *                                                    kernel_grad.py:51-60)
  *   sk_backward_gram   (no reference counterpart: Gram backward composed from
  *                       kernel_backward per pair)
+ *   sk_value_and_grad_gram  the same, also returning the Gram entries (as
+ *                       kernel_batch_backward returns values, kernel_grad.py:64-98)
  *
  * Conventions
  *   - every array pointer is DEVICE memory, C-contiguous float64, borrowed for
@@ -131,6 +133,20 @@ int sk_backward_gram(const double *x, const double *y, int64_t n1, int64_t n2, i
                      double sigma, int64_t row_begin, int64_t row_end, const double *cot,
                      double *grad_x, double *grad_y, void *workspace, size_t workspace_bytes,
                      void *stream);
+
+/* Fused value + gradient of a Gram block: the backward above, plus the Gram
+ * entries G[a - row_begin, b] it solves anyway on its forward pass, written to
+ * `values` (leading dimension n2; symmetric: the solved upper triangle of the
+ * [row_begin, row_end) square is mirrored, entries b < row_begin are left
+ * untouched).  This is the Gram counterpart of the reference's
+ * kernel_batch_backward, which returns the values with the gradients
+ * (kernel_grad.py:64-98); it saves the separate forward solve of
+ * sk_forward_gram when both are needed.  Uses the backward's workspace. */
+int sk_value_and_grad_gram(const double *x, const double *y, int64_t n1, int64_t n2,
+                           int64_t L1, int64_t L2, int64_t d, int lam1, int lam2,
+                           int static_kernel, double sigma, int64_t row_begin, int64_t row_end,
+                           const double *cot, double *values, double *grad_x, double *grad_y,
+                           void *workspace, size_t workspace_bytes, void *stream);
 
 #ifdef __cplusplus
 }

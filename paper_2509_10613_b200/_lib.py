@@ -44,6 +44,8 @@ SIGNATURES = {
                                          _sz),
     "sk_backward_gram": ([_dp, _dp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd, _i64,
                           _i64, _dp, _dp, _dp, _vp, _sz, _vp], _ci),
+    "sk_value_and_grad_gram": ([_dp, _dp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd,
+                                _i64, _i64, _dp, _dp, _dp, _dp, _vp, _sz, _vp], _ci),
 }
 
 _lib = None

@@ -175,3 +175,29 @@ def sig_kernel_gram(x, y=None, dyadic_order=0, static_kernel=None, transform=Non
     out_dtype = torch.promote_types(x.dtype, y.dtype)
     G = _SigKernelGramFn.apply(x.to(torch.float64), y.to(torch.float64), l1, l2, kind, sigma)
     return G.to(out_dtype)
+
+
+def sig_kernel_gram_value_and_grad(x, y=None, cotangent=None, dyadic_order=0, static_kernel=None):
+    """Gram matrix and its gradient in ONE fused pass: returns (G, dF/dx, dF/dy)
+    for F = sum_ab cotangent[a, b] G[a, b] (cotangent None = ones, the reference
+    default kernel_grad.py:81-82); dF/dy is None when y is None (symmetric: both
+    slots land in dF/dx).
+
+    This is the Gram counterpart of the reference's kernel_batch_backward, which
+    returns values and gradients from one call (kernel_grad.py:64-98): the
+    backward's own forward solve produces G, so no separate forward runs.
+    Not an autograd op -- use sig_kernel_gram for autograd graphs."""
+    sym = y is None or y is x
+    x, _ = _batched(_prep(x, "x"), "x")
+    l1, l2 = _orders(dyadic_order)
+    kind, sigma = ops.static_kind(static_kernel)
+    xd = x.detach().to(torch.float64)
+    yd = None
+    if not sym:
+        yd, _ = _batched(_prep(y, "y"), "y")
+        yd = yd.detach().to(torch.float64)
+    n1, n2 = xd.shape[0], (xd if sym else yd).shape[0]
+    if cotangent is None:
+        cotangent = torch.ones((n1, n2), dtype=torch.float64, device=xd.device)
+    G, gx, gy = ops.value_and_grad_gram(xd, yd, l1, l2, kind, sigma, cotangent)
+    return G, gx, gy

@@ -715,6 +715,32 @@ size_t sk_backward_gram_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int6
   return q;
 }
 
+int sk_value_and_grad_gram(const double* x, const double* y, int64_t n1, int64_t n2,
+                           int64_t L1, int64_t L2, int64_t d, int lam1, int lam2,
+                           int static_kernel, double sigma, int64_t row_begin, int64_t row_end,
+                           const double* cot, double* values, double* grad_x, double* grad_y,
+                           void* ws, size_t ws_bytes, void* stream) {
+  const bool sym = (y == nullptr);
+  if (sym && (n2 != n1 || L2 != L1))
+    return fail(SK_INVALID_ARGUMENT, "symmetric Gram needs n2 == n1 and L2 == L1");
+  if (row_begin < 0 || row_end > n1 || row_begin > row_end)
+    return fail(SK_INVALID_ARGUMENT, "row range out of bounds");
+  if (!cot) return fail(SK_INVALID_ARGUMENT, "Gram backward needs the cotangent matrix");
+  if (!values) return fail(SK_INVALID_ARGUMENT, "values buffer missing");
+  if (int rc = backward_impl(x, sym ? x : y, n1, n2, L1, L2, d, lam1, lam2, static_kernel, sigma,
+                             sym ? GRAM_SYM : GRAM_CROSS, row_begin, row_end, cot, values,
+                             grad_x, grad_y, ws, ws_bytes, (cudaStream_t)stream, nullptr))
+    return rc;
+  const int64_t span = row_end - row_begin;
+  if (sym && span > 1) {
+    int blocks = (int)std::min<int64_t>((span * span + 255) / 256, 4096);
+    mirror_upper<<<blocks, 256, 0, (cudaStream_t)stream>>>(values, n2, (int)row_begin,
+                                                           (int)row_end);
+    SK_CUDA(cudaGetLastError());
+  }
+  return SK_OK;
+}
+
 int sk_backward_gram(const double* x, const double* y, int64_t n1, int64_t n2, int64_t L1,
                      int64_t L2, int64_t d, int lam1, int lam2, int static_kernel,
                      double sigma, int64_t row_begin, int64_t row_end, const double* cot,

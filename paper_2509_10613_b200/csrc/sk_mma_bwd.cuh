@@ -89,6 +89,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
   const int nstrips = (M1 + 7) >> 3;
   const int NT8 = (NC + 3 + 7) >> 3;
   const int NTS = 8 * (NT8 + 2);  // diagonal rows per strip in rowck
+  const int u_star = ((M1 - 1) & 7) >> 1, r_star = (M1 - 1) & 1;  // lane/row of the final cell
   const int64_t slot = (int64_t)blockIdx.x * WPC + warp;
   double* __restrict__ rowck = ba.rowck + slot * ba.rowck_stride;
   double2* __restrict__ colck = reinterpret_cast<double2*>(ba.colck + slot * ba.colck_stride);
@@ -147,6 +148,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
     };
 
     // ------------------------------------------------ phase A: forward + checkpoints
+    double kval = 0.0;  // the pair's kernel value (fused value + gradient calls)
     for (int strip = 0; strip < ((ba.exp & 2) ? 0 : nstrips); ++strip) {
       __syncwarp();
       double bf[8][KS];  // dX of pair h, row 8 strip + lane/4, component 4kk + lane%4
@@ -226,6 +228,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
             kl1 = k1;
             bot = k1;
             if (u == 3 && !last) hrow[c] = k1;
+            if (EDGE && last && u == u_star && c == NC - 1) kval = r_star ? k1 : k0;
           }
           rck[(int64_t)(8 * T + m) * 32] = bot;  // diagonal index = column + lane
         }
@@ -244,6 +247,9 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       for (int e = 8 * NT8; e < NTS; ++e) rck[(int64_t)e * 32] = bot;
       cp_async_wait<0>();
     }
+
+    if (ba.values && valid && u == u_star && !(ba.exp & 2))
+      ba.values[(int64_t)(a - pb.r0) * pb.ldo + b] = kval;
 
     // ------------------------------------------------ phase B: reverse sweep
     for (int e = lane; e < 8 * NT8 * DP; e += 32) gcs[e] = 0.0;

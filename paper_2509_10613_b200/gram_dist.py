@@ -153,3 +153,41 @@ def sig_kernel_gram_sharded(x, y=None, dyadic_order=0, static_kernel=None, group
     xx = x.to(torch.float64)
     yy = None if sym else y.to(torch.float64)
     return _ShardedGramFn.apply(xx, yy, l1, l2, kind, sigma, group)
+
+
+def value_and_grad_sharded(x, y=None, cotangent=None, dyadic_order=0, static_kernel=None,
+                           group=None):
+    """Fused G + gradient across all ranks of `group` (sig_kernel_gram_value_and_grad
+    sharded by balanced row blocks): every rank gets the full G (all-gather of
+    its rows, then the mirror) and the full dF/dx (dF/dy) (all-gather of the
+    partials, summed in rank order).  cotangent must be identical on all ranks."""
+    if x.dim() != 3:
+        raise InvalidArgument("x must be (n, L, d)")
+    sym = y is None or y is x
+    l1, l2 = _orders(dyadic_order)
+    kind, sigma = ops.static_kind(static_kernel)
+    xx = x.detach().to(torch.float64)
+    yy = None if sym else y.detach().to(torch.float64)
+    world, rank = _world(group)
+    n1, n2 = xx.shape[0], (xx.shape[0] if sym else yy.shape[0])
+    if cotangent is None:
+        cotangent = torch.ones((n1, n2), dtype=torch.float64, device=xx.device)
+    if world == 1:
+        return ops.value_and_grad_gram(xx, yy, l1, l2, kind, sigma, cotangent)
+    ranges_all = [row_blocks(n1, world, r, sym) for r in range(world)]
+    gx = torch.zeros_like(xx)
+    gy = None if sym else torch.zeros_like(yy)
+    parts = []
+    for rg in ranges_all[rank]:
+        out, _, _ = ops.value_and_grad_gram(xx, yy, l1, l2, kind, sigma, cotangent, rows=rg,
+                                            grad_x=gx, grad_y=gy)
+        parts.append(out)
+    local = torch.cat(parts, 0) if parts else torch.zeros((0, n2), dtype=torch.float64,
+                                                         device=xx.device)
+    G = _gather_rows(local, ranges_all, n1, n2, group)
+    if sym:
+        ops.mirror_upper(G)
+    gx = _gather_sum(gx, group)
+    if gy is not None:
+        gy = _gather_sum(gy, group)
+    return G, gx, gy

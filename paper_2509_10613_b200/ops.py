@@ -168,6 +168,38 @@ def backward_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, grad_x=None, gr
     return grad_x, grad_y
 
 
+def value_and_grad_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, out=None, grad_x=None,
+                        grad_y=None):
+    """One fused pass: G rows [r0, r1) (as forward_gram) and dF/dx (dF/dy) of
+    F = sum cot[a, b] G[a, b] (accumulated as backward_gram), from the
+    backward's own forward solve (sk_value_and_grad_gram)."""
+    lib = _lib.load()
+    x = _paths(x, "x")
+    sym = y is None
+    yy = x if sym else _paths(y, "y")
+    n1, L1, d = x.shape
+    n2, L2 = yy.shape[0], yy.shape[1]
+    if yy.shape[2] != d:
+        raise InvalidArgument(f"path dimensions differ: {d} vs {yy.shape[2]}")
+    r0, r1 = (0, n1) if rows is None else (int(rows[0]), int(rows[1]))
+    cot = cot.to(torch.float64).contiguous()
+    if out is None:
+        out = torch.empty((r1 - r0, n2), dtype=torch.float64, device=x.device)
+    if grad_x is None:
+        grad_x = torch.zeros_like(x)
+    if grad_y is None and not sym:
+        grad_y = torch.zeros_like(yy)
+    if n1 == 0 or n2 == 0 or r1 <= r0:
+        return out, grad_x, grad_y
+    nb = lib.sk_backward_gram_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind, int(sym))
+    ws = _workspace(nb, x.device)
+    _lib.check(lib.sk_value_and_grad_gram(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
+                                          lam1, lam2, kind, sigma, r0, r1, _ptr(cot), _ptr(out),
+                                          _ptr(grad_x), _ptr(grad_y) if not sym else None,
+                                          _ptr(ws), ws.numel(), _stream()))
+    return out, grad_x, grad_y
+
+
 def mirror_upper(G: torch.Tensor) -> torch.Tensor:
     """In place: lower triangle := upper triangle (kernel.py:177-179)."""
     lib = _lib.load()

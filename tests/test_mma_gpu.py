@@ -118,3 +118,28 @@ def test_gram_backward_mma_row_blocks_sum(mods):
         ops.backward_gram(cu(X), None, 0, 0, 0, 1.0, cu(C), rows=r, grad_x=acc)
     assert rel_err(acc.cpu().numpy(), full.cpu().numpy()) < 1e-13
     assert rel_err(full.cpu().numpy(), orc.gram_backward(X, None, C, 0, 0)) < TOL
+
+
+@pytest.mark.parametrize("n1,n2,L,d,lam", [(9, 9, 33, 8, 0), (6, 11, 40, 16, 0), (12, 12, 70, 5, 0),
+                                           (5, 5, 17, 3, 1), (4, 7, 12, 6, 1)])
+def test_value_and_grad_gram(mods, n1, n2, L, d, lam):
+    """Fused G + gradient == separate forward Gram and backward (bitwise for the
+    values: same forward arithmetic), vs the oracle within 1e-10."""
+    import paper_2509_10613_b200 as sk
+    ops, orc = mods
+    rng = np.random.default_rng(n1 + 3 * L + d)
+    X = random_paths(rng, n1, L, d)
+    Y = None if n1 == n2 else random_paths(rng, n2, L, d)
+    C = rng.standard_normal((n1, n2))
+    G, gx, gy = sk.sig_kernel_gram_value_and_grad(cu(X), None if Y is None else cu(Y), cu(C),
+                                                  dyadic_order=lam)
+    Gf = ops.forward_gram(cu(X), None if Y is None else cu(Y), lam, lam, 0, 1.0)
+    np.testing.assert_array_equal(G.cpu().numpy(), Gf.cpu().numpy())
+    assert rel_err(G.cpu().numpy(), orc.kernel_gram(X, Y, lam, lam)) < TOL
+    want = orc.gram_backward(X, Y, C, lam, lam)
+    if Y is None:
+        assert gy is None
+        assert rel_err(gx.cpu().numpy(), want) < TOL
+    else:
+        assert rel_err(gx.cpu().numpy(), want[0]) < TOL
+        assert rel_err(gy.cpu().numpy(), want[1]) < TOL
