@@ -166,30 +166,42 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       auto aslot = [&](int t) -> double2* {
         return ((t & 2) ? reinterpret_cast<double2*>(sD) : sP);
       };
-      Frag<KS> af, an;  // A operands, alternating between iterations (no copies)
+      Frag<KS> af;
       loadA(0, af.v);
 #pragma unroll
       for (int h = 0; h < 8; ++h) ptile_r(aslot(0), 0, h, af.v, bf);
       loadA(1, af.v);
 #pragma unroll
       for (int h = 0; h < 8; ++h) ptile_r(aslot(1), 1, h, af.v, bf);
-      loadA(2, af.v);
-      loadA(3, an.v);
-      // the strip's top row (lane u = 0's input, written by the strip above)
-      // streams through a shared ring (the idle dX staging area) HPD
-      // iterations ahead: the checkpoint stores push it out of L2
-      constexpr int HPD = 4;
+      // Two input streams go through shared rings HPD iterations ahead (the
+      // checkpoint stores push them out of L2): the strip's top row (lane u = 0,
+      // written by the strip above; in the idle dX area) and the dY rows of the
+      // p tiles (A operand; in the idle staging area for d = 8, after the top
+      // row ring for d = 16).  One cp.async group per iteration carries both.
+      constexpr int HPD = (DP == 16) ? 3 : 4;
+      constexpr int RA = HPD + 1;  // A ring depth (iterations)
       double* __restrict__ sH = sX;  // [8 iterations][8 pairs][8 columns]
-      auto issue_h = [&](int T) {
+      double* __restrict__ sA = (DP == 16) ? sX + 512 : sS;  // [RA][8 columns][DP]
+      static_assert(DP != 16 || 512 + RA * 8 * DP <= 64 * XSTR, "A ring must fit after the top row ring");
+      static_assert(DP == 16 || RA * 8 * DP <= Cf::STG, "A ring must fit in the staging area");
+      auto issue_in = [&](int T) {  // top row of iteration T, dY of tile T+2
         if (strip > 0 && u == 0) {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
             cp_async16(sH + (T & 7) * 64 + g * 8 + 2 * q, hrow + 8 * T + 2 * q, true);
         }
+        const int t = T + 2;
+#pragma unroll
+        for (int e = lane; e < 8 * DP / 2; e += 32) {
+          const int col = 8 * t + e / (DP / 2), q = e % (DP / 2);
+          const bool v = col < NC;
+          cp_async16(sA + ((t % RA) * 8 + e / (DP / 2)) * DP + 2 * q,
+                     cpath + (int64_t)(v ? col : 0) * DP + 2 * q, v);
+        }
         cp_async_commit();
       };
 #pragma unroll
-      for (int T = 0; T < HPD; ++T) issue_h(T);
+      for (int T = 0; T < HPD; ++T) issue_in(T);
       // checkpoint rows keep lane (g, u) at position 8u + g, so lane u = 3's
       // values (the strip handoff) are one contiguous 64-B quarter row
       double* __restrict__ rck = rowck + (int64_t)strip * NTS * 32 + 8 * u + g;
@@ -200,20 +212,24 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       // one 8-step iteration; EDGE iterations hold columns outside [0, NC)
       // acur: A operand of tile T+2 (loaded two iterations ago); the buffer is
       // refilled with tile T+4's after this iteration's DMMAs
-      auto iterA = [&](auto edge, int T, Frag<KS>& acur) {
+      auto iterA = [&](auto edge, int T) {
         constexpr bool EDGE = decltype(edge)::value;
-        issue_h(T + HPD);
-        cp_async_wait<HPD>();  // this iteration's top row landed (lane-private)
+        issue_in(T + HPD);
+        cp_async_wait<HPD>();  // this iteration's top row and tile T+2's dY landed
+        __syncwarp();          // (the dY ring is shared by the warp)
         double hcur[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) hcur[m] = (strip > 0) ? sH[(T & 7) * 64 + g * 8 + m] : 1.0;
+        double acur[KS];  // A operand of tile T+2: dY[col 8(T+2) + lane/4][4kk + lane%4]
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) acur[kk] = sA[(((T + 2) % RA) * 8 + g) * DP + 4 * kk + u];
         cck[(int64_t)T * 32] = make_double2(kl0, kl1);  // values at node column 8T - u
         double2* __restrict__ r0 = aslot(T);
         double2* __restrict__ r1 = aslot(T - 1);
         const int s0 = T & 1, s1 = (T - 1) & 1;  // slot within the ring half
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
-          ptile_r(aslot(T + 2), (T + 2) & 1, m, acur.v, bf);  // tile T+2, pair m, under the recurrence
+          ptile_r(aslot(T + 2), (T + 2) & 1, m, acur, bf);  // tile T+2, pair m, under the recurrence
           const int c = 8 * T + m - u;
           const int sl = (m - u < 0) ? s1 : s0;
           const double2 pv = ((m - u < 0) ? r1 : r0)[(sl * 8 + ((m - u) & 7)) * PSTR + psw(m - u, lane)];
@@ -232,16 +248,11 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           }
           rck[(int64_t)(8 * T + m) * 32] = bot;  // diagonal index = column + lane
         }
-        loadA(T + 4, acur.v);
         __syncwarp();  // tile T+2 visible, tile T-1 dead
       };
-      for (int T = 0; T < NT8; T += 2) {
-        if (T == 0 || 8 * T + 8 > NC) iterA(std::true_type{}, T, af);
-        else iterA(std::false_type{}, T, af);
-        if (T + 1 < NT8) {
-          if (8 * T + 16 > NC) iterA(std::true_type{}, T + 1, an);
-          else iterA(std::false_type{}, T + 1, an);
-        }
+      for (int T = 0; T < NT8; ++T) {
+        if (T == 0 || 8 * T + 8 > NC) iterA(std::true_type{}, T);
+        else iterA(std::false_type{}, T);
       }
       // rows read by the phase-B recompute past the last step: keep them finite
       for (int e = 8 * NT8; e < NTS; ++e) rck[(int64_t)e * 32] = bot;
