@@ -425,7 +425,21 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         // ---- 3. p tile blk-2 into tile blk's slot (its latency hides under the
         // maps), then the gradient maps on tile blk
 #pragma unroll
-        for (int h = 0; h < 8 && !(ba.exp & 8); ++h) ptile(sP, blk & 1, h, af);
+        for (int h = 0; h < 8 && !(ba.exp & 8); h += 8) {
+          // all 8 pairs' chains side by side, k-step outermost (same per-chain
+          // order as ptile, so the values are unchanged)
+          double c[8][2];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              dmma(c[q][0], c[q][1], af[kk], sX[(8 * q + g) * XSTR + xsw(8 * q + g, 4 * kk + u)]);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            sP[(((blk & 1) * 8 + g) * PSTR) + psw(g, 4 * q + u)] = make_double2(c[q][0], c[q][1]);
+        }
         const double* __restrict__ Dt = sD + (blk & 1) * Cf::DTILE;
         if (!(ba.exp & 4)) {
 #pragma unroll
@@ -438,19 +452,26 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           }
         }
         // gy = D^T dX over the tile's 64 rows: four independent DMMA chains per
-        // component tile (fixed order, so results stay deterministic)
+        // component tile, all chains side by side (fixed order: deterministic)
+        {
+          double c[NN][4][2];
 #pragma unroll
-        for (int n = 0; n < NN; ++n) {
-          double c[4][2];
+          for (int n = 0; n < NN; ++n)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) c[j][0] = c[j][1] = 0.0;
+            for (int j = 0; j < 4; ++j) c[n][j][0] = c[n][j][1] = 0.0;
 #pragma unroll
-          for (int kk = 0; kk < 16; ++kk)
-            dmma(c[kk & 3][0], c[kk & 3][1], Dt[g * DSTR + dsw(g, 4 * kk + u)],
-                 sX[(4 * kk + u) * XSTR + xsw(4 * kk + u, 8 * n + g)]);
-          *reinterpret_cast<double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u) =
-              make_double2(gco[n].x + ((c[0][0] + c[1][0]) + (c[2][0] + c[3][0])),
-                           gco[n].y + ((c[0][1] + c[1][1]) + (c[2][1] + c[3][1])));
+          for (int kk = 0; kk < 16; ++kk) {
+            const double a_ = Dt[g * DSTR + dsw(g, 4 * kk + u)];
+#pragma unroll
+            for (int n = 0; n < NN; ++n)
+              dmma(c[n][kk & 3][0], c[n][kk & 3][1], a_,
+                   sX[(4 * kk + u) * XSTR + xsw(4 * kk + u, 8 * n + g)]);
+          }
+#pragma unroll
+          for (int n = 0; n < NN; ++n)
+            *reinterpret_cast<double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u) =
+                make_double2(gco[n].x + ((c[n][0][0] + c[n][1][0]) + (c[n][2][0] + c[n][3][0])),
+                             gco[n].y + ((c[n][0][1] + c[n][1][1]) + (c[n][2][1] + c[n][3][1])));
         }
         }
         __syncwarp();
