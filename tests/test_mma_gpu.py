@@ -143,3 +143,38 @@ def test_value_and_grad_gram(mods, n1, n2, L, d, lam):
     else:
         assert rel_err(gx.cpu().numpy(), want[0]) < TOL
         assert rel_err(gy.cpu().numpy(), want[1]) < TOL
+
+
+def test_value_and_grad_gram_long_and_ragged(mods):
+    """Long paths (many 8-column tiles, several strips) and a tile count that is
+    not a multiple of 8 pairs, symmetric, against the oracle on a sub-block."""
+    import paper_2509_10613_b200 as sk
+    ops, orc = mods
+    rng = np.random.default_rng(21)
+    X = random_paths(rng, 13, 1030, 9)
+    C = rng.standard_normal((13, 13))
+    G, gx, _ = sk.sig_kernel_gram_value_and_grad(cu(X), None, cu(C))
+    assert rel_err(G.cpu().numpy(), orc.kernel_gram(X, None, 0, 0)) < TOL
+    assert rel_err(gx.cpu().numpy(), orc.gram_backward(X, None, C, 0, 0)) < TOL
+
+
+def test_value_and_grad_row_blocks_assemble(mods):
+    """The multi-GPU split (gram_dist.row_blocks) run sequentially on one GPU:
+    the row blocks' G rows and summed gradients equal the single call."""
+    import paper_2509_10613_b200 as sk
+    from paper_2509_10613_b200 import gram_dist
+    ops, _ = mods
+    rng = np.random.default_rng(22)
+    X = random_paths(rng, 19, 45, 8)
+    C = torch.ones((19, 19), dtype=torch.float64, device="cuda")
+    G, gx, _ = sk.sig_kernel_gram_value_and_grad(cu(X), None, C)
+    world = 3
+    Gs = torch.zeros_like(G)
+    gs = torch.zeros_like(gx)
+    for r in range(world):
+        for rg in gram_dist.row_blocks(19, world, r, True):
+            out, _, _ = ops.value_and_grad_gram(cu(X), None, 0, 0, 0, 1.0, C, rows=rg, grad_x=gs)
+            Gs[rg[0]:rg[1]] = out
+    ops.mirror_upper(Gs)
+    np.testing.assert_array_equal(Gs.cpu().numpy(), G.cpu().numpy())
+    assert rel_err(gs.cpu().numpy(), gx.cpu().numpy()) < 1e-13

@@ -1,6 +1,6 @@
 """One full BASELINE config 5 step on one GPU: symmetric sig_kernel_gram of
-8192 Brownian paths (L=1024, d=8, lambda=0), fp64 forward + backward
-(cotangent ones), device-timed, with a sub-block parity check against the C
+8192 Brownian paths (L=1024, d=8, lambda=0), fp64 G + gradient (cotangent
+ones; argv[2] = "fused" (default, one value+grad pass) or "split"), device-timed, with a sub-block parity check against the C
 oracle.  Writes a JSON summary (evidence run; bench.py's default is C3)."""
 import json
 import sys
@@ -21,27 +21,43 @@ Xd = torch.as_tensor(X, device="cuda")
 C = torch.ones((n, n), dtype=torch.float64, device="cuda")
 peak = ops.dfma_peak()
 torch.cuda.synchronize()
-e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-t0 = time.time()
-e[0].record()
-G = ops.forward_gram(Xd, None, 0, 0, 0, 1.0)
-e[1].record()
-gx, _ = ops.backward_gram(Xd, None, 0, 0, 0, 1.0, C)
-e[2].record()
-torch.cuda.synchronize()
-wall = time.time() - t0
-fwd_s = e[0].elapsed_time(e[1]) / 1e3
-bwd_s = e[1].elapsed_time(e[2]) / 1e3
+mode = sys.argv[2] if len(sys.argv) > 2 else "fused"
 pairs = n * (n + 1) // 2
 cells = pairs * (L - 1) ** 2
-out = {"config": f"C5 sym Gram n={n} L={L} d={d} lambda=0 fp64 fwd+bwd, cotangent ones, 1 GPU",
-       "fwd_s": fwd_s, "bwd_s": bwd_s, "step_s": fwd_s + bwd_s, "wall_s": wall,
-       "cells": cells, "cells_per_s": cells / (fwd_s + bwd_s),
-       "gram_entries_per_s": n * n / (fwd_s + bwd_s),
-       "fwd_frac_of_dfma": cells * 15 / fwd_s / peak,
-       "bwd_frac_of_dfma_algorithmic": cells * 25 / bwd_s / peak,
-       "step_frac_of_dfma_algorithmic": cells * 40 / (fwd_s + bwd_s) / peak,
-       "dfma_peak_fma_per_s": peak}
+t0 = time.time()
+if mode == "fused":
+    # one value + gradient pass (sig_kernel_gram_value_and_grad's kernel call)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e[0].record()
+    G, gx, _ = ops.value_and_grad_gram(Xd, None, 0, 0, 0, 1.0, C)
+    e[1].record()
+    torch.cuda.synchronize()
+    step_s = e[0].elapsed_time(e[1]) / 1e3
+    out = {"config": f"C5 sym Gram n={n} L={L} d={d} lambda=0 fp64 G + gradient (fused value+grad "
+                     f"pass), cotangent ones, 1 GPU",
+           "step_s": step_s, "wall_s": time.time() - t0,
+           "cells": cells, "cells_per_s": cells / step_s, "gram_entries_per_s": n * n / step_s,
+           "step_frac_of_dfma_algorithmic": cells * 40 / step_s / peak,
+           "executed_frac_of_dfma": cells * (27 + 4 * d) / step_s / peak,
+           "dfma_peak_fma_per_s": peak}
+else:
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    e[0].record()
+    G = ops.forward_gram(Xd, None, 0, 0, 0, 1.0)
+    e[1].record()
+    gx, _ = ops.backward_gram(Xd, None, 0, 0, 0, 1.0, C)
+    e[2].record()
+    torch.cuda.synchronize()
+    fwd_s = e[0].elapsed_time(e[1]) / 1e3
+    bwd_s = e[1].elapsed_time(e[2]) / 1e3
+    out = {"config": f"C5 sym Gram n={n} L={L} d={d} lambda=0 fp64 fwd+bwd, cotangent ones, 1 GPU",
+           "fwd_s": fwd_s, "bwd_s": bwd_s, "step_s": fwd_s + bwd_s, "wall_s": time.time() - t0,
+           "cells": cells, "cells_per_s": cells / (fwd_s + bwd_s),
+           "gram_entries_per_s": n * n / (fwd_s + bwd_s),
+           "fwd_frac_of_dfma": cells * 15 / fwd_s / peak,
+           "bwd_frac_of_dfma_algorithmic": cells * 25 / bwd_s / peak,
+           "step_frac_of_dfma_algorithmic": cells * 40 / (fwd_s + bwd_s) / peak,
+           "dfma_peak_fma_per_s": peak}
 # parity of a sub-block (first 6 paths) and symmetry
 sys.path.insert(0, ROOT)
 from oracle import oracle as orc  # noqa: E402  (checker only)
