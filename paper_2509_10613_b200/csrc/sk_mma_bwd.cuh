@@ -12,29 +12,39 @@
 //
 // Work per fine cell: p = <dx_i, dy_j> twice (forward checkpoint pass and the
 // block recompute), gx and gy: 4d FMAs, all on DMMA; the recurrences (forward
-// 7 DP ops, adjoint 10, recompute 7) on the FMA pipe.  In r01 the FMA-pipe-only
+// 7 DP ops, adjoint ~15, recompute 7) on the FMA pipe.  In r01 the FMA-pipe-only
 // backward was issue/latency bound at ~10 % of the FP64 roofline.
 //
-// Mapping (one warp = one Gram tile of 8 pairs (a0+g, b), lane = 4g + u):
-//   phase A  forward wavefront exactly as sk_mma_fwd.cuh (lane u owns rows
-//            2u, 2u+1 of each 8-row strip, skew 1 column per lane), plus
-//            checkpoints: every lane's bottom row, diagonal layout
-//            rowck[strip][step][lane] (one coalesced 256-B store per step), and
-//            every lane's two values at its block boundaries colck[strip][blk][lane];
+// Mapping (one warp = one Gram tile of 8 pairs (a0+g, b), lane = 4g + u;
+// 2-warp CTAs, 4 CTAs = 8 warps per SM, bounded by 255 registers and ~28 KB
+// of shared memory per warp):
+//   phase A  forward wavefront as sk_mma_fwd.cuh (lane u owns rows 2u, 2u+1 of
+//            each 8-row strip, skew 1 column per lane; p tiles two ahead in a
+//            4-slot ring that borrows the idle D ring), plus checkpoints: every
+//            lane's bottom row, diagonal layout rowck[strip][step][8u+g] (one
+//            coalesced 256-B store per step), and every lane's two values at
+//            its block boundaries colck[strip][blk][lane].  The strip's top row
+//            and the p tiles' dY rows stream through cp.async rings 3-4
+//            iterations ahead.  Value + gradient calls also write G here;
 //   phase B  strips bottom-up, blocks of 8 lane-relative columns right-to-left
 //            (lane u's block blk = columns 8blk-u .. 8blk-u+7):
-//            1. p tiles blk, blk-1 (DMMA, computed two blocks ahead into a 2-slot
-//               shared ring) -> each lane recomputes its 2 x 8 forward values in
-//               registers from its own checkpoints (no inter-lane dependency);
+//            1. each lane recomputes its 2 x 8 forward values in registers from
+//               its own checkpoints (staged one block ahead by lane-private
+//               cp.async) and p from a 2-slot DMMA tile ring;
 //            2. reverse sweep of the block, lane u one column behind lane u+1,
-//               adjoint messages by __shfl_down_sync; D per cell into a 2-tile
+//               adjoint messages by __shfl_down_sync (affine in the received
+//               message: one FMA on the lane chain); D per cell into a 2-tile
 //               shared ring [column][row];
-//            3. tile blk's D is now complete for all 64 rows: gx += D dY (DMMA,
-//               accumulators in registers for the strip) and gy = D^T dX (DMMA
-//               over the 64 rows of the tile, dX staged in shared memory),
-//               added to the column path's scratch.
-//   Increment gradients are telescoped to point gradients once per tile and
-//   flushed with fp64 atomics (several tiles share a path), kernel_grad.py:55-60.
+//            3. p tile blk-2 into the dead slot, then, tile blk's D being
+//               complete for all 64 rows: gx += D dY (DMMA, accumulators in
+//               registers for the strip) and gy = D^T dX (DMMA over the 64 rows
+//               of the tile, dX staged in shared memory), added to the column
+//               path's scratch.
+//   Shared tiles are unpadded with XOR swizzles (psw / dsw / xsw): every
+//   fragment store and load is bank-conflict-free.
+//   Increment gradients are telescoped to point gradients (rows: per strip
+//   from registers; columns: once per tile from the scratch) and flushed with
+//   fp64 atomics (several tiles share a path), kernel_grad.py:55-60.
 #pragma once
 #include <type_traits>
 
