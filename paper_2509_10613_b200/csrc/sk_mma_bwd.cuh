@@ -159,18 +159,33 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
 
     // ------------------------------------------------ phase A: forward + checkpoints
     double kval = 0.0;  // the pair's kernel value (fused value + gradient calls)
+    // B fragments: dX of pair h, row 8 strip + lane/4, component 4kk + lane%4;
+    // the next strip's are loaded one strip ahead
+    double bfn[8][KS];
+    auto load_bf = [&](int strip, double (&b)[8][KS]) {
+      const int row = strip * 8 + g;
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        const int ah = min(a0 + h, pb.r1 - 1);
+        const double* rp = pb.R.p + (int64_t)ah * pb.R.path_stride + (int64_t)row * DP + u;
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) b[h][kk] = (row < M1) ? __ldg(rp + 4 * kk) : 0.0;
+      }
+    };
+    // (measured: the prefetch pays for d = 8, costs registers for d = 16)
+    constexpr bool PFB = DP <= 8;
+    if (PFB) load_bf(0, bfn);
     for (int strip = 0; strip < ((ba.exp & 2) ? 0 : nstrips); ++strip) {
       __syncwarp();
-      double bf[8][KS];  // dX of pair h, row 8 strip + lane/4, component 4kk + lane%4
-      {
-        const int row = strip * 8 + g;
+      double bf[8][KS];
+      if constexpr (PFB) {
 #pragma unroll
-        for (int h = 0; h < 8; ++h) {
-          const int ah = min(a0 + h, pb.r1 - 1);
-          const double* rp = pb.R.p + (int64_t)ah * pb.R.path_stride + (int64_t)row * DP + u;
+        for (int h = 0; h < 8; ++h)
 #pragma unroll
-          for (int kk = 0; kk < KS; ++kk) bf[h][kk] = (row < M1) ? __ldg(rp + 4 * kk) : 0.0;
-        }
+          for (int kk = 0; kk < KS; ++kk) bf[h][kk] = bfn[h][kk];
+        if (strip + 1 < nstrips) load_bf(strip + 1, bfn);
+      } else {
+        load_bf(strip, bf);
       }
       // phase A ring: 4 tiles, slots 0-1 in sP and 2-3 in the (idle) D region
       auto aslot = [&](int t) -> double2* {

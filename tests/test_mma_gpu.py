@@ -178,3 +178,19 @@ def test_value_and_grad_row_blocks_assemble(mods):
     ops.mirror_upper(Gs)
     np.testing.assert_array_equal(Gs.cpu().numpy(), G.cpu().numpy())
     assert rel_err(gs.cpu().numpy(), gx.cpu().numpy()) < 1e-13
+
+
+def test_value_and_grad_gram_swapped_orientation(mods):
+    """Cross Gram whose column paths are longer (the orientation swap of
+    kernel.py:164-170: r01 kernels) still returns G and both gradients."""
+    import paper_2509_10613_b200 as sk
+    ops, orc = mods
+    rng = np.random.default_rng(31)
+    X = random_paths(rng, 5, 14, 6)
+    Y = random_paths(rng, 6, 29, 6)
+    C = rng.standard_normal((5, 6))
+    G, gx, gy = sk.sig_kernel_gram_value_and_grad(cu(X), cu(Y), cu(C))
+    assert rel_err(G.cpu().numpy(), orc.kernel_gram(X, Y, 0, 0)) < TOL
+    wx, wy = orc.gram_backward(X, Y, C, 0, 0)
+    assert rel_err(gx.cpu().numpy(), wx) < TOL
+    assert rel_err(gy.cpu().numpy(), wy) < TOL
