@@ -32,9 +32,8 @@
 //               its own checkpoints (staged one block ahead by lane-private
 //               cp.async) and p from a 2-slot DMMA tile ring;
 //            2. reverse sweep of the block, lane u one column behind lane u+1,
-//               adjoint messages by __shfl_down_sync (affine in the received
-//               message: one FMA on the lane chain); D per cell into a 2-tile
-//               shared ring [column][row];
+//               adjoint messages by __shfl_down_sync; D per cell into a
+//               2-tile shared ring [column][row];
 //            3. p tile blk-2 into the dead slot, then, tile blk's D being
 //               complete for all 64 rows: gx += D dY (DMMA, accumulators in
 //               registers for the strip) and gy = D^T dX (DMMA over the 64 rows
@@ -51,6 +50,12 @@
 #include "sk_mma_fwd.cuh"
 
 namespace sk {
+
+// 1: the adjoint message to lane u-1 as one FMA of the received one (+3 DP ops
+// per column, shorter lane chain); 0: the chain as written (measured faster)
+#ifndef SK_AFFINE_MSG
+#define SK_AFFINE_MSG 0
+#endif
 
 template <int K>
 struct Frag {
@@ -413,12 +418,12 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           if (EDGE && (c < 0 || c >= NC)) pv = make_double2(0.0, 0.0);
           const Coef c0 = coef(pv.x), c1 = coef(pv.y);
           double lam1, lam0;
-          if constexpr (EDGE) {
+          if constexpr (EDGE || SK_AFFINE_MSG == 0) {
             // rows 1 then 0, the message chain as written (final-cell seed here)
             lam1 = aR1 + recv;
-            if (fin1 && c == NC - 1) lam1 += wcot;
+            if (EDGE && fin1 && c == NC - 1) lam1 += wcot;
             lam0 = aR0 + (c1.A * lam1 - bR1);
-            if (fin0 && c == NC - 1) lam0 += wcot;
+            if (EDGE && fin0 && c == NC - 1) lam0 += wcot;
             sendm = c0.A * lam0 - bR0;
           } else {
             // the message to lane u-1 is affine in recv: one FMA on the
