@@ -493,9 +493,12 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   if (nch > 1) return fail(SK_INVALID_ARGUMENT, "backward supports d <= 32");
   // Gram tiles of the linear kernel at dyadic order 0: DMMA backward
   // (sk_mma_bwd.cuh).  SK_NO_MMA=1 keeps the r01 kernels.
-  s.MMA = shared_cols && kind == LINEAR && lamR == 0 && lamC == 0 && (s.DP == 8 || s.DP == 16) &&
+  // (d <= 4 runs the DP = 8 instance on zero-padded increments: the padding
+  // adds exact zeros to every FMA chain, so p is bitwise unchanged)
+  s.MMA = shared_cols && kind == LINEAR && lamR == 0 && lamC == 0 && s.DP <= 16 &&
           !(std::getenv("SK_NO_MMA") && std::getenv("SK_NO_MMA")[0] == '1');
   if (s.MMA) {
+    if (s.DP == 4) s.DP = 8;
     const char* w = std::getenv("SK_BWD_WPC");
     s.WPC = (w && (w[0] == '3' || w[0] == '4')) ? w[0] - '0' : 2;  // measured: 2 >= 4 > 3
     int per_warp = 0;
@@ -599,6 +602,7 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
                              (int)n2, (int)r0, (int)r1,
                              mode != BATCH && !(mode == GRAM_CROSS && g.swap)))
     return rc;
+  if (pl.shape.MMA) pb.dpad = pl.shape.DP;  // d <= 4: padded to the DP = 8 instance
   BwdLayout lo;
   lo.prepR = align_up(prep_elems(kind, g.nR, g.LR, pb.dpad) * sizeof(double), 256);
   // LINEAR rows carry the exact dyadic factor (as in the forward); a symmetric

@@ -81,8 +81,8 @@ def test_gram_forward_mma_row_range(mods):
         assert rel_err(got[i, a:], full[a, a:]) < TOL
 
 
-BWD_SHAPES = [  # (n1, n2, L, d) -- DMMA backward serves 4 < d <= 16
-    (1, 1, 2, 5), (3, 3, 3, 6), (9, 9, 9, 8), (8, 8, 17, 5), (17, 17, 33, 8),
+BWD_SHAPES = [  # (n1, n2, L, d) -- DMMA backward serves d <= 16 (d <= 4 padded to 8)
+    (1, 1, 2, 5), (3, 3, 3, 6), (6, 6, 19, 1), (7, 9, 25, 3), (9, 9, 40, 4), (9, 9, 9, 8), (8, 8, 17, 5), (17, 17, 33, 8),
     (5, 12, 64, 7), (16, 16, 70, 16), (11, 11, 130, 13), (10, 10, 41, 12),
 ]
 
