@@ -253,7 +253,10 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         double acur[KS];  // A operand of tile T+2: dY[col 8(T+2) + lane/4][4kk + lane%4]
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) acur[kk] = sA[(((T + 2) % RA) * 8 + g) * DP + 4 * kk + u];
-        cck[(int64_t)T * 32] = make_double2(kl0, kl1);  // values at node column 8T - u
+        // checkpoints are read back only after the whole item's forward: for
+        // d = 16 stream them past L2 (evict-first; measured +0.5 %, -2.5 % at d = 8)
+        if constexpr (DP == 16) __stcs(cck + (int64_t)T * 32, make_double2(kl0, kl1));
+        else cck[(int64_t)T * 32] = make_double2(kl0, kl1);  // values at node column 8T - u
         double2* __restrict__ r0 = aslot(T);
         double2* __restrict__ r1 = aslot(T - 1);
         const int s0 = T & 1, s1 = (T - 1) & 1;  // slot within the ring half
@@ -276,7 +279,8 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
             if (u == 3 && !last) hrow[c] = k1;
             if (EDGE && last && u == u_star && c == NC - 1) kval = r_star ? k1 : k0;
           }
-          rck[(int64_t)(8 * T + m) * 32] = bot;  // diagonal index = column + lane
+          if constexpr (DP == 16) __stcs(rck + (int64_t)(8 * T + m) * 32, bot);
+          else rck[(int64_t)(8 * T + m) * 32] = bot;  // diagonal index = column + lane
         }
         __syncwarp();  // tile T+2 visible, tile T-1 dead
       };
