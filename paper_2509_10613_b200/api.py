@@ -201,3 +201,33 @@ def sig_kernel_gram_value_and_grad(x, y=None, cotangent=None, dyadic_order=0, st
         cotangent = torch.ones((n1, n2), dtype=torch.float64, device=xd.device)
     G, gx, gy = ops.value_and_grad_gram(xd, yd, l1, l2, kind, sigma, cotangent)
     return G, gx, gy
+
+
+def sig_mmd(x, y, dyadic_order=0, static_kernel=None):
+    """Biased squared maximum mean discrepancy between the path sets x (n, L1, d)
+    and y (m, L2, d) under the signature kernel:
+        MMD^2 = mean(K_xx) + mean(K_yy) - 2 mean(K_xy),
+    differentiable through sig_kernel_gram (a loss built on
+    the Gram hot path)."""
+    kxx = sig_kernel_gram(x, None, dyadic_order, static_kernel)
+    kyy = sig_kernel_gram(y, None, dyadic_order, static_kernel)
+    kxy = sig_kernel_gram(x, y, dyadic_order, static_kernel)
+    return kxx.mean() + kyy.mean() - 2.0 * kxy.mean()
+
+
+def sig_mmd_value_and_grad(x, y, dyadic_order=0, static_kernel=None):
+    """sig_mmd and its gradients (dMMD/dx, dMMD/dy) from three fused value +
+    gradient Gram passes (the cotangents of a mean are constants, so no
+    separate forward solve runs).  Not an autograd op."""
+    x, _ = _batched(_prep(x, "x"), "x")
+    y, _ = _batched(_prep(y, "y"), "y")
+    n, m = x.shape[0], y.shape[0]
+    dev = x.device
+    cxx = torch.full((n, n), 1.0 / (n * n), dtype=torch.float64, device=dev)
+    cyy = torch.full((m, m), 1.0 / (m * m), dtype=torch.float64, device=dev)
+    cxy = torch.full((n, m), -2.0 / (n * m), dtype=torch.float64, device=dev)
+    kxx, gxx, _ = sig_kernel_gram_value_and_grad(x, None, cxx, dyadic_order, static_kernel)
+    kyy, gyy, _ = sig_kernel_gram_value_and_grad(y, None, cyy, dyadic_order, static_kernel)
+    kxy, gx, gy = sig_kernel_gram_value_and_grad(x, y, cxy, dyadic_order, static_kernel)
+    mmd = kxx.mean() + kyy.mean() - 2.0 * kxy.mean()
+    return mmd, gxx + gx, gyy + gy

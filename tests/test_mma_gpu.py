@@ -194,3 +194,31 @@ def test_value_and_grad_gram_swapped_orientation(mods):
     wx, wy = orc.gram_backward(X, Y, C, 0, 0)
     assert rel_err(gx.cpu().numpy(), wx) < TOL
     assert rel_err(gy.cpu().numpy(), wy) < TOL
+
+
+@pytest.mark.parametrize("lam", [0, 1])
+def test_sig_mmd(mods, lam):
+    """MMD^2 from the Gram hot path: value vs the oracle Grams, gradients of the
+    fused API vs autograd vs the oracle Gram backward."""
+    import paper_2509_10613_b200 as sk
+    ops, orc = mods
+    rng = np.random.default_rng(41 + lam)
+    X = random_paths(rng, 7, 30, 8)
+    Y = random_paths(rng, 5, 30, 8)
+    want = (orc.kernel_gram(X, None, lam, lam).mean() + orc.kernel_gram(Y, None, lam, lam).mean()
+            - 2 * orc.kernel_gram(X, Y, lam, lam).mean())
+    xt = cu(X).requires_grad_(True)
+    yt = cu(Y).requires_grad_(True)
+    v = sk.sig_mmd(xt, yt, lam)
+    v.backward()
+    v2, gx2, gy2 = sk.sig_mmd_value_and_grad(cu(X), cu(Y), lam)
+    assert abs(v.item() - want) <= 1e-10 * abs(want) + 1e-14
+    assert abs(v2.item() - want) <= 1e-10 * abs(want) + 1e-14
+    gxw = (orc.gram_backward(X, None, np.full((7, 7), 1 / 49), lam, lam)
+           + orc.gram_backward(X, Y, np.full((7, 5), -2 / 35), lam, lam)[0])
+    gyw = (orc.gram_backward(Y, None, np.full((5, 5), 1 / 25), lam, lam)
+           + orc.gram_backward(X, Y, np.full((7, 5), -2 / 35), lam, lam)[1])
+    assert rel_err(xt.grad.cpu().numpy(), gxw) < TOL
+    assert rel_err(yt.grad.cpu().numpy(), gyw) < TOL
+    assert rel_err(gx2.cpu().numpy(), gxw) < TOL
+    assert rel_err(gy2.cpu().numpy(), gyw) < TOL
