@@ -4,6 +4,8 @@
         [--dyadic-x N] [--dyadic-y N] [--output k.sgt] \
         [--cotangent c.sgt --grad-output-x gx.sgt --grad-output-y gy.sgt]
     python -m paper_2509_10613_b200.cli gram --input x.sgt [--input2 y.sgt] --output g.sgt
+    python -m paper_2509_10613_b200.cli bench --task gram-value-grad --batch 64 --length 256 \
+        --dim 8 [--reps N] [--roofline] [--json] [--output r.json]
 
 Same subcommands, flags, file format and exit codes (0 ok, 2 usage, 1 data
 error) as the reference CLI's `kernel` and `gram` (sigcore/cli.py:53-73,
@@ -53,6 +55,22 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--dyadic-x", type=int, default=0)
     p.add_argument("--dyadic-y", type=int, default=0)
     p.add_argument("--output", required=True)
+    _common(p)
+    # the reference's `bench` (sigcore/cli.py:81-92, bench.py:59-98) on the GPU
+    # kernels, with Gram tasks; report: schemas/bench_report_gpu.schema.json
+    from .bench_tasks import TASKS
+    p = sub.add_parser("bench", help="time a task on the GPU; minimum over repetitions")
+    p.add_argument("--task", choices=TASKS, required=True)
+    p.add_argument("--batch", type=int, default=32)
+    p.add_argument("--length", type=int, default=128)
+    p.add_argument("--dim", type=int, default=4)
+    p.add_argument("--dyadic-x", type=int, default=0)
+    p.add_argument("--dyadic-y", type=int, default=0)
+    p.add_argument("--reps", type=int, default=50)
+    p.add_argument("--roofline", action="store_true",
+                   help="measure the FP64 peak live and report roofline_frac")
+    p.add_argument("--json", action="store_true", help="print the report as JSON")
+    p.add_argument("--output", default=None, help="also write the JSON report here")
     _common(p)
     return ap
 
@@ -143,6 +161,25 @@ def _gram(args) -> int:
     return 0
 
 
+def _bench(args) -> int:
+    from . import ops
+    from .bench_tasks import run_bench
+    peak = ops.dfma_peak() if args.roofline else None
+    report = run_bench(args.task, batch=args.batch, length=args.length, dim=args.dim,
+                       dyadic_x=args.dyadic_x, dyadic_y=args.dyadic_y, reps=args.reps,
+                       scalar_width=32 if args.dtype == "f32" else 64, peak_fma=peak)
+    text = report.to_json(indent=2)
+    if args.output is not None:
+        with open(args.output, "w") as fh:
+            fh.write(text + "\n")
+    if args.json:
+        print(text)
+    else:
+        print(f"{report.task} shape={report.shape} reps={report.repetitions} "
+              f"min={report.minimum:.6f}s cells/s={report.cells_per_s:.3e}")
+    return 0
+
+
 def main(argv=None) -> int:
     parser = build_parser()
     args = parser.parse_args(argv)
@@ -150,7 +187,7 @@ def main(argv=None) -> int:
         if args.grad_output_x is None or args.grad_output_y is None:
             parser.error("--cotangent requires --grad-output-x and --grad-output-y")
     try:
-        return {"kernel": _kernel, "gram": _gram}[args.command](args)
+        return {"kernel": _kernel, "gram": _gram, "bench": _bench}[args.command](args)
     except (InvalidArgument, InvalidState, FormatError, NativeUnavailable, OSError) as exc:
         print(f"sigkernel-b200: error: {exc}", file=sys.stderr)
         return 1

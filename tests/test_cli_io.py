@@ -116,3 +116,53 @@ class TestCliGpu:
         p.write_bytes(b"nope")
         r = run_cli("gram", "--input", str(p), "--output", str(tmp_path / "g.sgt"))
         assert r.returncode == 1
+
+
+def test_bench_report_schema_cpu():
+    """The GPU bench report keeps the reference's fields and validates against
+    schemas/bench_report_gpu.schema.json (no GPU needed for the report object)."""
+    import json
+    import os
+
+    import jsonschema
+
+    from paper_2509_10613_b200.bench_tasks import TASKS, BenchReport
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    schema = json.load(open(os.path.join(root, "schemas", "bench_report_gpu.schema.json")))
+    for task in TASKS:
+        r = BenchReport(task=task, shape={"B": 4, "L": 16, "d": 3, "dyadic_x": 0, "dyadic_y": 1},
+                        repetitions=3, times=[0.3, 0.2, 0.25], cells=4 * 15 * 30)
+        d = json.loads(r.to_json())
+        jsonschema.validate(d, schema)
+        assert d["minimum"] == 0.2 and abs(d["cells_per_s"] - 1800 / 0.2) < 1e-6
+        for k in ("task", "shape", "repetitions", "times", "minimum", "threads", "scalar_width"):
+            assert k in d  # the reference report's fields (sigcore/bench.py:38-47)
+
+
+def test_bench_parser_accepts_reference_flags():
+    from paper_2509_10613_b200 import cli
+    a = cli.build_parser().parse_args(["bench", "--task", "kernel-fwd", "--batch", "8",
+                                       "--length", "64", "--dim", "4", "--dyadic-x", "1",
+                                       "--reps", "5", "--json"])
+    assert a.task == "kernel-fwd" and a.reps == 5 and a.json
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("task", ["kernel-fwd", "kernel-bwd", "gram-fwd", "gram-bwd",
+                                  "gram-value-grad"])
+def test_bench_tasks_gpu(task, tmp_path):
+    """Every bench task runs on the GPU through the CLI and emits a report that
+    validates against the extended schema."""
+    import json
+
+    import jsonschema
+    out = tmp_path / "r.json"
+    r = subprocess.run([sys.executable, "-m", "paper_2509_10613_b200.cli", "bench", "--task", task,
+                        "--batch", "9", "--length", "40", "--dim", "6", "--reps", "3",
+                        "--roofline", "--output", str(out)],
+                       cwd=ROOT, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    d = json.loads(out.read_text())
+    schema = json.load(open(os.path.join(ROOT, "schemas", "bench_report_gpu.schema.json")))
+    jsonschema.validate(d, schema)
+    assert d["task"] == task and d["cells_per_s"] > 0 and d["roofline_frac"] > 0
