@@ -213,11 +213,20 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # test hook: SK_BENCH_ONE_GPU=1 puts every rank on cuda:0 and uses gloo, so
+    # the N > 1 code path (row blocks, all-gathers, max over ranks) can be
+    # exercised on a one-GPU box (its timings are meaningless)
+    one_gpu = os.environ.get("SK_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     import paper_2509_10613_b200 as sk
     from paper_2509_10613_b200 import gram_dist, ops
