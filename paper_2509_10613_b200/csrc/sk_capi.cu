@@ -44,6 +44,27 @@ static int device_sms() {
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
+// Budget for the backward's per-slot workspace (checkpoints grow with L^2 / 8
+// per in-flight tile): half the device memory, or SK_WS_BUDGET_GB.  Long paths
+// get fewer slots (fewer resident warps) instead of an allocation failure.
+static double ws_budget_bytes() {
+  if (const char* e = std::getenv("SK_WS_BUDGET_GB")) return std::atof(e) * 1e9;
+  size_t fr = 0, tot = 0;
+  if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 64e9;
+  }
+  return 0.5 * (double)tot;
+}
+
+// Shrinks the grid so that slots * per_slot_bytes fits the budget.
+static void cap_slots(int64_t& blocks, int64_t& slots, int warps, double per_slot_bytes) {
+  const double budget = ws_budget_bytes();
+  if ((double)slots * per_slot_bytes <= budget) return;
+  blocks = std::max<int64_t>(1, (int64_t)(budget / (per_slot_bytes * warps)));
+  slots = blocks * warps;
+}
+
 // ---------------------------------------------------------------- prep kernels
 // Increments (kernel.py:74-75 np.diff) into a zero-padded [n][L-1][dpad] array.
 __global__ void prep_increments(const double* __restrict__ x, int64_t n, int64_t L, int64_t d,
@@ -531,6 +552,8 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
     pl.row_stride = 8 * (NT8 + 5);
     pl.dbuf_stride = 0;
     pl.gscr_stride = 8 * NT8 * s.DP;
+    cap_slots(pl.blocks, pl.slots, s.WPC,
+              8.0 * (pl.rowck_stride + pl.colck_stride + pl.gscr_stride + 16 * pl.row_stride));
     return SK_OK;
   }
   s.R = bwd_rows_per_lane(s.DP);
@@ -571,6 +594,9 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   pl.row_stride = (int64_t)align_up((size_t)(M2 + 1), 32);
   pl.dbuf_stride = kind == RBF ? (int64_t)align_up((size_t)(M1c * M2c), 32) : 0;
   pl.gscr_stride = kind == LINEAR ? (int64_t)align_up((size_t)((M1c + M2c) * s.DP), 32) : 0;
+  cap_slots(pl.blocks, pl.slots, warps,
+            8.0 * (pl.rowck_stride + pl.colck_stride + pl.pck_stride + pl.dbuf_stride +
+                   pl.gscr_stride + 2 * pl.row_stride));
   return SK_OK;
 }
 

@@ -222,3 +222,24 @@ def test_sig_mmd(mods, lam):
     assert rel_err(yt.grad.cpu().numpy(), gyw) < TOL
     assert rel_err(gx2.cpu().numpy(), gxw) < TOL
     assert rel_err(gy2.cpu().numpy(), gyw) < TOL
+
+
+@pytest.mark.parametrize("no_mma", [False, True])
+def test_backward_workspace_budget_caps_slots(mods, no_mma):
+    """With a tiny workspace budget the backward runs on fewer resident slots
+    (each warp loops over more tiles) and returns the same gradient."""
+    ops, orc = mods
+    rng = np.random.default_rng(51)
+    X = random_paths(rng, 20, 37, 8)
+    C = rng.standard_normal((20, 20))
+    if no_mma:
+        os.environ["SK_NO_MMA"] = "1"
+    try:
+        full, _ = ops.backward_gram(cu(X), None, 0, 0, 0, 1.0, cu(C))
+        os.environ["SK_WS_BUDGET_GB"] = "0.000001"
+        capped, _ = ops.backward_gram(cu(X), None, 0, 0, 0, 1.0, cu(C))
+    finally:
+        os.environ.pop("SK_WS_BUDGET_GB", None)
+        os.environ.pop("SK_NO_MMA", None)
+    assert rel_err(capped.cpu().numpy(), full.cpu().numpy()) < 1e-13
+    assert rel_err(full.cpu().numpy(), orc.gram_backward(X, None, C, 0, 0)) < TOL
