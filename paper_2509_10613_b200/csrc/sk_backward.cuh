@@ -688,39 +688,62 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       auto Dat = [&](int i, int j) -> double {
         return (i >= 0 && j >= 0 && i < pb.M1c && j < pb.M2c) ? D[(int64_t)i * pb.M2c + j] : 0.0;
       };
+      // one distance and one exp per (i, j) and side (r01 recomputed them for
+      // every component k); the per-k sums keep their order, so the values
+      // are unchanged
       for (int i = u; i < L1n; i += 32) {
-        for (int k = 0; k < dR; ++k) {
-          double acc = 0.0;
-          for (int j = 0; j < L2n; ++j) {
-            const double G = Dat(i - 1, j - 1) - Dat(i - 1, j) - Dat(i, j - 1) + Dat(i, j);
-            if (G == 0.0) continue;
-            double s2 = 0.0;
-            for (int kk = 0; kk < dR; ++kk) {
-              const double t = xp[(int64_t)i * pb.dpad + kk] - yp[(int64_t)j * pb.dpad + kk];
-              s2 = fma(t, t, s2);
-            }
-            const double K = exp(-s2 * pb.inv2s2);
-            acc = fma(G * K * pb.invs2, yp[(int64_t)j * pb.dpad + k] - xp[(int64_t)i * pb.dpad + k], acc);
-          }
-          grad_add(gR + (int64_t)i * dR + k, acc, atomic);
+        double xi[DP], acc[DP];
+#pragma unroll
+        for (int k = 0; k < DP; ++k) {
+          xi[k] = xp[(int64_t)i * pb.dpad + k];
+          acc[k] = 0.0;
         }
+        for (int j = 0; j < L2n; ++j) {
+          const double G = Dat(i - 1, j - 1) - Dat(i - 1, j) - Dat(i, j - 1) + Dat(i, j);
+          if (G == 0.0) continue;
+          double yj[DP];
+#pragma unroll
+          for (int k = 0; k < DP; ++k) yj[k] = yp[(int64_t)j * pb.dpad + k];
+          double s2 = 0.0;  // padded components are 0 on both sides: exact no-ops
+#pragma unroll
+          for (int kk = 0; kk < DP; ++kk) {
+            const double t = xi[kk] - yj[kk];
+            s2 = fma(t, t, s2);
+          }
+          const double w = G * exp(-s2 * pb.inv2s2) * pb.invs2;
+#pragma unroll
+          for (int k = 0; k < DP; ++k) acc[k] = fma(w, yj[k] - xi[k], acc[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < DP; ++k)
+          if (k < dR) grad_add(gR + (int64_t)i * dR + k, acc[k], atomic);
       }
       for (int j = u; j < L2n; j += 32) {
-        for (int k = 0; k < dR; ++k) {
-          double acc = 0.0;
-          for (int i = 0; i < L1n; ++i) {
-            const double G = Dat(i - 1, j - 1) - Dat(i - 1, j) - Dat(i, j - 1) + Dat(i, j);
-            if (G == 0.0) continue;
-            double s2 = 0.0;
-            for (int kk = 0; kk < dR; ++kk) {
-              const double t = xp[(int64_t)i * pb.dpad + kk] - yp[(int64_t)j * pb.dpad + kk];
-              s2 = fma(t, t, s2);
-            }
-            const double K = exp(-s2 * pb.inv2s2);
-            acc = fma(G * K * pb.invs2, xp[(int64_t)i * pb.dpad + k] - yp[(int64_t)j * pb.dpad + k], acc);
-          }
-          grad_add(gC + (int64_t)j * dR + k, acc, atomic);
+        double yj[DP], acc[DP];
+#pragma unroll
+        for (int k = 0; k < DP; ++k) {
+          yj[k] = yp[(int64_t)j * pb.dpad + k];
+          acc[k] = 0.0;
         }
+        for (int i = 0; i < L1n; ++i) {
+          const double G = Dat(i - 1, j - 1) - Dat(i - 1, j) - Dat(i, j - 1) + Dat(i, j);
+          if (G == 0.0) continue;
+          double xi[DP];
+#pragma unroll
+          for (int k = 0; k < DP; ++k) xi[k] = xp[(int64_t)i * pb.dpad + k];
+          double s2 = 0.0;  // padded components are 0 on both sides: exact no-ops
+#pragma unroll
+          for (int kk = 0; kk < DP; ++kk) {
+            const double t = xi[kk] - yj[kk];
+            s2 = fma(t, t, s2);
+          }
+          const double w = G * exp(-s2 * pb.inv2s2) * pb.invs2;
+#pragma unroll
+          for (int k = 0; k < DP; ++k) acc[k] = fma(w, xi[k] - yj[k], acc[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < DP; ++k)
+          if (k < dR) grad_add(gC + (int64_t)j * dR + k, acc[k], atomic);
       }
       __syncwarp();
     }
