@@ -195,9 +195,11 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
     if (!fn) return fail(SK_INVALID_ARGUMENT, "no DMMA forward instance for this shape");
     pl.shape = s;
     pl.fn = fn;
-    pl.threads = 128;
+    const char* fw = std::getenv("SK_FWD_WPC");  // warps per CTA (tuning knob)
+    const int fwpc = (fw && (fw[0] == '1' || fw[0] == '4')) ? fw[0] - '0' : 2;  // measured: 2 >= 4
+    pl.threads = 32 * fwpc;
     pl.P = 8;
-    pl.smem_bytes = per_warp * 4;
+    pl.smem_bytes = per_warp * fwpc;
     pl.nitems = gram_items(mode, n2, r0, r1, pl.P);
     if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              pl.smem_bytes) != cudaSuccess)
@@ -208,8 +210,8 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
       (void)cudaGetLastError();
       occ = 1;
     }
-    pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + 3) / 4, (int64_t)occ * sms));
-    pl.slots = pl.blocks * 4 * pl.P;
+    pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + fwpc - 1) / fwpc, (int64_t)occ * sms));
+    pl.slots = pl.blocks * fwpc * pl.P;
     // lane u = 0 prefetches the handoff row 8 columns ahead of an 8-step tile loop
     pl.hand_stride = 8 * ((M2c + 10) / 8 + 2);
     return SK_OK;
