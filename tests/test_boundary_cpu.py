@@ -56,6 +56,14 @@ def test_errors_map_to_reference_exceptions(lib):
     rc = lib.sk_backward_gram(None, None, 2, 2, 5, 5, 2, 0, 0, 0, 1.0, 0, 2, None, None, None,
                               None, 0, None)
     assert rc == _lib.SK_INVALID_ARGUMENT  # cotangent required
+    import ctypes
+    dummy = ctypes.c_double(0.0)
+    rc = lib.sk_value_and_grad_gram(None, None, 2, 2, 5, 5, 2, 0, 0, 0, 1.0, 0, 2,
+                                    ctypes.addressof(dummy), None, None, None, None, 0, None)
+    assert rc == _lib.SK_INVALID_ARGUMENT and b"values" in lib.sk_last_error()
+    rc = lib.sk_value_and_grad_gram(None, None, 2, 3, 5, 5, 2, 0, 0, 0, 1.0, 0, 2,
+                                    ctypes.addressof(dummy), None, None, None, None, 0, None)
+    assert rc == _lib.SK_INVALID_ARGUMENT  # symmetric needs n2 == n1
 
 
 def test_workspace_queries_positive(lib):
