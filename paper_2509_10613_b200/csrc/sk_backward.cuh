@@ -698,8 +698,12 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           xi[k] = xp[(int64_t)i * pb.dpad + k];
           acc[k] = 0.0;
         }
+        double pu = 0.0, pc = 0.0;  // D(i-1, j-1), D(i, j-1) carried along j
         for (int j = 0; j < L2n; ++j) {
-          const double G = Dat(i - 1, j - 1) - Dat(i - 1, j) - Dat(i, j - 1) + Dat(i, j);
+          const double cu = Dat(i - 1, j), cc = Dat(i, j);
+          const double G = pu - cu - pc + cc;
+          pu = cu;
+          pc = cc;
           if (G == 0.0) continue;
           double yj[DP];
 #pragma unroll
@@ -725,8 +729,12 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           yj[k] = yp[(int64_t)j * pb.dpad + k];
           acc[k] = 0.0;
         }
+        double pl_ = 0.0, pr_ = 0.0;  // D(i-1, j-1), D(i-1, j) carried along i
         for (int i = 0; i < L1n; ++i) {
-          const double G = Dat(i - 1, j - 1) - Dat(i - 1, j) - Dat(i, j - 1) + Dat(i, j);
+          const double cl = Dat(i, j - 1), cr = Dat(i, j);
+          const double G = pl_ - pr_ - cl + cr;
+          pl_ = cl;
+          pr_ = cr;
           if (G == 0.0) continue;
           double xi[DP];
 #pragma unroll

@@ -224,11 +224,14 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
   pl.shape = s;
   pl.fn = fn;
   pl.smem_bytes = smem;
-  pl.threads = s.XW ? 32 * s.W : 128;
   pl.P = s.XW ? 1 : 32 / s.G;
-  const int warps = pl.threads / 32;
   if (mode == BATCH) pl.nitems = (npairs + pl.P - 1) / pl.P;
   else pl.nitems = gram_items(mode, n2, r0, r1, pl.P);
+  // few work items: smaller CTAs spread them over all SMs (each SM has its own
+  // FP64 pipe); e.g. BASELINE config 1 (32 pairs) used 8 SMs with 4-warp CTAs
+  const int fw_warps = (int)std::min<int64_t>(4, std::max<int64_t>(1, ceil_div(pl.nitems, sms)));
+  pl.threads = s.XW ? 32 * s.W : 32 * fw_warps;
+  const int warps = pl.threads / 32;
   if (smem > 0 &&
       cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
           cudaSuccess)
@@ -566,7 +569,10 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   if (!fn) return fail(SK_INVALID_ARGUMENT, "no backward kernel instance for this shape");
   pl.shape = s;
   pl.fn = fn;
-  pl.threads = 128;
+  pl.nitems = mode == BATCH ? npairs : gram_items(mode, n2, r0, r1, 1);
+  const int sms = device_sms();
+  // few pairs (BASELINE config 2: 256): smaller CTAs spread them over all SMs
+  pl.threads = 32 * (int)std::min<int64_t>(4, std::max<int64_t>(1, ceil_div(pl.nitems, sms)));
   const int warps = pl.threads / 32;
   pl.smem_bytes = smd * (int)sizeof(double) * warps;
   if (pl.smem_bytes > 48 * 1024) {
@@ -574,8 +580,6 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
                              pl.smem_bytes) != cudaSuccess)
       (void)cudaGetLastError();
   }
-  pl.nitems = mode == BATCH ? npairs : gram_items(mode, n2, r0, r1, 1);
-  const int sms = device_sms();
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, pl.threads,
                                                     pl.smem_bytes) != cudaSuccess ||
