@@ -152,6 +152,15 @@ def cpu_baseline(n_sample, L, d, lam, budget_s=10.0):
             "entries_per_s": n_sample * n_sample * reps / el}
 
 
+def config_dict(name, world):
+    """The workload's config (identical on both arms of the bench)."""
+    n, L, d, lam, desc = CONFIGS[name]
+    return {"workload": desc, "n": n, "L": L, "d": d, "dyadic_order": lam,
+            "static_kernel": "linear", "cotangent": "ones", "symmetric": True,
+            "parallelism": f"gram row blocks x{world}",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference CPU algorithm (oracle port), rank 0 only."""
     if rank != 0:
@@ -182,7 +191,8 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference _make_paths, seed 0)",
-        "config": {"workload": desc, "n": n, "L": L, "d": d, "dyadic_order": lam},
+        "config": config_dict(args.config, world),
+        "sample": f"{n_sample}x{n_sample} symmetric sub-Gram per step",
         "gram_entries_per_s": n_sample * n_sample / t,
         "cpu_baseline": {"value": value, "unit": "cells/s", "cores": threads, "kind": "port",
                          "sample": sample},
@@ -416,10 +426,7 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic Brownian paths (reference _make_paths generator, seed 0)",
-            "config": {"workload": desc, "n": n, "L": L, "d": d, "dyadic_order": lam,
-                       "static_kernel": "linear", "cotangent": "ones", "symmetric": True,
-                       "parallelism": f"gram row blocks x{world}",
-                       "l2": "flushed between timed steps (256 MiB write)"},
+            "config": config_dict(args.config, world),
             "gram_entries_per_s": n * n / t_step,
             "step": "one fused value + gradient pass per row block (G and dF/dX; the Gram "
                     "counterpart of the reference's kernel_batch_backward, which returns values "

@@ -218,16 +218,24 @@ def sig_mmd(x, y, dyadic_order=0, static_kernel=None):
 def sig_mmd_value_and_grad(x, y, dyadic_order=0, static_kernel=None):
     """sig_mmd and its gradients (dMMD/dx, dMMD/dy) from three fused value +
     gradient Gram passes (the cotangents of a mean are constants, so no
-    separate forward solve runs).  Not an autograd op."""
+    separate forward solve runs).  Not an autograd op.  Values and gradients
+    come back in promote_types(x.dtype, y.dtype), like sig_mmd."""
     x, _ = _batched(_prep(x, "x"), "x")
     y, _ = _batched(_prep(y, "y"), "y")
+    out_dtype = torch.promote_types(x.dtype, y.dtype)
     n, m = x.shape[0], y.shape[0]
     dev = x.device
+    xd = x.detach().to(torch.float64)
+    # the cross term must be a cross Gram even when y is x (a symmetric call
+    # would fold both gradient slots into dF/dx and return no dF/dy)
+    yd = y.detach().to(torch.float64)
+    if yd.data_ptr() == xd.data_ptr():
+        yd = yd.clone()
     cxx = torch.full((n, n), 1.0 / (n * n), dtype=torch.float64, device=dev)
     cyy = torch.full((m, m), 1.0 / (m * m), dtype=torch.float64, device=dev)
     cxy = torch.full((n, m), -2.0 / (n * m), dtype=torch.float64, device=dev)
-    kxx, gxx, _ = sig_kernel_gram_value_and_grad(x, None, cxx, dyadic_order, static_kernel)
-    kyy, gyy, _ = sig_kernel_gram_value_and_grad(y, None, cyy, dyadic_order, static_kernel)
-    kxy, gx, gy = sig_kernel_gram_value_and_grad(x, y, cxy, dyadic_order, static_kernel)
+    kxx, gxx, _ = sig_kernel_gram_value_and_grad(xd, None, cxx, dyadic_order, static_kernel)
+    kyy, gyy, _ = sig_kernel_gram_value_and_grad(yd, None, cyy, dyadic_order, static_kernel)
+    kxy, gx, gy = sig_kernel_gram_value_and_grad(xd, yd, cxy, dyadic_order, static_kernel)
     mmd = kxx.mean() + kyy.mean() - 2.0 * kxy.mean()
-    return mmd, gxx + gx, gyy + gy
+    return mmd.to(out_dtype), (gxx + gx).to(out_dtype), (gyy + gy).to(out_dtype)

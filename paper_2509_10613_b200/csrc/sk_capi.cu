@@ -13,7 +13,10 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 
 #include "../../include/sigkernel.h"
 #include "sk_backward.cuh"
@@ -35,11 +38,70 @@ static int fail(int code, const std::string& msg) {
       return fail(SK_CUDA_ERROR, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// ------------------------------------------------------------ host caches
+// Planning runs on every call (the workspace query and the launch), so every
+// driver query it needs is cached per device: SM count, memory budget, the
+// dynamic-shared-memory opt-in and the occupancy of each kernel instance.
+static std::mutex g_mu;
+static constexpr int kMaxDev = 64;
+
+static int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  return dev < kMaxDev ? dev : 0;
+}
+
 static int device_sms() {
-  int dev = 0, sms = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
-  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
-  return sms > 0 ? sms : 148;
+  static int cache[kMaxDev] = {0};
+  const int dev = current_device();
+  if (cache[dev] > 0) return cache[dev];
+  int sms = 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 148;
+  }
+  cache[dev] = sms > 0 ? sms : 148;
+  return cache[dev];
+}
+
+// Blocks of `fn` resident per SM at (threads, smem); opts the kernel into
+// `smem` bytes of dynamic shared memory first (once per device and size).
+static int occupancy(const void* fn, int threads, int smem) {
+  struct Key {
+    const void* fn;
+    int threads, smem, dev;
+    bool operator==(const Key& o) const {
+      return fn == o.fn && threads == o.threads && smem == o.smem && dev == o.dev;
+    }
+  };
+  struct Hash {
+    size_t operator()(const Key& k) const {
+      return std::hash<const void*>()(k.fn) ^ ((size_t)k.threads << 20) ^ ((size_t)k.smem << 32) ^
+             (size_t)k.dev;
+    }
+  };
+  static std::unordered_map<Key, int, Hash> cache;
+  const Key key{fn, threads, smem, current_device()};
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    (void)cudaGetLastError();
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess ||
+      occ < 1) {
+    (void)cudaGetLastError();
+    occ = 1;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  cache[key] = occ;
+  return occ;
 }
 
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -48,13 +110,21 @@ static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 // per in-flight tile): half the device memory, or SK_WS_BUDGET_GB.  Long paths
 // get fewer slots (fewer resident warps) instead of an allocation failure.
 static double ws_budget_bytes() {
-  if (const char* e = std::getenv("SK_WS_BUDGET_GB")) return std::atof(e) * 1e9;
+  static const double env_gb = [] {
+    const char* e = std::getenv("SK_WS_BUDGET_GB");
+    return (e && e[0]) ? std::atof(e) : 0.0;
+  }();
+  if (env_gb > 0) return env_gb * 1e9;
+  static double cache[kMaxDev] = {0};
+  const int dev = current_device();
+  if (cache[dev] > 0) return cache[dev];
   size_t fr = 0, tot = 0;
   if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) {
     (void)cudaGetLastError();
     return 64e9;
   }
-  return 0.5 * (double)tot;
+  cache[dev] = 0.5 * (double)tot;
+  return cache[dev];
 }
 
 // Shrinks the grid so that slots * per_slot_bytes fits the budget.
@@ -66,25 +136,35 @@ static void cap_slots(int64_t& blocks, int64_t& slots, int warps, double per_slo
 }
 
 // ---------------------------------------------------------------- prep kernels
-// Increments (kernel.py:74-75 np.diff) into a zero-padded [n][L-1][dpad] array.
-__global__ void prep_increments(const double* __restrict__ x, int64_t n, int64_t L, int64_t d,
-                                int dpad, double scale, double* __restrict__ out) {
-  int64_t total = n * (L - 1) * dpad;
+// Both sides of a call in ONE launch (rows side, then the columns side):
+// increments (kernel.py:74-75 np.diff, scaled, zero-padded to dpad) for the
+// linear kernel, padded nodes for RBF.
+struct PrepSide {
+  const double* x;
+  int64_t n, L;
+  double scale;
+  double* out;
+};
+__global__ void prep_sides(PrepSide s0, PrepSide s1, int nsides, int rbf, int64_t d, int dpad) {
+  const int64_t rows0 = s0.n * (rbf ? s0.L : s0.L - 1);
+  const int64_t rows1 = nsides > 1 ? s1.n * (rbf ? s1.L : s1.L - 1) : 0;
+  const int64_t total = (rows0 + rows1) * dpad;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t k = e % dpad, i = (e / dpad) % (L - 1), p = e / (dpad * (L - 1));
-    out[e] = (k < d) ? (x[(p * L + i + 1) * d + k] - x[(p * L + i) * d + k]) * scale : 0.0;
-  }
-}
-
-// Nodes into a zero-padded [n][L][dpad] array (RBF static kernel).
-__global__ void prep_nodes(const double* __restrict__ x, int64_t n, int64_t L, int64_t d,
-                           int dpad, double* __restrict__ out) {
-  int64_t total = n * L * dpad;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t k = e % dpad, i = (e / dpad) % L, p = e / (dpad * L);
-    out[e] = (k < d) ? x[(p * L + i) * d + k] : 0.0;
+    const int64_t rowg = e / dpad, k = e % dpad;
+    const bool first = rowg < rows0;
+    const PrepSide& sd = first ? s0 : s1;
+    const int64_t row = first ? rowg : rowg - rows0;
+    double v = 0.0;
+    if (k < d) {
+      if (rbf) {
+        v = sd.x[row * d + k];
+      } else {
+        const int64_t p = row / (sd.L - 1), i = row % (sd.L - 1);
+        v = (sd.x[(p * sd.L + i + 1) * d + k] - sd.x[(p * sd.L + i) * d + k]) * sd.scale;
+      }
+    }
+    sd.out[row * dpad + k] = v;
   }
 }
 
@@ -201,15 +281,7 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
     pl.P = 8;
     pl.smem_bytes = per_warp * fwpc;
     pl.nitems = gram_items(mode, n2, r0, r1, pl.P);
-    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             pl.smem_bytes) != cudaSuccess)
-      (void)cudaGetLastError();
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, pl.threads,
-                                                      pl.smem_bytes) != cudaSuccess || occ < 1) {
-      (void)cudaGetLastError();
-      occ = 1;
-    }
+    const int occ = occupancy((const void*)fn, pl.threads, pl.smem_bytes);
     pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + fwpc - 1) / fwpc, (int64_t)occ * sms));
     pl.slots = pl.blocks * fwpc * pl.P;
     // lane u = 0 prefetches the handoff row 8 columns ahead of an 8-step tile loop
@@ -232,17 +304,7 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
   const int fw_warps = (int)std::min<int64_t>(4, std::max<int64_t>(1, ceil_div(pl.nitems, sms)));
   pl.threads = s.XW ? 32 * s.W : 32 * fw_warps;
   const int warps = pl.threads / 32;
-  if (smem > 0 &&
-      cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
-          cudaSuccess)
-    (void)cudaGetLastError();
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, pl.threads, smem) !=
-          cudaSuccess ||
-      occ < 1) {
-    (void)cudaGetLastError();
-    occ = 1;
-  }
+  const int occ = occupancy((const void*)fn, pl.threads, smem);
   int64_t want = s.XW ? pl.nitems : (pl.nitems + warps - 1) / warps;
   pl.blocks = std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)occ * sms));
   pl.slots = s.XW ? pl.blocks : pl.blocks * warps * pl.P;
@@ -255,13 +317,16 @@ static size_t prep_elems(int kind, int64_t n, int64_t L, int dpad) {
   return kind == RBF ? (size_t)n * L * dpad : (size_t)n * (L - 1) * dpad;
 }
 
-static void launch_prep(int kind, const double* x, int64_t n, int64_t L, int64_t d, int dpad,
-                        double* out, cudaStream_t st, double scale = 1.0) {
-  size_t total = prep_elems(kind, n, L, dpad);
+// Prepares the rows side (scaled by `scale`) and, unless `share`, the columns
+// side, in one launch.
+static void launch_prep(int kind, const double* xr, int64_t nR, int64_t LR, const double* xc,
+                        int64_t nC, int64_t LC, bool share, int64_t d, int dpad, double* outR,
+                        double* outC, cudaStream_t st, double scale) {
+  const size_t total = prep_elems(kind, nR, LR, dpad) + (share ? 0 : prep_elems(kind, nC, LC, dpad));
   if (total == 0) return;
-  int blocks = (int)std::min<size_t>((total + 255) / 256, 4096);
-  if (kind == RBF) prep_nodes<<<blocks, 256, 0, st>>>(x, n, L, d, dpad, out);
-  else prep_increments<<<blocks, 256, 0, st>>>(x, n, L, d, dpad, scale, out);
+  const int blocks = (int)std::min<size_t>((total + 255) / 256, 4096);
+  PrepSide s0{xr, nR, LR, scale, outR}, s1{xc, nC, LC, 1.0, outC};
+  prep_sides<<<blocks, 256, 0, st>>>(s0, s1, share ? 1 : 2, kind == RBF ? 1 : 0, d, dpad);
 }
 
 static int validate(int64_t L1, int64_t L2, int64_t d, int lam1, int lam2, int kind,
@@ -367,8 +432,8 @@ static int forward_impl(const double* x, const double* y, int64_t n1, int64_t n2
   double* hand = reinterpret_cast<double*>(base + lo.prepR + lo.prepC);
   const double* xr = g.swap ? y : x;
   const double* xc = g.swap ? x : y;
-  launch_prep(kind, xr, g.nR, g.LR, d, pb.dpad, prepR, st, fold ? pb.scale : 1.0);
-  if (!share) launch_prep(kind, xc, g.nC, g.LC, d, pb.dpad, prepC, st);
+  launch_prep(kind, xr, g.nR, g.LR, xc, g.nC, g.LC, share, d, pb.dpad, prepR, prepC, st,
+              fold ? pb.scale : 1.0);
   if (fold) pb.pscale = 1.0;
   pb.R.p = prepR;
   pb.R.rows = (int)(g.LR - 1);
@@ -534,17 +599,9 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
     pl.fn = fn;
     pl.threads = 32 * s.WPC;
     pl.smem_bytes = per_warp * (int)sizeof(double) * s.WPC;
-    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             pl.smem_bytes) != cudaSuccess)
-      (void)cudaGetLastError();
     pl.nitems = gram_items(mode, n2, r0, r1, 8);
     const int sms = device_sms();
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, pl.threads,
-                                                      pl.smem_bytes) != cudaSuccess || occ < 1) {
-      (void)cudaGetLastError();
-      occ = 1;
-    }
+    const int occ = occupancy((const void*)fn, pl.threads, pl.smem_bytes);
     pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + s.WPC - 1) / s.WPC,
                                                        (int64_t)occ * sms));
     pl.slots = pl.blocks * s.WPC;
@@ -575,18 +632,7 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   pl.threads = 32 * (int)std::min<int64_t>(4, std::max<int64_t>(1, ceil_div(pl.nitems, sms)));
   const int warps = pl.threads / 32;
   pl.smem_bytes = smd * (int)sizeof(double) * warps;
-  if (pl.smem_bytes > 48 * 1024) {
-    if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             pl.smem_bytes) != cudaSuccess)
-      (void)cudaGetLastError();
-  }
-  int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, pl.threads,
-                                                    pl.smem_bytes) != cudaSuccess ||
-      occ < 1) {
-    (void)cudaGetLastError();
-    occ = 1;
-  }
+  const int occ = occupancy((const void*)fn, pl.threads, pl.smem_bytes);
   pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + warps - 1) / warps,
                                                      (int64_t)occ * sms));
   pl.slots = pl.blocks * warps;
@@ -690,8 +736,8 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   ba.rows_exclusive = (1 << g.lamR) <= pl.shape.R ? 1 : 0;
   const double* xr = g.swap ? y : x;
   const double* xc = g.swap ? x : y;
-  launch_prep(kind, xr, g.nR, g.LR, d, pb.dpad, prepR, st, fold ? pb.scale : 1.0);
-  if (!share) launch_prep(kind, xc, g.nC, g.LC, d, pb.dpad, prepC, st);
+  launch_prep(kind, xr, g.nR, g.LR, xc, g.nC, g.LC, share, d, pb.dpad, prepR, prepC, st,
+              fold ? pb.scale : 1.0);
   if (fold) pb.pscale = 1.0;
   pb.R.p = prepR;
   pb.R.rows = (int)(g.LR - 1);
@@ -712,7 +758,12 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   ba.atomic = mode == BATCH ? 0 : 1;
   ba.cot = cot;
   ba.values = values;
+#ifdef SK_PROFILING
+  // profiling experiments (tools/build_variant.sh -DSK_PROFILING): skip phases
   ba.exp = std::getenv("SK_EXP") ? std::atoi(std::getenv("SK_EXP")) : 0;
+#else
+  ba.exp = 0;  // release builds never read SK_EXP (it would corrupt results)
+#endif
   pl.fn<<<(unsigned)pl.blocks, pl.threads, pl.smem_bytes, st>>>(pb, ba);
   SK_CUDA(cudaGetLastError());
   return SK_OK;

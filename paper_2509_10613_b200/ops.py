@@ -17,8 +17,24 @@ def _ptr(t):
     return t.data_ptr() if t is not None else None
 
 
-def _stream():
-    return torch.cuda.current_stream().cuda_stream
+def _stream(device=None):
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _same_device(t, ref, name):
+    if t is not None and t.device != ref.device:
+        raise InvalidArgument(f"{name} is on {t.device}, expected {ref.device}")
+
+
+def _cotangent(cot, shape, ref, name="cotangent"):
+    """Validated float64 contiguous cotangent of exactly `shape` on ref's device
+    (the kernels index it as a dense array of that shape)."""
+    if not isinstance(cot, torch.Tensor):
+        raise InvalidArgument(f"{name} must be a torch tensor")
+    if tuple(cot.shape) != tuple(shape):
+        raise InvalidArgument(f"{name} must have shape {tuple(shape)}, got {tuple(cot.shape)}")
+    _same_device(cot, ref, name)
+    return cot.to(torch.float64).contiguous()
 
 
 def _workspace(nbytes: int, device) -> torch.Tensor:
@@ -35,6 +51,13 @@ def _paths(t: torch.Tensor, name: str) -> torch.Tensor:
     if not t.is_cuda:
         raise InvalidArgument(f"{name} must live on a CUDA device")
     return t.to(torch.float64).contiguous()
+
+
+def _grad_buffer(g, ref, name):
+    if g.shape != ref.shape or g.dtype != torch.float64 or not g.is_contiguous():
+        raise InvalidArgument(f"{name} must be a contiguous float64 tensor of shape "
+                              f"{tuple(ref.shape)}")
+    _same_device(g, ref, name)
 
 
 def static_kind(static_kernel):
@@ -58,14 +81,16 @@ def forward_batch(x, y, lam1: int, lam2: int, kind: int, sigma: float) -> torch.
         raise InvalidArgument(f"batch sizes differ: {B} vs {y.shape[0]}")
     if y.shape[2] != d:
         raise InvalidArgument(f"path dimensions differ: {d} vs {y.shape[2]}")
+    _same_device(y, x, "y")
     L2 = y.shape[1]
     out = torch.empty(B, dtype=torch.float64, device=x.device)
     if B == 0:
         return out
-    nb = lib.sk_forward_batch_workspace_bytes(B, L1, L2, d, lam1, lam2, kind)
-    ws = _workspace(nb, x.device)
-    _lib.check(lib.sk_forward_batch(_ptr(x), _ptr(y), B, L1, L2, d, lam1, lam2, kind, sigma,
-                                    _ptr(out), _ptr(ws), ws.numel(), _stream()))
+    with torch.cuda.device(x.device):
+        nb = lib.sk_forward_batch_workspace_bytes(B, L1, L2, d, lam1, lam2, kind)
+        ws = _workspace(nb, x.device)
+        _lib.check(lib.sk_forward_batch(_ptr(x), _ptr(y), B, L1, L2, d, lam1, lam2, kind, sigma,
+                                        _ptr(out), _ptr(ws), ws.numel(), _stream(x.device)))
     return out
 
 
@@ -80,16 +105,18 @@ def forward_gram(x, y, lam1: int, lam2: int, kind: int, sigma: float,
     n2, L2 = yy.shape[0], yy.shape[1]
     if yy.shape[2] != d:
         raise InvalidArgument(f"path dimensions differ: {d} vs {yy.shape[2]}")
+    _same_device(yy, x, "y")
     r0, r1 = (0, n1) if rows is None else (int(rows[0]), int(rows[1]))
     if out is None:
         out = torch.empty((r1 - r0, n2), dtype=torch.float64, device=x.device)
     if n1 == 0 or n2 == 0 or r1 <= r0:
         return out
-    nb = lib.sk_forward_gram_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind, int(sym))
-    ws = _workspace(nb, x.device)
-    _lib.check(lib.sk_forward_gram(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d, lam1,
-                                   lam2, kind, sigma, r0, r1, _ptr(out), _ptr(ws), ws.numel(),
-                                   _stream()))
+    with torch.cuda.device(x.device):
+        nb = lib.sk_forward_gram_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind, int(sym))
+        ws = _workspace(nb, x.device)
+        _lib.check(lib.sk_forward_gram(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
+                                       lam1, lam2, kind, sigma, r0, r1, _ptr(out), _ptr(ws),
+                                       ws.numel(), _stream(x.device)))
     return out
 
 
@@ -99,10 +126,11 @@ def solve_delta(delta: torch.Tensor, lam1: int, lam2: int) -> torch.Tensor:
     delta = delta.to(torch.float64).contiguous()
     B, r1, r2 = delta.shape
     out = torch.empty(B, dtype=torch.float64, device=delta.device)
-    nb = lib.sk_solve_delta_workspace_bytes(B, r1, r2, lam1, lam2)
-    ws = _workspace(nb, delta.device)
-    _lib.check(lib.sk_solve_delta(_ptr(delta), B, r1, r2, lam1, lam2, _ptr(out), _ptr(ws),
-                                  ws.numel(), _stream()))
+    with torch.cuda.device(delta.device):
+        nb = lib.sk_solve_delta_workspace_bytes(B, r1, r2, lam1, lam2)
+        ws = _workspace(nb, delta.device)
+        _lib.check(lib.sk_solve_delta(_ptr(delta), B, r1, r2, lam1, lam2, _ptr(out), _ptr(ws),
+                                      ws.numel(), _stream(delta.device)))
     return out
 
 
@@ -112,7 +140,9 @@ def solve_delta_grid(delta: torch.Tensor, lam1: int, lam2: int) -> torch.Tensor:
     r1, r2 = delta.shape
     grid = torch.empty(((r1 << lam1) + 1, (r2 << lam2) + 1), dtype=torch.float64,
                        device=delta.device)
-    _lib.check(lib.sk_solve_delta_grid(_ptr(delta), r1, r2, lam1, lam2, _ptr(grid), _stream()))
+    with torch.cuda.device(delta.device):
+        _lib.check(lib.sk_solve_delta_grid(_ptr(delta), r1, r2, lam1, lam2, _ptr(grid),
+                                           _stream(delta.device)))
     return grid
 
 
@@ -127,17 +157,19 @@ def backward_batch(x, y, lam1, lam2, kind, sigma, cot, want_values=False):
         raise InvalidArgument(f"batch sizes differ: {B} vs {y.shape[0]}")
     if y.shape[2] != d:
         raise InvalidArgument(f"path dimensions differ: {d} vs {y.shape[2]}")
-    cot = cot.to(torch.float64).contiguous() if cot is not None else None
+    _same_device(y, x, "y")
+    cot = _cotangent(cot, (B,), x) if cot is not None else None
     gx = torch.empty_like(x)
     gy = torch.empty_like(y)
     vals = torch.empty(B, dtype=torch.float64, device=x.device) if want_values else None
     if B == 0:
         return vals, gx, gy
-    nb = lib.sk_backward_batch_workspace_bytes(B, L1, L2, d, lam1, lam2, kind)
-    ws = _workspace(nb, x.device)
-    _lib.check(lib.sk_backward_batch(_ptr(x), _ptr(y), B, L1, L2, d, lam1, lam2, kind, sigma,
-                                     _ptr(cot), _ptr(vals), _ptr(gx), _ptr(gy), _ptr(ws),
-                                     ws.numel(), _stream()))
+    with torch.cuda.device(x.device):
+        nb = lib.sk_backward_batch_workspace_bytes(B, L1, L2, d, lam1, lam2, kind)
+        ws = _workspace(nb, x.device)
+        _lib.check(lib.sk_backward_batch(_ptr(x), _ptr(y), B, L1, L2, d, lam1, lam2, kind, sigma,
+                                         _ptr(cot), _ptr(vals), _ptr(gx), _ptr(gy), _ptr(ws),
+                                         ws.numel(), _stream(x.device)))
     return vals, gx, gy
 
 
@@ -151,20 +183,27 @@ def backward_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, grad_x=None, gr
     yy = x if sym else _paths(y, "y")
     n1, L1, d = x.shape
     n2, L2 = yy.shape[0], yy.shape[1]
+    if yy.shape[2] != d:
+        raise InvalidArgument(f"path dimensions differ: {d} vs {yy.shape[2]}")
+    _same_device(yy, x, "y")
     r0, r1 = (0, n1) if rows is None else (int(rows[0]), int(rows[1]))
-    cot = cot.to(torch.float64).contiguous()
+    cot = _cotangent(cot, (n1, n2), x)
     if grad_x is None:
         grad_x = torch.zeros_like(x)
     if grad_y is None and not sym:
         grad_y = torch.zeros_like(yy)
+    _grad_buffer(grad_x, x, "grad_x")
+    if not sym:
+        _grad_buffer(grad_y, yy, "grad_y")
     if n1 == 0 or n2 == 0 or r1 <= r0:
         return grad_x, grad_y
-    nb = lib.sk_backward_gram_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind, int(sym))
-    ws = _workspace(nb, x.device)
-    _lib.check(lib.sk_backward_gram(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d, lam1,
-                                    lam2, kind, sigma, r0, r1, _ptr(cot), _ptr(grad_x),
-                                    _ptr(grad_y) if not sym else None, _ptr(ws), ws.numel(),
-                                    _stream()))
+    with torch.cuda.device(x.device):
+        nb = lib.sk_backward_gram_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind, int(sym))
+        ws = _workspace(nb, x.device)
+        _lib.check(lib.sk_backward_gram(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
+                                        lam1, lam2, kind, sigma, r0, r1, _ptr(cot), _ptr(grad_x),
+                                        _ptr(grad_y) if not sym else None, _ptr(ws), ws.numel(),
+                                        _stream(x.device)))
     return grad_x, grad_y
 
 
@@ -181,22 +220,28 @@ def value_and_grad_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, out=None,
     n2, L2 = yy.shape[0], yy.shape[1]
     if yy.shape[2] != d:
         raise InvalidArgument(f"path dimensions differ: {d} vs {yy.shape[2]}")
+    _same_device(yy, x, "y")
     r0, r1 = (0, n1) if rows is None else (int(rows[0]), int(rows[1]))
-    cot = cot.to(torch.float64).contiguous()
+    cot = _cotangent(cot, (n1, n2), x)
     if out is None:
         out = torch.empty((r1 - r0, n2), dtype=torch.float64, device=x.device)
     if grad_x is None:
         grad_x = torch.zeros_like(x)
     if grad_y is None and not sym:
         grad_y = torch.zeros_like(yy)
+    _grad_buffer(grad_x, x, "grad_x")
+    if not sym:
+        _grad_buffer(grad_y, yy, "grad_y")
     if n1 == 0 or n2 == 0 or r1 <= r0:
         return out, grad_x, grad_y
-    nb = lib.sk_backward_gram_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind, int(sym))
-    ws = _workspace(nb, x.device)
-    _lib.check(lib.sk_value_and_grad_gram(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
-                                          lam1, lam2, kind, sigma, r0, r1, _ptr(cot), _ptr(out),
-                                          _ptr(grad_x), _ptr(grad_y) if not sym else None,
-                                          _ptr(ws), ws.numel(), _stream()))
+    with torch.cuda.device(x.device):
+        nb = lib.sk_backward_gram_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind, int(sym))
+        ws = _workspace(nb, x.device)
+        _lib.check(lib.sk_value_and_grad_gram(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2,
+                                              d, lam1, lam2, kind, sigma, r0, r1, _ptr(cot),
+                                              _ptr(out), _ptr(grad_x),
+                                              _ptr(grad_y) if not sym else None, _ptr(ws),
+                                              ws.numel(), _stream(x.device)))
     return out, grad_x, grad_y
 
 
@@ -204,7 +249,8 @@ def mirror_upper(G: torch.Tensor) -> torch.Tensor:
     """In place: lower triangle := upper triangle (kernel.py:177-179)."""
     lib = _lib.load()
     n = G.shape[0]
-    _lib.check(lib.sk_mirror_upper(_ptr(G), n, G.stride(0), _stream()))
+    with torch.cuda.device(G.device):
+        _lib.check(lib.sk_mirror_upper(_ptr(G), n, G.stride(0), _stream(G.device)))
     return G
 
 
