@@ -264,17 +264,21 @@ def main():
         Optionally records (start, end) events."""
         if ev is not None:
             ev[0].record()
-        gx = torch.zeros_like(X)
-        parts = [ops.value_and_grad_gram(X, None, lam, lam, 0, 1.0, C, rows=rg, grad_x=gx)[0]
-                 for rg in ranges]
+        if world == 1:
+            parts = [ops.value_and_grad_gram(X, None, lam, lam, 0, 1.0, C)[0]]
+            gx = None
+        else:  # exact accumulators: bitwise the one-GPU gradient (gram_dist)
+            acc = ops.GradAcc(n, L, d, dev).init(C, n, n, True)
+            parts = [ops.value_and_grad_gram(X, None, lam, lam, 0, 1.0, C, rows=rg,
+                                             acc_x=acc)[0] for rg in ranges]
         if ev is not None:
             ev[1].record()
         if world > 1:
             local_rows = torch.cat(parts, 0)
             ranges_all = [gram_dist.row_blocks(n, world, r, True) for r in range(world)]
-            G = gram_dist._gather_rows(local_rows, ranges_all, n, n, group)
+            G = gram_dist._gather_rows(local_rows, ranges_all, n, n, group, symmetric=True)
             ops.mirror_upper(G)
-            gx = gram_dist._gather_sum(gx, group)
+            gx = gram_dist._allreduce_acc(acc, group).finalize()
         return parts, gx
 
     def step_unfused(ev):

@@ -24,6 +24,8 @@
  *                       kernel_backward per pair)
  *   sk_value_and_grad_gram  the same, also returning the Gram entries (as
  *                       kernel_batch_backward returns values, kernel_grad.py:64-98)
+ *   sk_backward_gram_acc + sk_grad_acc_*  the Gram backward into exact
+ *                       accumulators (split- and GPU-count-invariant gradients)
  *
  * Conventions
  *   - every array pointer is DEVICE memory, C-contiguous float64, borrowed for
@@ -124,10 +126,14 @@ size_t sk_backward_gram_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int6
  * (rows a in [row_begin, row_end); symmetric: pairs a <= b, weighted by
  * cot[a,b] + cot[b,a] because G mirrors the upper triangle).  cot is the FULL
  * (n1, n2) cotangent.  grad_x += dF/dx, grad_y += dF/dy (grad_y unused when
- * y == NULL: both sides land in grad_x).  Gradients ACCUMULATE into the
- * caller's buffers with device atomics (zero them first); values are
- * deterministic to rounding, not bitwise, across runs.  The batch backward
- * (no shared paths) is bitwise deterministic. */
+ * y == NULL: both sides land in grad_x).  Inside the call the pair
+ * contributions are summed EXACTLY (integer fixed-point limbs, see
+ * sk_grad_acc_* below), so the result is bitwise reproducible run to run and
+ * independent of the launch geometry (reference contract: no reduction order
+ * may vary, tests/test_kernel.py:156-171).  For
+ * results that are also bitwise independent of how the rows are split across
+ * calls or GPUs, use sk_backward_gram_acc.  The batch backward (no shared
+ * paths) writes each pair's gradient exclusively. */
 int sk_backward_gram(const double *x, const double *y, int64_t n1, int64_t n2, int64_t L1,
                      int64_t L2, int64_t d, int lam1, int lam2, int static_kernel,
                      double sigma, int64_t row_begin, int64_t row_end, const double *cot,
@@ -147,6 +153,36 @@ int sk_value_and_grad_gram(const double *x, const double *y, int64_t n1, int64_t
                            int static_kernel, double sigma, int64_t row_begin, int64_t row_end,
                            const double *cot, double *values, double *grad_x, double *grad_y,
                            void *workspace, size_t workspace_bytes, void *stream);
+
+/* ---- exact Gram-gradient accumulators ------------------------------------
+ * A gradient of n paths (L, d) accumulated as fixed-point int64 limbs:
+ * blob = [8 x int64 metadata][n*L*d x 4 x int64 limbs].  Contributions are
+ * added with integer atomics, so the sum is exact and independent of order;
+ * blobs of several calls/ranks combine by adding the limbs as integers
+ * (e.g. NCCL all-reduce SUM on int64) and taking the MAX of the metadata.
+ * The anchor (scale) is fixed at init from max|cot| and max(n1, n2): every
+ * call and rank feeding one gradient must init with the same full cotangent.
+ * A contribution beyond the accumulator's range (~2^66 x n x max|cot|) or a
+ * non-finite one sets a flag and the finalize step returns NaN. */
+size_t sk_grad_acc_bytes(int64_t n, int64_t L, int64_t d);
+int sk_grad_acc_init(void *acc, int64_t n, int64_t L, int64_t d, const double *cot, int64_t n1,
+                     int64_t n2, int symmetric, void *stream);
+/* grad = value (accumulate == 0) or grad += value */
+int sk_grad_acc_finalize(const void *acc, int64_t n, int64_t L, int64_t d, double *grad,
+                         int accumulate, void *stream);
+
+size_t sk_backward_gram_acc_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                            int64_t d, int lam1, int lam2, int static_kernel,
+                                            int symmetric);
+/* sk_backward_gram / sk_value_and_grad_gram into caller accumulators: adds the
+ * gradient of the pairs with rows in [row_begin, row_end) to acc_x (and acc_y;
+ * NULL when y == NULL).  values (nullable) receives the Gram entries as in
+ * sk_value_and_grad_gram. */
+int sk_backward_gram_acc(const double *x, const double *y, int64_t n1, int64_t n2, int64_t L1,
+                         int64_t L2, int64_t d, int lam1, int lam2, int static_kernel,
+                         double sigma, int64_t row_begin, int64_t row_end, const double *cot,
+                         double *values, void *acc_x, void *acc_y, void *workspace,
+                         size_t workspace_bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -46,6 +46,13 @@ SIGNATURES = {
                           _i64, _dp, _dp, _dp, _vp, _sz, _vp], _ci),
     "sk_value_and_grad_gram": ([_dp, _dp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd,
                                 _i64, _i64, _dp, _dp, _dp, _dp, _vp, _sz, _vp], _ci),
+    "sk_grad_acc_bytes": ([_i64, _i64, _i64], _sz),
+    "sk_grad_acc_init": ([_vp, _i64, _i64, _i64, _dp, _i64, _i64, _ci, _vp], _ci),
+    "sk_grad_acc_finalize": ([_vp, _i64, _i64, _i64, _dp, _ci, _vp], _ci),
+    "sk_backward_gram_acc_workspace_bytes": ([_i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _ci],
+                                             _sz),
+    "sk_backward_gram_acc": ([_dp, _dp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd, _i64,
+                              _i64, _dp, _dp, _vp, _vp, _vp, _sz, _vp], _ci),
 }
 
 _lib = None

@@ -30,6 +30,8 @@
 //     seeded by the strips below and finished by lane 0; RBF uses a per-pair
 //     coarse buffer (DBUF).  Increment gradients are telescoped to point
 //     gradients once per pair (kernel_grad.py:51-60).
+//   * Gram gradients go into exact fixed-point accumulators (FixAcc,
+//     sk_common.cuh), bitwise independent of the order pairs finish in;
 //   * nothing proportional to the fine grid is stored per pair beyond the
 //     checkpoints (1/R + 1/(CB*S*F) of the grid).
 #pragma once
@@ -45,9 +47,12 @@ enum MapMode : int { FUSED = 0, DBUF = 1 };
 #define SK_EXP 0
 #endif
 
-__device__ __forceinline__ void grad_add(double* p, double v, bool atomic) {
-  if (atomic) atomicAdd(p, v);
-  else *p += v;
+// Batch: the pair owns its gradient rows (plain add into the zeroed output);
+// Gram: exact fixed-point accumulation (FixAcc, sk_common.cuh).
+__device__ __forceinline__ void grad_add(double* g, const FixAcc& f, int64_t e, double v,
+                                         bool gram) {
+  if (gram) fix_add(f, e, v);
+  else g[e] += v;
 }
 
 constexpr int pow2_at_least(int n) {
@@ -331,9 +336,13 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       for (int64_t e = u; e < (int64_t)pb.M1c * DP; e += 32) gxs[e] = 0.0;
     }
     __syncwarp();
-    double* __restrict__ gR = ba.gradR + pr * ba.gR_path;
-    double* __restrict__ gC = ba.gradC + pc * ba.gC_path;
     const bool atomic = ba.atomic != 0;
+    double* __restrict__ gR = atomic ? nullptr : ba.gradR + pr * ba.gR_path;
+    double* __restrict__ gC = atomic ? nullptr : ba.gradC + pc * ba.gC_path;
+    const FixAcc fxR = atomic ? fix_make(ba.accR, ba.metaR) : FixAcc{};
+    const FixAcc fxC = atomic ? fix_make(ba.accC, ba.metaC) : FixAcc{};
+    const int64_t eR = atomic ? pr * ba.gR_path : 0;  // element offsets into the accumulators
+    const int64_t eC = atomic ? pc * ba.gC_path : 0;
 
     for (int strip = nstrips - 1; strip >= 0; --strip) {
       const int rbase = strip * H + u * R;
@@ -667,14 +676,14 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         double v = 0.0;
         if (p >= 1) v += gxs[(int64_t)(p - 1) * DP + k];
         if (p < pb.M1c) v -= gxs[(int64_t)p * DP + k];
-        grad_add(gR + e, v, atomic);
+        grad_add(gR, fxR, eR + e, v, atomic);
       }
       for (int64_t e = u; e < (int64_t)(pb.M2c + 1) * dR; e += 32) {
         const int p = (int)(e / dR), k = (int)(e % dR);
         double v = 0.0;
         if (p >= 1) v += gcs[(int64_t)(p - 1) * DP + k];
         if (p < pb.M2c) v -= gcs[(int64_t)p * DP + k];
-        grad_add(gC + e, v, atomic);
+        grad_add(gC, fxC, eC + e, v, atomic);
       }
       __syncwarp();
     } else {
@@ -720,7 +729,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         }
 #pragma unroll
         for (int k = 0; k < DP; ++k)
-          if (k < dR) grad_add(gR + (int64_t)i * dR + k, acc[k], atomic);
+          if (k < dR) grad_add(gR, fxR, eR + (int64_t)i * dR + k, acc[k], atomic);
       }
       for (int j = u; j < L2n; j += 32) {
         double yj[DP], acc[DP];
@@ -751,7 +760,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         }
 #pragma unroll
         for (int k = 0; k < DP; ++k)
-          if (k < dR) grad_add(gC + (int64_t)j * dR + k, acc[k], atomic);
+          if (k < dR) grad_add(gC, fxC, eC + (int64_t)j * dR + k, acc[k], atomic);
       }
       __syncwarp();
     }

@@ -206,6 +206,103 @@ __global__ void grid_kernel(const double* __restrict__ delta, int r1, int r2, in
   }
 }
 
+// ------------------------------------------- exact Gram-gradient accumulators
+// Accumulator blob (sk_grad_acc_bytes): [meta: 8 x u64][elements x 4 x u64],
+// see FixAcc in sk_common.cuh.
+constexpr int64_t kAccMeta = 8;
+
+static size_t acc_bytes(int64_t n, int64_t L, int64_t d) {
+  return (size_t)(kAccMeta + n * L * d * 4) * sizeof(unsigned long long);
+}
+
+__device__ __forceinline__ unsigned long long umax64(unsigned long long a, unsigned long long b) {
+  return a > b ? a : b;
+}
+
+// meta[0] = max|cot| (bit pattern), meta[2] = nscale; up to two metas.
+__global__ void fix_init_kernel(const double* __restrict__ cot, int64_t count, double nscale,
+                                unsigned long long* meta_a, unsigned long long* meta_b) {
+  unsigned long long m = 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x)
+    m = umax64(m, (unsigned long long)__double_as_longlong(fabs(cot[e])));
+  for (int o = 16; o > 0; o >>= 1) m = umax64(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) {
+    atomicMax(meta_a, m);
+    if (meta_b) atomicMax(meta_b, m);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    meta_a[2] = (unsigned long long)__double_as_longlong(nscale);
+    if (meta_b) meta_b[2] = (unsigned long long)__double_as_longlong(nscale);
+  }
+}
+
+// grad (+)= value of the accumulated limbs; NaN everywhere if the overflow
+// flag is set.  The limbs are carry-normalised first, so the value is a
+// function of the exact integer sum only (tests/fixpt_ref.py restates it).
+__global__ void fix_finalize_kernel(const unsigned long long* __restrict__ blob, int64_t nelem,
+                                    double* __restrict__ grad, int accumulate) {
+  const unsigned long long* meta = blob;
+  const long long* acc = reinterpret_cast<const long long*>(blob + kAccMeta);
+  const int E = fix_anchor(__longlong_as_double((long long)meta[0]),
+                           __longlong_as_double((long long)meta[2]));
+  const bool bad = meta[1] != 0;
+  const double u3 = ldexp(1.0, E - 42), u2 = ldexp(1.0, E - 84), u1 = ldexp(1.0, E - 126),
+               u0 = ldexp(1.0, E - 168);
+  constexpr long long M = (1ll << 42) - 1;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nelem;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const longlong2 lo = reinterpret_cast<const longlong2*>(acc)[2 * e];
+    const longlong2 hi = reinterpret_cast<const longlong2*>(acc)[2 * e + 1];
+    long long a0 = lo.x, a1 = lo.y, a2 = hi.x, a3 = hi.y;
+    auto normalize = [&]() {
+      a1 += a0 >> 42;
+      a0 &= M;
+      a2 += a1 >> 42;
+      a1 &= M;
+      a3 += a2 >> 42;
+      a2 &= M;
+    };
+    normalize();
+    // magnitude first (all four digits non-negative: no cancellation in the
+    // fp64 sum), then the sign
+    const bool neg = a3 < 0;
+    if (neg) {
+      a0 = -a0;
+      a1 = -a1;
+      a2 = -a2;
+      a3 = -a3;
+      normalize();
+    }
+    double v = (double)a3 * u3 + ((double)a2 * u2 + ((double)a1 * u1 + (double)a0 * u0));
+    if (neg) v = -v;
+    if (bad) v = __longlong_as_double(0x7ff8000000000000ll);
+    grad[e] = accumulate ? grad[e] + v : v;
+  }
+}
+
+static int acc_init(unsigned long long* blob_a, unsigned long long* blob_b, size_t bytes_a,
+                    size_t bytes_b, const double* cot, int64_t n1, int64_t n2, bool sym,
+                    cudaStream_t st) {
+  SK_CUDA(cudaMemsetAsync(blob_a, 0, bytes_a, st));
+  if (blob_b) SK_CUDA(cudaMemsetAsync(blob_b, 0, bytes_b, st));
+  const int64_t count = n1 * n2;
+  const double nscale = (double)std::max(n1, n2) * (sym ? 2.0 : 1.0);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, 1024));
+  fix_init_kernel<<<blocks, 256, 0, st>>>(cot, count, nscale, blob_a, blob_b);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
+static int acc_finalize(const unsigned long long* blob, int64_t nelem, double* grad,
+                        bool accumulate, cudaStream_t st) {
+  if (nelem <= 0) return SK_OK;
+  const int blocks = (int)std::min<int64_t>((nelem + 255) / 256, 8 * 148);
+  fix_finalize_kernel<<<blocks, 256, 0, st>>>(blob, nelem, grad, accumulate ? 1 : 0);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
+}
+
 // ------------------------------------------------------------------- planning
 struct Geometry {
   // oriented problem (rows = longer fine axis)
@@ -654,14 +751,18 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
 
 struct BwdLayout {
   size_t prepR = 0, prepC = 0, rowck = 0, colck = 0, pck = 0, rows = 0, dbuf = 0, gscr = 0,
-         total = 0;
+         accx = 0, accy = 0, total = 0;
 };
 
+// Gram gradients go through exact accumulators: the caller's (acc_x / acc_y,
+// sk_backward_gram_acc) or, when those are NULL, per-call ones in the
+// workspace that are finalised into grad_x / grad_y (+=) at the end.
 static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n2, int64_t L1,
                          int64_t L2, int64_t d, int lam1, int lam2, int kind, double sigma,
                          int mode, int64_t r0, int64_t r1, const double* cot, double* values,
                          double* grad_x, double* grad_y, void* ws, size_t ws_bytes,
-                         cudaStream_t st, size_t* query) {
+                         cudaStream_t st, size_t* query, void* acc_x = nullptr,
+                         void* acc_y = nullptr) {
   if (int rc = validate(L1, L2, d, lam1, lam2, kind, sigma)) return rc;
   const bool sym = mode == GRAM_SYM;
   Geometry g = orient(n1, n2, L1, L2, lam1, lam2);
@@ -695,7 +796,12 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   lo.rows = align_up((size_t)row_slots * pl.row_stride * 2 * sizeof(double), 256);
   lo.dbuf = align_up((size_t)pl.slots * pl.dbuf_stride * sizeof(double), 256);
   lo.gscr = align_up((size_t)pl.slots * pl.gscr_stride * sizeof(double), 256);
-  lo.total = lo.prepR + lo.prepC + lo.rowck + lo.colck + lo.pck + lo.rows + lo.dbuf + lo.gscr;
+  const bool gram = mode != BATCH;
+  const bool own_acc = gram && acc_x == nullptr;
+  lo.accx = own_acc ? align_up(acc_bytes(n1, L1, d), 256) : 0;
+  lo.accy = (own_acc && !sym) ? align_up(acc_bytes(n2, L2, d), 256) : 0;
+  lo.total = lo.prepR + lo.prepC + lo.rowck + lo.colck + lo.pck + lo.rows + lo.dbuf + lo.gscr +
+             lo.accx + lo.accy;
   if (query) {
     *query = lo.total;
     return SK_OK;
@@ -709,7 +815,11 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   if (ws_bytes < lo.total)
     return fail(SK_INVALID_ARGUMENT, "workspace too small: need " + std::to_string(lo.total) +
                                          " bytes, got " + std::to_string(ws_bytes));
-  if (!grad_x || (!sym && !grad_y)) return fail(SK_INVALID_ARGUMENT, "gradient buffers missing");
+  if (own_acc || !gram) {
+    if (!grad_x || (!sym && !grad_y)) return fail(SK_INVALID_ARGUMENT, "gradient buffers missing");
+  } else if (!sym && !acc_y) {
+    return fail(SK_INVALID_ARGUMENT, "cross Gram needs both accumulators");
+  }
   char* base = static_cast<char*>(ws);
   double* prepR = reinterpret_cast<double*>(base);
   double* prepC = share ? prepR : reinterpret_cast<double*>(base + lo.prepR);
@@ -733,6 +843,19 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   p += lo.dbuf;
   ba.gscr = reinterpret_cast<double*>(p);
   ba.gscr_stride = pl.gscr_stride;
+  p += lo.gscr;
+  unsigned long long* blob_x = static_cast<unsigned long long*>(acc_x);
+  unsigned long long* blob_y = static_cast<unsigned long long*>(acc_y);
+  if (own_acc) {
+    blob_x = reinterpret_cast<unsigned long long*>(p);
+    p += lo.accx;
+    blob_y = sym ? nullptr : reinterpret_cast<unsigned long long*>(p);
+    p += lo.accy;
+    if (int rc = acc_init(blob_x, blob_y, acc_bytes(n1, L1, d), acc_bytes(n2, L2, d), cot, n1, n2,
+                          sym, st))
+      return rc;
+  }
+  if (sym) blob_y = blob_x;
   ba.rows_exclusive = (1 << g.lamR) <= pl.shape.R ? 1 : 0;
   const double* xr = g.swap ? y : x;
   const double* xc = g.swap ? x : y;
@@ -752,6 +875,14 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   double* gx_cols = sym ? grad_x : (g.swap ? grad_x : grad_y);
   ba.gradR = gx_rows;
   ba.gradC = gx_cols;
+  if (gram) {
+    unsigned long long* br = g.swap && !sym ? blob_y : blob_x;
+    unsigned long long* bc = g.swap && !sym ? blob_x : blob_y;
+    ba.metaR = br;
+    ba.metaC = bc;
+    ba.accR = br + kAccMeta;
+    ba.accC = bc + kAccMeta;
+  }
   ba.gR_path = g.LR * d;
   ba.gC_path = g.LC * d;
   ba.d = (int)d;
@@ -766,6 +897,11 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
 #endif
   pl.fn<<<(unsigned)pl.blocks, pl.threads, pl.smem_bytes, st>>>(pb, ba);
   SK_CUDA(cudaGetLastError());
+  if (own_acc) {
+    if (int rc = acc_finalize(blob_x, n1 * L1 * d, grad_x, true, st)) return rc;
+    if (!sym)
+      if (int rc = acc_finalize(blob_y, n2 * L2 * d, grad_y, true, st)) return rc;
+  }
   return SK_OK;
 }
 
@@ -841,6 +977,67 @@ int sk_backward_gram(const double* x, const double* y, int64_t n1, int64_t n2, i
   return backward_impl(x, sym ? x : y, n1, n2, L1, L2, d, lam1, lam2, static_kernel, sigma,
                        sym ? GRAM_SYM : GRAM_CROSS, row_begin, row_end, cot, nullptr, grad_x,
                        grad_y, ws, ws_bytes, (cudaStream_t)stream, nullptr);
+}
+
+size_t sk_grad_acc_bytes(int64_t n, int64_t L, int64_t d) {
+  if (n < 0 || L < 0 || d < 0) return 0;
+  return acc_bytes(n, L, d);
+}
+
+int sk_grad_acc_init(void* acc, int64_t n, int64_t L, int64_t d, const double* cot, int64_t n1,
+                     int64_t n2, int symmetric, void* stream) {
+  if (!acc || n < 0 || L < 0 || d < 0 || n1 < 0 || n2 < 0)
+    return fail(SK_INVALID_ARGUMENT, "bad accumulator arguments");
+  if (n1 * n2 > 0 && !cot) return fail(SK_INVALID_ARGUMENT, "cotangent missing");
+  return acc_init(static_cast<unsigned long long*>(acc), nullptr, acc_bytes(n, L, d), 0, cot, n1,
+                  n2, symmetric != 0, (cudaStream_t)stream);
+}
+
+int sk_grad_acc_finalize(const void* acc, int64_t n, int64_t L, int64_t d, double* grad,
+                         int accumulate, void* stream) {
+  if (!acc || !grad || n < 0 || L < 0 || d < 0)
+    return fail(SK_INVALID_ARGUMENT, "bad accumulator arguments");
+  return acc_finalize(static_cast<const unsigned long long*>(acc), n * L * d, grad,
+                      accumulate != 0, (cudaStream_t)stream);
+}
+
+int sk_backward_gram_acc(const double* x, const double* y, int64_t n1, int64_t n2, int64_t L1,
+                         int64_t L2, int64_t d, int lam1, int lam2, int static_kernel,
+                         double sigma, int64_t row_begin, int64_t row_end, const double* cot,
+                         double* values, void* acc_x, void* acc_y, void* ws, size_t ws_bytes,
+                         void* stream) {
+  const bool sym = (y == nullptr);
+  if (sym && (n2 != n1 || L2 != L1))
+    return fail(SK_INVALID_ARGUMENT, "symmetric Gram needs n2 == n1 and L2 == L1");
+  if (row_begin < 0 || row_end > n1 || row_begin > row_end)
+    return fail(SK_INVALID_ARGUMENT, "row range out of bounds");
+  if (!cot) return fail(SK_INVALID_ARGUMENT, "Gram backward needs the cotangent matrix");
+  if (!acc_x) return fail(SK_INVALID_ARGUMENT, "accumulator missing");
+  if (int rc = backward_impl(x, sym ? x : y, n1, n2, L1, L2, d, lam1, lam2, static_kernel, sigma,
+                             sym ? GRAM_SYM : GRAM_CROSS, row_begin, row_end, cot, values,
+                             nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream, nullptr,
+                             acc_x, acc_y))
+    return rc;
+  const int64_t span = row_end - row_begin;
+  if (values && sym && span > 1) {
+    int blocks = (int)std::min<int64_t>((span * span + 255) / 256, 4096);
+    mirror_upper<<<blocks, 256, 0, (cudaStream_t)stream>>>(values, n2, (int)row_begin,
+                                                           (int)row_end);
+    SK_CUDA(cudaGetLastError());
+  }
+  return SK_OK;
+}
+
+size_t sk_backward_gram_acc_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                            int64_t d, int lam1, int lam2, int static_kernel,
+                                            int symmetric) {
+  size_t q = 0;
+  char dummy = 0;  // non-NULL accumulator: the workspace holds no accumulators
+  if (backward_impl(nullptr, nullptr, n1, n2, L1, L2, d, lam1, lam2, static_kernel, 1.0,
+                    symmetric ? GRAM_SYM : GRAM_CROSS, 0, n1, nullptr, nullptr, nullptr,
+                    nullptr, nullptr, 0, nullptr, &q, &dummy, &dummy))
+    return 0;
+  return q;
 }
 
 }  // extern "C"

@@ -73,11 +73,17 @@ struct BwdArgs {
   int64_t gscr_stride;
   int rows_exclusive;  // 2^lam1 <= R: every coarse row belongs to one lane
   // outputs (point gradients, real dimension d)
-  double* gradR;  // gradient of the grid-row path set
-  double* gradC;  // gradient of the grid-column path set
+  double* gradR;  // BATCH: gradient of the grid-row path set
+  double* gradC;  // BATCH: gradient of the grid-column path set
+  // GRAM: exact fixed-point accumulators of the row / column path sets
+  // ([path][L][d][4] int64) and their metadata (see FixAcc)
+  unsigned long long* accR;
+  unsigned long long* accC;
+  unsigned long long* metaR;
+  unsigned long long* metaC;
   int64_t gR_path, gC_path;  // elements per path (L * d)
   int d;
-  int atomic;  // accumulate with atomics (Gram: several pairs share a path)
+  int atomic;  // Gram: accumulate into accR / accC (several pairs share a path)
   const double* cot;  // BATCH: [npairs] (nullptr = ones); GRAM: [n1][n2]
   double* values;     // BATCH: optional kernel values
   int exp;            // profiling experiments (env SK_EXP, default 0): 1 skips phase B,
@@ -86,6 +92,79 @@ struct BwdArgs {
 };
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---------------------------------------------------------------------------
+// Exact (order-independent) accumulation of Gram gradients.
+//
+// A Gram gradient element receives one contribution per Gram tile that
+// touches its path, from many warps and -- when sharded -- many GPUs.  fp64
+// atomics make the result depend on arrival order; the reference contract is
+// that no floating-point reduction order may vary (/root/reference/SPEC.md:261,
+// pkg/tests/test_kernel.py:156-171).  Here every contribution v is converted
+// exactly (no rounding except below the lowest limb) to a signed fixed-point
+// number with four 42-bit chunks relative to a per-call anchor 2^E, and the
+// chunks are added into four int64 limbs with integer atomics.  Integer
+// addition is associative, so the sums -- and the fp64 value made from them --
+// are bitwise identical for any schedule, any row-block split and any number of
+// GPUs (the limbs of several ranks are summed as integers).
+//
+//   element layout: acc[elem][4] (limb 3 = top chunk, unit 2^(E-42); limb k
+//   unit 2^(E-42(4-k))), 32 bytes = one sector per element;
+//   anchor: E = exponent of (nscale * max|cot|) + 64, nscale = max(n1, n2)
+//   (x2 symmetric) -- every gradient element is a sum of at most that many
+//   cotangent-weighted pair gradients, so E sits ~64 bits above realistic
+//   magnitudes and the lowest limb resolves 2^-104 of the bound;
+//   a contribution with |v| >= 2^(E+2) (or inf/NaN) sets the overflow flag and
+//   the finalize step writes NaN (never a silent wrong value).
+// meta[0]: max|cot| bit pattern (atomicMax; non-negative doubles order like
+// their bits), meta[1]: flags, meta[2]: nscale (double bits).
+struct FixAcc {
+  unsigned long long* acc;  // [elements][4]
+  unsigned long long* meta;
+  double s3;                // 2^(42 - E): contribution -> top-chunk units
+};
+
+__host__ __device__ inline int fix_anchor(double maxc, double nscale) {
+  const double m = maxc * nscale;
+  if (!(m > 0.0) || !(m < 1e300)) return 0;
+  int e = 0;
+  (void)frexp(m, &e);  // m < 2^e
+  e += 64;
+  return e < -900 ? -900 : (e > 960 ? 960 : e);
+}
+
+__device__ __forceinline__ FixAcc fix_make(unsigned long long* acc, unsigned long long* meta) {
+  FixAcc f;
+  f.acc = acc;
+  f.meta = meta;
+  const int E = fix_anchor(__longlong_as_double((long long)meta[0]),
+                           __longlong_as_double((long long)meta[2]));
+  f.s3 = ldexp(1.0, 42 - E);
+  return f;
+}
+
+__device__ __forceinline__ void fix_add(const FixAcc& f, int64_t elem, double v) {
+  if (v == 0.0) return;  // adds nothing (keeps padded / dead lanes off the atomics)
+  double x = v * f.s3;
+  if (!(fabs(x) < 0x1p44)) {  // overflow, inf or NaN: flagged, finalize writes NaN
+    atomicOr(f.meta + 1, 1ull);
+    return;
+  }
+  // exact splits: each step removes the integer part and shifts the (exact)
+  // remainder up by 42 bits; only the last chunk is rounded
+  const double c3 = trunc(x);
+  x = (x - c3) * 0x1p42;
+  const double c2 = trunc(x);
+  x = (x - c2) * 0x1p42;
+  const double c1 = trunc(x);
+  x = (x - c1) * 0x1p42;
+  const double c0 = rint(x);
+  unsigned long long* p = f.acc + elem * 4;
+  atomicAdd(p + 3, (unsigned long long)(long long)c3);
+  atomicAdd(p + 2, (unsigned long long)(long long)c2);
+  atomicAdd(p + 1, (unsigned long long)(long long)c1);
+  atomicAdd(p + 0, (unsigned long long)(long long)c0);
+}
 
 // Work item -> (a0, b): the item covers pairs (a0 + g, b), g < P.
 // GRAM_CROSS: a-blocks of P rows of [r0, r1) x all b.

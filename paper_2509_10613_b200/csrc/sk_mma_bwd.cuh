@@ -42,8 +42,9 @@
 //   Shared tiles are unpadded with XOR swizzles (psw / dsw / xsw): every
 //   fragment store and load is bank-conflict-free.
 //   Increment gradients are telescoped to point gradients (rows: per strip
-//   from registers; columns: once per tile from the scratch) and flushed with
-//   fp64 atomics (several tiles share a path), kernel_grad.py:55-60.
+//   from registers; columns: once per tile from the scratch) and flushed into
+//   exact fixed-point accumulators (FixAcc, sk_common.cuh: integer atomics, so
+//   the result is bitwise independent of tile order), kernel_grad.py:55-60.
 #pragma once
 #include <type_traits>
 
@@ -111,6 +112,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
   double* __restrict__ hrow = ba.hand + (slot * 8 + g) * ba.row_stride;
   double* __restrict__ arow = ba.adj + (slot * 8 + g) * ba.row_stride;
   double* __restrict__ gcs = ba.gscr + slot * ba.gscr_stride;  // column gradients [8*NT8][DP]
+  const FixAcc fxR = fix_make(ba.accR, ba.metaR), fxC = fix_make(ba.accC, ba.metaC);
 
   for (int64_t item = slot; item < pb.nitems; item += (int64_t)gridDim.x * WPC) {
     int a0, b;
@@ -528,15 +530,15 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           const double up0 = __shfl_up_sync(0xffffffffu, gx[h][n][0], 4);
           const double up1 = __shfl_up_sync(0xffffffffu, gx[h][n][1], 4);
           if (!hv || rho >= M1) continue;
-          double* gp = ba.gradR + (int64_t)ah * ba.gR_path;
+          const int64_t gp = (int64_t)ah * ba.gR_path;
           const int k = 8 * n + 2 * u;
           const double v0 = (g > 0 ? up0 : 0.0) - gx[h][n][0];
           const double v1 = (g > 0 ? up1 : 0.0) - gx[h][n][1];
-          if (k < dR) atomicAdd(gp + (int64_t)rho * dR + k, v0);
-          if (k + 1 < dR) atomicAdd(gp + (int64_t)rho * dR + k + 1, v1);
+          if (k < dR) fix_add(fxR, gp + (int64_t)rho * dR + k, v0);
+          if (k + 1 < dR) fix_add(fxR, gp + (int64_t)rho * dR + k + 1, v1);
           if (g == 7 || rho == M1 - 1) {  // point rho + 1 (next strip's row 0 adds the rest)
-            if (k < dR) atomicAdd(gp + (int64_t)(rho + 1) * dR + k, gx[h][n][0]);
-            if (k + 1 < dR) atomicAdd(gp + (int64_t)(rho + 1) * dR + k + 1, gx[h][n][1]);
+            if (k < dR) fix_add(fxR, gp + (int64_t)(rho + 1) * dR + k, gx[h][n][0]);
+            if (k + 1 < dR) fix_add(fxR, gp + (int64_t)(rho + 1) * dR + k + 1, gx[h][n][1]);
           }
         }
       }
@@ -546,13 +548,13 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
     // column-side gradient (summed over the tile's pairs and strips), telescoped
     {
       const int dR = ba.d;
-      double* gC = ba.gradC + (int64_t)b * ba.gC_path;
+      const int64_t gC = (int64_t)b * ba.gC_path;
       for (int e = lane; e < (NC + 1) * dR; e += 32) {
         const int p = e / dR, k = e % dR;
         double v = 0.0;
         if (p >= 1) v += gcs[(int64_t)(p - 1) * DP + k];
         if (p < NC) v -= gcs[(int64_t)p * DP + k];
-        atomicAdd(gC + e, v);
+        fix_add(fxC, gC + e, v);
       }
     }
     __syncwarp();

@@ -22,19 +22,26 @@ from .api import _orders
 from .errors import InvalidArgument
 
 
+TILE = 8  # Gram tile height of the DMMA kernels (pairs (a0 + g, b), g < 8)
+
+
 def row_blocks(n: int, world: int, rank: int, symmetric: bool = True) -> list[tuple[int, int]]:
     """Row ranges owned by `rank`.
 
     symmetric: 2*world equal blocks, rank gets blocks rank and 2*world-1-rank
-    (balanced upper-triangle pair counts); otherwise one contiguous block."""
+    (balanced upper-triangle pair counts); otherwise one contiguous block.
+    Block boundaries are multiples of TILE (the kernels' 8-path Gram tile
+    height), so every rank sees the same tiles as a one-GPU run and the exact
+    gradient accumulators sum to bitwise the one-GPU gradient."""
     if world <= 1:
         return [(0, n)]
     if not symmetric:
         step = -(-n // world)
+        step = -(-step // TILE) * TILE
         lo, hi = min(n, rank * step), min(n, (rank + 1) * step)
         return [(lo, hi)] if hi > lo else []
     nb = 2 * world
-    bounds = [round(k * n / nb) for k in range(nb + 1)]
+    bounds = [min(n, TILE * round(k * n / nb / TILE)) for k in range(nb)] + [n]
     out = []
     for k in (rank, nb - 1 - rank):
         lo, hi = bounds[k], bounds[k + 1]
@@ -56,15 +63,44 @@ def _world(group):
     return dist.get_world_size(group), dist.get_rank(group)
 
 
-def _gather_rows(local_rows: torch.Tensor, ranges_all, n1: int, n2: int, group) -> torch.Tensor:
-    """All-gather per-rank row blocks (padded to equal size) into a full (n1, n2)."""
+def _upper_mask(ranges, n, device):
+    """Boolean mask of the solved (b >= a) entries of the concatenated row
+    blocks `ranges` of a symmetric (n, n) Gram."""
+    rows = torch.cat([torch.arange(lo, hi, device=device) for lo, hi in ranges]) if ranges \
+        else torch.zeros(0, dtype=torch.long, device=device)
+    return torch.arange(n, device=device).view(1, n) >= rows.view(-1, 1)
+
+
+def _gather_rows(local_rows: torch.Tensor, ranges_all, n1: int, n2: int, group,
+                 symmetric: bool = False) -> torch.Tensor:
+    """All-gather per-rank row blocks into a full (n1, n2).  Symmetric: only the
+    solved upper-triangle entries travel (packed, padded to the largest rank),
+    about half the bytes of full rows; the caller mirrors."""
     world = len(ranges_all)
+    dev = local_rows.device
+    if symmetric:
+        counts = [int(sum((n2 - a) for lo, hi in r for a in range(lo, hi))) for r in ranges_all]
+        rank = dist.get_rank(group)
+        mine = local_rows[_upper_mask(ranges_all[rank], n2, dev)]
+        pad = torch.zeros(max(counts), dtype=local_rows.dtype, device=dev)
+        pad[: mine.numel()] = mine
+        gathered = torch.empty(world * max(counts), dtype=pad.dtype, device=dev)
+        dist.all_gather_into_tensor(gathered, pad, group=group)
+        G = torch.zeros((n1, n2), dtype=pad.dtype, device=dev)
+        for r, ranges in enumerate(ranges_all):
+            if not ranges:
+                continue
+            idx = torch.cat([torch.arange(lo, hi, device=dev) for lo, hi in ranges])
+            blk = G[idx]
+            blk[_upper_mask(ranges, n2, dev)] = gathered[r * max(counts): r * max(counts) + counts[r]]
+            G[idx] = blk
+        return G
     maxrows = max(sum(hi - lo for lo, hi in r) for r in ranges_all)
-    pad = torch.zeros((maxrows, n2), dtype=local_rows.dtype, device=local_rows.device)
+    pad = torch.zeros((maxrows, n2), dtype=local_rows.dtype, device=dev)
     pad[: local_rows.shape[0]] = local_rows
-    gathered = torch.empty((world * maxrows, n2), dtype=pad.dtype, device=pad.device)
+    gathered = torch.empty((world * maxrows, n2), dtype=pad.dtype, device=dev)
     dist.all_gather_into_tensor(gathered, pad, group=group)
-    G = torch.empty((n1, n2), dtype=pad.dtype, device=pad.device)
+    G = torch.empty((n1, n2), dtype=pad.dtype, device=dev)
     for r, ranges in enumerate(ranges_all):
         off = r * maxrows
         for lo, hi in ranges:
@@ -73,18 +109,13 @@ def _gather_rows(local_rows: torch.Tensor, ranges_all, n1: int, n2: int, group) 
     return G
 
 
-def _gather_sum(t: torch.Tensor, group) -> torch.Tensor:
-    """All-gather equal-shape partials and sum them in fixed rank order."""
-    world, _ = _world(group)
-    t = t.contiguous()
-    flat = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype,
-                       device=t.device)
-    dist.all_gather_into_tensor(flat, t, group=group)
-    buf = flat.view((world,) + tuple(t.shape))
-    out = buf[0].clone()
-    for r in range(1, world):
-        out += buf[r]
-    return out
+def _allreduce_acc(acc, group):
+    """Combine the exact gradient accumulators of all ranks: the limbs add as
+    integers (exact, order-free), the metadata (identical anchor, OR of the
+    overflow flags) by MAX."""
+    dist.all_reduce(acc.limbs, op=dist.ReduceOp.SUM, group=group)
+    dist.all_reduce(acc.meta, op=dist.ReduceOp.MAX, group=group)
+    return acc
 
 
 def gram_forward_sharded(x, y, l1, l2, kind, sigma, group=None) -> torch.Tensor:
@@ -98,26 +129,35 @@ def gram_forward_sharded(x, y, l1, l2, kind, sigma, group=None) -> torch.Tensor:
     parts = [ops.forward_gram(x, y, l1, l2, kind, sigma, rows=rg) for rg in mine]
     local = torch.cat(parts, 0) if parts else torch.zeros((0, n2), dtype=torch.float64,
                                                          device=x.device)
-    G = _gather_rows(local, ranges_all, n1, n2, group)
+    G = _gather_rows(local, ranges_all, n1, n2, group, symmetric=sym)
     if sym:
         ops.mirror_upper(G)
     return G
+
+
+def _accumulators(x, y, cot, sym):
+    n1, L1, d = x.shape
+    acc_x = ops.GradAcc(n1, L1, d, x.device).init(cot, n1, y.shape[0] if y is not None else n1,
+                                                   sym)
+    acc_y = None
+    if not sym:
+        acc_y = ops.GradAcc(y.shape[0], y.shape[1], d, x.device).init(cot, n1, y.shape[0], False)
+    return acc_x, acc_y
 
 
 def gram_backward_sharded(x, y, l1, l2, kind, sigma, cot, group=None):
     world, rank = _world(group)
     sym = y is None
     n1 = x.shape[0]
-    gx = torch.zeros_like(x, dtype=torch.float64)
-    gy = None if sym else torch.zeros_like(y, dtype=torch.float64)
+    acc_x, acc_y = _accumulators(x, y, cot, sym)
     ranges = row_blocks(n1, world, rank, sym) if world > 1 else [(0, n1)]
     for rg in ranges:
-        ops.backward_gram(x, y, l1, l2, kind, sigma, cot, rows=rg, grad_x=gx, grad_y=gy)
+        ops.backward_gram(x, y, l1, l2, kind, sigma, cot, rows=rg, acc_x=acc_x, acc_y=acc_y)
     if world > 1:
-        gx = _gather_sum(gx, group)
-        if gy is not None:
-            gy = _gather_sum(gy, group)
-    return gx, gy
+        _allreduce_acc(acc_x, group)
+        if acc_y is not None:
+            _allreduce_acc(acc_y, group)
+    return acc_x.finalize(), (None if acc_y is None else acc_y.finalize())
 
 
 class _ShardedGramFn(torch.autograd.Function):
@@ -175,19 +215,18 @@ def value_and_grad_sharded(x, y=None, cotangent=None, dyadic_order=0, static_ker
     if world == 1:
         return ops.value_and_grad_gram(xx, yy, l1, l2, kind, sigma, cotangent)
     ranges_all = [row_blocks(n1, world, r, sym) for r in range(world)]
-    gx = torch.zeros_like(xx)
-    gy = None if sym else torch.zeros_like(yy)
+    acc_x, acc_y = _accumulators(xx, yy, cotangent, sym)
     parts = []
     for rg in ranges_all[rank]:
         out, _, _ = ops.value_and_grad_gram(xx, yy, l1, l2, kind, sigma, cotangent, rows=rg,
-                                            grad_x=gx, grad_y=gy)
+                                            acc_x=acc_x, acc_y=acc_y)
         parts.append(out)
     local = torch.cat(parts, 0) if parts else torch.zeros((0, n2), dtype=torch.float64,
                                                          device=xx.device)
-    G = _gather_rows(local, ranges_all, n1, n2, group)
+    G = _gather_rows(local, ranges_all, n1, n2, group, symmetric=sym)
     if sym:
         ops.mirror_upper(G)
-    gx = _gather_sum(gx, group)
-    if gy is not None:
-        gy = _gather_sum(gy, group)
-    return G, gx, gy
+    _allreduce_acc(acc_x, group)
+    if acc_y is not None:
+        _allreduce_acc(acc_y, group)
+    return G, acc_x.finalize(), (None if acc_y is None else acc_y.finalize())

@@ -173,11 +173,52 @@ def backward_batch(x, y, lam1, lam2, kind, sigma, cot, want_values=False):
     return vals, gx, gy
 
 
-def backward_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, grad_x=None, grad_y=None):
-    """Accumulate dF/dx (and dF/dy) of F = sum cot[a, b] G[a, b] into grad buffers.
+class GradAcc:
+    """Exact (order-independent) accumulator of a Gram gradient for n paths of
+    shape (L, d): int64 fixed-point limbs (include/sigkernel.h, sk_grad_acc_*).
 
-    cot is the full (n1, n2) cotangent; rows restricts the solved X rows."""
-    lib = _lib.load()
+    Sums into it are bitwise independent of tile order, of how the Gram rows
+    are split across calls, and of how many GPUs contributed (gram_dist sums
+    the limbs of all ranks as integers).  `limbs` and `meta` are int64 views
+    for collectives: limbs add (SUM), meta combines with MAX."""
+
+    META = 8
+
+    def __init__(self, n, L, d, device):
+        lib = _lib.load()
+        self.shape = (int(n), int(L), int(d))
+        nbytes = lib.sk_grad_acc_bytes(n, L, d)
+        self.blob = torch.empty(nbytes // 8, dtype=torch.int64, device=device)
+        self.meta = self.blob[: self.META]
+        self.limbs = self.blob[self.META:]
+
+    def init(self, cot, n1, n2, symmetric):
+        """Zero the limbs and fix the anchor from the FULL (n1, n2) cotangent
+        (every call and rank sharing this gradient must pass the same one)."""
+        lib = _lib.load()
+        cot = _cotangent(cot, (n1, n2), self.blob)
+        with torch.cuda.device(self.blob.device):
+            _lib.check(lib.sk_grad_acc_init(_ptr(self.blob), *self.shape, _ptr(cot), n1, n2,
+                                            int(bool(symmetric)), _stream(self.blob.device)))
+        return self
+
+    def finalize(self, out=None, accumulate=False):
+        """fp64 gradient (n, L, d): out = value, or out += value."""
+        lib = _lib.load()
+        if out is None:
+            out = torch.empty(self.shape, dtype=torch.float64, device=self.blob.device)
+            accumulate = False
+        if (tuple(out.shape) != self.shape or out.dtype != torch.float64
+                or not out.is_contiguous()):
+            raise InvalidArgument(f"out must be a contiguous float64 tensor of shape {self.shape}")
+        _same_device(out, self.blob, "out")
+        with torch.cuda.device(self.blob.device):
+            _lib.check(lib.sk_grad_acc_finalize(_ptr(self.blob), *self.shape, _ptr(out),
+                                                int(bool(accumulate)), _stream(self.blob.device)))
+        return out
+
+
+def _gram_args(x, y):
     x = _paths(x, "x")
     sym = y is None
     yy = x if sym else _paths(y, "y")
@@ -186,8 +227,51 @@ def backward_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, grad_x=None, gr
     if yy.shape[2] != d:
         raise InvalidArgument(f"path dimensions differ: {d} vs {yy.shape[2]}")
     _same_device(yy, x, "y")
+    return x, yy, sym, n1, n2, L1, L2, d
+
+
+def _rows(rows, n1):
     r0, r1 = (0, n1) if rows is None else (int(rows[0]), int(rows[1]))
+    if r0 < 0 or r1 > n1 or r0 > r1:
+        raise InvalidArgument(f"row range {(r0, r1)} out of bounds for {n1} rows")
+    return r0, r1
+
+
+def _check_acc(acc, n, L, d, x, name):
+    if not isinstance(acc, GradAcc) or acc.shape != (n, L, d):
+        raise InvalidArgument(f"{name} must be a GradAcc of shape {(n, L, d)}")
+    _same_device(acc.blob, x, name)
+
+
+def backward_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, grad_x=None, grad_y=None,
+                  acc_x=None, acc_y=None):
+    """dF/dx (and dF/dy) of F = sum cot[a, b] G[a, b] over the pairs with a in
+    rows; cot is the full (n1, n2) cotangent.
+
+    Default: grad_x (grad_y) += this call's gradient (new zero buffers if None);
+    the sum inside the call is exact, so one call is bitwise reproducible.
+    With acc_x (acc_y) GradAcc accumulators, the call adds into them instead and
+    returns them (finalize() at the end): any split of the rows into calls then
+    gives bitwise the same gradient."""
+    lib = _lib.load()
+    x, yy, sym, n1, n2, L1, L2, d = _gram_args(x, y)
+    r0, r1 = _rows(rows, n1)
     cot = _cotangent(cot, (n1, n2), x)
+    if acc_x is not None:
+        _check_acc(acc_x, n1, L1, d, x, "acc_x")
+        if not sym:
+            _check_acc(acc_y, n2, L2, d, x, "acc_y")
+        if n1 == 0 or n2 == 0 or r1 <= r0:
+            return acc_x, acc_y
+        with torch.cuda.device(x.device):
+            nb = lib.sk_backward_gram_acc_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind,
+                                                          int(sym))
+            ws = _workspace(nb, x.device)
+            _lib.check(lib.sk_backward_gram_acc(
+                _ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d, lam1, lam2, kind, sigma,
+                r0, r1, _ptr(cot), None, _ptr(acc_x.blob), None if sym else _ptr(acc_y.blob),
+                _ptr(ws), ws.numel(), _stream(x.device)))
+        return acc_x, acc_y
     if grad_x is None:
         grad_x = torch.zeros_like(x)
     if grad_y is None and not sym:
@@ -208,23 +292,34 @@ def backward_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, grad_x=None, gr
 
 
 def value_and_grad_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, out=None, grad_x=None,
-                        grad_y=None):
+                        grad_y=None, acc_x=None, acc_y=None):
     """One fused pass: G rows [r0, r1) (as forward_gram) and dF/dx (dF/dy) of
-    F = sum cot[a, b] G[a, b] (accumulated as backward_gram), from the
-    backward's own forward solve (sk_value_and_grad_gram)."""
+    F = sum cot[a, b] G[a, b] (as backward_gram, including its accumulator
+    mode), from the backward's own forward solve (sk_value_and_grad_gram)."""
     lib = _lib.load()
-    x = _paths(x, "x")
-    sym = y is None
-    yy = x if sym else _paths(y, "y")
-    n1, L1, d = x.shape
-    n2, L2 = yy.shape[0], yy.shape[1]
-    if yy.shape[2] != d:
-        raise InvalidArgument(f"path dimensions differ: {d} vs {yy.shape[2]}")
-    _same_device(yy, x, "y")
-    r0, r1 = (0, n1) if rows is None else (int(rows[0]), int(rows[1]))
+    x, yy, sym, n1, n2, L1, L2, d = _gram_args(x, y)
+    r0, r1 = _rows(rows, n1)
     cot = _cotangent(cot, (n1, n2), x)
     if out is None:
         out = torch.empty((r1 - r0, n2), dtype=torch.float64, device=x.device)
+    if tuple(out.shape) != (r1 - r0, n2) or out.dtype != torch.float64 or not out.is_contiguous():
+        raise InvalidArgument(f"out must be a contiguous float64 ({r1 - r0}, {n2}) tensor")
+    _same_device(out, x, "out")
+    if acc_x is not None:
+        _check_acc(acc_x, n1, L1, d, x, "acc_x")
+        if not sym:
+            _check_acc(acc_y, n2, L2, d, x, "acc_y")
+        if n1 == 0 or n2 == 0 or r1 <= r0:
+            return out, acc_x, acc_y
+        with torch.cuda.device(x.device):
+            nb = lib.sk_backward_gram_acc_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind,
+                                                          int(sym))
+            ws = _workspace(nb, x.device)
+            _lib.check(lib.sk_backward_gram_acc(
+                _ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d, lam1, lam2, kind, sigma,
+                r0, r1, _ptr(cot), _ptr(out), _ptr(acc_x.blob),
+                None if sym else _ptr(acc_y.blob), _ptr(ws), ws.numel(), _stream(x.device)))
+        return out, acc_x, acc_y
     if grad_x is None:
         grad_x = torch.zeros_like(x)
     if grad_y is None and not sym:

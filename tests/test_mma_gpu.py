@@ -107,16 +107,22 @@ def test_gram_backward_mma(mods, n1, n2, L, d):
 
 
 def test_gram_backward_mma_row_blocks_sum(mods):
-    """Row blocks (the multi-GPU split, gram_dist.py) add up to the full gradient."""
+    """Row blocks (the multi-GPU split, gram_dist.py) add up to the full gradient:
+    bitwise through the exact accumulators for tile-aligned blocks (the ones
+    gram_dist makes), within rounding for arbitrary blocks summed in fp64."""
     ops, orc = mods
     rng = np.random.default_rng(11)
     X = random_paths(rng, 21, 37, 8)
     C = rng.standard_normal((21, 21))
     full, _ = ops.backward_gram(cu(X), None, 0, 0, 0, 1.0, cu(C))
-    acc = torch.zeros_like(full)
+    acc = ops.GradAcc(21, 37, 8, torch.device("cuda")).init(cu(C), 21, 21, True)
+    for r in ((0, 8), (8, 16), (16, 21)):
+        ops.backward_gram(cu(X), None, 0, 0, 0, 1.0, cu(C), rows=r, acc_x=acc)
+    np.testing.assert_array_equal(acc.finalize().cpu().numpy(), full.cpu().numpy())
+    g = torch.zeros_like(full)
     for r in ((0, 4), (4, 13), (13, 21)):
-        ops.backward_gram(cu(X), None, 0, 0, 0, 1.0, cu(C), rows=r, grad_x=acc)
-    assert rel_err(acc.cpu().numpy(), full.cpu().numpy()) < 1e-13
+        ops.backward_gram(cu(X), None, 0, 0, 0, 1.0, cu(C), rows=r, grad_x=g)
+    assert rel_err(g.cpu().numpy(), full.cpu().numpy()) < 1e-13
     assert rel_err(full.cpu().numpy(), orc.gram_backward(X, None, C, 0, 0)) < TOL
 
 
