@@ -139,8 +139,12 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   double* __restrict__ hrow = ba.hand + slot * ba.row_stride;
   double* __restrict__ arow = ba.adj + slot * ba.row_stride;
   double* __restrict__ dbuf = (MAP == DBUF) ? ba.dbuf + slot * ba.dbuf_stride : nullptr;
-  double* __restrict__ gxs = ba.gscr + slot * ba.gscr_stride;  // [M1c][DP]
-  double* __restrict__ gcs = gxs + (int64_t)pb.M1c * DP;       // [M2c][DP]
+  // LINEAR + DBUF serves d > 32 (several DP-chunks): the increment gradients
+  // are formed after the sweep from the stored coarse adjoint, all chunks
+  constexpr bool WIDE = (KIND == LINEAR) && (MAP == DBUF);
+  const int GW = WIDE ? pb.dpad : DP;  // row length of the increment-gradient scratch
+  double* __restrict__ gxs = ba.gscr + slot * ba.gscr_stride;  // [M1c][GW]
+  double* __restrict__ gcs = gxs + (int64_t)pb.M1c * GW;       // [M2c][GW]
 #define SK_ROWCK(strip, d, q, ln) rowck[(((int64_t)(strip) * NT + (d)) * SF + (q)) * 32 + (ln)]
 
   for (int64_t item = slot; item < pb.nitems; item += (int64_t)gridDim.x * nw) {
@@ -180,7 +184,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
     // coefficients of column col from its ring record (RBF carries K across columns)
     double Kl[RC + 1], Kr[RC + 1];
     int jcur = -1;
-    auto colcoef = [&](const RowRegs<KIND, DP, RC>& rr, int col, Coef (&cfo)[RC],
+    auto colcoef = [&](const RowRegs<KIND, DP, RC>& rr, int col, int i0, Coef (&cfo)[RC],
                        double (&po)[RC]) {
       const double* rec = SK_REC(col);
       const bool cv = (col >= 0) && (col < NC);
@@ -195,6 +199,21 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         }
 #pragma unroll
         for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy);
+        if (WIDE && pb.nch > 1 && cv) {  // d > 32: further chunks, as the forward
+          const int jc = (col * F) >> pb.lam2;
+          for (int ch = 1; ch < pb.nch; ++ch) {
+            double dyc[DP], xc[DP];
+            load_vec<DP>(dyc, cbase + (int64_t)jc * pb.dpad + ch * DP);
+#pragma unroll
+            for (int c = 0; c < RC; ++c) {
+              const int i = i0 + c;
+              if (i < pb.M1c) {
+                load_vec<DP>(xc, pb.R.p + pr * pb.R.path_stride + (int64_t)i * pb.dpad + ch * DP);
+                p[c] += dot<DP>(xc, dyc);
+              }
+            }
+          }
+        }
       } else {
         const int jc = (col * F) >> pb.lam2;
         if (cv && jc != jcur) {
@@ -286,7 +305,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             const int col = js * S + s;
             Coef cf[RC];
             double pv[RC];
-            colcoef(rr, col, cf, pv);
+            colcoef(rr, col, i0, cf, pv);
 #pragma unroll
             for (int c = 0; c < RC; ++c) pck_s[((tau * S + s) * RC + c) * 32] = pv[c];
 #pragma unroll
@@ -683,6 +702,60 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         double v = 0.0;
         if (p >= 1) v += gcs[(int64_t)(p - 1) * DP + k];
         if (p < pb.M2c) v -= gcs[(int64_t)p * DP + k];
+        grad_add(gC, fxC, eC + e, v, atomic);
+      }
+      __syncwarp();
+    } else if constexpr (WIDE) {
+      // d > 32: gx_i = sum_j D_ij dy_j, gy_j = sum_i D_ij dx_i (kernel_grad.py:53-54)
+      // from the stored coarse adjoint D (dbuf, carries the dyadic factor), one
+      // 32-wide chunk of components at a time, then telescoped as above
+      __syncwarp();
+      const double* D = dbuf;
+      const double* xp = pb.R.p + pr * pb.R.path_stride;  // rows carry the dyadic factor
+      const double unscale = 1.0 / pb.scale;               // exact (power of two)
+      for (int ch = 0; ch < pb.nch; ++ch) {
+        for (int i = u; i < pb.M1c; i += 32) {
+          double acc[DP];
+#pragma unroll
+          for (int k = 0; k < DP; ++k) acc[k] = 0.0;
+          for (int j = 0; j < pb.M2c; ++j) {
+            const double w = D[(int64_t)i * pb.M2c + j];
+            double yj[DP];
+            load_vec<DP>(yj, cbase + (int64_t)j * pb.dpad + ch * DP);
+#pragma unroll
+            for (int k = 0; k < DP; ++k) acc[k] = fma(w, yj[k], acc[k]);
+          }
+#pragma unroll
+          for (int k = 0; k < DP; ++k) gxs[(int64_t)i * GW + ch * DP + k] = acc[k];
+        }
+        for (int j = u; j < pb.M2c; j += 32) {
+          double acc[DP];
+#pragma unroll
+          for (int k = 0; k < DP; ++k) acc[k] = 0.0;
+          for (int i = 0; i < pb.M1c; ++i) {
+            const double w = D[(int64_t)i * pb.M2c + j];
+            double xi[DP];
+            load_vec<DP>(xi, xp + (int64_t)i * pb.dpad + ch * DP);
+#pragma unroll
+            for (int k = 0; k < DP; ++k) acc[k] = fma(w, xi[k], acc[k]);
+          }
+#pragma unroll
+          for (int k = 0; k < DP; ++k) gcs[(int64_t)j * GW + ch * DP + k] = acc[k] * unscale;
+        }
+      }
+      __syncwarp();
+      for (int64_t e = u; e < (int64_t)(pb.M1c + 1) * dR; e += 32) {
+        const int p = (int)(e / dR), k = (int)(e % dR);
+        double v = 0.0;
+        if (p >= 1) v += gxs[(int64_t)(p - 1) * GW + k];
+        if (p < pb.M1c) v -= gxs[(int64_t)p * GW + k];
+        grad_add(gR, fxR, eR + e, v, atomic);
+      }
+      for (int64_t e = u; e < (int64_t)(pb.M2c + 1) * dR; e += 32) {
+        const int p = (int)(e / dR), k = (int)(e % dR);
+        double v = 0.0;
+        if (p >= 1) v += gcs[(int64_t)(p - 1) * GW + k];
+        if (p < pb.M2c) v -= gcs[(int64_t)p * GW + k];
         grad_add(gC, fxC, eC + e, v, atomic);
       }
       __syncwarp();

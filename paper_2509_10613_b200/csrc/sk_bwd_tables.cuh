@@ -5,11 +5,13 @@
 
 namespace sk {
 
-template <int KIND, int DP, int R, int FR, int F>
+template <int KIND, int DP, int R, int FR, int F, bool WIDE = false>
 inline void sk_bwd_leaf(BwdFn& fn, int& smem_doubles) {
   constexpr int S = bwd_steps_cols(DP, F);
   constexpr int CB = bwd_block_steps(DP, R, F, S);
-  constexpr int MAP = (KIND == LINEAR) ? FUSED : DBUF;
+  // LINEAR maps the adjoint in the sweep (FUSED) unless d > 32 (WIDE: stored
+  // coarse adjoint, mapped chunk by chunk after the sweep)
+  constexpr int MAP = (KIND == LINEAR && !WIDE) ? FUSED : DBUF;
   fn = bwd_kernel<KIND, DP, R, FR, F, CB, MAP, S>;
   smem_doubles = BwdSmem<DP, R, R / FR, F, CB, S>::TOTAL;  // per warp
 }
@@ -46,6 +48,18 @@ inline BwdFn sk_bwd_select(const BwdShape& s, int& smem_doubles) {
       else sk_bwd_table<KIND, 16, 2>(s, fn, smem_doubles);
       break;
     case 32: sk_bwd_table<KIND, 32, 1>(s, fn, smem_doubles); break;
+    default: break;
+  }
+  return fn;
+}
+
+// d > 32 (linear kernel): DP = 32 chunks, one row per lane.
+inline BwdFn sk_bwd_select_wide(const BwdShape& s, int& smem_doubles) {
+  BwdFn fn = nullptr;
+  switch (s.F) {
+    case 1: sk_bwd_leaf<LINEAR, 32, 1, 1, 1, true>(fn, smem_doubles); break;
+    case 2: sk_bwd_leaf<LINEAR, 32, 1, 1, 2, true>(fn, smem_doubles); break;
+    case 4: sk_bwd_leaf<LINEAR, 32, 1, 1, 4, true>(fn, smem_doubles); break;
     default: break;
   }
   return fn;

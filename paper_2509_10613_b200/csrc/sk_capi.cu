@@ -678,12 +678,12 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   BwdShape s{};
   s.kind = kind;
   s.DP = pick_dp(d, nch);
-  if (nch > 1) return fail(SK_INVALID_ARGUMENT, "backward supports d <= 32");
+  const bool wide = nch > 1;  // d > 32: DP-chunks, adjoint mapped after the sweep
   // Gram tiles of the linear kernel at dyadic order 0: DMMA backward
   // (sk_mma_bwd.cuh).  SK_NO_MMA=1 keeps the r01 kernels.
   // (d <= 4 runs the DP = 8 instance on zero-padded increments: the padding
   // adds exact zeros to every FMA chain, so p is bitwise unchanged)
-  s.MMA = shared_cols && kind == LINEAR && lamR == 0 && lamC == 0 && s.DP <= 16 &&
+  s.MMA = shared_cols && kind == LINEAR && lamR == 0 && lamC == 0 && s.DP <= 16 && !wide &&
           !(std::getenv("SK_NO_MMA") && std::getenv("SK_NO_MMA")[0] == '1');
   if (s.MMA) {
     if (s.DP == 4) s.DP = 8;
@@ -719,7 +719,9 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   s.FR = std::min(1 << std::min(lamR, 3), s.R);
   s.F = std::min(1 << std::min(lamC, 2), 4);
   int smd = 0;
-  BwdFn fn = kind == LINEAR ? select_bwd_linear(s, smd) : select_bwd_rbf(s, smd);
+  BwdFn fn = kind == RBF ? select_bwd_rbf(s, smd)
+             : wide      ? select_bwd_wide(s, smd)
+                         : select_bwd_linear(s, smd);
   if (!fn) return fail(SK_INVALID_ARGUMENT, "no backward kernel instance for this shape");
   pl.shape = s;
   pl.fn = fn;
@@ -741,8 +743,8 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   pl.colck_stride = (int64_t)align_up((size_t)(nstrips * NB * s.R * 32), 32);
   pl.pck_stride = (int64_t)align_up((size_t)(nstrips * NT * Sc * (s.R / s.FR) * 32), 32);
   pl.row_stride = (int64_t)align_up((size_t)(M2 + 1), 32);
-  pl.dbuf_stride = kind == RBF ? (int64_t)align_up((size_t)(M1c * M2c), 32) : 0;
-  pl.gscr_stride = kind == LINEAR ? (int64_t)align_up((size_t)((M1c + M2c) * s.DP), 32) : 0;
+  pl.dbuf_stride = (kind == RBF || wide) ? (int64_t)align_up((size_t)(M1c * M2c), 32) : 0;
+  pl.gscr_stride = kind == LINEAR ? (int64_t)align_up((size_t)((M1c + M2c) * s.DP * nch), 32) : 0;
   cap_slots(pl.blocks, pl.slots, warps,
             8.0 * (pl.rowck_stride + pl.colck_stride + pl.pck_stride + pl.dbuf_stride +
                    pl.gscr_stride + 2 * pl.row_stride));

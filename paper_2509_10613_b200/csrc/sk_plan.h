@@ -32,6 +32,7 @@ struct BwdShape {
 
 BwdFn select_bwd_linear(const BwdShape& s, int& smem_doubles);
 BwdFn select_bwd_rbf(const BwdShape& s, int& smem_doubles);
+BwdFn select_bwd_wide(const BwdShape& s, int& smem_doubles);  // linear, d > 32
 BwdFn select_bwd_mma(int DP, int WPC, int& smem_doubles_per_warp);
 
 // Per-kind instance tables (one translation unit each, compiled in parallel).

@@ -177,3 +177,44 @@ def test_autograd_loss_backward(sk, oracle):
     G = s.sig_kernel_gram(Xt, dyadic_order=0)
     (G * cu(C)).sum().backward()
     assert rel_err(Xt.grad.cpu().numpy(), oracle.gram_backward(X, None, C)) < TOL
+
+
+@pytest.mark.parametrize("B,L1,L2,d,l1,l2", [
+    (3, 20, 17, 33, 0, 0), (2, 40, 31, 64, 0, 0), (2, 25, 30, 50, 1, 2), (2, 12, 70, 100, 2, 0)])
+def test_wide_paths_vs_oracle(sk, oracle, B, L1, L2, d, l1, l2):
+    """d > 32: DP-chunked dot products, coarse adjoint mapped chunk by chunk
+    after the sweep (the reference handles any d, kernel_grad.py:27-61)."""
+    _, ops = sk
+    rng = np.random.default_rng(d + L1)
+    x = make_paths(rng, B, L1, d)
+    y = make_paths(rng, B, L2, d)
+    cot = rng.standard_normal(B)
+    wv, wx, wy = oracle.kernel_batch_backward(x, y, l1, l2, cot)
+    v, gx, gy = bwd(ops, x, y, l1, l2, cot)
+    assert rel_err(v, wv) < TOL
+    assert rel_err(gx, wx) < TOL
+    assert rel_err(gy, wy) < TOL
+
+
+@pytest.mark.parametrize("n1,n2,L,d,lam", [(7, None, 21, 33, 0), (5, 6, 18, 64, 1), (9, None, 15, 40, 1)])
+def test_wide_gram_vs_oracle(sk, oracle, n1, n2, L, d, lam):
+    """Gram backward and the fused value + gradient at d > 32."""
+    s, ops = sk
+    rng = np.random.default_rng(n1 * d + L)
+    X = make_paths(rng, n1, L, d)
+    Y = None if n2 is None else make_paths(rng, n2, L + 2, d)
+    C = rng.standard_normal((n1, n1 if n2 is None else n2))
+    G, gx, gy = s.sig_kernel_gram_value_and_grad(cu(X), None if Y is None else cu(Y), cu(C),
+                                                 dyadic_order=lam)
+    assert rel_err(G.cpu().numpy(), oracle.kernel_gram(X, Y, lam, lam)) < TOL
+    want = oracle.gram_backward(X, Y, C, lam, lam)
+    if Y is None:
+        assert rel_err(gx.cpu().numpy(), want) < TOL
+    else:
+        assert rel_err(gx.cpu().numpy(), want[0]) < TOL
+        assert rel_err(gy.cpu().numpy(), want[1]) < TOL
+    # autograd through sig_kernel_gram
+    xt = cu(X).requires_grad_(True)
+    Gt = s.sig_kernel_gram(xt, None if Y is None else cu(Y), dyadic_order=lam)
+    (Gt * cu(C)).sum().backward()
+    assert rel_err(xt.grad.cpu().numpy(), want if Y is None else want[0]) < TOL

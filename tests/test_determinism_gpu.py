@@ -44,7 +44,7 @@ def _inputs(n1, n2, L, d, seed):
 @pytest.mark.parametrize("n1,n2,L,d,lam,kind", CASES)
 def test_run_to_run_bitwise(mods, n1, n2, L, d, lam, kind):
     ops, _, orc = mods
-    X, Y, C = _inputs(n1, n2, L, d, n1 + L)
+    X, Y, C = _inputs(n1, n2, L, d, n1 + abs(L))
     outs = []
     for _ in range(3):
         gx, gy = ops.backward_gram(cu(X), None if Y is None else cu(Y), lam, lam, kind, 0.8, cu(C))
@@ -67,7 +67,7 @@ def test_row_splits_and_gpu_counts_bitwise(mods, n1, n2, L, d, lam, kind):
     """Full Gram in one call == any tile-aligned split into calls == per-rank
     accumulators (gram_dist.row_blocks for 2, 4 and 8 'GPUs') summed as integers."""
     ops, gram_dist, _ = mods
-    X, Y, C = _inputs(n1, n2, L, d, 7 * n1 + L)
+    X, Y, C = _inputs(n1, n2, L, d, 7 * n1 + abs(L))
     L = abs(L)
     x, y, c = cu(X), (None if Y is None else cu(Y)), cu(C)
     sym = Y is None
