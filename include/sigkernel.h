@@ -95,6 +95,26 @@ int sk_forward_gram(const double *x, const double *y, int64_t n1, int64_t n2, in
                     double sigma, int64_t row_begin, int64_t row_end, double *out,
                     void *workspace, size_t workspace_bytes, void *stream);
 
+/* FP32 arithmetic (linear static kernel): float32 paths in, float32 values out.
+ * Same wavefront as the fp64 kernels with the cell in small-correction form
+ * k = (u - k_diag) + (u (p/2 + q) + k_diag q), u = k_up + k_left, q = p^2/12
+ * (fp32 rounding of A = 1 + p/2 + ... would swallow small p).  Accuracy vs
+ * the fp64 reference: ~1e-5..6e-5 relative up to ~1000 fine cells per axis,
+ * growing ~linearly with the axis length (BASELINE config 4: ~1e-3); the
+ * reference's own float32 path keeps fp64 arithmetic (kernel.py:36-38), which
+ * the fp64 entry points reproduce.  Symmetric Gram: y == NULL. */
+size_t sk_forward_batch_f32_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d,
+                                            int lam1, int lam2);
+int sk_forward_batch_f32(const float *x, const float *y, int64_t B, int64_t L1, int64_t L2,
+                         int64_t d, int lam1, int lam2, float *out, void *workspace,
+                         size_t workspace_bytes, void *stream);
+size_t sk_forward_gram_f32_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                           int64_t d, int lam1, int lam2, int symmetric);
+int sk_forward_gram_f32(const float *x, const float *y, int64_t n1, int64_t n2, int64_t L1,
+                        int64_t L2, int64_t d, int lam1, int lam2, int64_t row_begin,
+                        int64_t row_end, float *out, void *workspace, size_t workspace_bytes,
+                        void *stream);
+
 size_t sk_solve_delta_workspace_bytes(int64_t B, int64_t r1, int64_t r2, int lam1, int lam2);
 /* out[b] = solve_goursat(delta_b) for delta (B, r1, r2) */
 int sk_solve_delta(const double *delta, int64_t B, int64_t r1, int64_t r2, int lam1,

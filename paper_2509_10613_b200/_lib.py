@@ -46,6 +46,12 @@ SIGNATURES = {
                           _i64, _dp, _dp, _dp, _vp, _sz, _vp], _ci),
     "sk_value_and_grad_gram": ([_dp, _dp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd,
                                 _i64, _i64, _dp, _dp, _dp, _dp, _vp, _sz, _vp], _ci),
+    "sk_forward_batch_f32_workspace_bytes": ([_i64, _i64, _i64, _i64, _ci, _ci], _sz),
+    "sk_forward_batch_f32": ([_vp, _vp, _i64, _i64, _i64, _i64, _ci, _ci, _vp, _vp, _sz, _vp],
+                             _ci),
+    "sk_forward_gram_f32_workspace_bytes": ([_i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci], _sz),
+    "sk_forward_gram_f32": ([_vp, _vp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _i64, _i64, _vp,
+                            _vp, _sz, _vp], _ci),
     "sk_grad_acc_bytes": ([_i64, _i64, _i64], _sz),
     "sk_grad_acc_init": ([_vp, _i64, _i64, _i64, _dp, _i64, _i64, _ci, _vp], _ci),
     "sk_grad_acc_finalize": ([_vp, _i64, _i64, _i64, _dp, _ci, _vp], _ci),

@@ -104,6 +104,59 @@ class _SigKernelGramFn(torch.autograd.Function):
                 gy if ctx.needs_input_grad[1] else None, None, None, None, None)
 
 
+class _SigKernelF32Fn(torch.autograd.Function):
+    """FP32-arithmetic forward; the backward is the exact fp64 one (as the
+    reference's kernel_backward forces float64, kernel_grad.py:20)."""
+
+    @staticmethod
+    def forward(ctx, x, y, l1, l2):
+        ctx.save_for_backward(x, y)
+        ctx.cfg = (l1, l2)
+        return ops.forward_batch_f32(x, y, l1, l2)
+
+    @staticmethod
+    def backward(ctx, cot):
+        x, y = ctx.saved_tensors
+        l1, l2 = ctx.cfg
+        _, gx, gy = ops.backward_batch(x.double(), y.double(), l1, l2, 0, 1.0, cot.double())
+        return (gx.to(x.dtype) if ctx.needs_input_grad[0] else None,
+                gy.to(y.dtype) if ctx.needs_input_grad[1] else None, None, None)
+
+
+class _SigKernelGramF32Fn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, y, l1, l2):
+        ctx.sym = y is None
+        ctx.cfg = (l1, l2)
+        ctx.save_for_backward(x) if ctx.sym else ctx.save_for_backward(x, y)
+        return ops.forward_gram_f32(x, y, l1, l2)
+
+    @staticmethod
+    def backward(ctx, cot):
+        l1, l2 = ctx.cfg
+        if ctx.sym:
+            (x,) = ctx.saved_tensors
+            gx, _ = ops.backward_gram(x.double(), None, l1, l2, 0, 1.0, cot.double())
+            return gx.to(x.dtype), None, None, None
+        x, y = ctx.saved_tensors
+        gx, gy = ops.backward_gram(x.double(), y.double(), l1, l2, 0, 1.0, cot.double())
+        return (gx.to(x.dtype) if ctx.needs_input_grad[0] else None,
+                gy.to(y.dtype) if ctx.needs_input_grad[1] else None, None, None)
+
+
+PRECISIONS = ("fp64", "fp32")
+
+
+def _precision(precision, kind):
+    if precision not in PRECISIONS:
+        raise InvalidArgument(f"precision must be one of {PRECISIONS}, got {precision!r}")
+    if precision == "fp32" and kind != 0:
+        # the RBF second difference K11 - K10 - K01 + K00 cancels catastrophically
+        # in fp32 (increments ~1e-4 of K): fp32 arithmetic is linear-only
+        raise InvalidArgument("precision='fp32' supports the linear static kernel only")
+    return precision == "fp32"
+
+
 def _prep(t, name):
     if not t.is_cuda:
         raise InvalidArgument(f"{name} must be a CUDA tensor (no CPU fallback)")
@@ -141,32 +194,48 @@ def path_transform(x: torch.Tensor, kind):
     raise InvalidArgument(f"unknown transform {kind!r}, expected one of {TRANSFORMS}")
 
 
-def sig_kernel(x, y, dyadic_order=0, static_kernel=None, transform=None):
+def sig_kernel(x, y, dyadic_order=0, static_kernel=None, transform=None, precision="fp64"):
     """k(x_b, y_b) for aligned batches (B, L1, d), (B, L2, d) -> (B,).
 
     A pair of (L, d) paths returns a 0-d tensor.  `transform` ("time_augment" or
-    "lead_lag") is applied to both paths first (pySigLib's path transforms)."""
+    "lead_lag") is applied to both paths first (pySigLib's path transforms).
+    precision: "fp64" (default; the reference's arithmetic -- float32 inputs are
+    solved in float64, kernel.py:36-38) or "fp32" (FP32-arithmetic kernels,
+    linear static kernel, float32 result; within ~1e-4 of fp64 up to a few
+    thousand fine cells per axis; gradients from the fp64
+    backward)."""
     x, sq = _batched(_prep(x, "x"), "x")
     y, _ = _batched(_prep(y, "y"), "y")
     x, y = path_transform(x, transform), path_transform(y, transform)
     l1, l2 = _orders(dyadic_order)
     kind, sigma = ops.static_kind(static_kernel)
+    if _precision(precision, kind):
+        k = _SigKernelF32Fn.apply(x.to(torch.float32), y.to(torch.float32), l1, l2)
+        return k[0] if sq else k
     out_dtype = torch.promote_types(x.dtype, y.dtype)
     k = _SigKernelFn.apply(x.to(torch.float64), y.to(torch.float64), l1, l2, kind, sigma)
     k = k.to(out_dtype)
     return k[0] if sq else k
 
 
-def sig_kernel_gram(x, y=None, dyadic_order=0, static_kernel=None, transform=None):
+def sig_kernel_gram(x, y=None, dyadic_order=0, static_kernel=None, transform=None,
+                    precision="fp64"):
     """Gram matrix G[a, b] = k(x_a, y_b) -> (n1, n2).
 
     y None (or y is x) -> symmetric: only a <= b is solved and the result is
-    mirrored, hence exactly symmetric (reference kernel.py:151-180)."""
+    mirrored, hence exactly symmetric (reference kernel.py:151-180).
+    precision: as sig_kernel."""
     sym = y is None or y is x
     x, _ = _batched(_prep(x, "x"), "x")
     x = path_transform(x, transform)
     l1, l2 = _orders(dyadic_order)
     kind, sigma = ops.static_kind(static_kernel)
+    if _precision(precision, kind):
+        if sym:
+            return _SigKernelGramF32Fn.apply(x.to(torch.float32), None, l1, l2)
+        y, _ = _batched(_prep(y, "y"), "y")
+        y = path_transform(y, transform)
+        return _SigKernelGramF32Fn.apply(x.to(torch.float32), y.to(torch.float32), l1, l2)
     if sym:
         G = _SigKernelGramFn.apply(x.to(torch.float64), None, l1, l2, kind, sigma)
         return G.to(x.dtype)

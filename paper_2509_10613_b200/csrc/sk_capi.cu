@@ -139,13 +139,16 @@ static void cap_slots(int64_t& blocks, int64_t& slots, int warps, double per_slo
 // Both sides of a call in ONE launch (rows side, then the columns side):
 // increments (kernel.py:74-75 np.diff, scaled, zero-padded to dpad) for the
 // linear kernel, padded nodes for RBF.
+template <typename T>
 struct PrepSide {
-  const double* x;
+  const T* x;
   int64_t n, L;
   double scale;
-  double* out;
+  T* out;
 };
-__global__ void prep_sides(PrepSide s0, PrepSide s1, int nsides, int rbf, int64_t d, int dpad) {
+template <typename T>
+__global__ void prep_sides(PrepSide<T> s0, PrepSide<T> s1, int nsides, int rbf, int64_t d,
+                           int dpad) {
   const int64_t rows0 = s0.n * (rbf ? s0.L : s0.L - 1);
   const int64_t rows1 = nsides > 1 ? s1.n * (rbf ? s1.L : s1.L - 1) : 0;
   const int64_t total = (rows0 + rows1) * dpad;
@@ -153,15 +156,15 @@ __global__ void prep_sides(PrepSide s0, PrepSide s1, int nsides, int rbf, int64_
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t rowg = e / dpad, k = e % dpad;
     const bool first = rowg < rows0;
-    const PrepSide& sd = first ? s0 : s1;
+    const PrepSide<T>& sd = first ? s0 : s1;
     const int64_t row = first ? rowg : rowg - rows0;
-    double v = 0.0;
+    T v = 0;
     if (k < d) {
       if (rbf) {
         v = sd.x[row * d + k];
       } else {
         const int64_t p = row / (sd.L - 1), i = row % (sd.L - 1);
-        v = (sd.x[(p * sd.L + i + 1) * d + k] - sd.x[(p * sd.L + i) * d + k]) * sd.scale;
+        v = (sd.x[(p * sd.L + i + 1) * d + k] - sd.x[(p * sd.L + i) * d + k]) * (T)sd.scale;
       }
     }
     sd.out[row * dpad + k] = v;
@@ -170,7 +173,8 @@ __global__ void prep_sides(PrepSide s0, PrepSide s1, int nsides, int rbf, int64_
 
 // Mirror the solved upper triangle into the lower one (kernel.py:177-179),
 // restricted to rows [r0, r1) (out holds those rows, leading dim ldo).
-__global__ void mirror_upper(double* __restrict__ out, int64_t ldo, int r0, int r1) {
+template <typename T = double>
+__global__ void mirror_upper(T* __restrict__ out, int64_t ldo, int r0, int r1) {
   int64_t span = r1 - r0;
   int64_t total = span * span;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -334,7 +338,7 @@ struct FwdPlan {
 // groups share the column path.
 static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, int64_t M1c,
                         int64_t M2c, int64_t npairs, bool gram, int mode, int n2, int r0,
-                        int r1) {
+                        int r1, bool f32 = false) {
   int nch = 1;
   FwdShape s{};
   s.kind = kind;
@@ -364,7 +368,7 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
   }
   // Gram tiles of the linear kernel at dyadic order 0: increment products on
   // the FP64 tensor cores (sk_mma_fwd.cuh).  SK_NO_MMA=1 keeps the r01 kernels.
-  s.MMA = gram && kind == LINEAR && lamR == 0 && lamC == 0 && nch == 1 && s.DP <= 16 &&
+  s.MMA = gram && !f32 && kind == LINEAR && lamR == 0 && lamC == 0 && nch == 1 && s.DP <= 16 &&
           !(std::getenv("SK_NO_MMA") && std::getenv("SK_NO_MMA")[0] == '1');
   if (s.MMA) {
     int per_warp = 0;
@@ -386,9 +390,10 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
     return SK_OK;
   }
   int smem = 0;
-  FwdFn fn = kind == LINEAR ? select_fwd_linear(s, smem)
-             : kind == RBF  ? select_fwd_rbf(s, smem)
-                            : select_fwd_delta(s, smem);
+  FwdFn fn = f32              ? (kind == LINEAR ? select_fwd_linear_f32(s, smem) : nullptr)
+             : kind == LINEAR ? select_fwd_linear(s, smem)
+             : kind == RBF    ? select_fwd_rbf(s, smem)
+                              : select_fwd_delta(s, smem);
   if (!fn) return fail(SK_INVALID_ARGUMENT, "no forward kernel instance for this shape");
   pl.shape = s;
   pl.fn = fn;
@@ -415,15 +420,16 @@ static size_t prep_elems(int kind, int64_t n, int64_t L, int dpad) {
 }
 
 // Prepares the rows side (scaled by `scale`) and, unless `share`, the columns
-// side, in one launch.
-static void launch_prep(int kind, const double* xr, int64_t nR, int64_t LR, const double* xc,
-                        int64_t nC, int64_t LC, bool share, int64_t d, int dpad, double* outR,
-                        double* outC, cudaStream_t st, double scale) {
+// side, in one launch (T: the arithmetic type of the kernels that read them).
+template <typename T>
+static void launch_prep(int kind, const T* xr, int64_t nR, int64_t LR, const T* xc, int64_t nC,
+                        int64_t LC, bool share, int64_t d, int dpad, T* outR, T* outC,
+                        cudaStream_t st, double scale) {
   const size_t total = prep_elems(kind, nR, LR, dpad) + (share ? 0 : prep_elems(kind, nC, LC, dpad));
   if (total == 0) return;
   const int blocks = (int)std::min<size_t>((total + 255) / 256, 4096);
-  PrepSide s0{xr, nR, LR, scale, outR}, s1{xc, nC, LC, 1.0, outC};
-  prep_sides<<<blocks, 256, 0, st>>>(s0, s1, share ? 1 : 2, kind == RBF ? 1 : 0, d, dpad);
+  PrepSide<T> s0{xr, nR, LR, scale, outR}, s1{xc, nC, LC, 1.0, outC};
+  prep_sides<T><<<blocks, 256, 0, st>>>(s0, s1, share ? 1 : 2, kind == RBF ? 1 : 0, d, dpad);
 }
 
 static int validate(int64_t L1, int64_t L2, int64_t d, int lam1, int lam2, int kind,
@@ -466,11 +472,11 @@ struct FwdLayout {
 };
 
 static FwdLayout fwd_layout(const FwdPlan& pl, int kind, int64_t nR, int64_t LR, int64_t nC,
-                            int64_t LC, int dpad, bool shared_paths) {
+                            int64_t LC, int dpad, bool shared_paths, size_t esz = sizeof(double)) {
   FwdLayout lo;
-  lo.prepR = align_up(prep_elems(kind, nR, LR, dpad) * sizeof(double), 256);
-  lo.prepC = shared_paths ? 0 : align_up(prep_elems(kind, nC, LC, dpad) * sizeof(double), 256);
-  lo.hand = align_up((size_t)pl.slots * pl.hand_stride * sizeof(double), 256);
+  lo.prepR = align_up(prep_elems(kind, nR, LR, dpad) * esz, 256);
+  lo.prepC = shared_paths ? 0 : align_up(prep_elems(kind, nC, LC, dpad) * esz, 256);
+  lo.hand = align_up((size_t)pl.slots * pl.hand_stride * esz, 256);
   lo.total = lo.prepR + lo.prepC + lo.hand;
   return lo;
 }
@@ -488,11 +494,16 @@ static Geometry orient(int64_t n1, int64_t n2, int64_t L1, int64_t L2, int lam1,
   return g;
 }
 
-static int forward_impl(const double* x, const double* y, int64_t n1, int64_t n2, int64_t L1,
+// f32: FP32 arithmetic kernels (linear static kernel): x, y, out are float
+// arrays; otherwise double.
+static int forward_impl(const void* x, const void* y, int64_t n1, int64_t n2, int64_t L1,
                         int64_t L2, int64_t d, int lam1, int lam2, int kind, double sigma,
-                        int mode, int64_t r0, int64_t r1, double* out, void* ws,
-                        size_t ws_bytes, cudaStream_t st, size_t* query) {
+                        int mode, int64_t r0, int64_t r1, void* out, void* ws,
+                        size_t ws_bytes, cudaStream_t st, size_t* query, bool f32 = false) {
   if (int rc = validate(L1, L2, d, lam1, lam2, kind, sigma)) return rc;
+  if (f32 && kind != LINEAR)
+    return fail(SK_INVALID_ARGUMENT, "FP32 arithmetic supports the linear static kernel only");
+  const size_t esz = f32 ? sizeof(float) : sizeof(double);
   const bool sym = mode == GRAM_SYM;
   Geometry g = orient(n1, n2, L1, L2, lam1, lam2);
   Problem pb = base_problem(kind, d, g.lamR, g.lamC, g.LR, g.LC, sigma);
@@ -507,14 +518,15 @@ static int forward_impl(const double* x, const double* y, int64_t n1, int64_t n2
   FwdPlan pl;
   const int64_t npairs = mode == BATCH ? n1 : (r1 - r0) * n2;
   if (int rc = plan_forward(pl, kind, d, g.lamR, g.lamC, pb.M1c, pb.M2c, npairs,
-                            mode != BATCH && !(mode == GRAM_CROSS && g.swap), mode, (int)n2, (int)r0, (int)r1))
+                            mode != BATCH && !(mode == GRAM_CROSS && g.swap), mode, (int)n2,
+                            (int)r0, (int)r1, f32))
     return rc;
   // LINEAR: the exact dyadic factor 2^-(lamR+lamC) is folded into the row
   // increments, so the kernel forms p without a multiply; a symmetric Gram then
   // needs a separate (unscaled) column copy when the factor is not 1.
   const bool fold = kind == LINEAR;
   const bool share = sym && !(fold && pb.scale != 1.0);
-  FwdLayout lo = fwd_layout(pl, kind, g.nR, g.LR, g.nC, g.LC, pb.dpad, share);
+  FwdLayout lo = fwd_layout(pl, kind, g.nR, g.LR, g.nC, g.LC, pb.dpad, share, esz);
   if (query) {
     *query = lo.total;
     return SK_OK;
@@ -524,28 +536,35 @@ static int forward_impl(const double* x, const double* y, int64_t n1, int64_t n2
     return fail(SK_INVALID_ARGUMENT, "workspace too small: need " + std::to_string(lo.total) +
                                          " bytes, got " + std::to_string(ws_bytes));
   char* base = static_cast<char*>(ws);
-  double* prepR = reinterpret_cast<double*>(base);
-  double* prepC = share ? prepR : reinterpret_cast<double*>(base + lo.prepR);
+  char* prepR = base;
+  char* prepC = share ? prepR : base + lo.prepR;
   double* hand = reinterpret_cast<double*>(base + lo.prepR + lo.prepC);
-  const double* xr = g.swap ? y : x;
-  const double* xc = g.swap ? x : y;
-  launch_prep(kind, xr, g.nR, g.LR, xc, g.nC, g.LC, share, d, pb.dpad, prepR, prepC, st,
-              fold ? pb.scale : 1.0);
+  const void* xr = g.swap ? y : x;
+  const void* xc = g.swap ? x : y;
+  if (f32)
+    launch_prep<float>(kind, (const float*)xr, g.nR, g.LR, (const float*)xc, g.nC, g.LC, share, d,
+                       pb.dpad, (float*)prepR, (float*)prepC, st, fold ? pb.scale : 1.0);
+  else
+    launch_prep<double>(kind, (const double*)xr, g.nR, g.LR, (const double*)xc, g.nC, g.LC, share,
+                        d, pb.dpad, (double*)prepR, (double*)prepC, st, fold ? pb.scale : 1.0);
   if (fold) pb.pscale = 1.0;
-  pb.R.p = prepR;
+  pb.R.p = reinterpret_cast<const double*>(prepR);
   pb.R.rows = (int)(g.LR - 1);
   pb.R.path_stride = (kind == RBF ? g.LR : g.LR - 1) * pb.dpad;
-  pb.C.p = prepC;
+  pb.C.p = reinterpret_cast<const double*>(prepC);
   pb.C.rows = (int)(g.LC - 1);
   pb.C.path_stride = (kind == RBF ? g.LC : g.LC - 1) * pb.dpad;
   pb.nitems = pl.nitems;
-  pb.out = out;
+  pb.out = static_cast<double*>(out);
   pl.fn<<<(unsigned)pl.blocks, pl.threads, pl.smem_bytes, st>>>(pb, hand, pl.hand_stride);
   SK_CUDA(cudaGetLastError());
   if (sym) {
     int64_t span = r1 - r0;
     int blocks = (int)std::min<int64_t>((span * span + 255) / 256, 4096);
-    if (span > 1) mirror_upper<<<blocks, 256, 0, st>>>(out, n2, (int)r0, (int)r1);
+    if (span > 1) {
+      if (f32) mirror_upper<float><<<blocks, 256, 0, st>>>((float*)out, n2, (int)r0, (int)r1);
+      else mirror_upper<double><<<blocks, 256, 0, st>>>((double*)out, n2, (int)r0, (int)r1);
+    }
     SK_CUDA(cudaGetLastError());
   }
   return SK_OK;
@@ -600,6 +619,46 @@ int sk_forward_gram(const double* x, const double* y, int64_t n1, int64_t n2, in
   return forward_impl(x, sym ? x : y, n1, n2, L1, L2, d, lam1, lam2, static_kernel, sigma,
                       sym ? GRAM_SYM : GRAM_CROSS, row_begin, row_end, out, ws, ws_bytes,
                       (cudaStream_t)stream, nullptr);
+}
+
+size_t sk_forward_batch_f32_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d,
+                                            int lam1, int lam2) {
+  size_t q = 0;
+  if (forward_impl(nullptr, nullptr, B, B, L1, L2, d, lam1, lam2, LINEAR, 1.0, BATCH, 0, B,
+                   nullptr, nullptr, 0, nullptr, &q, true))
+    return 0;
+  return q;
+}
+
+int sk_forward_batch_f32(const float* x, const float* y, int64_t B, int64_t L1, int64_t L2,
+                         int64_t d, int lam1, int lam2, float* out, void* ws, size_t ws_bytes,
+                         void* stream) {
+  if (B < 0) return fail(SK_INVALID_ARGUMENT, "negative batch");
+  return forward_impl(x, y, B, B, L1, L2, d, lam1, lam2, LINEAR, 1.0, BATCH, 0, B, out, ws,
+                      ws_bytes, (cudaStream_t)stream, nullptr, true);
+}
+
+size_t sk_forward_gram_f32_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                           int64_t d, int lam1, int lam2, int symmetric) {
+  size_t q = 0;
+  if (forward_impl(nullptr, nullptr, n1, n2, L1, L2, d, lam1, lam2, LINEAR, 1.0,
+                   symmetric ? GRAM_SYM : GRAM_CROSS, 0, n1, nullptr, nullptr, 0, nullptr, &q,
+                   true))
+    return 0;
+  return q;
+}
+
+int sk_forward_gram_f32(const float* x, const float* y, int64_t n1, int64_t n2, int64_t L1,
+                        int64_t L2, int64_t d, int lam1, int lam2, int64_t row_begin,
+                        int64_t row_end, float* out, void* ws, size_t ws_bytes, void* stream) {
+  const bool sym = (y == nullptr);
+  if (sym && (n2 != n1 || L2 != L1))
+    return fail(SK_INVALID_ARGUMENT, "symmetric Gram needs n2 == n1 and L2 == L1");
+  if (row_begin < 0 || row_end > n1 || row_begin > row_end)
+    return fail(SK_INVALID_ARGUMENT, "row range out of bounds");
+  return forward_impl(x, sym ? x : y, n1, n2, L1, L2, d, lam1, lam2, LINEAR, 1.0,
+                      sym ? GRAM_SYM : GRAM_CROSS, row_begin, row_end, out, ws, ws_bytes,
+                      (cudaStream_t)stream, nullptr, true);
 }
 
 static int solve_delta_impl(const double* delta, int64_t B, int64_t r1, int64_t r2, int lam1,
@@ -861,8 +920,8 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   ba.rows_exclusive = (1 << g.lamR) <= pl.shape.R ? 1 : 0;
   const double* xr = g.swap ? y : x;
   const double* xc = g.swap ? x : y;
-  launch_prep(kind, xr, g.nR, g.LR, xc, g.nC, g.LC, share, d, pb.dpad, prepR, prepC, st,
-              fold ? pb.scale : 1.0);
+  launch_prep<double>(kind, xr, g.nR, g.LR, xc, g.nC, g.LC, share, d, pb.dpad, prepR, prepC, st,
+                      fold ? pb.scale : 1.0);
   if (fold) pb.pscale = 1.0;
   pb.R.p = prepR;
   pb.R.rows = (int)(g.LR - 1);
@@ -959,7 +1018,7 @@ int sk_value_and_grad_gram(const double* x, const double* y, int64_t n1, int64_t
   const int64_t span = row_end - row_begin;
   if (sym && span > 1) {
     int blocks = (int)std::min<int64_t>((span * span + 255) / 256, 4096);
-    mirror_upper<<<blocks, 256, 0, (cudaStream_t)stream>>>(values, n2, (int)row_begin,
+    mirror_upper<double><<<blocks, 256, 0, (cudaStream_t)stream>>>(values, n2, (int)row_begin,
                                                            (int)row_end);
     SK_CUDA(cudaGetLastError());
   }
@@ -1023,7 +1082,7 @@ int sk_backward_gram_acc(const double* x, const double* y, int64_t n1, int64_t n
   const int64_t span = row_end - row_begin;
   if (values && sym && span > 1) {
     int blocks = (int)std::min<int64_t>((span * span + 255) / 256, 4096);
-    mirror_upper<<<blocks, 256, 0, (cudaStream_t)stream>>>(values, n2, (int)row_begin,
+    mirror_upper<double><<<blocks, 256, 0, (cudaStream_t)stream>>>(values, n2, (int)row_begin,
                                                            (int)row_end);
     SK_CUDA(cudaGetLastError());
   }
@@ -1081,7 +1140,7 @@ extern "C" int sk_mirror_upper(double* g, int64_t n, int64_t ld, void* stream) {
   if (n < 0 || ld < n) return fail(SK_INVALID_ARGUMENT, "bad matrix shape");
   if (n < 2) return SK_OK;
   int blocks = (int)std::min<int64_t>((n * n + 255) / 256, 4096);
-  mirror_upper<<<blocks, 256, 0, (cudaStream_t)stream>>>(g, ld, 0, (int)n);
+  mirror_upper<double><<<blocks, 256, 0, (cudaStream_t)stream>>>(g, ld, 0, (int)n);
   SK_CUDA(cudaGetLastError());
   return SK_OK;
 }

@@ -29,11 +29,12 @@
 
 namespace sk {
 
-template <int KIND, int DP, int F, int P>
+template <int KIND, int DP, int F, int P, typename T = double>
 struct FwdRec {
-  static constexpr int CD = (KIND == DELTA) ? 0 : DP;  // column data doubles
+  static constexpr int VEC = 16 / (int)sizeof(T);      // elements per 16-byte copy
+  static constexpr int CD = (KIND == DELTA) ? 0 : DP;  // column data elements
   static constexpr int RAW = CD + P * F;               // + handoff values per group
-  static constexpr int REC = (RAW + 1) & ~1;           // 16-byte aligned records
+  static constexpr int REC = (RAW + VEC - 1) & ~(VEC - 1);  // 16-byte aligned records
 };
 
 template <bool XW, int G, int S>
@@ -48,20 +49,22 @@ struct FwdRing {
 // Issue the ring records of columns [col0, col0 + S): column data of coarse
 // column jc(col) and the handoff values of every group (strip > 0).  One warp
 // issues; a single commit group per step.
-template <int KIND, int DP, int F, int P, int S, int SLOTS>
-__device__ __forceinline__ void fwd_issue(double* ring, const Problem& pb, int64_t pc,
-                                          const double* hrow0, int64_t hand_stride, int col0,
+template <int KIND, int DP, int F, int P, int S, int SLOTS, typename T = double>
+__device__ __forceinline__ void fwd_issue(T* ring, const Problem& pb, int64_t pc,
+                                          const T* hrow0, int64_t hand_stride, int col0,
                                           int NC, int strip, int lane) {
-  using Rc = FwdRec<KIND, DP, F, P>;
-  constexpr int CH = Rc::CD / 2;  // 16-byte chunks of column data
+  using Rc = FwdRec<KIND, DP, F, P, T>;
+  constexpr int VEC = Rc::VEC;
+  constexpr int CH = Rc::CD / VEC;  // 16-byte chunks of column data
+  const T* cdata = reinterpret_cast<const T*>(pb.C.p);
   for (int e = lane; e < S * CH; e += 32) {
     const int s = e / CH, c = e % CH;
     const int col = col0 + s;
     const bool valid = (col >= 0) && (col < NC);
     const int jc = valid ? ((col * F) >> pb.lam2) : 0;
     const int node = (KIND == RBF) ? jc + 1 : jc;
-    const double* src = pb.C.p + pc * pb.C.path_stride + (int64_t)node * pb.dpad + 2 * c;
-    cp_async16(ring + ((col & (SLOTS - 1)) * Rc::REC) + 2 * c, src, valid);
+    const T* src = cdata + pc * pb.C.path_stride + (int64_t)node * pb.dpad + VEC * c;
+    cp_async16(ring + ((col & (SLOTS - 1)) * Rc::REC) + VEC * c, src, valid);
   }
   if (strip > 0) {
     for (int e = lane; e < S * P * F; e += 32) {
@@ -69,8 +72,8 @@ __device__ __forceinline__ void fwd_issue(double* ring, const Problem& pb, int64
       const int g = q / F, f = q % F;
       const int col = col0 + s;
       const bool valid = (col >= 0) && (col < NC);
-      const double* src = hrow0 + g * hand_stride + (valid ? col * F + f + 1 : 0);
-      cp_async8(ring + ((col & (SLOTS - 1)) * Rc::REC) + Rc::CD + q, src, valid);
+      const T* src = hrow0 + g * hand_stride + (valid ? col * F + f + 1 : 0);
+      cp_async_elem<T>(ring + ((col & (SLOTS - 1)) * Rc::REC) + Rc::CD + q, src, valid);
     }
   }
   cp_async_commit();
@@ -85,20 +88,27 @@ __device__ __forceinline__ void fwd_issue(double* ring, const Problem& pb, int64
 //   G     lanes per pair (4 or 32); ignored when XW (G = blockDim.x)
 //   XW    cross-warp lane groups (one pair per CTA)
 //   S     columns per step
+//   T     arithmetic type: double (the reference's fp64 arithmetic) or float
+//         (the fp32 kernels: LINEAR only, small-correction cell, path data,
+//         handoff rows and outputs are float arrays behind the same pointers)
 // Every group of a warp must share the column path (Gram tiles / one pair).
-template <int KIND, int DP, int R, int FR, int F, int G, bool XW, int S>
+template <int KIND, int DP, int R, int FR, int F, int G, bool XW, int S, typename T = double>
 __global__ void __launch_bounds__(XW ? 512 : 128)
-fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
+fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
   constexpr int RC = R / FR;
   constexpr int P = XW ? 1 : 32 / G;
   constexpr int SF = S * F;
-  using Rec = FwdRec<KIND, DP, F, P>;
+  using Rec = FwdRec<KIND, DP, F, P, T>;
   using Rg = FwdRing<XW, G, S>;
+  using Cf = CoefOf<T>;
   constexpr int REC = Rec::REC;
   constexpr int SLOTS = Rg::SLOTS;
   constexpr int PF = Rg::PF;
-  extern __shared__ double smem_fwd[];
-  __shared__ double xbuf[XW ? 2 : 1][XW ? 16 : 1][SF];
+  static_assert(sizeof(T) == 8 || KIND == LINEAR, "fp32 kernels: linear static kernel only");
+  extern __shared__ double smem_fwd_raw[];
+  T* smem_fwd = reinterpret_cast<T*>(smem_fwd_raw);
+  T* hand = reinterpret_cast<T*>(hand_);
+  __shared__ T xbuf[XW ? 2 : 1][XW ? 16 : 1][SF];
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -106,7 +116,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
   const int Grt = XW ? (int)blockDim.x : G;
   const int g = XW ? 0 : lane / G;
   const int u = XW ? (int)threadIdx.x : lane % G;
-  double* ring = XW ? smem_fwd : smem_fwd + (size_t)warp * SLOTS * REC;
+  T* ring = XW ? smem_fwd : smem_fwd + (size_t)warp * SLOTS * REC;
 
   const int M1 = pb.M1c << pb.lam1;
   const int M2 = pb.M2c << pb.lam2;
@@ -120,8 +130,8 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
   const int s_star = (NC - 1) % S;       // sub-step of the last column
 
   const int64_t slot0 = XW ? (int64_t)blockIdx.x : ((int64_t)blockIdx.x * nw + warp) * P;
-  const double* hrow0 = hand + slot0 * hand_stride;  // group g's row: + g * hand_stride
-  double* __restrict__ hrow = hand + (slot0 + g) * hand_stride;
+  const T* hrow0 = hand + slot0 * hand_stride;  // group g's row: + g * hand_stride
+  T* __restrict__ hrow = hand + (slot0 + g) * hand_stride;
   const bool issuer = !XW || warp == 0;
 
   const int64_t item0 = XW ? blockIdx.x : (int64_t)blockIdx.x * nw + warp;
@@ -137,16 +147,16 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
       resolve_pair(pb, item, P, 0, pr0, pc, oi0, pi0);
       if (!valid) pr = pr0;
     }
-    double outv = 0.0;
+    T outv = 0;
 
-    for (int t = u; t <= M2; t += Grt) hrow[t] = 1.0;
+    for (int t = u; t <= M2; t += Grt) hrow[t] = T(1);
     if (XW) __syncthreads(); else __syncwarp();
 
     for (int strip = 0; strip < nstrips; ++strip) {
       const int rbase = strip * H + u * R;  // 0-based fine row of the lane's first row
       const int i0 = rbase >> pb.lam1;
-      RowRegs<KIND, DP, RC> rr;
-      if constexpr (KIND != DELTA) load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
+      RowRegs<KIND, DP, RC, T> rr;
+      if constexpr (KIND != DELTA) load_rows<KIND, DP, RC, T>(rr, pb, pr, i0, 0);
       double Kl[RC + 1], Kr[RC + 1];  // RBF: K at node columns jc, jc+1
       int jcur = -1;
       if constexpr (KIND == RBF) {
@@ -159,35 +169,48 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
       }
       if (issuer) {
         for (int q = 0; q < PF; ++q)
-          fwd_issue<KIND, DP, F, P, S, SLOTS>(ring, pb, pc, hrow0, hand_stride, q * S, NC, strip,
-                                              lane);
+          fwd_issue<KIND, DP, F, P, S, SLOTS, T>(ring, pb, pc, hrow0, hand_stride, q * S, NC,
+                                                 strip, lane);
       }
 
       // coefficients of the S columns of step js (reads the ring; no recurrence)
-      auto col_coefs = [&](int col, Coef (&cfo)[RC]) {
+      auto col_coefs = [&](int col, Cf (&cfo)[RC]) {
         {
-          const double* rec = ring + (col & (SLOTS - 1)) * REC;
-          double p[RC];
+          const T* rec = ring + (col & (SLOTS - 1)) * REC;
+          T p[RC];
           if constexpr (KIND == LINEAR) {
-            double dy[DP];
+            T dy[DP];
+            if constexpr (sizeof(T) == 8) {
 #pragma unroll
-            for (int k = 0; k < DP; k += 2) {
-              const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
-              dy[k] = t2.x;
-              dy[k + 1] = t2.y;
+              for (int k = 0; k < DP; k += 2) {
+                const double2 t2 = *reinterpret_cast<const double2*>(rec + k);
+                dy[k] = t2.x;
+                dy[k + 1] = t2.y;
+              }
+            } else {
+#pragma unroll
+              for (int k = 0; k < DP; k += 4) {
+                const float4 t4 = *reinterpret_cast<const float4*>(rec + k);
+                dy[k] = t4.x;
+                dy[k + 1] = t4.y;
+                dy[k + 2] = t4.z;
+                dy[k + 3] = t4.w;
+              }
             }
 #pragma unroll
             for (int c = 0; c < RC; ++c) p[c] = dot<DP>(rr.v[c], dy);
             if (DP == 32 && pb.nch > 1 && col >= 0 && col < NC) {  // d > 32: further chunks
               const int jc = (col * F) >> pb.lam2;
+              const T* cdata = reinterpret_cast<const T*>(pb.C.p);
+              const T* rdata = reinterpret_cast<const T*>(pb.R.p);
               for (int ch = 1; ch < pb.nch; ++ch) {
-                double dyc[DP], xc[DP];
-                load_vec<DP>(dyc, pb.C.p + pc * pb.C.path_stride + (int64_t)jc * pb.dpad + ch * DP);
+                T dyc[DP], xc[DP];
+                load_vec<DP>(dyc, cdata + pc * pb.C.path_stride + (int64_t)jc * pb.dpad + ch * DP);
 #pragma unroll
                 for (int c = 0; c < RC; ++c) {
                   const int i = i0 + c;
                   if (i < pb.M1c) {
-                    load_vec<DP>(xc, pb.R.p + pr * pb.R.path_stride + (int64_t)i * pb.dpad + ch * DP);
+                    load_vec<DP>(xc, rdata + pr * pb.R.path_stride + (int64_t)i * pb.dpad + ch * DP);
                     p[c] += dot<DP>(xc, dyc);
                   }
                 }
@@ -195,7 +218,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
             }
             if (pb.pscale != 1.0) {
 #pragma unroll
-              for (int c = 0; c < RC; ++c) p[c] *= pb.pscale;
+              for (int c = 0; c < RC; ++c) p[c] *= (T)pb.pscale;
             }
           } else if constexpr (KIND == RBF) {
             const int jc = (col * F) >> pb.lam2;
@@ -231,22 +254,22 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
           for (int c = 0; c < RC; ++c) cfo[c] = coef(p[c]);
         }
       };
-      auto step_coefs = [&](int js, Coef (&cfo)[S][RC]) {
+      auto step_coefs = [&](int js, Cf (&cfo)[S][RC]) {
 #pragma unroll
         for (int s = 0; s < S; ++s) col_coefs(js * S + s, cfo[s]);
       };
 
-      double kl[R];
+      T kl[R];
 #pragma unroll
-      for (int r = 0; r < R; ++r) kl[r] = 1.0;
-      double topc = 1.0;
-      double bot[SF];
+      for (int r = 0; r < R; ++r) kl[r] = T(1);
+      T topc = T(1);
+      T bot[SF];
 #pragma unroll
-      for (int q = 0; q < SF; ++q) bot[q] = 1.0;
+      for (int q = 0; q < SF; ++q) bot[q] = T(1);
       // wide paths (DP >= 16) pipeline the next step's coefficients behind the
       // recurrence; narrow ones keep the registers for S columns per step
       constexpr bool PIPE = DP >= 16;
-      Coef cf[S][RC];
+      Cf cf[S][RC];
       if constexpr (PIPE) {
         if (issuer) cp_async_wait<PF - 1>();  // step 0 landed
         if (XW) __syncthreads(); else __syncwarp();
@@ -256,8 +279,8 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
       const int nsteps = NSTEP + Grt - 1;
       for (int tau = 0; tau < nsteps; ++tau) {
         if (issuer) {
-          fwd_issue<KIND, DP, F, P, S, SLOTS>(ring, pb, pc, hrow0, hand_stride, (tau + PF) * S, NC,
-                                              strip, lane);
+          fwd_issue<KIND, DP, F, P, S, SLOTS, T>(ring, pb, pc, hrow0, hand_stride, (tau + PF) * S,
+                                                 NC, strip, lane);
           if constexpr (PIPE) cp_async_wait<PF - 1>();  // steps <= tau + 1 landed
           else cp_async_wait<PF>();                     // step tau landed
         }
@@ -265,10 +288,10 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
         const int js = tau - u;
         const bool active = (js >= 0) && (js < NSTEP);
         // software pipeline: next step's coefficients overlap this step's recurrence
-        Coef cfn[PIPE ? S : 1][RC];
+        Cf cfn[PIPE ? S : 1][RC];
         if constexpr (PIPE) step_coefs(js + 1, cfn);
 
-        double tv[SF];
+        T tv[SF];
         if constexpr (XW) {
 #pragma unroll
           for (int q = 0; q < SF; ++q) tv[q] = __shfl_up_sync(0xffffffffu, bot[q], 1);
@@ -285,9 +308,9 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
           if (u == 0) {
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-              const double* rec = ring + ((col0 + s) & (SLOTS - 1)) * REC + Rec::CD + g * F;
+              const T* rec = ring + ((col0 + s) & (SLOTS - 1)) * REC + Rec::CD + g * F;
 #pragma unroll
-              for (int f = 0; f < F; ++f) tv[s * F + f] = (strip == 0) ? 1.0 : rec[f];
+              for (int f = 0; f < F; ++f) tv[s * F + f] = (strip == 0) ? T(1) : rec[f];
             }
           }
 #pragma unroll
@@ -297,11 +320,11 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
 #pragma unroll
             for (int f = 0; f < F; ++f) {
               const int q = s * F + f;
-              double up = tv[q];
-              double dg = (q == 0) ? topc : tv[q - 1];
+              T up = tv[q];
+              T dg = (q == 0) ? topc : tv[q - 1];
 #pragma unroll
               for (int r = 0; r < R; ++r) {
-                const double nk = cell(up, kl[r], dg, cf[s][r / FR]);
+                const T nk = cell(up, kl[r], dg, cf[s][r / FR]);
                 dg = kl[r];
                 kl[r] = nk;
                 up = nk;
@@ -341,15 +364,15 @@ fwd_kernel(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
       if (issuer) cp_async_wait<0>();
       if (XW) __syncthreads(); else __syncwarp();
     }
-    if (u == u_star && valid) pb.out[oidx] = outv;
+    if (u == u_star && valid) reinterpret_cast<T*>(pb.out)[oidx] = outv;
   }
 }
 
 // Dynamic shared memory of one fwd_kernel CTA (bytes).
-template <int KIND, int DP, int F, int G, bool XW, int S>
+template <int KIND, int DP, int F, int G, bool XW, int S, typename T = double>
 constexpr int fwd_smem_bytes(int warps) {
-  using Rec = FwdRec<KIND, DP, F, XW ? 1 : 32 / G>;
-  return (XW ? 1 : warps) * FwdRing<XW, G, S>::SLOTS * Rec::REC * (int)sizeof(double);
+  using Rec = FwdRec<KIND, DP, F, XW ? 1 : 32 / G, T>;
+  return (XW ? 1 : warps) * FwdRing<XW, G, S>::SLOTS * Rec::REC * (int)sizeof(T);
 }
 
 }  // namespace sk

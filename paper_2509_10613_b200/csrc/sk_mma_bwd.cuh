@@ -387,7 +387,10 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         const double2 kleft = *reinterpret_cast<const double2*>(st + 9 * 32 + 2 * lane);
         double av[8];  // lane u = 3: adjoint messages of the strip below
 #pragma unroll
-        for (int i = 0; i < 8; ++i) av[i] = st[11 * 32 + g * 8 + i];
+        for (int i = 0; i < 8; ++i) {
+          av[i] = st[11 * 32 + g * 8 + i];
+          if (EDGE && 8 * blk - 3 + i < 0) av[i] = 0.0;  // left of column 0: never written
+        }
         // the staging records are lane-private: refill them for block blk-1
         if (blk > 0) stage_block(blk - 1);
 
@@ -451,9 +454,13 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           bR1 = c1.B * lam1;
           aR0 = c0.A * lam0;
           bR0 = c0.B * lam0;
+          // columns outside [0, NC) store exact zeros: their slots are read by
+          // the tile maps as dead columns later (x 0 dY), so no garbage (e.g.
+          // the never-written adjoint messages left of column 0) may reach them
+          const bool cdead = EDGE && (c < 0 || c >= NC);
           *reinterpret_cast<double2*>(sD + ((c >> 3) & 1) * Cf::DTILE + (c & 7) * DSTR +
                                       dsw(c, 2 * lane)) =
-              make_double2(D0, D1);
+              cdead ? make_double2(0.0, 0.0) : make_double2(D0, D1);
           if (u == 0 && (!EDGE || c >= 0)) arow[c + 3] = sendm;
         }
         __syncwarp();  // tile blk's D complete, p tile blk dead

@@ -120,6 +120,60 @@ def forward_gram(x, y, lam1: int, lam2: int, kind: int, sigma: float,
     return out
 
 
+def _paths32(t, name):
+    t = _paths(t, name) if t.dtype != torch.float32 else t
+    if t.dim() != 3 or t.shape[1] < 2:
+        raise InvalidArgument(f"{name} must be (B, L, d) with L >= 2")
+    if not t.is_cuda:
+        raise InvalidArgument(f"{name} must live on a CUDA device")
+    return t.to(torch.float32).contiguous()
+
+
+def forward_batch_f32(x, y, lam1: int, lam2: int) -> torch.Tensor:
+    """FP32-arithmetic forward (linear static kernel): float32 in, float32 out.
+    The cell uses the small-correction form (sk_cell.cuh Coef32)."""
+    lib = _lib.load()
+    x = _paths32(x, "x")
+    y = _paths32(y, "y")
+    B, L1, d = x.shape
+    if y.shape[0] != B or y.shape[2] != d:
+        raise InvalidArgument(f"shapes differ: {tuple(x.shape)} vs {tuple(y.shape)}")
+    _same_device(y, x, "y")
+    out = torch.empty(B, dtype=torch.float32, device=x.device)
+    if B == 0:
+        return out
+    with torch.cuda.device(x.device):
+        nb = lib.sk_forward_batch_f32_workspace_bytes(B, L1, y.shape[1], d, lam1, lam2)
+        ws = _workspace(nb, x.device)
+        _lib.check(lib.sk_forward_batch_f32(_ptr(x), _ptr(y), B, L1, y.shape[1], d, lam1, lam2,
+                                            _ptr(out), _ptr(ws), ws.numel(), _stream(x.device)))
+    return out
+
+
+def forward_gram_f32(x, y, lam1: int, lam2: int, rows=None) -> torch.Tensor:
+    """FP32-arithmetic Gram forward (linear static kernel); y None = symmetric."""
+    lib = _lib.load()
+    x = _paths32(x, "x")
+    sym = y is None
+    yy = x if sym else _paths32(y, "y")
+    n1, L1, d = x.shape
+    n2, L2 = yy.shape[0], yy.shape[1]
+    if yy.shape[2] != d:
+        raise InvalidArgument(f"path dimensions differ: {d} vs {yy.shape[2]}")
+    _same_device(yy, x, "y")
+    r0, r1 = _rows(rows, n1)
+    out = torch.empty((r1 - r0, n2), dtype=torch.float32, device=x.device)
+    if n1 == 0 or n2 == 0 or r1 <= r0:
+        return out
+    with torch.cuda.device(x.device):
+        nb = lib.sk_forward_gram_f32_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, int(sym))
+        ws = _workspace(nb, x.device)
+        _lib.check(lib.sk_forward_gram_f32(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
+                                           lam1, lam2, r0, r1, _ptr(out), _ptr(ws), ws.numel(),
+                                           _stream(x.device)))
+    return out
+
+
 def solve_delta(delta: torch.Tensor, lam1: int, lam2: int) -> torch.Tensor:
     """Kernel values for given increment matrices delta (B, r1, r2)."""
     lib = _lib.load()

@@ -79,7 +79,9 @@ def test_row_splits_and_gpu_counts_bitwise(mods, n1, n2, L, d, lam, kind):
         return ax, ay
 
     full_x, full_y = ops.backward_gram(x, y, lam, lam, kind, 0.8, c)
-    for split in ([(0, n1)], [(0, 8), (8, n1)], [(0, 8), (8, 16), (16, n1)]):
+    for cuts in ([], [8], [8, 16]):
+        bounds = [0] + [c for c in cuts if c < n1] + [n1]
+        split = list(zip(bounds[:-1], bounds[1:]))
         ax, ay = accs()
         for rg in split:
             ops.backward_gram(x, y, lam, lam, kind, 0.8, c, rows=rg, acc_x=ax, acc_y=ay)
