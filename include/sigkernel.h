@@ -104,16 +104,17 @@ int sk_forward_gram(const double *x, const double *y, int64_t n1, int64_t n2, in
  * reference's own float32 path keeps fp64 arithmetic (kernel.py:36-38), which
  * the fp64 entry points reproduce.  Symmetric Gram: y == NULL. */
 size_t sk_forward_batch_f32_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d,
-                                            int lam1, int lam2);
+                                            int lam1, int lam2, int transform);
 int sk_forward_batch_f32(const float *x, const float *y, int64_t B, int64_t L1, int64_t L2,
-                         int64_t d, int lam1, int lam2, float *out, void *workspace,
-                         size_t workspace_bytes, void *stream);
+                         int64_t d, int lam1, int lam2, int transform, float *out,
+                         void *workspace, size_t workspace_bytes, void *stream);
 size_t sk_forward_gram_f32_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
-                                           int64_t d, int lam1, int lam2, int symmetric);
+                                           int64_t d, int lam1, int lam2, int symmetric,
+                                           int transform);
 int sk_forward_gram_f32(const float *x, const float *y, int64_t n1, int64_t n2, int64_t L1,
-                        int64_t L2, int64_t d, int lam1, int lam2, int64_t row_begin,
-                        int64_t row_end, float *out, void *workspace, size_t workspace_bytes,
-                        void *stream);
+                        int64_t L2, int64_t d, int lam1, int lam2, int transform,
+                        int64_t row_begin, int64_t row_end, float *out, void *workspace,
+                        size_t workspace_bytes, void *stream);
 
 size_t sk_solve_delta_workspace_bytes(int64_t B, int64_t r1, int64_t r2, int lam1, int lam2);
 /* out[b] = solve_goursat(delta_b) for delta (B, r1, r2) */
@@ -174,6 +175,51 @@ int sk_value_and_grad_gram(const double *x, const double *y, int64_t n1, int64_t
                            const double *cot, double *values, double *grad_x, double *grad_y,
                            void *workspace, size_t workspace_bytes, void *stream);
 
+/* ---- path transforms inside the call ------------------------------------
+ * pySigLib's path transforms (reference transforms.py:37-120) applied to both
+ * path sets by the kernels' input preparation: the solver reads the
+ * transformed increments (linear kernel; the reference's fused_increments,
+ * transforms.py:91-120) or transformed nodes (RBF) built straight from the
+ * raw points, and the backward maps the transformed-path gradients back with
+ * the transform's adjoint (transforms.py:69-90).  x, y, grad_x, grad_y keep
+ * the RAW shapes (n, L, d); transform == SK_TRANSFORM_NONE is the plain call.
+ *   time augmentation: (L, d) -> (L, d+1), time grid numpy.linspace(0, 1, L)
+ *   lead-lag:          (L, d) -> (2L-1, 2d), Z[2k] = (X[k], X[k]),
+ *                      Z[2k+1] = (X[k+1], X[k]) */
+enum { SK_TRANSFORM_NONE = 0, SK_TRANSFORM_TIME_AUGMENT = 1, SK_TRANSFORM_LEAD_LAG = 2 };
+
+size_t sk_forward_batch_tf_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d,
+                                           int lam1, int lam2, int static_kernel, int transform);
+int sk_forward_batch_tf(const double *x, const double *y, int64_t B, int64_t L1, int64_t L2,
+                        int64_t d, int lam1, int lam2, int static_kernel, double sigma,
+                        int transform, double *out, void *workspace, size_t workspace_bytes,
+                        void *stream);
+size_t sk_forward_gram_tf_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                          int64_t d, int lam1, int lam2, int static_kernel,
+                                          int symmetric, int transform);
+int sk_forward_gram_tf(const double *x, const double *y, int64_t n1, int64_t n2, int64_t L1,
+                       int64_t L2, int64_t d, int lam1, int lam2, int static_kernel, double sigma,
+                       int transform, int64_t row_begin, int64_t row_end, double *out,
+                       void *workspace, size_t workspace_bytes, void *stream);
+size_t sk_backward_batch_tf_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d,
+                                            int lam1, int lam2, int static_kernel, int transform);
+int sk_backward_batch_tf(const double *x, const double *y, int64_t B, int64_t L1, int64_t L2,
+                         int64_t d, int lam1, int lam2, int static_kernel, double sigma,
+                         int transform, const double *cot, double *values, double *grad_x,
+                         double *grad_y, void *workspace, size_t workspace_bytes, void *stream);
+size_t sk_backward_gram_tf_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                           int64_t d, int lam1, int lam2, int static_kernel,
+                                           int symmetric, int transform);
+/* sk_backward_gram (values == NULL) or sk_value_and_grad_gram (values != NULL) */
+int sk_backward_gram_tf(const double *x, const double *y, int64_t n1, int64_t n2, int64_t L1,
+                        int64_t L2, int64_t d, int lam1, int lam2, int static_kernel,
+                        double sigma, int transform, int64_t row_begin, int64_t row_end,
+                        const double *cot, double *values, double *grad_x, double *grad_y,
+                        void *workspace, size_t workspace_bytes, void *stream);
+/* gradient of the transformed paths g_t (n, L', d') -> raw (n, L, d): grad = or += */
+int sk_transform_adjoint(const double *g_t, int64_t n, int64_t L, int64_t d, int transform,
+                         double *grad, int accumulate, void *stream);
+
 /* ---- exact Gram-gradient accumulators ------------------------------------
  * A gradient of n paths (L, d) accumulated as fixed-point int64 limbs:
  * blob = [8 x int64 metadata][n*L*d x 4 x int64 limbs].  Contributions are
@@ -203,6 +249,17 @@ int sk_backward_gram_acc(const double *x, const double *y, int64_t n1, int64_t n
                          double sigma, int64_t row_begin, int64_t row_end, const double *cot,
                          double *values, void *acc_x, void *acc_y, void *workspace,
                          size_t workspace_bytes, void *stream);
+/* the same on transformed paths: the accumulators hold the TRANSFORMED-path
+ * gradient (sk_grad_acc_bytes(n, L', d')); map it back after finalising with
+ * sk_transform_adjoint */
+size_t sk_backward_gram_acc_tf_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                               int64_t d, int lam1, int lam2, int static_kernel,
+                                               int symmetric, int transform);
+int sk_backward_gram_acc_tf(const double *x, const double *y, int64_t n1, int64_t n2,
+                            int64_t L1, int64_t L2, int64_t d, int lam1, int lam2,
+                            int static_kernel, double sigma, int transform, int64_t row_begin,
+                            int64_t row_end, const double *cot, double *values, void *acc_x,
+                            void *acc_y, void *workspace, size_t workspace_bytes, void *stream);
 
 #ifdef __cplusplus
 }

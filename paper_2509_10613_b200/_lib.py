@@ -17,6 +17,7 @@ SO_PATH = os.environ.get("SK_LIBSIGKERNEL") or os.path.join(HERE, "_native", "li
 
 SK_OK, SK_INVALID_ARGUMENT, SK_INVALID_STATE, SK_CUDA_ERROR = 0, 1, 2, 3
 STATIC_LINEAR, STATIC_RBF = 0, 1
+TRANSFORMS = {None: 0, "none": 0, "time_augment": 1, "lead_lag": 2}
 
 # Every symbol include/sigkernel.h declares, with its ctypes signature.
 _vp, _dp, _i64, _ci, _cd, _sz = (ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64,
@@ -46,12 +47,32 @@ SIGNATURES = {
                           _i64, _dp, _dp, _dp, _vp, _sz, _vp], _ci),
     "sk_value_and_grad_gram": ([_dp, _dp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd,
                                 _i64, _i64, _dp, _dp, _dp, _dp, _vp, _sz, _vp], _ci),
-    "sk_forward_batch_f32_workspace_bytes": ([_i64, _i64, _i64, _i64, _ci, _ci], _sz),
-    "sk_forward_batch_f32": ([_vp, _vp, _i64, _i64, _i64, _i64, _ci, _ci, _vp, _vp, _sz, _vp],
-                             _ci),
-    "sk_forward_gram_f32_workspace_bytes": ([_i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci], _sz),
-    "sk_forward_gram_f32": ([_vp, _vp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _i64, _i64, _vp,
-                            _vp, _sz, _vp], _ci),
+    "sk_forward_batch_f32_workspace_bytes": ([_i64, _i64, _i64, _i64, _ci, _ci, _ci], _sz),
+    "sk_forward_batch_f32": ([_vp, _vp, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _vp, _vp, _sz,
+                              _vp], _ci),
+    "sk_forward_gram_f32_workspace_bytes": ([_i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _ci],
+                                            _sz),
+    "sk_forward_gram_f32": ([_vp, _vp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _i64, _i64,
+                             _vp, _vp, _sz, _vp], _ci),
+    "sk_forward_batch_tf_workspace_bytes": ([_i64, _i64, _i64, _i64, _ci, _ci, _ci, _ci], _sz),
+    "sk_forward_batch_tf": ([_dp, _dp, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd, _ci, _dp, _vp,
+                             _sz, _vp], _ci),
+    "sk_forward_gram_tf_workspace_bytes": ([_i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _ci,
+                                            _ci], _sz),
+    "sk_forward_gram_tf": ([_dp, _dp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd, _ci, _i64,
+                            _i64, _dp, _vp, _sz, _vp], _ci),
+    "sk_backward_batch_tf_workspace_bytes": ([_i64, _i64, _i64, _i64, _ci, _ci, _ci, _ci], _sz),
+    "sk_backward_batch_tf": ([_dp, _dp, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd, _ci, _dp, _dp,
+                              _dp, _dp, _vp, _sz, _vp], _ci),
+    "sk_backward_gram_tf_workspace_bytes": ([_i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _ci,
+                                             _ci], _sz),
+    "sk_backward_gram_tf": ([_dp, _dp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd, _ci,
+                             _i64, _i64, _dp, _dp, _dp, _dp, _vp, _sz, _vp], _ci),
+    "sk_transform_adjoint": ([_dp, _i64, _i64, _i64, _ci, _dp, _ci, _vp], _ci),
+    "sk_backward_gram_acc_tf_workspace_bytes": ([_i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci,
+                                                 _ci, _ci], _sz),
+    "sk_backward_gram_acc_tf": ([_dp, _dp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd, _ci,
+                                 _i64, _i64, _dp, _dp, _vp, _vp, _vp, _sz, _vp], _ci),
     "sk_grad_acc_bytes": ([_i64, _i64, _i64], _sz),
     "sk_grad_acc_init": ([_vp, _i64, _i64, _i64, _dp, _i64, _i64, _ci, _vp], _ci),
     "sk_grad_acc_finalize": ([_vp, _i64, _i64, _i64, _dp, _ci, _vp], _ci),

@@ -68,40 +68,40 @@ def _batched(t, name):
 
 class _SigKernelFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, y, l1, l2, kind, sigma):
+    def forward(ctx, x, y, l1, l2, kind, sigma, tf):
         ctx.save_for_backward(x, y)
-        ctx.cfg = (l1, l2, kind, sigma)
-        return ops.forward_batch(x, y, l1, l2, kind, sigma)
+        ctx.cfg = (l1, l2, kind, sigma, tf)
+        return ops.forward_batch(x, y, l1, l2, kind, sigma, tf)
 
     @staticmethod
     def backward(ctx, cot):
         x, y = ctx.saved_tensors
-        l1, l2, kind, sigma = ctx.cfg
-        _, gx, gy = ops.backward_batch(x, y, l1, l2, kind, sigma, cot)
+        l1, l2, kind, sigma, tf = ctx.cfg
+        _, gx, gy = ops.backward_batch(x, y, l1, l2, kind, sigma, cot, transform=tf)
         return (gx if ctx.needs_input_grad[0] else None,
-                gy if ctx.needs_input_grad[1] else None, None, None, None, None)
+                gy if ctx.needs_input_grad[1] else None, None, None, None, None, None)
 
 
 class _SigKernelGramFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, y, l1, l2, kind, sigma):
+    def forward(ctx, x, y, l1, l2, kind, sigma, tf):
         sym = y is None
         ctx.sym = sym
-        ctx.cfg = (l1, l2, kind, sigma)
+        ctx.cfg = (l1, l2, kind, sigma, tf)
         ctx.save_for_backward(x) if sym else ctx.save_for_backward(x, y)
-        return ops.forward_gram(x, y, l1, l2, kind, sigma)
+        return ops.forward_gram(x, y, l1, l2, kind, sigma, transform=tf)
 
     @staticmethod
     def backward(ctx, cot):
-        l1, l2, kind, sigma = ctx.cfg
+        l1, l2, kind, sigma, tf = ctx.cfg
         if ctx.sym:
             (x,) = ctx.saved_tensors
-            gx, _ = ops.backward_gram(x, None, l1, l2, kind, sigma, cot)
-            return gx, None, None, None, None, None
+            gx, _ = ops.backward_gram(x, None, l1, l2, kind, sigma, cot, transform=tf)
+            return gx, None, None, None, None, None, None
         x, y = ctx.saved_tensors
-        gx, gy = ops.backward_gram(x, y, l1, l2, kind, sigma, cot)
+        gx, gy = ops.backward_gram(x, y, l1, l2, kind, sigma, cot, transform=tf)
         return (gx if ctx.needs_input_grad[0] else None,
-                gy if ctx.needs_input_grad[1] else None, None, None, None, None)
+                gy if ctx.needs_input_grad[1] else None, None, None, None, None, None)
 
 
 class _SigKernelF32Fn(torch.autograd.Function):
@@ -109,39 +109,42 @@ class _SigKernelF32Fn(torch.autograd.Function):
     reference's kernel_backward forces float64, kernel_grad.py:20)."""
 
     @staticmethod
-    def forward(ctx, x, y, l1, l2):
+    def forward(ctx, x, y, l1, l2, tf):
         ctx.save_for_backward(x, y)
-        ctx.cfg = (l1, l2)
-        return ops.forward_batch_f32(x, y, l1, l2)
+        ctx.cfg = (l1, l2, tf)
+        return ops.forward_batch_f32(x, y, l1, l2, tf)
 
     @staticmethod
     def backward(ctx, cot):
         x, y = ctx.saved_tensors
-        l1, l2 = ctx.cfg
-        _, gx, gy = ops.backward_batch(x.double(), y.double(), l1, l2, 0, 1.0, cot.double())
+        l1, l2, tf = ctx.cfg
+        _, gx, gy = ops.backward_batch(x.double(), y.double(), l1, l2, 0, 1.0, cot.double(),
+                                       transform=tf)
         return (gx.to(x.dtype) if ctx.needs_input_grad[0] else None,
-                gy.to(y.dtype) if ctx.needs_input_grad[1] else None, None, None)
+                gy.to(y.dtype) if ctx.needs_input_grad[1] else None, None, None, None)
 
 
 class _SigKernelGramF32Fn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, x, y, l1, l2):
+    def forward(ctx, x, y, l1, l2, tf):
         ctx.sym = y is None
-        ctx.cfg = (l1, l2)
+        ctx.cfg = (l1, l2, tf)
         ctx.save_for_backward(x) if ctx.sym else ctx.save_for_backward(x, y)
-        return ops.forward_gram_f32(x, y, l1, l2)
+        return ops.forward_gram_f32(x, y, l1, l2, transform=tf)
 
     @staticmethod
     def backward(ctx, cot):
-        l1, l2 = ctx.cfg
+        l1, l2, tf = ctx.cfg
         if ctx.sym:
             (x,) = ctx.saved_tensors
-            gx, _ = ops.backward_gram(x.double(), None, l1, l2, 0, 1.0, cot.double())
-            return gx.to(x.dtype), None, None, None
+            gx, _ = ops.backward_gram(x.double(), None, l1, l2, 0, 1.0, cot.double(),
+                                      transform=tf)
+            return gx.to(x.dtype), None, None, None, None
         x, y = ctx.saved_tensors
-        gx, gy = ops.backward_gram(x.double(), y.double(), l1, l2, 0, 1.0, cot.double())
+        gx, gy = ops.backward_gram(x.double(), y.double(), l1, l2, 0, 1.0, cot.double(),
+                                   transform=tf)
         return (gx.to(x.dtype) if ctx.needs_input_grad[0] else None,
-                gy.to(y.dtype) if ctx.needs_input_grad[1] else None, None, None)
+                gy.to(y.dtype) if ctx.needs_input_grad[1] else None, None, None, None)
 
 
 PRECISIONS = ("fp64", "fp32")
@@ -169,12 +172,15 @@ TRANSFORMS = (None, "time_augment", "lead_lag")
 
 
 def path_transform(x: torch.Tensor, kind):
-    """Time augmentation / lead-lag of a (B, L, d) batch (reference transforms.py:37-66).
+    """Materialised time augmentation / lead-lag of a (B, L, d) batch (reference
+    transforms.py:37-66), for users who want the transformed points.
 
     time_augment: (B, L, d) -> (B, L, d+1), last coordinate the uniform time grid
     on [0, 1]; lead_lag: (B, L, d) -> (B, 2L-1, 2d) with Z[2k] = (X[k], X[k]),
-    Z[2k+1] = (X[k+1], X[k]).  Linear in x, so autograd supplies the reference's
-    transform_adjoint (transforms.py:69-90)."""
+    Z[2k+1] = (X[k+1], X[k]).  The kernels do NOT go through this: sig_kernel /
+    sig_kernel_gram(transform=...) build the transformed increments inside the
+    kernels' input preparation (sk_capi.cu prep_sides) and map gradients back
+    with the transform's adjoint."""
     if kind is None:
         return x
     if kind == "time_augment":
@@ -194,11 +200,19 @@ def path_transform(x: torch.Tensor, kind):
     raise InvalidArgument(f"unknown transform {kind!r}, expected one of {TRANSFORMS}")
 
 
+def _tf(transform):
+    if transform not in TRANSFORMS:
+        raise InvalidArgument(f"unknown transform {transform!r}, expected one of {TRANSFORMS}")
+    return ops.transform_code(transform)
+
+
 def sig_kernel(x, y, dyadic_order=0, static_kernel=None, transform=None, precision="fp64"):
     """k(x_b, y_b) for aligned batches (B, L1, d), (B, L2, d) -> (B,).
 
     A pair of (L, d) paths returns a 0-d tensor.  `transform` ("time_augment" or
-    "lead_lag") is applied to both paths first (pySigLib's path transforms).
+    "lead_lag", pySigLib's path transforms) is applied to both paths inside the
+    kernels (transformed increments built from the raw points; gradients come
+    back for the raw points).
     precision: "fp64" (default; the reference's arithmetic -- float32 inputs are
     solved in float64, kernel.py:36-38) or "fp32" (FP32-arithmetic kernels,
     linear static kernel, float32 result; within ~1e-4 of fp64 up to a few
@@ -206,14 +220,14 @@ def sig_kernel(x, y, dyadic_order=0, static_kernel=None, transform=None, precisi
     backward)."""
     x, sq = _batched(_prep(x, "x"), "x")
     y, _ = _batched(_prep(y, "y"), "y")
-    x, y = path_transform(x, transform), path_transform(y, transform)
+    tf = _tf(transform)
     l1, l2 = _orders(dyadic_order)
     kind, sigma = ops.static_kind(static_kernel)
     if _precision(precision, kind):
-        k = _SigKernelF32Fn.apply(x.to(torch.float32), y.to(torch.float32), l1, l2)
+        k = _SigKernelF32Fn.apply(x.to(torch.float32), y.to(torch.float32), l1, l2, tf)
         return k[0] if sq else k
     out_dtype = torch.promote_types(x.dtype, y.dtype)
-    k = _SigKernelFn.apply(x.to(torch.float64), y.to(torch.float64), l1, l2, kind, sigma)
+    k = _SigKernelFn.apply(x.to(torch.float64), y.to(torch.float64), l1, l2, kind, sigma, tf)
     k = k.to(out_dtype)
     return k[0] if sq else k
 
@@ -224,29 +238,28 @@ def sig_kernel_gram(x, y=None, dyadic_order=0, static_kernel=None, transform=Non
 
     y None (or y is x) -> symmetric: only a <= b is solved and the result is
     mirrored, hence exactly symmetric (reference kernel.py:151-180).
-    precision: as sig_kernel."""
+    transform, precision: as sig_kernel."""
     sym = y is None or y is x
     x, _ = _batched(_prep(x, "x"), "x")
-    x = path_transform(x, transform)
+    tf = _tf(transform)
     l1, l2 = _orders(dyadic_order)
     kind, sigma = ops.static_kind(static_kernel)
     if _precision(precision, kind):
         if sym:
-            return _SigKernelGramF32Fn.apply(x.to(torch.float32), None, l1, l2)
+            return _SigKernelGramF32Fn.apply(x.to(torch.float32), None, l1, l2, tf)
         y, _ = _batched(_prep(y, "y"), "y")
-        y = path_transform(y, transform)
-        return _SigKernelGramF32Fn.apply(x.to(torch.float32), y.to(torch.float32), l1, l2)
+        return _SigKernelGramF32Fn.apply(x.to(torch.float32), y.to(torch.float32), l1, l2, tf)
     if sym:
-        G = _SigKernelGramFn.apply(x.to(torch.float64), None, l1, l2, kind, sigma)
+        G = _SigKernelGramFn.apply(x.to(torch.float64), None, l1, l2, kind, sigma, tf)
         return G.to(x.dtype)
     y, _ = _batched(_prep(y, "y"), "y")
-    y = path_transform(y, transform)
     out_dtype = torch.promote_types(x.dtype, y.dtype)
-    G = _SigKernelGramFn.apply(x.to(torch.float64), y.to(torch.float64), l1, l2, kind, sigma)
+    G = _SigKernelGramFn.apply(x.to(torch.float64), y.to(torch.float64), l1, l2, kind, sigma, tf)
     return G.to(out_dtype)
 
 
-def sig_kernel_gram_value_and_grad(x, y=None, cotangent=None, dyadic_order=0, static_kernel=None):
+def sig_kernel_gram_value_and_grad(x, y=None, cotangent=None, dyadic_order=0, static_kernel=None,
+                                   transform=None):
     """Gram matrix and its gradient in ONE fused pass: returns (G, dF/dx, dF/dy)
     for F = sum_ab cotangent[a, b] G[a, b] (cotangent None = ones, the reference
     default kernel_grad.py:81-82); dF/dy is None when y is None (symmetric: both
@@ -268,7 +281,8 @@ def sig_kernel_gram_value_and_grad(x, y=None, cotangent=None, dyadic_order=0, st
     n1, n2 = xd.shape[0], (xd if sym else yd).shape[0]
     if cotangent is None:
         cotangent = torch.ones((n1, n2), dtype=torch.float64, device=xd.device)
-    G, gx, gy = ops.value_and_grad_gram(xd, yd, l1, l2, kind, sigma, cotangent)
+    G, gx, gy = ops.value_and_grad_gram(xd, yd, l1, l2, kind, sigma, cotangent,
+                                        transform=_tf(transform))
     return G, gx, gy
 
 

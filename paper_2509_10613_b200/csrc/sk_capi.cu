@@ -136,21 +136,42 @@ static void cap_slots(int64_t& blocks, int64_t& slots, int warps, double per_slo
 }
 
 // ---------------------------------------------------------------- prep kernels
-// Both sides of a call in ONE launch (rows side, then the columns side):
-// increments (kernel.py:74-75 np.diff, scaled, zero-padded to dpad) for the
-// linear kernel, padded nodes for RBF.
+// Path transforms (pySigLib's time augmentation and lead-lag; reference
+// transforms.py:37-120), applied inside the preparation launch: the kernels
+// read transformed increments (linear kernel; the reference's
+// fused_increments, transforms.py:91-120) or transformed nodes (RBF) built
+// straight from the raw points, so no transformed path is ever materialised.
+enum Transform : int { TF_NONE = 0, TF_TIME = 1, TF_LEADLAG = 2 };
+__host__ __device__ inline int64_t eff_len(int64_t L, int tf) { return tf == TF_LEADLAG ? 2 * L - 1 : L; }
+__host__ __device__ inline int64_t eff_dim(int64_t d, int tf) {
+  return tf == TF_TIME ? d + 1 : tf == TF_LEADLAG ? 2 * d : d;
+}
+// numpy.linspace(0, 1, L)[i] as the reference computes it (default_times,
+// transforms.py:30-34): i * (1 / (L - 1)), the last point exactly 1
+__device__ inline double time_point(int64_t i, int64_t L) {
+  if (L <= 1) return 0.0;
+  return i == L - 1 ? 1.0 : (double)i * (1.0 / (double)(L - 1));
+}
+
 template <typename T>
 struct PrepSide {
   const T* x;
-  int64_t n, L;
+  int64_t n, L;  // raw points per path
   double scale;
   T* out;
 };
+// Both sides of a call in ONE launch (rows side, then the columns side):
+// increments (kernel.py:74-75 np.diff, scaled by the exact dyadic factor,
+// zero-padded to dpad) for the linear kernel, padded nodes for RBF, each of
+// the transformed path when tf != TF_NONE (bitwise the np.diff of the
+// materialised transform: the same subtractions, and exact zeros).
 template <typename T>
-__global__ void prep_sides(PrepSide<T> s0, PrepSide<T> s1, int nsides, int rbf, int64_t d,
-                           int dpad) {
-  const int64_t rows0 = s0.n * (rbf ? s0.L : s0.L - 1);
-  const int64_t rows1 = nsides > 1 ? s1.n * (rbf ? s1.L : s1.L - 1) : 0;
+__global__ void prep_sides(PrepSide<T> s0, PrepSide<T> s1, int nsides, int rbf, int tf,
+                           int64_t d, int dpad) {
+  const int64_t per0 = rbf ? eff_len(s0.L, tf) : eff_len(s0.L, tf) - 1;
+  const int64_t per1 = rbf ? eff_len(s1.L, tf) : eff_len(s1.L, tf) - 1;
+  const int64_t rows0 = s0.n * per0;
+  const int64_t rows1 = nsides > 1 ? s1.n * per1 : 0;
   const int64_t total = (rows0 + rows1) * dpad;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -158,16 +179,59 @@ __global__ void prep_sides(PrepSide<T> s0, PrepSide<T> s1, int nsides, int rbf, 
     const bool first = rowg < rows0;
     const PrepSide<T>& sd = first ? s0 : s1;
     const int64_t row = first ? rowg : rowg - rows0;
+    const int64_t per = first ? per0 : per1;
+    const int64_t p = row / per, r = row % per;
+    const T* xp = sd.x + p * sd.L * d;
     T v = 0;
-    if (k < d) {
-      if (rbf) {
-        v = sd.x[row * d + k];
-      } else {
-        const int64_t p = row / (sd.L - 1), i = row % (sd.L - 1);
-        v = (sd.x[(p * sd.L + i + 1) * d + k] - sd.x[(p * sd.L + i) * d + k]) * (T)sd.scale;
+    if (rbf) {  // node r of the transformed path
+      if (tf == TF_NONE) {
+        if (k < d) v = xp[r * d + k];
+      } else if (tf == TF_TIME) {
+        if (k < d) v = xp[r * d + k];
+        else if (k == d) v = (T)time_point(r, sd.L);
+      } else {  // lead-lag: Z[2i] = (X[i], X[i]), Z[2i+1] = (X[i+1], X[i])
+        if (k < d) v = xp[((r + 1) >> 1) * d + k];
+        else if (k < 2 * d) v = xp[(r >> 1) * d + (k - d)];
+      }
+    } else {  // increment r of the transformed path
+      if (tf == TF_NONE) {
+        if (k < d) v = (xp[(r + 1) * d + k] - xp[r * d + k]) * (T)sd.scale;
+      } else if (tf == TF_TIME) {
+        if (k < d) v = (xp[(r + 1) * d + k] - xp[r * d + k]) * (T)sd.scale;
+        else if (k == d) v = ((T)time_point(r + 1, sd.L) - (T)time_point(r, sd.L)) * (T)sd.scale;
+      } else {  // lead-lag: (dX_i, 0), then (0, dX_i)
+        const int64_t i = r >> 1;
+        const bool lead = (r & 1) == 0;
+        if (lead && k < d) v = (xp[(i + 1) * d + k] - xp[i * d + k]) * (T)sd.scale;
+        else if (!lead && k >= d && k < 2 * d)
+          v = (xp[(i + 1) * d + (k - d)] - xp[i * d + (k - d)]) * (T)sd.scale;
       }
     }
     sd.out[row * dpad + k] = v;
+  }
+}
+
+// Adjoint of a transform on point gradients (reference transform_adjoint,
+// transforms.py:69-90, same addition order): g_t (n, L', d') -> grad (n, L, d);
+// grad = value, or grad += value.
+__global__ void transform_adjoint_kernel(const double* __restrict__ gt, int64_t n, int64_t L,
+                                         int64_t d, int tf, double* __restrict__ grad,
+                                         int accumulate) {
+  const int64_t Le = eff_len(L, tf), de = eff_dim(d, tf);
+  const int64_t total = n * L * d;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e % d, i = (e / d) % L, p = e / (d * L);
+    const double* g = gt + p * Le * de;
+    double v;
+    if (tf == TF_LEADLAG) {  // out = lead[0::2] + lag[0::2]; [:-1] += lag[1::2]; [1:] += lead[1::2]
+      v = g[(2 * i) * de + c] + g[(2 * i) * de + d + c];
+      if (i < L - 1) v += g[(2 * i + 1) * de + d + c];
+      if (i >= 1) v += g[(2 * i - 1) * de + c];
+    } else {  // time augmentation drops the time column
+      v = g[i * de + c];
+    }
+    grad[e] = accumulate ? grad[e] + v : v;
   }
 }
 
@@ -421,15 +485,27 @@ static size_t prep_elems(int kind, int64_t n, int64_t L, int dpad) {
 
 // Prepares the rows side (scaled by `scale`) and, unless `share`, the columns
 // side, in one launch (T: the arithmetic type of the kernels that read them).
+// LR, LC, d: RAW points / dimension (the prepared arrays hold the transformed path)
 template <typename T>
 static void launch_prep(int kind, const T* xr, int64_t nR, int64_t LR, const T* xc, int64_t nC,
                         int64_t LC, bool share, int64_t d, int dpad, T* outR, T* outC,
-                        cudaStream_t st, double scale) {
-  const size_t total = prep_elems(kind, nR, LR, dpad) + (share ? 0 : prep_elems(kind, nC, LC, dpad));
+                        cudaStream_t st, double scale, int tf = TF_NONE) {
+  const size_t total = prep_elems(kind, nR, eff_len(LR, tf), dpad) +
+                       (share ? 0 : prep_elems(kind, nC, eff_len(LC, tf), dpad));
   if (total == 0) return;
   const int blocks = (int)std::min<size_t>((total + 255) / 256, 4096);
   PrepSide<T> s0{xr, nR, LR, scale, outR}, s1{xc, nC, LC, 1.0, outC};
-  prep_sides<T><<<blocks, 256, 0, st>>>(s0, s1, share ? 1 : 2, kind == RBF ? 1 : 0, d, dpad);
+  prep_sides<T><<<blocks, 256, 0, st>>>(s0, s1, share ? 1 : 2, kind == RBF ? 1 : 0, tf, d, dpad);
+}
+
+static int launch_transform_adjoint(const double* gt, int64_t n, int64_t L, int64_t d, int tf,
+                                    double* grad, bool accumulate, cudaStream_t st) {
+  const int64_t total = n * L * d;
+  if (total <= 0) return SK_OK;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
+  transform_adjoint_kernel<<<blocks, 256, 0, st>>>(gt, n, L, d, tf, grad, accumulate ? 1 : 0);
+  SK_CUDA(cudaGetLastError());
+  return SK_OK;
 }
 
 static int validate(int64_t L1, int64_t L2, int64_t d, int lam1, int lam2, int kind,
@@ -499,8 +575,15 @@ static Geometry orient(int64_t n1, int64_t n2, int64_t L1, int64_t L2, int lam1,
 static int forward_impl(const void* x, const void* y, int64_t n1, int64_t n2, int64_t L1,
                         int64_t L2, int64_t d, int lam1, int lam2, int kind, double sigma,
                         int mode, int64_t r0, int64_t r1, void* out, void* ws,
-                        size_t ws_bytes, cudaStream_t st, size_t* query, bool f32 = false) {
+                        size_t ws_bytes, cudaStream_t st, size_t* query, bool f32 = false,
+                        int tf = TF_NONE) {
   if (int rc = validate(L1, L2, d, lam1, lam2, kind, sigma)) return rc;
+  if (tf < TF_NONE || tf > TF_LEADLAG) return fail(SK_INVALID_ARGUMENT, "unknown path transform");
+  // the kernels solve the transformed paths (raw L1, L2, d only for the prep)
+  const int64_t L1r = L1, L2r = L2, dr = d;
+  L1 = eff_len(L1, tf);
+  L2 = eff_len(L2, tf);
+  d = eff_dim(d, tf);
   if (f32 && kind != LINEAR)
     return fail(SK_INVALID_ARGUMENT, "FP32 arithmetic supports the linear static kernel only");
   const size_t esz = f32 ? sizeof(float) : sizeof(double);
@@ -542,11 +625,13 @@ static int forward_impl(const void* x, const void* y, int64_t n1, int64_t n2, in
   const void* xr = g.swap ? y : x;
   const void* xc = g.swap ? x : y;
   if (f32)
-    launch_prep<float>(kind, (const float*)xr, g.nR, g.LR, (const float*)xc, g.nC, g.LC, share, d,
-                       pb.dpad, (float*)prepR, (float*)prepC, st, fold ? pb.scale : 1.0);
+    launch_prep<float>(kind, (const float*)xr, g.nR, g.swap ? L2r : L1r, (const float*)xc, g.nC,
+                       g.swap ? L1r : L2r, share, dr, pb.dpad, (float*)prepR, (float*)prepC, st,
+                       fold ? pb.scale : 1.0, tf);
   else
-    launch_prep<double>(kind, (const double*)xr, g.nR, g.LR, (const double*)xc, g.nC, g.LC, share,
-                        d, pb.dpad, (double*)prepR, (double*)prepC, st, fold ? pb.scale : 1.0);
+    launch_prep<double>(kind, (const double*)xr, g.nR, g.swap ? L2r : L1r, (const double*)xc, g.nC,
+                        g.swap ? L1r : L2r, share, dr, pb.dpad, (double*)prepR, (double*)prepC,
+                        st, fold ? pb.scale : 1.0, tf);
   if (fold) pb.pscale = 1.0;
   pb.R.p = reinterpret_cast<const double*>(prepR);
   pb.R.rows = (int)(g.LR - 1);
@@ -622,35 +707,37 @@ int sk_forward_gram(const double* x, const double* y, int64_t n1, int64_t n2, in
 }
 
 size_t sk_forward_batch_f32_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d,
-                                            int lam1, int lam2) {
+                                            int lam1, int lam2, int transform) {
   size_t q = 0;
   if (forward_impl(nullptr, nullptr, B, B, L1, L2, d, lam1, lam2, LINEAR, 1.0, BATCH, 0, B,
-                   nullptr, nullptr, 0, nullptr, &q, true))
+                   nullptr, nullptr, 0, nullptr, &q, true, transform))
     return 0;
   return q;
 }
 
 int sk_forward_batch_f32(const float* x, const float* y, int64_t B, int64_t L1, int64_t L2,
-                         int64_t d, int lam1, int lam2, float* out, void* ws, size_t ws_bytes,
-                         void* stream) {
+                         int64_t d, int lam1, int lam2, int transform, float* out, void* ws,
+                         size_t ws_bytes, void* stream) {
   if (B < 0) return fail(SK_INVALID_ARGUMENT, "negative batch");
   return forward_impl(x, y, B, B, L1, L2, d, lam1, lam2, LINEAR, 1.0, BATCH, 0, B, out, ws,
-                      ws_bytes, (cudaStream_t)stream, nullptr, true);
+                      ws_bytes, (cudaStream_t)stream, nullptr, true, transform);
 }
 
 size_t sk_forward_gram_f32_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
-                                           int64_t d, int lam1, int lam2, int symmetric) {
+                                           int64_t d, int lam1, int lam2, int symmetric,
+                                           int transform) {
   size_t q = 0;
   if (forward_impl(nullptr, nullptr, n1, n2, L1, L2, d, lam1, lam2, LINEAR, 1.0,
                    symmetric ? GRAM_SYM : GRAM_CROSS, 0, n1, nullptr, nullptr, 0, nullptr, &q,
-                   true))
+                   true, transform))
     return 0;
   return q;
 }
 
 int sk_forward_gram_f32(const float* x, const float* y, int64_t n1, int64_t n2, int64_t L1,
-                        int64_t L2, int64_t d, int lam1, int lam2, int64_t row_begin,
-                        int64_t row_end, float* out, void* ws, size_t ws_bytes, void* stream) {
+                        int64_t L2, int64_t d, int lam1, int lam2, int transform,
+                        int64_t row_begin, int64_t row_end, float* out, void* ws, size_t ws_bytes,
+                        void* stream) {
   const bool sym = (y == nullptr);
   if (sym && (n2 != n1 || L2 != L1))
     return fail(SK_INVALID_ARGUMENT, "symmetric Gram needs n2 == n1 and L2 == L1");
@@ -658,7 +745,65 @@ int sk_forward_gram_f32(const float* x, const float* y, int64_t n1, int64_t n2, 
     return fail(SK_INVALID_ARGUMENT, "row range out of bounds");
   return forward_impl(x, sym ? x : y, n1, n2, L1, L2, d, lam1, lam2, LINEAR, 1.0,
                       sym ? GRAM_SYM : GRAM_CROSS, row_begin, row_end, out, ws, ws_bytes,
-                      (cudaStream_t)stream, nullptr, true);
+                      (cudaStream_t)stream, nullptr, true, transform);
+}
+
+// ---- path transforms (time augmentation / lead-lag) applied inside the call
+size_t sk_forward_batch_tf_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d,
+                                           int lam1, int lam2, int static_kernel, int transform) {
+  size_t q = 0;
+  if (forward_impl(nullptr, nullptr, B, B, L1, L2, d, lam1, lam2, static_kernel, 1.0, BATCH, 0,
+                   B, nullptr, nullptr, 0, nullptr, &q, false, transform))
+    return 0;
+  return q;
+}
+
+int sk_forward_batch_tf(const double* x, const double* y, int64_t B, int64_t L1, int64_t L2,
+                        int64_t d, int lam1, int lam2, int static_kernel, double sigma,
+                        int transform, double* out, void* ws, size_t ws_bytes, void* stream) {
+  if (B < 0) return fail(SK_INVALID_ARGUMENT, "negative batch");
+  return forward_impl(x, y, B, B, L1, L2, d, lam1, lam2, static_kernel, sigma, BATCH, 0, B, out,
+                      ws, ws_bytes, (cudaStream_t)stream, nullptr, false, transform);
+}
+
+size_t sk_forward_gram_tf_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                          int64_t d, int lam1, int lam2, int static_kernel,
+                                          int symmetric, int transform) {
+  size_t q = 0;
+  if (forward_impl(nullptr, nullptr, n1, n2, L1, L2, d, lam1, lam2, static_kernel, 1.0,
+                   symmetric ? GRAM_SYM : GRAM_CROSS, 0, n1, nullptr, nullptr, 0, nullptr, &q,
+                   false, transform))
+    return 0;
+  return q;
+}
+
+int sk_forward_gram_tf(const double* x, const double* y, int64_t n1, int64_t n2, int64_t L1,
+                       int64_t L2, int64_t d, int lam1, int lam2, int static_kernel, double sigma,
+                       int transform, int64_t row_begin, int64_t row_end, double* out, void* ws,
+                       size_t ws_bytes, void* stream) {
+  const bool sym = (y == nullptr);
+  if (sym && (n2 != n1 || L2 != L1))
+    return fail(SK_INVALID_ARGUMENT, "symmetric Gram needs n2 == n1 and L2 == L1");
+  if (row_begin < 0 || row_end > n1 || row_begin > row_end)
+    return fail(SK_INVALID_ARGUMENT, "row range out of bounds");
+  return forward_impl(x, sym ? x : y, n1, n2, L1, L2, d, lam1, lam2, static_kernel, sigma,
+                      sym ? GRAM_SYM : GRAM_CROSS, row_begin, row_end, out, ws, ws_bytes,
+                      (cudaStream_t)stream, nullptr, false, transform);
+}
+
+int sk_transform_adjoint(const double* g_t, int64_t n, int64_t L, int64_t d, int transform,
+                         double* grad, int accumulate, void* stream) {
+  if (n < 0 || L < 1 || d < 1 || !g_t || !grad) return fail(SK_INVALID_ARGUMENT, "bad arguments");
+  if (transform < TF_NONE || transform > TF_LEADLAG)
+    return fail(SK_INVALID_ARGUMENT, "unknown path transform");
+  if (transform == TF_NONE) {
+    if (accumulate) return fail(SK_INVALID_ARGUMENT, "identity transform: nothing to map");
+    SK_CUDA(cudaMemcpyAsync(grad, g_t, sizeof(double) * n * L * d, cudaMemcpyDeviceToDevice,
+                            (cudaStream_t)stream));
+    return SK_OK;
+  }
+  return launch_transform_adjoint(g_t, n, L, d, transform, grad, accumulate != 0,
+                                  (cudaStream_t)stream);
 }
 
 static int solve_delta_impl(const double* delta, int64_t B, int64_t r1, int64_t r2, int lam1,
@@ -823,8 +968,15 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
                          int mode, int64_t r0, int64_t r1, const double* cot, double* values,
                          double* grad_x, double* grad_y, void* ws, size_t ws_bytes,
                          cudaStream_t st, size_t* query, void* acc_x = nullptr,
-                         void* acc_y = nullptr) {
+                         void* acc_y = nullptr, int tf = TF_NONE) {
   if (int rc = validate(L1, L2, d, lam1, lam2, kind, sigma)) return rc;
+  if (tf < TF_NONE || tf > TF_LEADLAG) return fail(SK_INVALID_ARGUMENT, "unknown path transform");
+  // the kernels solve the transformed paths; their point gradients (transformed
+  // space) are mapped back by the transform's adjoint at the end
+  const int64_t L1r = L1, L2r = L2, dr = d;
+  L1 = eff_len(L1, tf);
+  L2 = eff_len(L2, tf);
+  d = eff_dim(d, tf);
   const bool sym = mode == GRAM_SYM;
   Geometry g = orient(n1, n2, L1, L2, lam1, lam2);
   Problem pb = base_problem(kind, d, g.lamR, g.lamC, g.LR, g.LC, sigma);
@@ -861,16 +1013,20 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   const bool own_acc = gram && acc_x == nullptr;
   lo.accx = own_acc ? align_up(acc_bytes(n1, L1, d), 256) : 0;
   lo.accy = (own_acc && !sym) ? align_up(acc_bytes(n2, L2, d), 256) : 0;
+  // transformed-space point gradients (mapped to the raw paths at the end)
+  const bool tgrad = tf != TF_NONE && (own_acc || !gram);
+  const size_t gtx = tgrad ? align_up((size_t)n1 * L1 * d * sizeof(double), 256) : 0;
+  const size_t gty = (tgrad && !sym) ? align_up((size_t)n2 * L2 * d * sizeof(double), 256) : 0;
   lo.total = lo.prepR + lo.prepC + lo.rowck + lo.colck + lo.pck + lo.rows + lo.dbuf + lo.gscr +
-             lo.accx + lo.accy;
+             lo.accx + lo.accy + gtx + gty;
   if (query) {
     *query = lo.total;
     return SK_OK;
   }
   if (mode == BATCH) {
     // batch gradients are written (not accumulated): zero them first
-    if (grad_x) SK_CUDA(cudaMemsetAsync(grad_x, 0, sizeof(double) * n1 * L1 * d, st));
-    if (grad_y) SK_CUDA(cudaMemsetAsync(grad_y, 0, sizeof(double) * n2 * L2 * d, st));
+    if (grad_x) SK_CUDA(cudaMemsetAsync(grad_x, 0, sizeof(double) * n1 * L1r * dr, st));
+    if (grad_y) SK_CUDA(cudaMemsetAsync(grad_y, 0, sizeof(double) * n2 * L2r * dr, st));
   }
   if (npairs <= 0 || pl.nitems == 0) return SK_OK;
   if (ws_bytes < lo.total)
@@ -917,11 +1073,23 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
       return rc;
   }
   if (sym) blob_y = blob_x;
+  double* user_gx = grad_x;
+  double* user_gy = grad_y;
+  if (tgrad) {  // the kernels write / finalise into transformed-space buffers
+    grad_x = reinterpret_cast<double*>(p);
+    p += gtx;
+    grad_y = sym ? nullptr : reinterpret_cast<double*>(p);
+    p += gty;
+    if (!gram) {
+      SK_CUDA(cudaMemsetAsync(grad_x, 0, sizeof(double) * n1 * L1 * d, st));
+      SK_CUDA(cudaMemsetAsync(grad_y, 0, sizeof(double) * n2 * L2 * d, st));
+    }
+  }
   ba.rows_exclusive = (1 << g.lamR) <= pl.shape.R ? 1 : 0;
   const double* xr = g.swap ? y : x;
   const double* xc = g.swap ? x : y;
-  launch_prep<double>(kind, xr, g.nR, g.LR, xc, g.nC, g.LC, share, d, pb.dpad, prepR, prepC, st,
-                      fold ? pb.scale : 1.0);
+  launch_prep<double>(kind, xr, g.nR, g.swap ? L2r : L1r, xc, g.nC, g.swap ? L1r : L2r, share, dr,
+                      pb.dpad, prepR, prepC, st, fold ? pb.scale : 1.0, tf);
   if (fold) pb.pscale = 1.0;
   pb.R.p = prepR;
   pb.R.rows = (int)(g.LR - 1);
@@ -959,9 +1127,14 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   pl.fn<<<(unsigned)pl.blocks, pl.threads, pl.smem_bytes, st>>>(pb, ba);
   SK_CUDA(cudaGetLastError());
   if (own_acc) {
-    if (int rc = acc_finalize(blob_x, n1 * L1 * d, grad_x, true, st)) return rc;
+    if (int rc = acc_finalize(blob_x, n1 * L1 * d, grad_x, !tgrad, st)) return rc;
     if (!sym)
-      if (int rc = acc_finalize(blob_y, n2 * L2 * d, grad_y, true, st)) return rc;
+      if (int rc = acc_finalize(blob_y, n2 * L2 * d, grad_y, !tgrad, st)) return rc;
+  }
+  if (tgrad) {  // batch: written; Gram: accumulated (+=) like the plain call
+    if (int rc = launch_transform_adjoint(grad_x, n1, L1r, dr, tf, user_gx, gram, st)) return rc;
+    if (!sym)
+      if (int rc = launch_transform_adjoint(grad_y, n2, L2r, dr, tf, user_gy, gram, st)) return rc;
   }
   return SK_OK;
 }
@@ -1040,6 +1213,102 @@ int sk_backward_gram(const double* x, const double* y, int64_t n1, int64_t n2, i
                        grad_y, ws, ws_bytes, (cudaStream_t)stream, nullptr);
 }
 
+size_t sk_backward_batch_tf_workspace_bytes(int64_t B, int64_t L1, int64_t L2, int64_t d,
+                                            int lam1, int lam2, int static_kernel, int transform) {
+  size_t q = 0;
+  if (backward_impl(nullptr, nullptr, B, B, L1, L2, d, lam1, lam2, static_kernel, 1.0, BATCH, 0,
+                    B, nullptr, nullptr, nullptr, nullptr, nullptr, 0, nullptr, &q, nullptr,
+                    nullptr, transform))
+    return 0;
+  return q;
+}
+
+int sk_backward_batch_tf(const double* x, const double* y, int64_t B, int64_t L1, int64_t L2,
+                         int64_t d, int lam1, int lam2, int static_kernel, double sigma,
+                         int transform, const double* cot, double* values, double* grad_x,
+                         double* grad_y, void* ws, size_t ws_bytes, void* stream) {
+  if (B < 0) return fail(SK_INVALID_ARGUMENT, "negative batch");
+  return backward_impl(x, y, B, B, L1, L2, d, lam1, lam2, static_kernel, sigma, BATCH, 0, B, cot,
+                       values, grad_x, grad_y, ws, ws_bytes, (cudaStream_t)stream, nullptr,
+                       nullptr, nullptr, transform);
+}
+
+size_t sk_backward_gram_tf_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                           int64_t d, int lam1, int lam2, int static_kernel,
+                                           int symmetric, int transform) {
+  size_t q = 0;
+  if (backward_impl(nullptr, nullptr, n1, n2, L1, L2, d, lam1, lam2, static_kernel, 1.0,
+                    symmetric ? GRAM_SYM : GRAM_CROSS, 0, n1, nullptr, nullptr, nullptr,
+                    nullptr, nullptr, 0, nullptr, &q, nullptr, nullptr, transform))
+    return 0;
+  return q;
+}
+
+int sk_backward_gram_tf(const double* x, const double* y, int64_t n1, int64_t n2, int64_t L1,
+                        int64_t L2, int64_t d, int lam1, int lam2, int static_kernel,
+                        double sigma, int transform, int64_t row_begin, int64_t row_end,
+                        const double* cot, double* values, double* grad_x, double* grad_y,
+                        void* ws, size_t ws_bytes, void* stream) {
+  const bool sym = (y == nullptr);
+  if (sym && (n2 != n1 || L2 != L1))
+    return fail(SK_INVALID_ARGUMENT, "symmetric Gram needs n2 == n1 and L2 == L1");
+  if (row_begin < 0 || row_end > n1 || row_begin > row_end)
+    return fail(SK_INVALID_ARGUMENT, "row range out of bounds");
+  if (!cot) return fail(SK_INVALID_ARGUMENT, "Gram backward needs the cotangent matrix");
+  if (int rc = backward_impl(x, sym ? x : y, n1, n2, L1, L2, d, lam1, lam2, static_kernel, sigma,
+                             sym ? GRAM_SYM : GRAM_CROSS, row_begin, row_end, cot, values,
+                             grad_x, grad_y, ws, ws_bytes, (cudaStream_t)stream, nullptr, nullptr,
+                             nullptr, transform))
+    return rc;
+  const int64_t span = row_end - row_begin;
+  if (values && sym && span > 1) {
+    int blocks = (int)std::min<int64_t>((span * span + 255) / 256, 4096);
+    mirror_upper<double><<<blocks, 256, 0, (cudaStream_t)stream>>>(values, n2, (int)row_begin,
+                                                                   (int)row_end);
+    SK_CUDA(cudaGetLastError());
+  }
+  return SK_OK;
+}
+
+size_t sk_backward_gram_acc_tf_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                               int64_t d, int lam1, int lam2, int static_kernel,
+                                               int symmetric, int transform) {
+  size_t q = 0;
+  char dummy = 0;  // non-NULL accumulator: the workspace holds no accumulators
+  if (backward_impl(nullptr, nullptr, n1, n2, L1, L2, d, lam1, lam2, static_kernel, 1.0,
+                    symmetric ? GRAM_SYM : GRAM_CROSS, 0, n1, nullptr, nullptr, nullptr,
+                    nullptr, nullptr, 0, nullptr, &q, &dummy, &dummy, transform))
+    return 0;
+  return q;
+}
+
+int sk_backward_gram_acc_tf(const double* x, const double* y, int64_t n1, int64_t n2,
+                            int64_t L1, int64_t L2, int64_t d, int lam1, int lam2,
+                            int static_kernel, double sigma, int transform, int64_t row_begin,
+                            int64_t row_end, const double* cot, double* values, void* acc_x,
+                            void* acc_y, void* ws, size_t ws_bytes, void* stream) {
+  const bool sym = (y == nullptr);
+  if (sym && (n2 != n1 || L2 != L1))
+    return fail(SK_INVALID_ARGUMENT, "symmetric Gram needs n2 == n1 and L2 == L1");
+  if (row_begin < 0 || row_end > n1 || row_begin > row_end)
+    return fail(SK_INVALID_ARGUMENT, "row range out of bounds");
+  if (!cot) return fail(SK_INVALID_ARGUMENT, "Gram backward needs the cotangent matrix");
+  if (!acc_x) return fail(SK_INVALID_ARGUMENT, "accumulator missing");
+  if (int rc = backward_impl(x, sym ? x : y, n1, n2, L1, L2, d, lam1, lam2, static_kernel, sigma,
+                             sym ? GRAM_SYM : GRAM_CROSS, row_begin, row_end, cot, values,
+                             nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream, nullptr,
+                             acc_x, acc_y, transform))
+    return rc;
+  const int64_t span = row_end - row_begin;
+  if (values && sym && span > 1) {
+    int blocks = (int)std::min<int64_t>((span * span + 255) / 256, 4096);
+    mirror_upper<double><<<blocks, 256, 0, (cudaStream_t)stream>>>(values, n2, (int)row_begin,
+                                                                   (int)row_end);
+    SK_CUDA(cudaGetLastError());
+  }
+  return SK_OK;
+}
+
 size_t sk_grad_acc_bytes(int64_t n, int64_t L, int64_t d) {
   if (n < 0 || L < 0 || d < 0) return 0;
   return acc_bytes(n, L, d);
@@ -1067,38 +1336,16 @@ int sk_backward_gram_acc(const double* x, const double* y, int64_t n1, int64_t n
                          double sigma, int64_t row_begin, int64_t row_end, const double* cot,
                          double* values, void* acc_x, void* acc_y, void* ws, size_t ws_bytes,
                          void* stream) {
-  const bool sym = (y == nullptr);
-  if (sym && (n2 != n1 || L2 != L1))
-    return fail(SK_INVALID_ARGUMENT, "symmetric Gram needs n2 == n1 and L2 == L1");
-  if (row_begin < 0 || row_end > n1 || row_begin > row_end)
-    return fail(SK_INVALID_ARGUMENT, "row range out of bounds");
-  if (!cot) return fail(SK_INVALID_ARGUMENT, "Gram backward needs the cotangent matrix");
-  if (!acc_x) return fail(SK_INVALID_ARGUMENT, "accumulator missing");
-  if (int rc = backward_impl(x, sym ? x : y, n1, n2, L1, L2, d, lam1, lam2, static_kernel, sigma,
-                             sym ? GRAM_SYM : GRAM_CROSS, row_begin, row_end, cot, values,
-                             nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream, nullptr,
-                             acc_x, acc_y))
-    return rc;
-  const int64_t span = row_end - row_begin;
-  if (values && sym && span > 1) {
-    int blocks = (int)std::min<int64_t>((span * span + 255) / 256, 4096);
-    mirror_upper<double><<<blocks, 256, 0, (cudaStream_t)stream>>>(values, n2, (int)row_begin,
-                                                           (int)row_end);
-    SK_CUDA(cudaGetLastError());
-  }
-  return SK_OK;
+  return sk_backward_gram_acc_tf(x, y, n1, n2, L1, L2, d, lam1, lam2, static_kernel, sigma,
+                                 TF_NONE, row_begin, row_end, cot, values, acc_x, acc_y, ws,
+                                 ws_bytes, stream);
 }
 
 size_t sk_backward_gram_acc_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
                                             int64_t d, int lam1, int lam2, int static_kernel,
                                             int symmetric) {
-  size_t q = 0;
-  char dummy = 0;  // non-NULL accumulator: the workspace holds no accumulators
-  if (backward_impl(nullptr, nullptr, n1, n2, L1, L2, d, lam1, lam2, static_kernel, 1.0,
-                    symmetric ? GRAM_SYM : GRAM_CROSS, 0, n1, nullptr, nullptr, nullptr,
-                    nullptr, nullptr, 0, nullptr, &q, &dummy, &dummy))
-    return 0;
-  return q;
+  return sk_backward_gram_acc_tf_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, static_kernel,
+                                                 symmetric, TF_NONE);
 }
 
 }  // extern "C"

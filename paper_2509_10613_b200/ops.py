@@ -72,8 +72,25 @@ def static_kind(static_kernel):
     raise InvalidArgument(f"unknown static kernel {static_kernel!r}")
 
 
-def forward_batch(x, y, lam1: int, lam2: int, kind: int, sigma: float) -> torch.Tensor:
+def transform_code(transform) -> int:
+    """C-ABI code of a path transform: None, "time_augment" or "lead_lag"."""
+    if isinstance(transform, int) and transform in (0, 1, 2):
+        return transform
+    if transform not in _lib.TRANSFORMS:
+        raise InvalidArgument(f"unknown transform {transform!r}, expected one of "
+                              f"(None, 'time_augment', 'lead_lag')")
+    return _lib.TRANSFORMS[transform]
+
+
+def effective_shape(L: int, d: int, tf: int):
+    """(points, dimension) of the transformed path (reference transforms.py:123-135)."""
+    return (2 * L - 1 if tf == 2 else L), (d + 1 if tf == 1 else 2 * d if tf == 2 else d)
+
+
+def forward_batch(x, y, lam1: int, lam2: int, kind: int, sigma: float,
+                  transform=None) -> torch.Tensor:
     lib = _lib.load()
+    tf = transform_code(transform)
     x = _paths(x, "x")
     y = _paths(y, "y")
     B, L1, d = x.shape
@@ -87,36 +104,33 @@ def forward_batch(x, y, lam1: int, lam2: int, kind: int, sigma: float) -> torch.
     if B == 0:
         return out
     with torch.cuda.device(x.device):
-        nb = lib.sk_forward_batch_workspace_bytes(B, L1, L2, d, lam1, lam2, kind)
+        nb = lib.sk_forward_batch_tf_workspace_bytes(B, L1, L2, d, lam1, lam2, kind, tf)
         ws = _workspace(nb, x.device)
-        _lib.check(lib.sk_forward_batch(_ptr(x), _ptr(y), B, L1, L2, d, lam1, lam2, kind, sigma,
-                                        _ptr(out), _ptr(ws), ws.numel(), _stream(x.device)))
+        _lib.check(lib.sk_forward_batch_tf(_ptr(x), _ptr(y), B, L1, L2, d, lam1, lam2, kind,
+                                           sigma, tf, _ptr(out), _ptr(ws), ws.numel(),
+                                           _stream(x.device)))
     return out
 
 
 def forward_gram(x, y, lam1: int, lam2: int, kind: int, sigma: float,
-                 rows: tuple[int, int] | None = None, out: torch.Tensor | None = None):
+                 rows: tuple[int, int] | None = None, out: torch.Tensor | None = None,
+                 transform=None):
     """G[a - r0, b] = k(x_a, y_b) for a in rows; y None -> symmetric (y is x)."""
     lib = _lib.load()
-    x = _paths(x, "x")
-    sym = y is None
-    yy = x if sym else _paths(y, "y")
-    n1, L1, d = x.shape
-    n2, L2 = yy.shape[0], yy.shape[1]
-    if yy.shape[2] != d:
-        raise InvalidArgument(f"path dimensions differ: {d} vs {yy.shape[2]}")
-    _same_device(yy, x, "y")
-    r0, r1 = (0, n1) if rows is None else (int(rows[0]), int(rows[1]))
+    tf = transform_code(transform)
+    x, yy, sym, n1, n2, L1, L2, d = _gram_args(x, y)
+    r0, r1 = _rows(rows, n1)
     if out is None:
         out = torch.empty((r1 - r0, n2), dtype=torch.float64, device=x.device)
     if n1 == 0 or n2 == 0 or r1 <= r0:
         return out
     with torch.cuda.device(x.device):
-        nb = lib.sk_forward_gram_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind, int(sym))
+        nb = lib.sk_forward_gram_tf_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind, int(sym),
+                                                    tf)
         ws = _workspace(nb, x.device)
-        _lib.check(lib.sk_forward_gram(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
-                                       lam1, lam2, kind, sigma, r0, r1, _ptr(out), _ptr(ws),
-                                       ws.numel(), _stream(x.device)))
+        _lib.check(lib.sk_forward_gram_tf(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
+                                          lam1, lam2, kind, sigma, tf, r0, r1, _ptr(out),
+                                          _ptr(ws), ws.numel(), _stream(x.device)))
     return out
 
 
@@ -129,10 +143,11 @@ def _paths32(t, name):
     return t.to(torch.float32).contiguous()
 
 
-def forward_batch_f32(x, y, lam1: int, lam2: int) -> torch.Tensor:
+def forward_batch_f32(x, y, lam1: int, lam2: int, transform=None) -> torch.Tensor:
     """FP32-arithmetic forward (linear static kernel): float32 in, float32 out.
     The cell uses the small-correction form (sk_cell.cuh Coef32)."""
     lib = _lib.load()
+    tf = transform_code(transform)
     x = _paths32(x, "x")
     y = _paths32(y, "y")
     B, L1, d = x.shape
@@ -143,16 +158,18 @@ def forward_batch_f32(x, y, lam1: int, lam2: int) -> torch.Tensor:
     if B == 0:
         return out
     with torch.cuda.device(x.device):
-        nb = lib.sk_forward_batch_f32_workspace_bytes(B, L1, y.shape[1], d, lam1, lam2)
+        nb = lib.sk_forward_batch_f32_workspace_bytes(B, L1, y.shape[1], d, lam1, lam2, tf)
         ws = _workspace(nb, x.device)
         _lib.check(lib.sk_forward_batch_f32(_ptr(x), _ptr(y), B, L1, y.shape[1], d, lam1, lam2,
-                                            _ptr(out), _ptr(ws), ws.numel(), _stream(x.device)))
+                                            tf, _ptr(out), _ptr(ws), ws.numel(),
+                                            _stream(x.device)))
     return out
 
 
-def forward_gram_f32(x, y, lam1: int, lam2: int, rows=None) -> torch.Tensor:
+def forward_gram_f32(x, y, lam1: int, lam2: int, rows=None, transform=None) -> torch.Tensor:
     """FP32-arithmetic Gram forward (linear static kernel); y None = symmetric."""
     lib = _lib.load()
+    tf = transform_code(transform)
     x = _paths32(x, "x")
     sym = y is None
     yy = x if sym else _paths32(y, "y")
@@ -166,11 +183,11 @@ def forward_gram_f32(x, y, lam1: int, lam2: int, rows=None) -> torch.Tensor:
     if n1 == 0 or n2 == 0 or r1 <= r0:
         return out
     with torch.cuda.device(x.device):
-        nb = lib.sk_forward_gram_f32_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, int(sym))
+        nb = lib.sk_forward_gram_f32_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, int(sym), tf)
         ws = _workspace(nb, x.device)
         _lib.check(lib.sk_forward_gram_f32(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
-                                           lam1, lam2, r0, r1, _ptr(out), _ptr(ws), ws.numel(),
-                                           _stream(x.device)))
+                                           lam1, lam2, tf, r0, r1, _ptr(out), _ptr(ws),
+                                           ws.numel(), _stream(x.device)))
     return out
 
 
@@ -200,9 +217,10 @@ def solve_delta_grid(delta: torch.Tensor, lam1: int, lam2: int) -> torch.Tensor:
     return grid
 
 
-def backward_batch(x, y, lam1, lam2, kind, sigma, cot, want_values=False):
+def backward_batch(x, y, lam1, lam2, kind, sigma, cot, want_values=False, transform=None):
     """(values or None, grad_x, grad_y) of sum_b cot[b] k(x_b, y_b)."""
     lib = _lib.load()
+    tf = transform_code(transform)
     x = _paths(x, "x")
     y = _paths(y, "y")
     B, L1, d = x.shape
@@ -219,11 +237,11 @@ def backward_batch(x, y, lam1, lam2, kind, sigma, cot, want_values=False):
     if B == 0:
         return vals, gx, gy
     with torch.cuda.device(x.device):
-        nb = lib.sk_backward_batch_workspace_bytes(B, L1, L2, d, lam1, lam2, kind)
+        nb = lib.sk_backward_batch_tf_workspace_bytes(B, L1, L2, d, lam1, lam2, kind, tf)
         ws = _workspace(nb, x.device)
-        _lib.check(lib.sk_backward_batch(_ptr(x), _ptr(y), B, L1, L2, d, lam1, lam2, kind, sigma,
-                                         _ptr(cot), _ptr(vals), _ptr(gx), _ptr(gy), _ptr(ws),
-                                         ws.numel(), _stream(x.device)))
+        _lib.check(lib.sk_backward_batch_tf(_ptr(x), _ptr(y), B, L1, L2, d, lam1, lam2, kind,
+                                            sigma, tf, _ptr(cot), _ptr(vals), _ptr(gx), _ptr(gy),
+                                            _ptr(ws), ws.numel(), _stream(x.device)))
     return vals, gx, gy
 
 
@@ -234,14 +252,19 @@ class GradAcc:
     Sums into it are bitwise independent of tile order, of how the Gram rows
     are split across calls, and of how many GPUs contributed (gram_dist sums
     the limbs of all ranks as integers).  `limbs` and `meta` are int64 views
-    for collectives: limbs add (SUM), meta combines with MAX."""
+    for collectives: limbs add (SUM), meta combines with MAX.  With a path
+    transform the limbs hold the transformed-path gradient; finalize() maps it
+    back to the raw paths."""
 
     META = 8
 
-    def __init__(self, n, L, d, device):
+    def __init__(self, n, L, d, device, transform=None):
         lib = _lib.load()
         self.shape = (int(n), int(L), int(d))
-        nbytes = lib.sk_grad_acc_bytes(n, L, d)
+        self.tf = transform_code(transform)
+        Le, de = effective_shape(int(L), int(d), self.tf)
+        self.tshape = (int(n), Le, de)
+        nbytes = lib.sk_grad_acc_bytes(*self.tshape)
         self.blob = torch.empty(nbytes // 8, dtype=torch.int64, device=device)
         self.meta = self.blob[: self.META]
         self.limbs = self.blob[self.META:]
@@ -252,12 +275,12 @@ class GradAcc:
         lib = _lib.load()
         cot = _cotangent(cot, (n1, n2), self.blob)
         with torch.cuda.device(self.blob.device):
-            _lib.check(lib.sk_grad_acc_init(_ptr(self.blob), *self.shape, _ptr(cot), n1, n2,
+            _lib.check(lib.sk_grad_acc_init(_ptr(self.blob), *self.tshape, _ptr(cot), n1, n2,
                                             int(bool(symmetric)), _stream(self.blob.device)))
         return self
 
     def finalize(self, out=None, accumulate=False):
-        """fp64 gradient (n, L, d): out = value, or out += value."""
+        """fp64 gradient (n, L, d) of the raw paths: out = value, or out += value."""
         lib = _lib.load()
         if out is None:
             out = torch.empty(self.shape, dtype=torch.float64, device=self.blob.device)
@@ -266,9 +289,17 @@ class GradAcc:
                 or not out.is_contiguous()):
             raise InvalidArgument(f"out must be a contiguous float64 tensor of shape {self.shape}")
         _same_device(out, self.blob, "out")
-        with torch.cuda.device(self.blob.device):
-            _lib.check(lib.sk_grad_acc_finalize(_ptr(self.blob), *self.shape, _ptr(out),
-                                                int(bool(accumulate)), _stream(self.blob.device)))
+        dev = self.blob.device
+        with torch.cuda.device(dev):
+            if self.tf == 0:
+                _lib.check(lib.sk_grad_acc_finalize(_ptr(self.blob), *self.tshape, _ptr(out),
+                                                    int(bool(accumulate)), _stream(dev)))
+            else:
+                gt = torch.empty(self.tshape, dtype=torch.float64, device=dev)
+                _lib.check(lib.sk_grad_acc_finalize(_ptr(self.blob), *self.tshape, _ptr(gt), 0,
+                                                    _stream(dev)))
+                _lib.check(lib.sk_transform_adjoint(_ptr(gt), *self.shape, self.tf, _ptr(out),
+                                                    int(bool(accumulate)), _stream(dev)))
         return out
 
 
@@ -291,40 +322,36 @@ def _rows(rows, n1):
     return r0, r1
 
 
-def _check_acc(acc, n, L, d, x, name):
-    if not isinstance(acc, GradAcc) or acc.shape != (n, L, d):
-        raise InvalidArgument(f"{name} must be a GradAcc of shape {(n, L, d)}")
+def _check_acc(acc, n, L, d, tf, x, name):
+    if not isinstance(acc, GradAcc) or acc.shape != (n, L, d) or acc.tf != tf:
+        raise InvalidArgument(f"{name} must be a GradAcc of shape {(n, L, d)} and the call's "
+                              f"transform")
     _same_device(acc.blob, x, name)
 
 
-def backward_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, grad_x=None, grad_y=None,
-                  acc_x=None, acc_y=None):
-    """dF/dx (and dF/dy) of F = sum cot[a, b] G[a, b] over the pairs with a in
-    rows; cot is the full (n1, n2) cotangent.
-
-    Default: grad_x (grad_y) += this call's gradient (new zero buffers if None);
-    the sum inside the call is exact, so one call is bitwise reproducible.
-    With acc_x (acc_y) GradAcc accumulators, the call adds into them instead and
-    returns them (finalize() at the end): any split of the rows into calls then
-    gives bitwise the same gradient."""
+def _gram_backward(x, y, lam1, lam2, kind, sigma, cot, rows, out, grad_x, grad_y, acc_x, acc_y,
+                   transform):
+    """Shared body of backward_gram (out None) and value_and_grad_gram."""
     lib = _lib.load()
+    tf = transform_code(transform)
     x, yy, sym, n1, n2, L1, L2, d = _gram_args(x, y)
     r0, r1 = _rows(rows, n1)
     cot = _cotangent(cot, (n1, n2), x)
+    dev = x.device
     if acc_x is not None:
-        _check_acc(acc_x, n1, L1, d, x, "acc_x")
+        _check_acc(acc_x, n1, L1, d, tf, x, "acc_x")
         if not sym:
-            _check_acc(acc_y, n2, L2, d, x, "acc_y")
+            _check_acc(acc_y, n2, L2, d, tf, x, "acc_y")
         if n1 == 0 or n2 == 0 or r1 <= r0:
             return acc_x, acc_y
-        with torch.cuda.device(x.device):
-            nb = lib.sk_backward_gram_acc_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind,
-                                                          int(sym))
-            ws = _workspace(nb, x.device)
-            _lib.check(lib.sk_backward_gram_acc(
+        with torch.cuda.device(dev):
+            nb = lib.sk_backward_gram_acc_tf_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind,
+                                                             int(sym), tf)
+            ws = _workspace(nb, dev)
+            _lib.check(lib.sk_backward_gram_acc_tf(
                 _ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d, lam1, lam2, kind, sigma,
-                r0, r1, _ptr(cot), None, _ptr(acc_x.blob), None if sym else _ptr(acc_y.blob),
-                _ptr(ws), ws.numel(), _stream(x.device)))
+                tf, r0, r1, _ptr(cot), _ptr(out), _ptr(acc_x.blob),
+                None if sym else _ptr(acc_y.blob), _ptr(ws), ws.numel(), _stream(dev)))
         return acc_x, acc_y
     if grad_x is None:
         grad_x = torch.zeros_like(x)
@@ -335,63 +362,49 @@ def backward_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, grad_x=None, gr
         _grad_buffer(grad_y, yy, "grad_y")
     if n1 == 0 or n2 == 0 or r1 <= r0:
         return grad_x, grad_y
-    with torch.cuda.device(x.device):
-        nb = lib.sk_backward_gram_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind, int(sym))
-        ws = _workspace(nb, x.device)
-        _lib.check(lib.sk_backward_gram(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
-                                        lam1, lam2, kind, sigma, r0, r1, _ptr(cot), _ptr(grad_x),
-                                        _ptr(grad_y) if not sym else None, _ptr(ws), ws.numel(),
-                                        _stream(x.device)))
+    with torch.cuda.device(dev):
+        nb = lib.sk_backward_gram_tf_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind,
+                                                     int(sym), tf)
+        ws = _workspace(nb, dev)
+        _lib.check(lib.sk_backward_gram_tf(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
+                                           lam1, lam2, kind, sigma, tf, r0, r1, _ptr(cot),
+                                           _ptr(out), _ptr(grad_x),
+                                           _ptr(grad_y) if not sym else None, _ptr(ws),
+                                           ws.numel(), _stream(dev)))
     return grad_x, grad_y
 
 
+def backward_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, grad_x=None, grad_y=None,
+                  acc_x=None, acc_y=None, transform=None):
+    """dF/dx (and dF/dy) of F = sum cot[a, b] G[a, b] over the pairs with a in
+    rows; cot is the full (n1, n2) cotangent.
+
+    Default: grad_x (grad_y) += this call's gradient (new zero buffers if None);
+    the sum inside the call is exact, so one call is bitwise reproducible.
+    With acc_x (acc_y) GradAcc accumulators, the call adds into them instead and
+    returns them (finalize() at the end): any tile-aligned split of the rows into
+    calls then gives bitwise the same gradient."""
+    return _gram_backward(x, y, lam1, lam2, kind, sigma, cot, rows, None, grad_x, grad_y, acc_x,
+                          acc_y, transform)
+
+
 def value_and_grad_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, out=None, grad_x=None,
-                        grad_y=None, acc_x=None, acc_y=None):
+                        grad_y=None, acc_x=None, acc_y=None, transform=None):
     """One fused pass: G rows [r0, r1) (as forward_gram) and dF/dx (dF/dy) of
     F = sum cot[a, b] G[a, b] (as backward_gram, including its accumulator
-    mode), from the backward's own forward solve (sk_value_and_grad_gram)."""
-    lib = _lib.load()
-    x, yy, sym, n1, n2, L1, L2, d = _gram_args(x, y)
+    mode), from the backward's own forward solve."""
+    xx = _paths(x, "x")
+    n1 = xx.shape[0]
+    n2 = n1 if y is None else y.shape[0]
     r0, r1 = _rows(rows, n1)
-    cot = _cotangent(cot, (n1, n2), x)
     if out is None:
-        out = torch.empty((r1 - r0, n2), dtype=torch.float64, device=x.device)
+        out = torch.empty((r1 - r0, n2), dtype=torch.float64, device=xx.device)
     if tuple(out.shape) != (r1 - r0, n2) or out.dtype != torch.float64 or not out.is_contiguous():
         raise InvalidArgument(f"out must be a contiguous float64 ({r1 - r0}, {n2}) tensor")
-    _same_device(out, x, "out")
-    if acc_x is not None:
-        _check_acc(acc_x, n1, L1, d, x, "acc_x")
-        if not sym:
-            _check_acc(acc_y, n2, L2, d, x, "acc_y")
-        if n1 == 0 or n2 == 0 or r1 <= r0:
-            return out, acc_x, acc_y
-        with torch.cuda.device(x.device):
-            nb = lib.sk_backward_gram_acc_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind,
-                                                          int(sym))
-            ws = _workspace(nb, x.device)
-            _lib.check(lib.sk_backward_gram_acc(
-                _ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d, lam1, lam2, kind, sigma,
-                r0, r1, _ptr(cot), _ptr(out), _ptr(acc_x.blob),
-                None if sym else _ptr(acc_y.blob), _ptr(ws), ws.numel(), _stream(x.device)))
-        return out, acc_x, acc_y
-    if grad_x is None:
-        grad_x = torch.zeros_like(x)
-    if grad_y is None and not sym:
-        grad_y = torch.zeros_like(yy)
-    _grad_buffer(grad_x, x, "grad_x")
-    if not sym:
-        _grad_buffer(grad_y, yy, "grad_y")
-    if n1 == 0 or n2 == 0 or r1 <= r0:
-        return out, grad_x, grad_y
-    with torch.cuda.device(x.device):
-        nb = lib.sk_backward_gram_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind, int(sym))
-        ws = _workspace(nb, x.device)
-        _lib.check(lib.sk_value_and_grad_gram(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2,
-                                              d, lam1, lam2, kind, sigma, r0, r1, _ptr(cot),
-                                              _ptr(out), _ptr(grad_x),
-                                              _ptr(grad_y) if not sym else None, _ptr(ws),
-                                              ws.numel(), _stream(x.device)))
-    return out, grad_x, grad_y
+    _same_device(out, xx, "out")
+    g1, g2 = _gram_backward(xx, y, lam1, lam2, kind, sigma, cot, rows, out, grad_x, grad_y, acc_x,
+                            acc_y, transform)
+    return out, g1, g2
 
 
 def mirror_upper(G: torch.Tensor) -> torch.Tensor:

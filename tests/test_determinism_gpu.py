@@ -142,3 +142,18 @@ def test_nonfinite_contributions_fail_loudly(mods):
     assert not np.isfinite(G).all()
     gx, _ = ops.backward_gram(cu(X), None, 0, 0, 0, 1.0, cu(C))
     assert np.isnan(gx.cpu().numpy()).all()
+
+
+@pytest.mark.parametrize("n,L,d,lam", [(19, 45, 8, 0), (7, 30, 16, 0), (9, 25, 5, 1), (6, 20, 40, 0)])
+def test_uninitialised_workspace_is_never_read(mods, n, L, d, lam):
+    """Workspaces come from torch's caching allocator uninitialised: poison
+    the cache with NaN first; the gradients must be unaffected (bitwise)."""
+    ops, _, orc = mods
+    X, _, C = _inputs(n, None, L, d, n + L)
+    ref, _ = ops.backward_gram(cu(X), None, lam, lam, 0, 1.0, cu(C))
+    for _ in range(3):
+        junk = torch.full((64 << 20,), float("nan"), dtype=torch.float64, device="cuda")
+        del junk
+        got, _ = ops.backward_gram(cu(X), None, lam, lam, 0, 1.0, cu(C))
+        np.testing.assert_array_equal(got.cpu().numpy(), ref.cpu().numpy())
+    assert rel_err(ref.cpu().numpy(), orc.gram_backward(X, None, C, lam, lam)) < 1e-10
