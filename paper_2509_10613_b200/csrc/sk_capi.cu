@@ -90,7 +90,8 @@ static int occupancy(const void* fn, int threads, int smem) {
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
   }
-  if (smem > 48 * 1024 &&
+  // (always: static shared memory counts against the 48 KB default too)
+  if (smem > 0 &&
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     (void)cudaGetLastError();
   int occ = 0;
@@ -421,14 +422,42 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
   // are too few to fill the GPU.
   if (gram) {
     s.G = (npairs * 4 >= target_lanes || lanes_per_pair <= 8) ? 4 : 32;
-  } else if (npairs * 32 >= target_lanes || lanes_per_pair <= 64 || kind != LINEAR || s.DP > 8) {
+  } else if (npairs * 32 >= target_lanes || lanes_per_pair <= 64 || kind == DELTA || s.DP > 8) {
+    // (the XW column ring spans 512 lanes of records: DP > 8 would not fit)
     s.G = 32;
   } else {
+    // few long pairs (BASELINE configs 2, 4): one pair per CTA of W warps, a
+    // single wavefront over 32W lanes (cross-warp hops through shared memory)
+    static const int wmax = [] {
+      const char* e = std::getenv("SK_FWD_XW_WMAX");  // tuning knob
+      const int v = (e && e[0]) ? std::atoi(e) : 16;
+      return v >= 2 && v <= 16 ? v : 16;
+    }();
+    // widen until the GPU is full or one strip covers the pair (measured at
+    // BASELINE config 2: one 8-warp strip 0.60 ms vs two 4-warp strips 0.70 ms)
     int W = 2;
-    while (W < 16 && npairs * 32 * W < target_lanes && 32 * W * 2 <= lanes_per_pair) W *= 2;
+    while (W < wmax && npairs * 32 * W < target_lanes && 32 * W < lanes_per_pair) W *= 2;
+    static const int wforce = [] {
+      const char* e = std::getenv("SK_FWD_XW_W");  // tuning knob: force the CTA width
+      const int v = (e && e[0]) ? std::atoi(e) : 0;
+      return (v == 2 || v == 4 || v == 8 || v == 16) ? v : 0;
+    }();
+    if (wforce) W = wforce;
     s.XW = true;
     s.W = W;
     s.G = 32 * W;
+  }
+  // short batch paths: the fewest rows per lane that still cover the pair
+  // with one warp (all lanes busy, short dependent chain per step)
+  bool short_r = false;
+  if (!gram && !s.XW && s.G == 32 && kind != DELTA && !f32 && nch == 1 && M1 < 32 * s.R) {
+    int r = 1;
+    while (32 * r < M1) r *= 2;
+    if (r < s.R) {
+      s.R = r;
+      s.FR = std::min(s.FR, r);
+      short_r = true;
+    }
   }
   // Gram tiles of the linear kernel at dyadic order 0: increment products on
   // the FP64 tensor cores (sk_mma_fwd.cuh).  SK_NO_MMA=1 keeps the r01 kernels.
@@ -455,6 +484,7 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
   }
   int smem = 0;
   FwdFn fn = f32              ? (kind == LINEAR ? select_fwd_linear_f32(s, smem) : nullptr)
+             : short_r        ? select_fwd_short(s, smem)
              : kind == LINEAR ? select_fwd_linear(s, smem)
              : kind == RBF    ? select_fwd_rbf(s, smem)
                               : select_fwd_delta(s, smem);
@@ -476,6 +506,13 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
   pl.slots = s.XW ? pl.blocks : pl.blocks * warps * pl.P;
   pl.hand_stride = (int64_t)align_up((size_t)((M2c << lamC) + 1), 4);
   (void)nch;
+  if (std::getenv("SK_DEBUG_PLAN")) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, (const void*)fn);
+    std::fprintf(stderr, "plan_forward: XW %d W %d G %d R %d DP %d threads %d smem %d occ %d blocks %lld "
+                 "static %zu maxdyn %d regs %d\n", (int)s.XW, s.W, s.G, s.R, s.DP, pl.threads, smem, occ,
+                 (long long)pl.blocks, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, fa.numRegs);
+  }
   return SK_OK;
 }
 

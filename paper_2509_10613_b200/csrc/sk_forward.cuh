@@ -37,6 +37,14 @@ struct FwdRec {
   static constexpr int REC = (RAW + VEC - 1) & ~(VEC - 1);  // 16-byte aligned records
 };
 
+// Ring slots (a power of two) for `lanes` lanes in flight: every lane's step
+// plus the PF prefetched steps, S column records each.
+__host__ __device__ constexpr int ring_slots(int lanes, int S, int PF) {
+  return ((lanes + PF + 1) * S) <= 32 ? 32 : ((lanes + PF + 1) * S) <= 64 ? 64
+         : ((lanes + PF + 1) * S) <= 128 ? 128 : ((lanes + PF + 1) * S) <= 256 ? 256
+         : ((lanes + PF + 1) * S) <= 512 ? 512 : ((lanes + PF + 1) * S) <= 1024 ? 1024 : 2048;
+}
+
 template <bool XW, int G, int S>
 struct FwdRing {
   static constexpr int PF = 2;  // steps in flight
@@ -49,8 +57,8 @@ struct FwdRing {
 // Issue the ring records of columns [col0, col0 + S): column data of coarse
 // column jc(col) and the handoff values of every group (strip > 0).  One warp
 // issues; a single commit group per step.
-template <int KIND, int DP, int F, int P, int S, int SLOTS, typename T = double>
-__device__ __forceinline__ void fwd_issue(T* ring, const Problem& pb, int64_t pc,
+template <int KIND, int DP, int F, int P, int S, typename T = double>
+__device__ __forceinline__ void fwd_issue(T* ring, int smask, const Problem& pb, int64_t pc,
                                           const T* hrow0, int64_t hand_stride, int col0,
                                           int NC, int strip, int lane) {
   using Rc = FwdRec<KIND, DP, F, P, T>;
@@ -64,7 +72,7 @@ __device__ __forceinline__ void fwd_issue(T* ring, const Problem& pb, int64_t pc
     const int jc = valid ? ((col * F) >> pb.lam2) : 0;
     const int node = (KIND == RBF) ? jc + 1 : jc;
     const T* src = cdata + pc * pb.C.path_stride + (int64_t)node * pb.dpad + VEC * c;
-    cp_async16(ring + ((col & (SLOTS - 1)) * Rc::REC) + VEC * c, src, valid);
+    cp_async16(ring + ((col & smask) * Rc::REC) + VEC * c, src, valid);
   }
   if (strip > 0) {
     for (int e = lane; e < S * P * F; e += 32) {
@@ -73,7 +81,7 @@ __device__ __forceinline__ void fwd_issue(T* ring, const Problem& pb, int64_t pc
       const int col = col0 + s;
       const bool valid = (col >= 0) && (col < NC);
       const T* src = hrow0 + g * hand_stride + (valid ? col * F + f + 1 : 0);
-      cp_async_elem<T>(ring + ((col & (SLOTS - 1)) * Rc::REC) + Rc::CD + q, src, valid);
+      cp_async_elem<T>(ring + ((col & smask) * Rc::REC) + Rc::CD + q, src, valid);
     }
   }
   cp_async_commit();
@@ -102,7 +110,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
   using Rg = FwdRing<XW, G, S>;
   using Cf = CoefOf<T>;
   constexpr int REC = Rec::REC;
-  constexpr int SLOTS = Rg::SLOTS;
+  constexpr int SLOTS = Rg::SLOTS;  // per warp (non-XW); XW: sized by the CTA's lanes
   constexpr int PF = Rg::PF;
   static_assert(sizeof(T) == 8 || KIND == LINEAR, "fp32 kernels: linear static kernel only");
   extern __shared__ double smem_fwd_raw[];
@@ -117,6 +125,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
   const int g = XW ? 0 : lane / G;
   const int u = XW ? (int)threadIdx.x : lane % G;
   T* ring = XW ? smem_fwd : smem_fwd + (size_t)warp * SLOTS * REC;
+  const int smask = (XW ? ring_slots((int)blockDim.x, S, PF) : SLOTS) - 1;
 
   const int M1 = pb.M1c << pb.lam1;
   const int M2 = pb.M2c << pb.lam2;
@@ -169,14 +178,14 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
       }
       if (issuer) {
         for (int q = 0; q < PF; ++q)
-          fwd_issue<KIND, DP, F, P, S, SLOTS, T>(ring, pb, pc, hrow0, hand_stride, q * S, NC,
-                                                 strip, lane);
+          fwd_issue<KIND, DP, F, P, S, T>(ring, smask, pb, pc, hrow0, hand_stride, q * S, NC,
+                                          strip, lane);
       }
 
       // coefficients of the S columns of step js (reads the ring; no recurrence)
       auto col_coefs = [&](int col, Cf (&cfo)[RC]) {
         {
-          const T* rec = ring + (col & (SLOTS - 1)) * REC;
+          const T* rec = ring + (col & smask) * REC;
           T p[RC];
           if constexpr (KIND == LINEAR) {
             T dy[DP];
@@ -268,7 +277,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
       for (int q = 0; q < SF; ++q) bot[q] = T(1);
       // wide paths (DP >= 16) pipeline the next step's coefficients behind the
       // recurrence; narrow ones keep the registers for S columns per step
-      constexpr bool PIPE = DP >= 16;
+      constexpr bool PIPE = DP >= 16 || (!XW && G == 32 && R <= 2);  // (short paths: latency)
       Cf cf[S][RC];
       if constexpr (PIPE) {
         if (issuer) cp_async_wait<PF - 1>();  // step 0 landed
@@ -279,8 +288,8 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
       const int nsteps = NSTEP + Grt - 1;
       for (int tau = 0; tau < nsteps; ++tau) {
         if (issuer) {
-          fwd_issue<KIND, DP, F, P, S, SLOTS, T>(ring, pb, pc, hrow0, hand_stride, (tau + PF) * S,
-                                                 NC, strip, lane);
+          fwd_issue<KIND, DP, F, P, S, T>(ring, smask, pb, pc, hrow0, hand_stride,
+                                          (tau + PF) * S, NC, strip, lane);
           if constexpr (PIPE) cp_async_wait<PF - 1>();  // steps <= tau + 1 landed
           else cp_async_wait<PF>();                     // step tau landed
         }
@@ -308,7 +317,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
           if (u == 0) {
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-              const T* rec = ring + ((col0 + s) & (SLOTS - 1)) * REC + Rec::CD + g * F;
+              const T* rec = ring + ((col0 + s) & smask) * REC + Rec::CD + g * F;
 #pragma unroll
               for (int f = 0; f < F; ++f) tv[s * F + f] = (strip == 0) ? T(1) : rec[f];
             }
@@ -372,7 +381,8 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
 template <int KIND, int DP, int F, int G, bool XW, int S, typename T = double>
 constexpr int fwd_smem_bytes(int warps) {
   using Rec = FwdRec<KIND, DP, F, XW ? 1 : 32 / G, T>;
-  return (XW ? 1 : warps) * FwdRing<XW, G, S>::SLOTS * Rec::REC * (int)sizeof(T);
+  return XW ? ring_slots(32 * warps, S, FwdRing<XW, G, S>::PF) * Rec::REC * (int)sizeof(T)
+            : warps * FwdRing<XW, G, S>::SLOTS * Rec::REC * (int)sizeof(T);
 }
 
 }  // namespace sk

@@ -38,6 +38,7 @@ BwdFn select_bwd_mma(int DP, int WPC, int& smem_doubles_per_warp);
 // Per-kind instance tables (one translation unit each, compiled in parallel).
 FwdFn select_fwd_linear(const FwdShape& s, int& smem);
 FwdFn select_fwd_linear_f32(const FwdShape& s, int& smem);  // FP32 arithmetic
+FwdFn select_fwd_short(const FwdShape& s, int& smem);       // short paths, fp64
 FwdFn select_fwd_rbf(const FwdShape& s, int& smem);
 FwdFn select_fwd_delta(const FwdShape& s, int& smem);
 FwdFn select_fwd_mma(int DP, int& smem_per_warp);
