@@ -261,6 +261,29 @@ int sk_backward_gram_acc_tf(const double *x, const double *y, int64_t n1, int64_
                             int64_t row_end, const double *cot, double *values, void *acc_x,
                             void *acc_y, void *workspace, size_t workspace_bytes, void *stream);
 
+/* ---- truncated signatures ------------------------------------------------
+ * Replaces sigcore's signature (signature.py:104-121) and signature_backward
+ * (signature_grad.py:20-53).  out (B, sk_signature_length(d', depth)): levels
+ * 1..depth back to back, row-major multi-indices (tensors.py layout); d' is
+ * the transformed dimension (d, d+1 time-augmented, 2d lead-lag).  times:
+ * optional (L,) time grid for the time augmentation (NULL = linspace(0, 1, L),
+ * reference PathBatch.times).  The forward issues the reference's Horner
+ * operations in the reference's order without FMA contraction (bitwise the
+ * reference's values); the backward is the reference's time-reversed
+ * deconstruction with deterministic, chunked reductions.  Supported
+ * (d', depth): d' <= 2 & depth <= 16, 4 & 10, 8 & 8, 16 & 6, 32 & 4. */
+int64_t sk_signature_length(int64_t d, int depth);
+size_t sk_signature_workspace_bytes(int64_t B, int64_t L, int64_t d, int depth, int transform);
+int sk_signature(const double *x, const double *times, int64_t B, int64_t L, int64_t d,
+                 int depth, int transform, double *out, void *workspace, size_t workspace_bytes,
+                 void *stream);
+size_t sk_signature_backward_workspace_bytes(int64_t B, int64_t L, int64_t d, int depth,
+                                             int transform);
+/* grad (B, L, d) = dF/dx for cot = dF/d(signature) (B, length); raw path shape */
+int sk_signature_backward(const double *x, const double *times, int64_t B, int64_t L, int64_t d,
+                          int depth, int transform, const double *cot, double *grad,
+                          void *workspace, size_t workspace_bytes, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,6 +53,8 @@ def lib():
         L.sko_increment_gram.argtypes = [dp, dp, i64, i64, i64, dp]
         L.sko_rbf_increment_gram.argtypes = [dp, dp, i64, i64, i64, cd, dp]
         L.sko_max_threads.restype = ci
+        L.sko_signature.argtypes = [dp, i64, i64, i64, ci, dp, ci]
+        L.sko_signature_backward.argtypes = [dp, i64, i64, i64, ci, dp, dp, ci]
         _lib = L
     return _lib
 
@@ -166,3 +168,72 @@ def gram_backward(x, y=None, cot=None, lam1=0, lam2=0, static_kernel=None, threa
     if rc:
         raise MemoryError("oracle allocation failed")
     return gx if symmetric else (gx, gy)
+
+
+# ------------------------------------------------------------ truncated signatures
+def _linspace_times(L):
+    """transforms.py:30-34 default_times (numpy.linspace)."""
+    return np.zeros(1) if L == 1 else np.linspace(0.0, 1.0, L)
+
+
+def fused_increments(x, kind=None, times=None):
+    """transforms.py:91-120: increments of the transformed path, (B, M', d')."""
+    x = _f64(x)
+    B, L, d = x.shape
+    dx = np.diff(x, axis=1)
+    if kind is None:
+        return np.ascontiguousarray(dx)
+    if kind == "time_augment":
+        t = _linspace_times(L) if times is None else np.asarray(times, dtype=np.float64)
+        out = np.empty((B, L - 1, d + 1))
+        out[:, :, :d] = dx
+        out[:, :, d] = np.diff(t)
+        return out
+    out = np.zeros((B, 2 * L - 2, 2 * d))
+    out[:, 0::2, :d] = dx
+    out[:, 1::2, d:] = dx
+    return out
+
+
+def transform_adjoint(g, kind):
+    """transforms.py:69-90."""
+    if kind is None:
+        return g
+    if kind == "time_augment":
+        return g[:, :, :-1].copy()
+    d = g.shape[2] // 2
+    lead, lag = g[:, :, :d], g[:, :, d:]
+    out = lead[:, 0::2] + lag[:, 0::2]
+    out[:, :-1] += lag[:, 1::2]
+    out[:, 1:] += lead[:, 1::2]
+    return out
+
+
+def signature_length(d, depth):
+    return sum(d ** k for k in range(1, depth + 1))
+
+
+def signature(x, depth, kind=None, times=None, threads=0):
+    """signature.py:104-121 (Horner; the C restatement of _kernels.py:115-172)."""
+    inc = fused_increments(x, kind, times)
+    B, M, d = inc.shape
+    out = np.empty((B, signature_length(d, depth)))
+    if lib().sko_signature(_p(inc), B, M, d, depth, _p(out), threads):
+        raise MemoryError("oracle allocation failed")
+    return out
+
+
+def signature_backward(x, depth, cot, kind=None, times=None, threads=0):
+    """signature_grad.py:20-53: the C restatement of sig_backward_path
+    (_kernels.py:182-266), then the telescoping and the transform adjoint."""
+    x = _f64(x)
+    inc = fused_increments(x, kind, times)
+    B, M, d = inc.shape
+    cot = _f64(cot).reshape(B, -1)
+    g = np.empty((B, M, d))
+    if lib().sko_signature_backward(_p(inc), B, M, d, depth, _p(cot), _p(g), threads):
+        raise MemoryError("oracle allocation failed")
+    grad_eff = np.zeros((B, M + 1, d))
+    grad_eff[:, :-1] -= g
+    grad_eff[:, 1:] += g
+    return transform_adjoint(grad_eff, kind)

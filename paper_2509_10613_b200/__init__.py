@@ -4,6 +4,7 @@ Public API (pySigLib style, torch autograd):
     sig_kernel, sig_kernel_gram, LinearKernel, RBFKernel
     sig_kernel_gram_value_and_grad (fused G + dF/dX, no autograd)
     sig_mmd (autograd), sig_mmd_value_and_grad (fused)
+    signature (truncated signatures, autograd; transforms inside the kernel)
 Reference-compatible numpy facade (sigcore names): paper_2509_10613_b200.sigcore_compat
 Multi-GPU Gram sharding: paper_2509_10613_b200.gram_dist
 """
@@ -11,9 +12,10 @@ Multi-GPU Gram sharding: paper_2509_10613_b200.gram_dist
 from .api import (LinearKernel, RBFKernel, sig_kernel, sig_kernel_gram,
                   sig_kernel_gram_value_and_grad, sig_mmd, sig_mmd_value_and_grad)
 from .errors import InvalidArgument, InvalidState, NativeUnavailable
+from .signature import signature
 
 __version__ = "0.1.0"
 
-__all__ = ["sig_kernel", "sig_kernel_gram", "sig_kernel_gram_value_and_grad", "sig_mmd",
+__all__ = ["signature", "sig_kernel", "sig_kernel_gram", "sig_kernel_gram_value_and_grad", "sig_mmd",
            "sig_mmd_value_and_grad", "LinearKernel", "RBFKernel", "InvalidArgument",
            "InvalidState", "NativeUnavailable", "__version__"]

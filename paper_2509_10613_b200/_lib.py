@@ -73,6 +73,12 @@ SIGNATURES = {
                                                  _ci, _ci], _sz),
     "sk_backward_gram_acc_tf": ([_dp, _dp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd, _ci,
                                  _i64, _i64, _dp, _dp, _vp, _vp, _vp, _sz, _vp], _ci),
+    "sk_signature_length": ([_i64, _ci], _i64),
+    "sk_signature_workspace_bytes": ([_i64, _i64, _i64, _ci, _ci], _sz),
+    "sk_signature": ([_dp, _dp, _i64, _i64, _i64, _ci, _ci, _dp, _vp, _sz, _vp], _ci),
+    "sk_signature_backward_workspace_bytes": ([_i64, _i64, _i64, _ci, _ci], _sz),
+    "sk_signature_backward": ([_dp, _dp, _i64, _i64, _i64, _ci, _ci, _dp, _dp, _vp, _sz, _vp],
+                              _ci),
     "sk_grad_acc_bytes": ([_i64, _i64, _i64], _sz),
     "sk_grad_acc_init": ([_vp, _i64, _i64, _i64, _dp, _i64, _i64, _ci, _vp], _ci),
     "sk_grad_acc_finalize": ([_vp, _i64, _i64, _i64, _dp, _ci, _vp], _ci),

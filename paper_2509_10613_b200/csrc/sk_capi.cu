@@ -30,6 +30,8 @@ static int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
+// error reporting for the other translation units (sk_signature.cu)
+int set_error(int code, const char* msg) { return fail(code, msg); }
 
 #define SK_CUDA(call)                                                              \
   do {                                                                             \

@@ -27,9 +27,17 @@ import torch
 from . import ops
 from .errors import InvalidArgument, InvalidState
 
+from .signature import (PathBatch, SigOptions, TensorShape, sig_tensor_shape,  # noqa: E402
+                        tensor_shape)
+from .signature import signature_backward_np as signature_backward  # noqa: E402
+from .signature import signature_np as signature  # noqa: E402
+
 __all__ = ["KernelConfig", "SolveResult", "InvalidArgument", "InvalidState", "increment_gram",
            "fine_cells", "solve_workspace_elements", "solve_goursat", "kernel_batch",
-           "kernel_gram", "kernel_backward", "kernel_batch_backward"]
+           "kernel_gram", "kernel_backward", "kernel_batch_backward",
+           # truncated signatures (reference signature.py, signature_grad.py, tensors.py)
+           "signature", "signature_backward", "SigOptions", "PathBatch", "TensorShape",
+           "tensor_shape", "sig_tensor_shape"]
 
 
 @dataclass(frozen=True)

@@ -150,3 +150,19 @@ def test_gram_backward_composition(oracle):
             wx[a] += ga[0]
             wy[b] += gb[0]
     assert rel_err(gx2, wx) < 1e-12 and rel_err(gy2, wy) < 1e-12
+
+
+def test_signature_oracle_pinned_to_reference(oracle):
+    """The C restatement of the reference's signature kernels against vectors
+    the reference itself produced (tests/golden/make_golden_signature.py):
+    forward and backward bitwise (same operations in the same order)."""
+    g = golden("signature")
+    kinds = {0: None, 1: "time_augment", 2: "lead_lag"}
+    for i in range(int(g["n"])):
+        depth, tf, custom = (int(v) for v in g[f"s{i}_meta"])
+        times = g[f"s{i}_times"] if custom else None
+        x = g[f"s{i}_x"]
+        sig = oracle.signature(x, depth, kinds[tf], times)
+        np.testing.assert_array_equal(sig, g[f"s{i}_sig"])
+        grad = oracle.signature_backward(x, depth, g[f"s{i}_cot"], kinds[tf], times)
+        np.testing.assert_array_equal(grad, g[f"s{i}_grad"])
