@@ -12,7 +12,7 @@ Multi-GPU Gram sharding: paper_2509_10613_b200.gram_dist
 from .api import (LinearKernel, RBFKernel, sig_kernel, sig_kernel_gram,
                   sig_kernel_gram_value_and_grad, sig_mmd, sig_mmd_value_and_grad)
 from .errors import InvalidArgument, InvalidState, NativeUnavailable
-from .signature import signature
+from .signatures import signature
 
 __version__ = "0.1.0"
 

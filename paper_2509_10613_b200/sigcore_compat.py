@@ -27,10 +27,10 @@ import torch
 from . import ops
 from .errors import InvalidArgument, InvalidState
 
-from .signature import (PathBatch, SigOptions, TensorShape, sig_tensor_shape,  # noqa: E402
+from .signatures import (PathBatch, SigOptions, TensorShape, sig_tensor_shape,  # noqa: E402
                         tensor_shape)
-from .signature import signature_backward_np as signature_backward  # noqa: E402
-from .signature import signature_np as signature  # noqa: E402
+from .signatures import signature_backward_np as signature_backward  # noqa: E402
+from .signatures import signature_np as signature  # noqa: E402
 
 __all__ = ["KernelConfig", "SolveResult", "InvalidArgument", "InvalidState", "increment_gram",
            "fine_cells", "solve_workspace_elements", "solve_goursat", "kernel_batch",
