@@ -56,37 +56,47 @@ __device__ __forceinline__ void grad_add(double* g, const FixAcc& f, int64_t e, 
 }
 
 constexpr int pow2_at_least(int n) {
-  return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : 256;
+  return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : n <= 512 ? 512
+         : n <= 1024 ? 1024 : 2048;
 }
 
-// Per-warp shared-memory layout (doubles).
-template <int DP, int R, int RC, int F, int CB, int S>
+// Shared-memory layout (doubles) of one lane group: a warp (NL = 32) or, for
+// cross-warp pairs (NW > 1), the whole CTA (NL = 32 NW lanes).
+template <int DP, int R, int RC, int F, int CB, int S, int NL = 32>
 struct BwdSmem {
   static constexpr int SF = S * F;
   // column ring: power of two when cheap, else the exact need (modulo indexing)
-  static constexpr int NEED = (2 * CB + 32) * S;
+  static constexpr int NEED = (2 * CB + NL) * S;
   static constexpr int SLOTS = (DP >= 16) ? ((NEED + 15) / 16) * 16 : pow2_at_least(NEED);
   static constexpr int REC = ((DP + F) + 1) & ~1;    // column data | handoff/adjoint (F)
-  static constexpr int NK = CB * SF * R;             // recomputed k values (x32 lanes)
-  static constexpr int NP = CB * S * RC;             // coarse p (then D) values (x32 lanes)
-  static constexpr int NTR = CB * SF + 1;            // top row of the block (x32 lanes)
-  static constexpr int TS = (CB + 1) * SF * 32;      // top-row checkpoints of the next block
+  static constexpr int NK = CB * SF * R;             // recomputed k values (x NL lanes)
+  static constexpr int NP = CB * S * RC;             // coarse p (then D) values (x NL lanes)
+  static constexpr int NTR = CB * SF + 1;            // top row of the block (x NL lanes)
+  static constexpr int TS = (CB + 1) * SF * NL;      // top-row checkpoints of the next block
   static constexpr int T0 = ((CB * SF + 1) + 1) & ~1; // lane 0's top row (strip above)
-  static constexpr int LS = R * 32;                  // left-column checkpoint
-  static constexpr int GS = CB * S * DP;             // lane 31's incoming column gradients (x2)
-  static constexpr int GROWS = (32 + CB) * S;        // gy accumulator rows (one per column)
+  static constexpr int LS = R * NL;                  // left-column checkpoint
+  static constexpr int GS = CB * S * DP;             // last lane's incoming column gradients (x2)
+  static constexpr int GROWS = (NL + CB) * S;        // gy accumulator rows (one per column)
   static constexpr int GSTR = DP + 2;                // row stride: conflict-free 16-B accesses
-  static constexpr int PS = CB * S * RC * 32;        // coarse p checkpoints of the next block
-  static constexpr int TOTAL =
-      SLOTS * REC + (NK + NP + NTR) * 32 + TS + T0 + LS + 2 * GS + GROWS * GSTR + 2 * DP + PS;
+  static constexpr int PS = CB * S * RC * NL;        // coarse p checkpoints of the next block
+  static constexpr int XCH = NL > 32 ? 4 * (NL / 32) * SF : 0;  // cross-warp hops (2 x 2 buffers)
+  static constexpr int TOTAL = SLOTS * REC + (NK + NP + NTR) * NL + TS + T0 + LS + 2 * GS +
+                               GROWS * GSTR + 2 * DP + PS + XCH;
 };
 
-template <int KIND, int DP, int R, int FR, int F, int CB, int MAP, int S>
-__global__ void __launch_bounds__(128, 2)
+//   NW    warps per pair: 1 = one pair per warp (Gram tiles, many pairs); > 1 =
+//         one pair per CTA, a single wavefront over NL = 32 NW lanes whose
+//         cross-warp hops (lane 31 -> lane 0 of the next warp forward, lane 0
+//         -> lane 31 of the previous warp backward) go through shared memory
+//         with one CTA barrier per step (few long pairs: BASELINE config 2)
+template <int KIND, int DP, int R, int FR, int F, int CB, int MAP, int S, int NW = 1>
+__global__ void __launch_bounds__(NW > 1 ? 32 * NW : 128, NW > 1 ? 1 : 2)
 bwd_kernel(Problem pb, BwdArgs ba) {
   constexpr int RC = R / FR;
   constexpr int SF = S * F;
-  using SM = BwdSmem<DP, R, RC, F, CB, S>;
+  constexpr int NL = 32 * NW;  // lanes per pair
+  constexpr bool XW = NW > 1;
+  using SM = BwdSmem<DP, R, RC, F, CB, S, NL>;
   constexpr int SLOTS = SM::SLOTS;
   constexpr int REC = SM::REC;
   constexpr int PF = 2;  // steps in flight in phase A
@@ -94,35 +104,42 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  double* ring = smem + (size_t)warp * SM::TOTAL;
+  const int u = XW ? (int)threadIdx.x : lane;  // lane of the pair's wavefront
+  double* ring = smem + (XW ? 0 : (size_t)warp * SM::TOTAL);
   double* sK = ring + SLOTS * REC;
-  double* sP = sK + SM::NK * 32;
-  double* sTR = sP + SM::NP * 32;
-  double* sTS = sTR + SM::NTR * 32;
+  double* sP = sK + SM::NK * NL;
+  double* sTR = sP + SM::NP * NL;
+  double* sTS = sTR + SM::NTR * NL;
   double* sT0 = sTS + SM::TS;
   double* sLS = sT0 + SM::T0;
   double* sGS0 = sLS + SM::LS;
   double* sGW = sGS0 + 2 * SM::GS;
-  double* sZero = sGW + SM::GROWS * SM::GSTR;  // DP zeros (lane 31's unseeded rows)
+  double* sZero = sGW + SM::GROWS * SM::GSTR;  // DP zeros (the last lane's unseeded rows)
   double* sGA = sZero + DP;                    // lane 0's coarse-column sums (2^lam2 > F)
   double* sPS = sGA + DP;                      // staged coarse p of the next block
-  for (int k = lane; k < DP; k += 32) sZero[k] = 0.0;
-  __syncwarp();
-#define SK_TR(q) sTR[(q) * 32 + lane]
-#define SK_KB(kap, s, f, r) sK[((((kap) * S + (s)) * F + (f)) * R + (r)) * 32 + lane]
-#define SK_PB(kap, s, c) sP[(((kap) * S + (s)) * RC + (c)) * 32 + lane]
+  double* sXA = sPS + SM::PS;                  // XW: [2][NW][SF] forward hops (bottom rows)
+  double* sXB = sXA + (XW ? 2 * NW * SF : 0);  // XW: [2][NW][SF] backward hops (messages)
+#define SK_BAR()                          \
+  do {                                     \
+    if constexpr (XW) __syncthreads();     \
+    else __syncwarp();                     \
+  } while (0)
+  for (int k = u; k < DP; k += NL) sZero[k] = 0.0;
+  SK_BAR();
+#define SK_TR(q) sTR[(q) * NL + u]
+#define SK_KB(kap, s, f, r) sK[((((kap) * S + (s)) * F + (f)) * R + (r)) * NL + u]
+#define SK_PB(kap, s, c) sP[(((kap) * S + (s)) * RC + (c)) * NL + u]
 #define SK_REC(col)                                                                     \
   (ring + ((SLOTS & (SLOTS - 1)) == 0 ? ((col) & (SLOTS - 1))                              \
                                       : (((col) + 4 * SLOTS) % SLOTS)) * REC)
 
-  const int u = lane;
   const int M1 = pb.M1c << pb.lam1;
   const int M2 = pb.M2c << pb.lam2;
   const int NC = M2 / F;                // columns per strip row
   const int NSTEP = (NC + S - 1) / S;   // steps per strip row
-  const int NT = NSTEP + 31;            // skewed steps per strip
+  const int NT = NSTEP + NL - 1;        // skewed steps per strip
   const int NB = (NT + CB - 1) / CB;
-  const int H = 32 * R;
+  const int H = NL * R;
   const int nstrips = (M1 + H - 1) / H;
   const int last_strip = (M1 - 1) / H;
   const int u_star = ((M1 - 1) % H) / R;
@@ -132,7 +149,8 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   // LINEAR rows carry the exact dyadic factor: gx needs it on D, gy does not
   const double gxs_scale = (KIND == LINEAR) ? pb.scale : 1.0;
 
-  const int64_t slot = (int64_t)blockIdx.x * nw + warp;
+  const int64_t slot = XW ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * nw + warp;
+  const int64_t item_step = XW ? (int64_t)gridDim.x : (int64_t)gridDim.x * nw;
   double* __restrict__ rowck = ba.rowck + slot * ba.rowck_stride;
   double* __restrict__ colck = ba.colck + slot * ba.colck_stride;
   double* __restrict__ pck = ba.pck + slot * ba.pck_stride;
@@ -145,9 +163,9 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   const int GW = WIDE ? pb.dpad : DP;  // row length of the increment-gradient scratch
   double* __restrict__ gxs = ba.gscr + slot * ba.gscr_stride;  // [M1c][GW]
   double* __restrict__ gcs = gxs + (int64_t)pb.M1c * GW;       // [M2c][GW]
-#define SK_ROWCK(strip, d, q, ln) rowck[(((int64_t)(strip) * NT + (d)) * SF + (q)) * 32 + (ln)]
+#define SK_ROWCK(strip, d, q, ln) rowck[(((int64_t)(strip) * NT + (d)) * SF + (q)) * NL + (ln)]
 
-  for (int64_t item = slot; item < pb.nitems; item += (int64_t)gridDim.x * nw) {
+  for (int64_t item = slot; item < pb.nitems; item += item_step) {
     // ---------------------------------------------------------- resolve pair
     int64_t pr = 0, pc = 0, oidx = 0, pidx = 0;
     const bool valid = resolve_pair(pb, item, 1, 0, pr, pc, oidx, pidx);
@@ -165,7 +183,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
     // ring records of columns [c0, c0 + n): column data + F handoff values (no commit)
     auto issue_cols = [&](int c0, int n, const double* hsrc, bool hvalid) {
       constexpr int PER = DP / 2 + F;
-      for (int e = lane; e < n * PER; e += 32) {
+      for (int e = u; e < n * PER; e += NL) {
         const int q = e / PER, w = e % PER;
         const int col = c0 + q;
         const bool cv = (col >= 0) && (col < NC);
@@ -243,8 +261,8 @@ bwd_kernel(Problem pb, BwdArgs ba) {
     };
 
     // ------------------------------------------- phase A: forward + checkpoints
-    for (int t = u; t <= M2; t += 32) hrow[t] = 1.0;
-    __syncwarp();
+    for (int t = u; t <= M2; t += NL) hrow[t] = 1.0;
+    SK_BAR();
     double kval = 0.0;
     for (int strip = 0; strip < nstrips; ++strip) {
       const int rbase = strip * H + u * R;
@@ -252,10 +270,10 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       RowRegs<KIND, DP, RC> rr;
       load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
       jcur = -1;
-      double* __restrict__ rowck_s = rowck + (int64_t)strip * NT * SF * 32 + lane;
+      double* __restrict__ rowck_s = rowck + (int64_t)strip * NT * SF * NL + u;
       // coarse p of every column this lane solves: the block recompute reads
       // it back instead of re-forming <dx_i, dy_j> (or the RBF exps)
-      double* __restrict__ pck_s = pck + (int64_t)strip * NT * S * RC * 32 + lane;
+      double* __restrict__ pck_s = pck + (int64_t)strip * NT * S * RC * NL + u;
       if constexpr (KIND == RBF) {
         double y0[DP];
         load_vec<DP>(y0, cbase);
@@ -275,22 +293,31 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       double bot[SF];
 #pragma unroll
       for (int q = 0; q < SF; ++q) bot[q] = 1.0;
+      if constexpr (XW) {  // lane 0 of warp w reads warp w-1's lane 31 from here
+        for (int e = u; e < 2 * NW * SF; e += NL) sXA[e] = 1.0;
+      }
       for (int tau = 0; tau < NT; ++tau) {
         issue_cols((tau + PF) * S, S, hrow, strip > 0);
         cp_async_commit();
         cp_async_wait<PF>();  // step tau landed
-        __syncwarp();
+        SK_BAR();
         if (tau % CB == 0) {
           // column checkpoint: values at node column (tau - u) * S * F
 #pragma unroll
           for (int r = 0; r < R; ++r)
-            colck[(((int64_t)strip * NB + tau / CB) * R + r) * 32 + lane] = kl[r];
+            colck[(((int64_t)strip * NB + tau / CB) * R + r) * NL + u] = kl[r];
         }
         const int js = tau - u;
         const bool active = (js >= 0) && (js < NSTEP);
         double tv[SF];
 #pragma unroll
         for (int q = 0; q < SF; ++q) tv[q] = __shfl_up_sync(0xffffffffu, bot[q], 1);
+        if constexpr (XW) {
+          if (lane == 0 && warp > 0) {
+#pragma unroll
+            for (int q = 0; q < SF; ++q) tv[q] = sXA[(((tau + 1) & 1) * NW + warp - 1) * SF + q];
+          }
+        }
         if (active) {
           if (u == 0) {
 #pragma unroll
@@ -307,7 +334,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             double pv[RC];
             colcoef(rr, col, i0, cf, pv);
 #pragma unroll
-            for (int c = 0; c < RC; ++c) pck_s[((tau * S + s) * RC + c) * 32] = pv[c];
+            for (int c = 0; c < RC; ++c) pck_s[((tau * S + s) * RC + c) * NL] = pv[c];
 #pragma unroll
             for (int f = 0; f < F; ++f) {
               const int q = s * F + f;
@@ -321,7 +348,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
                 up = nk;
               }
               bot[q] = up;
-              rowck_s[(tau * SF + q) * 32] = up;  // diagonal index = step + writer lane = tau
+              rowck_s[(tau * SF + q) * NL] = up;  // diagonal index = step + writer lane = tau
             }
             if (strip == last_strip && u == u_star && col == NC - 1) {
 #pragma unroll
@@ -330,7 +357,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             }
           }
           topc = tv[SF - 1];
-          if (u == 31) {
+          if (u == NL - 1) {
 #pragma unroll
             for (int s = 0; s < S; ++s) {
               const int col = js * S + s;
@@ -341,20 +368,26 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             }
           }
         }
+        if constexpr (XW) {
+          if (lane == 31 && warp < NW - 1) {
+#pragma unroll
+            for (int q = 0; q < SF; ++q) sXA[((tau & 1) * NW + warp) * SF + q] = bot[q];
+          }
+        }
       }
       cp_async_wait<0>();
-      __syncwarp();
+      SK_BAR();
     }
     if (ba.values && u == u_star) ba.values[oidx] = kval;
 
     // ------------------------------------------------ phase B: reverse sweep
-    for (int t = u; t <= M2; t += 32) arow[t] = 0.0;
+    for (int t = u; t <= M2; t += NL) arow[t] = 0.0;
     if constexpr (MAP == DBUF) {
-      for (int64_t e = u; e < (int64_t)pb.M1c * pb.M2c; e += 32) dbuf[e] = 0.0;
+      for (int64_t e = u; e < (int64_t)pb.M1c * pb.M2c; e += NL) dbuf[e] = 0.0;
     } else {
-      for (int64_t e = u; e < (int64_t)pb.M1c * DP; e += 32) gxs[e] = 0.0;
+      for (int64_t e = u; e < (int64_t)pb.M1c * DP; e += NL) gxs[e] = 0.0;
     }
-    __syncwarp();
+    SK_BAR();
     const bool atomic = ba.atomic != 0;
     double* __restrict__ gR = atomic ? nullptr : ba.gradR + pr * ba.gR_path;
     double* __restrict__ gC = atomic ? nullptr : ba.gradC + pc * ba.gC_path;
@@ -373,46 +406,47 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       // left checkpoint (single buffers, consumed by the recompute) and lane
       // 31's incoming column gradients (double buffered, used by the sweep)
       auto issue_block = [&](int blk, bool first) {
-        if (first) issue_cols((blk * CB - 31) * S, (CB + 31) * S, arow, true);
-        else issue_cols((blk * CB - 31) * S, CB * S, arow, true);  // the new columns only
+        if (first) issue_cols((blk * CB - (NL - 1)) * S, (CB + NL - 1) * S, arow, true);
+        else issue_cols((blk * CB - (NL - 1)) * S, CB * S, arow, true);  // the new columns only
         {
           const int dlo = blk * CB - 2;  // rowck[strip][d][q][*], d in [blk*CB-2, blk*CB+CB-2]
           constexpr int NCH = SM::TS / 2;
-          for (int e = lane; e < NCH; e += 32) {
-            const int row = e / (SF * 16);  // (CB+1) rows of SF*32 doubles
+          constexpr int ROWT = SF * NL / 2;  // 16-byte chunks per diagonal row
+          for (int e = u; e < NCH; e += NL) {
+            const int row = e / ROWT;  // (CB+1) rows of SF*NL doubles
             const int d = dlo + row;
             const bool v = (d >= 0) && (d < NT);
             cp_async16(sTS + 2 * e,
-                       rowck + (((int64_t)strip * NT + (v ? d : 0)) * SF) * 32 + 2 * (e % (SF * 16)),
+                       rowck + (((int64_t)strip * NT + (v ? d : 0)) * SF) * NL + 2 * (e % ROWT),
                        v);
           }
         }
         if (strip > 0) {
-          // lane 0's top row: nodes t = blk*CB*SF + q, written by strip-1's lane 31
-          for (int q = lane; q <= CB * SF; q += 32) {
+          // lane 0's top row: nodes t = blk*CB*SF + q, written by strip-1's last lane
+          for (int q = u; q <= CB * SF; q += NL) {
             const int t = blk * CB * SF + q;
             const bool v = (t >= 1) && (t <= M2);
             const int js = v ? (t - 1) / SF : 0, qs = v ? (t - 1) % SF : 0;
-            cp_async8(sT0 + q, &SK_ROWCK(strip - 1, js + 31, qs, 31), v);
+            cp_async8(sT0 + q, &SK_ROWCK(strip - 1, js + NL - 1, qs, NL - 1), v);
           }
         }
-        for (int e = lane; e < SM::LS / 2; e += 32)
-          cp_async16(sLS + 2 * e, colck + (((int64_t)strip * NB + blk) * R) * 32 + 2 * e, true);
+        for (int e = u; e < SM::LS / 2; e += NL)
+          cp_async16(sLS + 2 * e, colck + (((int64_t)strip * NB + blk) * R) * NL + 2 * e, true);
         {
           // coarse p: lane u's step js0 + kap sits at diagonal index blk*CB + kap
-          constexpr int ROWC = S * RC * 16;  // 16-byte chunks per diagonal row
-          for (int e = lane; e < CB * ROWC; e += 32) {
+          constexpr int ROWC = S * RC * NL / 2;  // 16-byte chunks per diagonal row
+          for (int e = u; e < CB * ROWC; e += NL) {
             const int d = blk * CB + e / ROWC;
             const bool v = d < NT;
             cp_async16(sPS + 2 * e,
-                       pck + ((int64_t)strip * NT + (v ? d : 0)) * S * RC * 32 + 2 * (e % ROWC), v);
+                       pck + ((int64_t)strip * NT + (v ? d : 0)) * S * RC * NL + 2 * (e % ROWC), v);
           }
         }
         if constexpr (MAP == FUSED) {
           double* gs = sGS0 + (blk & 1) * SM::GS;
-          for (int e = lane; e < CB * S * (DP / 2); e += 32) {
+          for (int e = u; e < CB * S * (DP / 2); e += NL) {
             const int ks = e / (DP / 2), w = e % (DP / 2);
-            const int col = (blk * CB - 31) * S + ks;  // lane 31's columns
+            const int col = (blk * CB - (NL - 1)) * S + ks;  // the last lane's columns
             const bool v = (col >= 0) && (col < NC) && (strip < nstrips - 1);
             const int jc = v ? ((col * F) >> pb.lam2) : 0;
             cp_async16(gs + ks * DP + 2 * w, gcs + (int64_t)jc * DP + 2 * w, v);
@@ -433,15 +467,19 @@ bwd_kernel(Problem pb, BwdArgs ba) {
 #pragma unroll
         for (int c = 0; c < ((MAP == FUSED) ? RC : 1); ++c) gxr[c][k] = 0.0;
 
+      int bstep = 0;  // XW: sweep-step parity of the backward hops
+      if constexpr (XW) {
+        for (int e = u; e < 2 * NW * SF; e += NL) sXB[e] = 0.0;
+      }
       issue_block(NB - 1, true);
       for (int blk = NB - 1; blk >= 0; --blk) {
         cp_async_wait<0>();
-        __syncwarp();
+        SK_BAR();
         const double* sGS = sGS0 + (blk & 1) * SM::GS;
         const int js0 = blk * CB - u;  // lane's first step in this block
         double kleft[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) kleft[r] = sLS[r * 32 + lane];
+        for (int r = 0; r < R; ++r) kleft[r] = sLS[r * NL + u];
 
         // ---- recompute the block's forward values into shared memory
         if (!(SK_EXP & 4)) {
@@ -458,7 +496,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
               v = sT0[q];
             } else {
               const int d = (t - 1) / SF + u - 1 - (blk * CB - 2);
-              v = sTS[(d * SF + (t - 1) % SF) * 32 + (u - 1)];
+              v = sTS[(d * SF + (t - 1) % SF) * NL + (u - 1)];
             }
             SK_TR(q) = v;
           }
@@ -476,7 +514,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
                 const bool cv = (col >= 0) && (col < NC);
 #pragma unroll
                 for (int c = 0; c < RC; ++c) {
-                  const double p = cv ? sPS[((kap * S + s) * RC + c) * 32 + lane] : 0.0;
+                  const double p = cv ? sPS[((kap * S + s) * RC + c) * NL + u] : 0.0;
                   SK_PB(kap, s, c) = p;
                   cf[c] = coef(p);
                 }
@@ -498,7 +536,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             }
           }
         }
-        __syncwarp();
+        SK_BAR();
         // staging buffers are free again: prefetch the next block under the sweep
         if (blk > 0) issue_block(blk - 1, false);
 
@@ -509,7 +547,14 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           double recv[SF];
 #pragma unroll
           for (int q = 0; q < SF; ++q) recv[q] = __shfl_down_sync(0xffffffffu, sendm[q], 1);
-          if (u == 31) {
+          if constexpr (XW) {
+            if (lane == 31 && warp < NW - 1) {
+#pragma unroll
+              for (int q = 0; q < SF; ++q)
+                recv[q] = sXB[(((bstep + 1) & 1) * NW + warp + 1) * SF + q];
+            }
+          }
+          if (u == NL - 1) {
 #pragma unroll
             for (int s = 0; s < S; ++s) {
               const int col = js * S + s;
@@ -551,9 +596,9 @@ bwd_kernel(Problem pb, BwdArgs ba) {
                 const double a = cf[c].A * lam;
                 const double b = cf[c].B * lam;
                 // forward values around the cell: left, up, up-left
-                const double kL = (qb > 0) ? sK[((qb - 1) * R + r) * 32 + lane] : kleft[r];
-                const double kU = (r > 0) ? sK[(qb * R + r - 1) * 32 + lane] : SK_TR(qb + 1);
-                const double kD = (r > 0) ? ((qb > 0) ? sK[((qb - 1) * R + r - 1) * 32 + lane]
+                const double kL = (qb > 0) ? sK[((qb - 1) * R + r) * NL + u] : kleft[r];
+                const double kU = (r > 0) ? sK[(qb * R + r - 1) * NL + u] : SK_TR(qb + 1);
+                const double kD = (r > 0) ? ((qb > 0) ? sK[((qb - 1) * R + r - 1) * NL + u]
                                                       : kleft[r - 1])
                                           : SK_TR(qb);
                 const double p6 = pk[c] * (1.0 / 6.0);
@@ -591,7 +636,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
               if (colv) {
                 double* row = sGW + (jj % SM::GROWS) * SM::GSTR;
                 const bool seed = ((jj + 1) & K2m) == 0;
-                const double* src = (u == 31) ? (seed ? (sGS + ((kap * S + s) * DP)) : sZero) : row;
+                const double* src = (u == NL - 1) ? (seed ? (sGS + ((kap * S + s) * DP)) : sZero) : row;
 #pragma unroll
                 for (int k = 0; k < DP; k += 2) {
                   double2 v = *reinterpret_cast<const double2*>(src + k);
@@ -624,12 +669,19 @@ bwd_kernel(Problem pb, BwdArgs ba) {
               for (int c = 0; c < RC; ++c) SK_PB(kap, s, c) = colv ? Dp[c] * pb.scale : 0.0;
             }
           }
-          __syncwarp();
+          if constexpr (XW) {
+            if (lane == 0 && warp > 0) {
+#pragma unroll
+              for (int q = 0; q < SF; ++q) sXB[((bstep & 1) * NW + warp) * SF + q] = sendm[q];
+            }
+          }
+          ++bstep;
+          SK_BAR();
         }
         if constexpr (MAP == DBUF) {
           // flush the block's coarse adjoint; lanes sharing coarse rows go in order
           const bool excl = ba.rows_exclusive != 0;
-          for (int ln = excl ? 0 : 31; ln >= 0; --ln) {
+          for (int ln = excl ? 0 : NL - 1; ln >= 0; --ln) {
             if (excl || u == ln) {
 #pragma unroll
               for (int kap = CB - 1; kap >= 0; --kap) {
@@ -647,10 +699,10 @@ bwd_kernel(Problem pb, BwdArgs ba) {
                 }
               }
             }
-            if (!excl) __syncwarp();
+            if (!excl) SK_BAR();
           }
         }
-        __syncwarp();
+        SK_BAR();
       }
       cp_async_wait<0>();
       if constexpr (MAP == FUSED) {
@@ -668,7 +720,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             }
           }
         } else {
-          for (int ln = 31; ln >= 0; --ln) {
+          for (int ln = NL - 1; ln >= 0; --ln) {
             if (u == ln) {
 #pragma unroll
               for (int c = 0; c < RC; ++c) {
@@ -679,42 +731,42 @@ bwd_kernel(Problem pb, BwdArgs ba) {
                 }
               }
             }
-            __syncwarp();
+            SK_BAR();
           }
         }
       }
-      __syncwarp();
+      SK_BAR();
     }
 
     if constexpr (MAP == FUSED) {
       // telescope increment gradients to point gradients (kernel_grad.py:55-60)
       // and flush once per pair, coalesced across the warp
-      __syncwarp();
-      for (int64_t e = u; e < (int64_t)(pb.M1c + 1) * dR; e += 32) {
+      SK_BAR();
+      for (int64_t e = u; e < (int64_t)(pb.M1c + 1) * dR; e += NL) {
         const int p = (int)(e / dR), k = (int)(e % dR);
         double v = 0.0;
         if (p >= 1) v += gxs[(int64_t)(p - 1) * DP + k];
         if (p < pb.M1c) v -= gxs[(int64_t)p * DP + k];
         grad_add(gR, fxR, eR + e, v, atomic);
       }
-      for (int64_t e = u; e < (int64_t)(pb.M2c + 1) * dR; e += 32) {
+      for (int64_t e = u; e < (int64_t)(pb.M2c + 1) * dR; e += NL) {
         const int p = (int)(e / dR), k = (int)(e % dR);
         double v = 0.0;
         if (p >= 1) v += gcs[(int64_t)(p - 1) * DP + k];
         if (p < pb.M2c) v -= gcs[(int64_t)p * DP + k];
         grad_add(gC, fxC, eC + e, v, atomic);
       }
-      __syncwarp();
+      SK_BAR();
     } else if constexpr (WIDE) {
       // d > 32: gx_i = sum_j D_ij dy_j, gy_j = sum_i D_ij dx_i (kernel_grad.py:53-54)
       // from the stored coarse adjoint D (dbuf, carries the dyadic factor), one
       // 32-wide chunk of components at a time, then telescoped as above
-      __syncwarp();
+      SK_BAR();
       const double* D = dbuf;
       const double* xp = pb.R.p + pr * pb.R.path_stride;  // rows carry the dyadic factor
       const double unscale = 1.0 / pb.scale;               // exact (power of two)
       for (int ch = 0; ch < pb.nch; ++ch) {
-        for (int i = u; i < pb.M1c; i += 32) {
+        for (int i = u; i < pb.M1c; i += NL) {
           double acc[DP];
 #pragma unroll
           for (int k = 0; k < DP; ++k) acc[k] = 0.0;
@@ -728,7 +780,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
 #pragma unroll
           for (int k = 0; k < DP; ++k) gxs[(int64_t)i * GW + ch * DP + k] = acc[k];
         }
-        for (int j = u; j < pb.M2c; j += 32) {
+        for (int j = u; j < pb.M2c; j += NL) {
           double acc[DP];
 #pragma unroll
           for (int k = 0; k < DP; ++k) acc[k] = 0.0;
@@ -743,26 +795,26 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           for (int k = 0; k < DP; ++k) gcs[(int64_t)j * GW + ch * DP + k] = acc[k] * unscale;
         }
       }
-      __syncwarp();
-      for (int64_t e = u; e < (int64_t)(pb.M1c + 1) * dR; e += 32) {
+      SK_BAR();
+      for (int64_t e = u; e < (int64_t)(pb.M1c + 1) * dR; e += NL) {
         const int p = (int)(e / dR), k = (int)(e % dR);
         double v = 0.0;
         if (p >= 1) v += gxs[(int64_t)(p - 1) * GW + k];
         if (p < pb.M1c) v -= gxs[(int64_t)p * GW + k];
         grad_add(gR, fxR, eR + e, v, atomic);
       }
-      for (int64_t e = u; e < (int64_t)(pb.M2c + 1) * dR; e += 32) {
+      for (int64_t e = u; e < (int64_t)(pb.M2c + 1) * dR; e += NL) {
         const int p = (int)(e / dR), k = (int)(e % dR);
         double v = 0.0;
         if (p >= 1) v += gcs[(int64_t)(p - 1) * GW + k];
         if (p < pb.M2c) v -= gcs[(int64_t)p * GW + k];
         grad_add(gC, fxC, eC + e, v, atomic);
       }
-      __syncwarp();
+      SK_BAR();
     } else {
       // RBF node adjoint G_ij = D[i-1,j-1] - D[i-1,j] - D[i,j-1] + D[i,j] (zero
       // padded); dF/dx_i = sum_j G_ij K_ij (y_j - x_i)/sigma^2, dF/dy_j = -sum_i (same)
-      __syncwarp();
+      SK_BAR();
       const double* D = dbuf;
       const double* xp = pb.R.p + pr * pb.R.path_stride;
       const double* yp = cbase;
@@ -773,7 +825,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       // one distance and one exp per (i, j) and side (r01 recomputed them for
       // every component k); the per-k sums keep their order, so the values
       // are unchanged
-      for (int i = u; i < L1n; i += 32) {
+      for (int i = u; i < L1n; i += NL) {
         double xi[DP], acc[DP];
 #pragma unroll
         for (int k = 0; k < DP; ++k) {
@@ -804,7 +856,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         for (int k = 0; k < DP; ++k)
           if (k < dR) grad_add(gR, fxR, eR + (int64_t)i * dR + k, acc[k], atomic);
       }
-      for (int j = u; j < L2n; j += 32) {
+      for (int j = u; j < L2n; j += NL) {
         double yj[DP], acc[DP];
 #pragma unroll
         for (int k = 0; k < DP; ++k) {
@@ -835,7 +887,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
         for (int k = 0; k < DP; ++k)
           if (k < dR) grad_add(gC, fxC, eC + (int64_t)j * dR + k, acc[k], atomic);
       }
-      __syncwarp();
+      SK_BAR();
     }
   }
 #undef SK_KB
@@ -843,6 +895,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
 #undef SK_REC
 #undef SK_TR
 #undef SK_ROWCK
+#undef SK_BAR
 }
 
 }  // namespace sk

@@ -961,30 +961,57 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   s.R = bwd_rows_per_lane(s.DP);
   s.FR = std::min(1 << std::min(lamR, 3), s.R);
   s.F = std::min(1 << std::min(lamC, 2), 4);
+  s.NW = 1;
+  const int sms = device_sms();
+  {
+    // few long pairs (BASELINE config 2: 256 pairs of 1020 fine rows): one pair
+    // per CTA of NW = 4 warps (measured at config 2: RBF 9.18 ms with one pair
+    // per warp, 3.29 ms at NW = 4, 3.93 ms at NW = 8 (one strip, longer skew))
+    const int64_t M1 = M1c << lamR;
+    const int64_t lanes_per_pair = (M1 + s.R - 1) / s.R;
+    static const int nw_force = [] {
+      const char* e = std::getenv("SK_BWD_XW_NW");  // tuning knob: 1 (off), 4 or 8
+      const int v = (e && e[0]) ? std::atoi(e) : 0;
+      return (v == 1 || v == 4 || v == 8) ? v : 0;
+    }();
+    if (mode == BATCH && !wide && s.DP <= 8 && npairs * 32 < (int64_t)sms * 512 &&
+        lanes_per_pair > 64) {
+      s.NW = 4;
+      if (nw_force) s.NW = nw_force;
+    }
+  }
   int smd = 0;
-  BwdFn fn = kind == RBF ? select_bwd_rbf(s, smd)
-             : wide      ? select_bwd_wide(s, smd)
-                         : select_bwd_linear(s, smd);
+  BwdFn fn = s.NW > 1 ? (kind == RBF ? select_bwd_xw_rbf(s, smd) : select_bwd_xw_linear(s, smd))
+             : kind == RBF ? select_bwd_rbf(s, smd)
+             : wide        ? select_bwd_wide(s, smd)
+                           : select_bwd_linear(s, smd);
   if (!fn) return fail(SK_INVALID_ARGUMENT, "no backward kernel instance for this shape");
   pl.shape = s;
   pl.fn = fn;
   pl.nitems = mode == BATCH ? npairs : gram_items(mode, n2, r0, r1, 1);
-  const int sms = device_sms();
-  // few pairs (BASELINE config 2: 256): smaller CTAs spread them over all SMs
-  pl.threads = 32 * (int)std::min<int64_t>(4, std::max<int64_t>(1, ceil_div(pl.nitems, sms)));
-  const int warps = pl.threads / 32;
-  pl.smem_bytes = smd * (int)sizeof(double) * warps;
+  const int NL = 32 * s.NW;  // lanes per pair
+  int warps = 1;             // lane groups (pairs in flight) per CTA
+  if (s.NW > 1) {
+    pl.threads = NL;
+    pl.smem_bytes = smd * (int)sizeof(double);
+  } else {
+    // few pairs: smaller CTAs spread them over all SMs
+    pl.threads = 32 * (int)std::min<int64_t>(4, std::max<int64_t>(1, ceil_div(pl.nitems, sms)));
+    warps = pl.threads / 32;
+    pl.smem_bytes = smd * (int)sizeof(double) * warps;
+  }
   const int occ = occupancy((const void*)fn, pl.threads, pl.smem_bytes);
   pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + warps - 1) / warps,
                                                      (int64_t)occ * sms));
   pl.slots = pl.blocks * warps;
   const int64_t M1 = M1c << lamR, M2 = M2c << lamC;
   const int64_t Sc = bwd_steps_cols(s.DP, s.F), NC = M2 / s.F, NSTEP = (NC + Sc - 1) / Sc,
-                NT = NSTEP + 31, CB = bwd_block_steps(s.DP, s.R, s.F, (int)Sc), NB = (NT + CB - 1) / CB;
-  const int64_t nstrips = (M1 + 32 * s.R - 1) / (32 * s.R);
-  pl.rowck_stride = (int64_t)align_up((size_t)(nstrips * NT * Sc * s.F * 32), 32);
-  pl.colck_stride = (int64_t)align_up((size_t)(nstrips * NB * s.R * 32), 32);
-  pl.pck_stride = (int64_t)align_up((size_t)(nstrips * NT * Sc * (s.R / s.FR) * 32), 32);
+                NT = NSTEP + NL - 1, CB = bwd_block_steps(s.DP, s.R, s.F, (int)Sc),
+                NB = (NT + CB - 1) / CB;
+  const int64_t nstrips = (M1 + NL * s.R - 1) / (NL * s.R);
+  pl.rowck_stride = (int64_t)align_up((size_t)(nstrips * NT * Sc * s.F * NL), 32);
+  pl.colck_stride = (int64_t)align_up((size_t)(nstrips * NB * s.R * NL), 32);
+  pl.pck_stride = (int64_t)align_up((size_t)(nstrips * NT * Sc * (s.R / s.FR) * NL), 32);
   pl.row_stride = (int64_t)align_up((size_t)(M2 + 1), 32);
   pl.dbuf_stride = (kind == RBF || wide) ? (int64_t)align_up((size_t)(M1c * M2c), 32) : 0;
   pl.gscr_stride = kind == LINEAR ? (int64_t)align_up((size_t)((M1c + M2c) * s.DP * nch), 32) : 0;

@@ -25,7 +25,8 @@ using BwdFn = void (*)(Problem, BwdArgs);
 
 struct BwdShape {
   int kind;
-  int DP, R, FR, F;  // as FwdShape; lanes per pair fixed at 32, CB = 8 / F
+  int DP, R, FR, F;  // as FwdShape; lanes per pair 32 NW, CB = 8 / F
+  int NW;            // warps per pair (1: one pair per warp; 4, 8: one pair per CTA)
   bool MMA;          // DMMA Gram tile kernel (sk_mma_bwd.cuh): LINEAR, order 0, DP 8/16
   int WPC;           // warps per CTA of the DMMA kernel
 };
@@ -33,6 +34,8 @@ struct BwdShape {
 BwdFn select_bwd_linear(const BwdShape& s, int& smem_doubles);
 BwdFn select_bwd_rbf(const BwdShape& s, int& smem_doubles);
 BwdFn select_bwd_wide(const BwdShape& s, int& smem_doubles);  // linear, d > 32
+BwdFn select_bwd_xw_linear(const BwdShape& s, int& smem_doubles);  // one pair per CTA
+BwdFn select_bwd_xw_rbf(const BwdShape& s, int& smem_doubles);
 BwdFn select_bwd_mma(int DP, int WPC, int& smem_doubles_per_warp);
 
 // Per-kind instance tables (one translation unit each, compiled in parallel).
