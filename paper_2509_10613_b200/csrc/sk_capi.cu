@@ -939,7 +939,7 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
     pl.fn = fn;
     pl.threads = 32 * s.WPC;
     pl.smem_bytes = per_warp * (int)sizeof(double) * s.WPC;
-    pl.nitems = gram_items(mode, n2, r0, r1, 8);
+    pl.nitems = gram_items(mode, n2, r0, r1, 8, false);
     const int sms = device_sms();
     const int occ = occupancy((const void*)fn, pl.threads, pl.smem_bytes);
     pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + s.WPC - 1) / s.WPC,
@@ -988,7 +988,7 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   if (!fn) return fail(SK_INVALID_ARGUMENT, "no backward kernel instance for this shape");
   pl.shape = s;
   pl.fn = fn;
-  pl.nitems = mode == BATCH ? npairs : gram_items(mode, n2, r0, r1, 1);
+  pl.nitems = mode == BATCH ? npairs : gram_items(mode, n2, r0, r1, 1, false);
   const int NL = 32 * s.NW;  // lanes per pair
   int warps = 1;             // lane groups (pairs in flight) per CTA
   if (s.NW > 1) {
@@ -1054,6 +1054,10 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   pb.swap = g.swap ? 1 : 0;
   pb.npairs = mode == BATCH ? n1 : 0;
   pb.ldo = n2;
+  // row-block-major tiles (gram_item_amajor) keep the row accumulators in L2 but put
+  // hundreds of warps on the same few paths (atomic contention): measured 1.29 s vs
+  // 1.25 s per C3 step with the column-major order, so it stays off
+  pb.amajor = 0;
   BwdPlan pl;
   const int64_t npairs = mode == BATCH ? n1 : (r1 - r0) * n2;
   if (int rc = plan_backward(pl, kind, d, g.lamR, g.lamC, pb.M1c, pb.M2c, mode, npairs,

@@ -50,6 +50,7 @@ struct Problem {
   int n1, n2;      // Gram sizes (X count, Y count)
   int r0, r1;      // Gram: X rows [r0, r1) handled by this call
   int swap;        // grid rows are the Y path (fine-axis orientation rule)
+  int amajor;      // Gram backward: items enumerated row-block major (see gram_item)
   // output
   double* out;
   int64_t ldo;
@@ -171,7 +172,36 @@ __device__ __forceinline__ void fix_add(const FixAcc& f, int64_t elem, double v)
 // GRAM_SYM:   only pairs a <= b (upper triangle, _kernels.py:421-425).
 //   b in [r0, r1-1): a-blocks over [r0, b+1)   (triangle part)
 //   b in [r1-1, n2): a-blocks over [r0, r1)     (rectangle part)
+// Row-block-major enumeration (Gram backward): the tiles of one row block
+// (a0 fixed, b ascending) are consecutive items, so the warps in flight share
+// a few row blocks and the row-side gradient accumulators they update stay in
+// L2.  SYM: block ab (a0 = r0 + P ab) holds tiles b in [a0, n2).
+__host__ __device__ inline int64_t amajor_prefix(int64_t ab, int64_t W, int P) {
+  return ab * W - (int64_t)P * (ab * (ab - 1) / 2);  // sum_{i<ab} (W - P i)
+}
+__device__ inline void gram_item_amajor(const Problem& pb, int64_t item, int P, int& a0, int& b) {
+  if (pb.mode == GRAM_CROSS) {
+    a0 = pb.r0 + (int)(item / pb.n2) * P;
+    b = (int)(item % pb.n2);
+    return;
+  }
+  const int64_t W = pb.n2 - pb.r0;
+  // largest ab with prefix(ab) <= item: P/2 ab^2 - (W + P/2) ab + item >= 0 side
+  const double hp = 0.5 * P, bq = W + hp;
+  double disc = bq * bq - 4.0 * hp * (double)item;
+  int64_t ab = (int64_t)((bq - sqrt(disc > 0 ? disc : 0.0)) / (2.0 * hp));
+  if (ab < 0) ab = 0;
+  while (amajor_prefix(ab + 1, W, P) <= item) ++ab;
+  while (ab > 0 && amajor_prefix(ab, W, P) > item) --ab;
+  a0 = pb.r0 + (int)(ab * P);
+  b = a0 + (int)(item - amajor_prefix(ab, W, P));
+}
+
 __device__ inline void gram_item(const Problem& pb, int64_t item, int P, int& a0, int& b) {
+  if (pb.amajor) {
+    gram_item_amajor(pb, item, P, a0, b);
+    return;
+  }
   int span = pb.r1 - pb.r0;
   if (pb.mode == GRAM_CROSS) {
     int64_t nblk = ceil_div(span, P);
@@ -207,9 +237,13 @@ __device__ inline void gram_item(const Problem& pb, int64_t item, int P, int& a0
   a0 = pb.r0 + (int)(rem % nblk) * P;
 }
 
-__host__ inline int64_t gram_items(int mode, int n2, int r0, int r1, int P) {
+__host__ inline int64_t gram_items(int mode, int n2, int r0, int r1, int P, bool amajor = false) {
   int64_t span = r1 - r0;
   if (span <= 0) return 0;
+  if (amajor) {
+    const int64_t nblk = ceil_div(span, P);
+    return mode == GRAM_CROSS ? nblk * n2 : amajor_prefix(nblk, (int64_t)n2 - r0, P);
+  }
   int64_t nblk = ceil_div(span, P);
   if (mode == GRAM_CROSS) return nblk * n2;
   int64_t nb = span - 1;
