@@ -911,7 +911,8 @@ struct BwdPlan {
   int smem_bytes = 0;
   int threads = 128;
   int64_t blocks = 0, slots = 0, nitems = 0;
-  int64_t rowck_stride = 0, colck_stride = 0, pck_stride = 0, row_stride = 0, dbuf_stride = 0, gscr_stride = 0;
+  int64_t rowck_stride = 0, colck_stride = 0, pck_stride = 0, row_stride = 0, dbuf_stride = 0, gscr_stride = 0,
+          rsum_stride = 0;
 };
 
 static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, int64_t M1c,
@@ -939,7 +940,7 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
     pl.fn = fn;
     pl.threads = 32 * s.WPC;
     pl.smem_bytes = per_warp * (int)sizeof(double) * s.WPC;
-    pl.nitems = gram_items(mode, n2, r0, r1, 8, false);
+    pl.nitems = super_items(mode, n2, r0, r1);
     const int sms = device_sms();
     const int occ = occupancy((const void*)fn, pl.threads, pl.smem_bytes);
     pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + s.WPC - 1) / s.WPC,
@@ -954,8 +955,10 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
     pl.row_stride = 8 * (NT8 + 5);
     pl.dbuf_stride = 0;
     pl.gscr_stride = 8 * NT8 * s.DP;
+    pl.rsum_stride = 8 * M1c * s.DP;
     cap_slots(pl.blocks, pl.slots, s.WPC,
-              8.0 * (pl.rowck_stride + pl.colck_stride + pl.gscr_stride + 16 * pl.row_stride));
+              8.0 * (pl.rowck_stride + pl.colck_stride + pl.gscr_stride + pl.rsum_stride +
+                     16 * pl.row_stride));
     return SK_OK;
   }
   s.R = bwd_rows_per_lane(s.DP);
@@ -1023,7 +1026,7 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
 
 struct BwdLayout {
   size_t prepR = 0, prepC = 0, rowck = 0, colck = 0, pck = 0, rows = 0, dbuf = 0, gscr = 0,
-         accx = 0, accy = 0, total = 0;
+         rsum = 0, accx = 0, accy = 0, total = 0;
 };
 
 // Gram gradients go through exact accumulators: the caller's (acc_x / acc_y,
@@ -1079,6 +1082,7 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   lo.rows = align_up((size_t)row_slots * pl.row_stride * 2 * sizeof(double), 256);
   lo.dbuf = align_up((size_t)pl.slots * pl.dbuf_stride * sizeof(double), 256);
   lo.gscr = align_up((size_t)pl.slots * pl.gscr_stride * sizeof(double), 256);
+  lo.rsum = align_up((size_t)pl.slots * pl.rsum_stride * sizeof(double), 256);
   const bool gram = mode != BATCH;
   const bool own_acc = gram && acc_x == nullptr;
   lo.accx = own_acc ? align_up(acc_bytes(n1, L1, d), 256) : 0;
@@ -1088,7 +1092,7 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   const size_t gtx = tgrad ? align_up((size_t)n1 * L1 * d * sizeof(double), 256) : 0;
   const size_t gty = (tgrad && !sym) ? align_up((size_t)n2 * L2 * d * sizeof(double), 256) : 0;
   lo.total = lo.prepR + lo.prepC + lo.rowck + lo.colck + lo.pck + lo.rows + lo.dbuf + lo.gscr +
-             lo.accx + lo.accy + gtx + gty;
+             lo.rsum + lo.accx + lo.accy + gtx + gty;
   if (query) {
     *query = lo.total;
     return SK_OK;
@@ -1131,6 +1135,9 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   ba.gscr = reinterpret_cast<double*>(p);
   ba.gscr_stride = pl.gscr_stride;
   p += lo.gscr;
+  ba.rsum = reinterpret_cast<double*>(p);
+  ba.rsum_stride = pl.rsum_stride;
+  p += lo.rsum;
   unsigned long long* blob_x = static_cast<unsigned long long*>(acc_x);
   unsigned long long* blob_y = static_cast<unsigned long long*>(acc_y);
   if (own_acc) {

@@ -72,6 +72,8 @@ struct BwdArgs {
   int64_t dbuf_stride;
   double* gscr;  // FUSED: per-slot increment gradients [M1c + M2c][DP]
   int64_t gscr_stride;
+  double* rsum;  // DMMA Gram: per-slot row-side increment gradients of a super-item [8][M1c][DP]
+  int64_t rsum_stride;
   int rows_exclusive;  // 2^lam1 <= R: every coarse row belongs to one lane
   // outputs (point gradients, real dimension d)
   double* gradR;  // BATCH: gradient of the grid-row path set
@@ -235,6 +237,46 @@ __device__ inline void gram_item(const Problem& pb, int64_t item, int P, int& a0
   int64_t nblk = ceil_div(span, P);
   b = pb.r1 - 1 + (int)(rem / nblk);
   a0 = pb.r0 + (int)(rem % nblk) * P;
+}
+
+// DMMA Gram backward work items ("super-items"): one 8-path row block a0 and
+// one canonical chunk of SK_SUPER_B consecutive column paths b (absolute
+// chunk index b / SK_SUPER_B).  The row-side gradients of the chunk's tiles
+// are summed in fp64 in b order inside the item and flushed once, so the
+// result does not depend on how rows are split across calls / GPUs (the
+// chunks and row blocks are the same in every split aligned to 8 rows).
+#define SK_SUPER_B 8
+__host__ __device__ inline int64_t super_chunks(int mode, int n2, int r0, int ab) {
+  if (mode == GRAM_CROSS) return (n2 + SK_SUPER_B - 1) / SK_SUPER_B;
+  return (int64_t)((n2 - 1) / SK_SUPER_B) - (r0 + 8 * ab) / SK_SUPER_B + 1;
+}
+__host__ inline int64_t super_items(int mode, int n2, int r0, int r1) {
+  const int nblk = (r1 - r0 + 7) / 8;
+  if (r1 <= r0) return 0;
+  if (mode == GRAM_CROSS) return (int64_t)nblk * super_chunks(mode, n2, r0, 0);
+  int64_t n = 0;
+  for (int ab = 0; ab < nblk; ++ab) n += super_chunks(mode, n2, r0, ab);
+  return n;
+}
+__device__ inline void super_item(const Problem& pb, int64_t s, int& ab, int& ch) {
+  if (pb.mode == GRAM_CROSS) {
+    const int64_t nc = super_chunks(pb.mode, pb.n2, pb.r0, 0);
+    ab = (int)(s / nc);
+    ch = (int)(s % nc);
+    return;
+  }
+  const int nblk = (pb.r1 - pb.r0 + 7) / 8;
+  int64_t acc = 0;
+  for (ab = 0; ab < nblk; ++ab) {
+    const int64_t nc = super_chunks(pb.mode, pb.n2, pb.r0, ab);
+    if (s < acc + nc) {
+      ch = (pb.r0 + 8 * ab) / SK_SUPER_B + (int)(s - acc);
+      return;
+    }
+    acc += nc;
+  }
+  ab = nblk;
+  ch = 0;
 }
 
 __host__ inline int64_t gram_items(int mode, int n2, int r0, int r1, int P, bool amajor = false) {

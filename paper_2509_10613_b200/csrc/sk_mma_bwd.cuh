@@ -113,10 +113,16 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
   double* __restrict__ arow = ba.adj + (slot * 8 + g) * ba.row_stride;
   double* __restrict__ gcs = ba.gscr + slot * ba.gscr_stride;  // column gradients [8*NT8][DP]
   const FixAcc fxR = fix_make(ba.accR, ba.metaR), fxC = fix_make(ba.accC, ba.metaC);
+  double* __restrict__ rs = ba.rsum + slot * ba.rsum_stride;  // [8][M1][DP]
 
-  for (int64_t item = slot; item < pb.nitems; item += (int64_t)gridDim.x * WPC) {
-    int a0, b;
-    gram_item(pb, item, 8, a0, b);
+  for (int64_t sitem = slot; sitem < pb.nitems; sitem += (int64_t)gridDim.x * WPC) {
+  int ab, chunk;
+  super_item(pb, sitem, ab, chunk);
+  const int a0 = pb.r0 + 8 * ab;
+  const int bbeg = max(chunk * SK_SUPER_B, pb.mode == GRAM_SYM ? a0 : 0);
+  const int bend = min(pb.n2, (chunk + 1) * SK_SUPER_B);
+  for (int b = bbeg; b < bend; ++b) {
+    const bool first_tile = b == bbeg;
     const int a = a0 + g;
     const bool valid = a < pb.r1 && !(pb.mode == GRAM_SYM && a > b);
     double wcot = 0.0;
@@ -524,28 +530,21 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         else blockB(std::false_type{}, blk);
       }
 
-      // row-side gradient of the strip, telescoped to points (kernel_grad.py:55-60):
-      // point r gets gx[r-1] - gx[r]; row r-1 sits 4 lanes up (same u)
-      const int dR = ba.d;
+      // row-side increment gradients of the strip into the super-item's sums
+      // (b ascending; flushed once per super-item below)
       const int rho = strip * 8 + g;
+      if (rho < M1) {
 #pragma unroll
-      for (int h = 0; h < 8; ++h) {
-        const int ah = a0 + h;
-        const bool hv = ah < pb.r1 && !(pb.mode == GRAM_SYM && ah > b);  // warp-uniform
+        for (int h = 0; h < 8; ++h) {
 #pragma unroll
-        for (int n = 0; n < NN; ++n) {
-          const double up0 = __shfl_up_sync(0xffffffffu, gx[h][n][0], 4);
-          const double up1 = __shfl_up_sync(0xffffffffu, gx[h][n][1], 4);
-          if (!hv || rho >= M1) continue;
-          const int64_t gp = (int64_t)ah * ba.gR_path;
-          const int k = 8 * n + 2 * u;
-          const double v0 = (g > 0 ? up0 : 0.0) - gx[h][n][0];
-          const double v1 = (g > 0 ? up1 : 0.0) - gx[h][n][1];
-          if (k < dR) fix_add(fxR, gp + (int64_t)rho * dR + k, v0);
-          if (k + 1 < dR) fix_add(fxR, gp + (int64_t)rho * dR + k + 1, v1);
-          if (g == 7 || rho == M1 - 1) {  // point rho + 1 (next strip's row 0 adds the rest)
-            if (k < dR) fix_add(fxR, gp + (int64_t)(rho + 1) * dR + k, gx[h][n][0]);
-            if (k + 1 < dR) fix_add(fxR, gp + (int64_t)(rho + 1) * dR + k + 1, gx[h][n][1]);
+          for (int n = 0; n < NN; ++n) {
+            double2* q = reinterpret_cast<double2*>(rs + ((int64_t)h * M1 + rho) * DP + 8 * n + 2 * u);
+            double2 v = make_double2(gx[h][n][0], gx[h][n][1]);
+            if (!first_tile) {
+              const double2 o = *q;
+              v = make_double2(o.x + v.x, o.y + v.y);
+            }
+            *q = v;
           }
         }
       }
@@ -565,7 +564,27 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       }
     }
     __syncwarp();
+  }  // tiles of the super-item
+  // row-side gradients of the super-item's 8 paths, telescoped to points
+  // (kernel_grad.py:55-60: point r gets g[r-1] - g[r]) and flushed once
+  {
+    const int dR = ba.d;
+    for (int h = 0; h < 8; ++h) {
+      const int ah = a0 + h;
+      if (ah >= pb.r1 || bbeg >= bend) continue;  // warp-uniform
+      const double* rh = rs + (int64_t)h * M1 * DP;
+      const int64_t gp = (int64_t)ah * ba.gR_path;
+      for (int e = lane; e < (M1 + 1) * dR; e += 32) {
+        const int p = e / dR, k = e % dR;
+        double v = 0.0;
+        if (p >= 1) v += rh[(int64_t)(p - 1) * DP + k];
+        if (p < M1) v -= rh[(int64_t)p * DP + k];
+        fix_add(fxR, gp + e, v);
+      }
+    }
+    __syncwarp();
   }
+  }  // super-items
 }
 
 }  // namespace sk
