@@ -186,6 +186,7 @@ def run_reference(args, rank, world):
     value = cells / t
     sample = (f"symmetric sub-Gram {n_sample}x{n_sample} of the {desc} workload per step "
               f"(cells/s is size-independent per pair; full config extrapolates linearly)")
+    stock = stock_reference(X[:8], C[:8, :8], lam, threads)
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "cells/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -198,7 +199,47 @@ def run_reference(args, rank, world):
                          "sample": sample},
         "e2e": {"value": value, "unit": "cells/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "value_source": "the C port (faster than stock sigcore, so the GPU/CPU ratio is "
+                        "conservative); stock sigcore timed beside it in stock_reference",
+        "stock_reference": stock,
     }), flush=True)
+
+
+def stock_reference(X, C, lam, threads):
+    """The unmodified reference (sigcore, Python + numba, installed into
+    baseline/_ref) on the same sub-Gram step: kernel_gram (kernel.py:151-180)
+    for G, then kernel_batch_backward (kernel_grad.py:64-98) over the upper
+    triangle's pairs for dF/dX (sigcore has no Gram backward).  Reported beside
+    the port; None when baseline/_ref or numba is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "sigcore")):
+        return {"unavailable": "baseline/_ref/sigcore not installed"}
+    sys.path.insert(0, ref)
+    try:
+        from sigcore.kernel import KernelConfig, kernel_gram
+        from sigcore.kernel_grad import kernel_batch_backward
+    except Exception as e:  # noqa: BLE001 - report, do not fail the arm
+        return {"unavailable": f"import sigcore failed: {type(e).__name__}: {e}"}
+    finally:
+        sys.path.remove(ref)
+    n, L = X.shape[0], X.shape[1]
+    cfg = KernelConfig(lam, lam)
+    ia, ib = np.triu_indices(n)
+
+    def step():
+        kernel_gram(X, None, cfg, threads=threads)
+        kernel_batch_backward(X[ia], X[ib], cfg, C[ia, ib], threads=threads)
+
+    kernel_gram(X[:2], None, cfg, threads=threads)  # numba JIT compile, untimed
+    kernel_batch_backward(X[:1], X[:1], cfg, None, threads=threads)
+    t0 = time.perf_counter()
+    step()
+    t = time.perf_counter() - t0
+    cells = len(ia) * ((L - 1) << lam) ** 2
+    return {"value": cells / t, "unit": "cells/s", "cores": threads, "kind": "reference",
+            "ms_per_step": t * 1e3,
+            "sample": f"symmetric sub-Gram {n}x{n}: sigcore.kernel_gram + "
+                      f"kernel_batch_backward over its {len(ia)} upper-triangle pairs"}
 
 
 def main():
