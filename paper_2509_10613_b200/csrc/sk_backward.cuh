@@ -80,8 +80,14 @@ struct BwdSmem {
   static constexpr int GSTR = DP + 2;                // row stride: conflict-free 16-B accesses
   static constexpr int PS = CB * S * RC * NL;        // coarse p checkpoints of the next block
   static constexpr int XCH = NL > 32 ? 4 * (NL / 32) * SF : 0;  // cross-warp hops (2 x 2 buffers)
-  static constexpr int TOTAL = SLOTS * REC + (NK + NP + NTR) * NL + TS + T0 + LS + 2 * GS +
-                               GROWS * GSTR + 2 * DP + PS + XCH;
+  static constexpr int MAIN = SLOTS * REC + (NK + NP + NTR) * NL + TS + T0 + LS + 2 * GS +
+                              GROWS * GSTR + 2 * DP + PS + XCH;
+  // RBF node-adjoint epilogue (after the sweep, reuses the region): a band of
+  // EH node rows x NL node columns -- D tile (EH+1) x (NL+1), weights EH x
+  // (NL+1), the band's row nodes, the chunk's column nodes
+  static constexpr int EH = NL >= 128 ? 16 : 8;
+  static constexpr int EPI = (EH + 1) * (NL + 1) + EH * (NL + 1) + EH * DP + NL * DP;
+  static constexpr int TOTAL = MAIN > EPI ? MAIN : EPI;
 };
 
 //   NW    warps per pair: 1 = one pair per warp (Gram tiles, many pairs); > 1 =
@@ -382,8 +388,12 @@ bwd_kernel(Problem pb, BwdArgs ba) {
 
     // ------------------------------------------------ phase B: reverse sweep
     for (int t = u; t <= M2; t += NL) arow[t] = 0.0;
+    // RBF (and WIDE) coarse adjoint: written once per cell when one (lane,
+    // step) covers whole coarse cells, else accumulated into a zeroed buffer
+    const bool dbuf_once = MAP == DBUF && ba.rows_exclusive != 0 && K2m == 0;
     if constexpr (MAP == DBUF) {
-      for (int64_t e = u; e < (int64_t)pb.M1c * pb.M2c; e += NL) dbuf[e] = 0.0;
+      if (!dbuf_once)
+        for (int64_t e = u; e < (int64_t)pb.M1c * pb.M2c; e += NL) dbuf[e] = 0.0;
     } else {
       for (int64_t e = u; e < (int64_t)pb.M1c * DP; e += NL) gxs[e] = 0.0;
     }
@@ -679,9 +689,29 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           SK_BAR();
         }
         if constexpr (MAP == DBUF) {
-          // flush the block's coarse adjoint; lanes sharing coarse rows go in order
+          // flush the block's coarse adjoint; lanes sharing coarse rows go in
+          // order.  When one (lane, step) covers whole coarse cells (rows
+          // exclusive, F = 2^lam2) every cell is written exactly once: plain
+          // stores (no read-modify-write), bitwise the same as 0 + v.
           const bool excl = ba.rows_exclusive != 0;
-          for (int ln = excl ? 0 : NL - 1; ln >= 0; --ln) {
+          if (dbuf_once) {
+#pragma unroll
+            for (int kap = CB - 1; kap >= 0; --kap) {
+#pragma unroll
+              for (int s = S - 1; s >= 0; --s) {
+                const int jj = (js0 + kap) * S + s;
+                if (jj >= 0 && jj < NC) {
+                  const int jc = (jj * F) >> pb.lam2;
+#pragma unroll
+                  for (int c = 0; c < RC; ++c) {
+                    const int i = i0 + c;
+                    if (i < pb.M1c) dbuf[(int64_t)i * pb.M2c + jc] = SK_PB(kap, s, c);
+                  }
+                }
+              }
+            }
+          }
+          for (int ln = (excl ? 0 : NL - 1) - (dbuf_once ? NL : 0); ln >= 0; --ln) {
             if (excl || u == ln) {
 #pragma unroll
               for (int kap = CB - 1; kap >= 0; --kap) {
@@ -813,79 +843,88 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       SK_BAR();
     } else {
       // RBF node adjoint G_ij = D[i-1,j-1] - D[i-1,j] - D[i,j-1] + D[i,j] (zero
-      // padded); dF/dx_i = sum_j G_ij K_ij (y_j - x_i)/sigma^2, dF/dy_j = -sum_i (same)
+      // padded); with W_ij = G_ij K_ij / sigma^2 (one distance, one exp per
+      // node pair): dF/dx_i = sum_j W_ij (y_j - x_i), dF/dy_j = sum_i W_ij (x_i - y_j).
+      // Chunks of NL node columns (lane u owns column j0 + u and its dF/dy_j
+      // chain), bands of EH node rows staged in shared memory (D tile, row
+      // nodes); W of the band goes to shared memory and the band's dF/dx
+      // chains (row, component) continue over the chunk's columns.  Both sums
+      // run in ascending index order, as a per-(i, j) loop would.
+      constexpr int EH = SM::EH, TW = NL + 1;
       SK_BAR();
       const double* D = dbuf;
       const double* xp = pb.R.p + pr * pb.R.path_stride;
       const double* yp = cbase;
       const int L1n = pb.M1c + 1, L2n = pb.M2c + 1;
-      auto Dat = [&](int i, int j) -> double {
-        return (i >= 0 && j >= 0 && i < pb.M1c && j < pb.M2c) ? D[(int64_t)i * pb.M2c + j] : 0.0;
-      };
-      // one distance and one exp per (i, j) and side (r01 recomputed them for
-      // every component k); the per-k sums keep their order, so the values
-      // are unchanged
-      for (int i = u; i < L1n; i += NL) {
-        double xi[DP], acc[DP];
+      const int nchunk = (L2n + NL - 1) / NL;
+      double* sDt = smem + (XW ? 0 : (size_t)warp * SM::TOTAL);  // [EH+1][TW]
+      double* sW = sDt + (EH + 1) * TW;                             // [EH][TW]
+      double* sXb = sW + EH * TW;                                   // [EH][DP]
+      double* sYc = sXb + EH * DP;                                  // [NL][DP]
+      double* gxa = gxs;  // [L1n][DP] dF/dx chains between column chunks
+      for (int ch = 0; ch < nchunk; ++ch) {
+        const int j0 = ch * NL, j = j0 + u;
+        const bool jv = j < L2n;
+        const int ncol = min(NL, L2n - j0);
+        double yj[DP], gy[DP];
 #pragma unroll
         for (int k = 0; k < DP; ++k) {
-          xi[k] = xp[(int64_t)i * pb.dpad + k];
-          acc[k] = 0.0;
+          yj[k] = jv ? yp[(int64_t)j * pb.dpad + k] : 0.0;
+          gy[k] = 0.0;
+          sYc[u * DP + k] = yj[k];
         }
-        double pu = 0.0, pc = 0.0;  // D(i-1, j-1), D(i, j-1) carried along j
-        for (int j = 0; j < L2n; ++j) {
-          const double cu = Dat(i - 1, j), cc = Dat(i, j);
-          const double G = pu - cu - pc + cc;
-          pu = cu;
-          pc = cc;
-          if (G == 0.0) continue;
-          double yj[DP];
-#pragma unroll
-          for (int k = 0; k < DP; ++k) yj[k] = yp[(int64_t)j * pb.dpad + k];
-          double s2 = 0.0;  // padded components are 0 on both sides: exact no-ops
-#pragma unroll
-          for (int kk = 0; kk < DP; ++kk) {
-            const double t = xi[kk] - yj[kk];
-            s2 = fma(t, t, s2);
+        for (int i0 = 0; i0 < L1n; i0 += EH) {
+          SK_BAR();  // previous band's W consumed
+          for (int e = u; e < (EH + 1) * TW; e += NL) {
+            const int rr = e / TW, cc = e % TW;
+            const int i = i0 - 1 + rr, jd = j0 - 1 + cc;
+            sDt[e] = (i >= 0 && jd >= 0 && i < pb.M1c && jd < pb.M2c)
+                         ? D[(int64_t)i * pb.M2c + jd] : 0.0;
           }
-          const double w = G * exp(-s2 * pb.inv2s2) * pb.invs2;
-#pragma unroll
-          for (int k = 0; k < DP; ++k) acc[k] = fma(w, yj[k] - xi[k], acc[k]);
-        }
-#pragma unroll
-        for (int k = 0; k < DP; ++k)
-          if (k < dR) grad_add(gR, fxR, eR + (int64_t)i * dR + k, acc[k], atomic);
-      }
-      for (int j = u; j < L2n; j += NL) {
-        double yj[DP], acc[DP];
-#pragma unroll
-        for (int k = 0; k < DP; ++k) {
-          yj[k] = yp[(int64_t)j * pb.dpad + k];
-          acc[k] = 0.0;
-        }
-        double pl_ = 0.0, pr_ = 0.0;  // D(i-1, j-1), D(i-1, j) carried along i
-        for (int i = 0; i < L1n; ++i) {
-          const double cl = Dat(i, j - 1), cr = Dat(i, j);
-          const double G = pl_ - pr_ - cl + cr;
-          pl_ = cl;
-          pr_ = cr;
-          if (G == 0.0) continue;
-          double xi[DP];
-#pragma unroll
-          for (int k = 0; k < DP; ++k) xi[k] = xp[(int64_t)i * pb.dpad + k];
-          double s2 = 0.0;  // padded components are 0 on both sides: exact no-ops
-#pragma unroll
-          for (int kk = 0; kk < DP; ++kk) {
-            const double t = xi[kk] - yj[kk];
-            s2 = fma(t, t, s2);
+          for (int e = u; e < EH * DP; e += NL) {
+            const int i = i0 + e / DP;
+            sXb[e] = i < L1n ? xp[(int64_t)i * pb.dpad + (e % DP)] : 0.0;
           }
-          const double w = G * exp(-s2 * pb.inv2s2) * pb.invs2;
+          SK_BAR();
+#pragma unroll 2
+          for (int r = 0; r < EH; ++r) {
+            const double G = sDt[r * TW + u] - sDt[r * TW + u + 1] - sDt[(r + 1) * TW + u] +
+                             sDt[(r + 1) * TW + u + 1];
+            double w = 0.0;
+            if (G != 0.0 && jv && i0 + r < L1n) {
+              double s2 = 0.0;  // padded components are 0 on both sides: exact no-ops
 #pragma unroll
-          for (int k = 0; k < DP; ++k) acc[k] = fma(w, xi[k] - yj[k], acc[k]);
+              for (int kk = 0; kk < DP; ++kk) {
+                const double t = sXb[r * DP + kk] - yj[kk];
+                s2 = fma(t, t, s2);
+              }
+              w = G * exp(-s2 * pb.inv2s2) * pb.invs2;
+#pragma unroll
+              for (int k = 0; k < DP; ++k) gy[k] = fma(w, sXb[r * DP + k] - yj[k], gy[k]);
+            }
+            sW[r * TW + u] = w;
+          }
+          SK_BAR();
+          // dF/dx chains of the band's rows over the chunk's columns
+          for (int e = u; e < EH * dR; e += NL) {
+            const int r = e / dR, k = e % dR, i = i0 + r;
+            if (i >= L1n) continue;
+            double acc = ch == 0 ? 0.0 : gxa[(int64_t)i * DP + k];
+            const double xk = sXb[r * DP + k];
+            for (int c = 0; c < ncol; ++c) {
+              const double w = sW[r * TW + c];
+              if (w != 0.0) acc = fma(w, sYc[c * DP + k] - xk, acc);
+            }
+            if (ch == nchunk - 1) grad_add(gR, fxR, eR + (int64_t)i * dR + k, acc, atomic);
+            else gxa[(int64_t)i * DP + k] = acc;
+          }
         }
+        if (jv) {
 #pragma unroll
-        for (int k = 0; k < DP; ++k)
-          if (k < dR) grad_add(gC, fxC, eC + (int64_t)j * dR + k, acc[k], atomic);
+          for (int k = 0; k < DP; ++k)
+            if (k < dR) grad_add(gC, fxC, eC + (int64_t)j * dR + k, gy[k], atomic);
+        }
+        SK_BAR();  // sYc reused by the next chunk
       }
       SK_BAR();
     }

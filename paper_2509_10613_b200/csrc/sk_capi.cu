@@ -1017,7 +1017,9 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   pl.pck_stride = (int64_t)align_up((size_t)(nstrips * NT * Sc * (s.R / s.FR) * NL), 32);
   pl.row_stride = (int64_t)align_up((size_t)(M2 + 1), 32);
   pl.dbuf_stride = (kind == RBF || wide) ? (int64_t)align_up((size_t)(M1c * M2c), 32) : 0;
-  pl.gscr_stride = kind == LINEAR ? (int64_t)align_up((size_t)((M1c + M2c) * s.DP * nch), 32) : 0;
+  // LINEAR: increment-gradient scratch; RBF: the epilogue's dF/dx chains [M1c+1][DP]
+  pl.gscr_stride = kind == LINEAR ? (int64_t)align_up((size_t)((M1c + M2c) * s.DP * nch), 32)
+                                  : (int64_t)align_up((size_t)((M1c + 1) * s.DP), 32);
   cap_slots(pl.blocks, pl.slots, warps,
             8.0 * (pl.rowck_stride + pl.colck_stride + pl.pck_stride + pl.dbuf_stride +
                    pl.gscr_stride + 2 * pl.row_stride));
