@@ -26,9 +26,10 @@ with NCCL all-gathers.
   cpu_baseline: the C oracle (restatement of the reference algorithm,
            OpenMP over pairs, all host threads) on a bounded sub-Gram
 
-`--impl reference` times the reference's CPU algorithm (the oracle port; the
-reference itself is Python+numba and is not installed on the GPU box) on the
-same metric with all host threads.
+`--impl reference` times the reference's CPU algorithm on the same metric with
+all host threads: the C oracle port (the line's value; faster than stock
+sigcore, so the ratio is conservative) and, beside it, the unmodified sigcore
+(Python + numba, pip-installed into baseline/_ref) on the same sub-Gram step.
 """
 
 from __future__ import annotations
@@ -150,6 +151,36 @@ def cpu_baseline(n_sample, L, d, lam, budget_s=10.0):
                       f"fwd+bwd, {reps} rep(s) in {el:.1f}s; oracle/sk_oracle.c (restates "
                       f"sigcore goursat_grid+goursat_backward per pair)",
             "entries_per_s": n_sample * n_sample * reps / el}
+
+
+def small_call_latency(dev, n=2000):
+    """Per-call cost of the small-problem path (BASELINE configs[0]: 32 pairs,
+    L=64, d=4, lambda 0) through the public API sig_kernel: host time per call
+    (calls enqueued back to back, one sync) and one blocking call (enqueue,
+    kernel, sync).  Not part of the timed step."""
+    import torch
+    import paper_2509_10613_b200 as sk
+    rng = np.random.default_rng(0)
+    x = torch.as_tensor(make_paths(rng, 32, 64, 4), device=dev)
+    y = torch.as_tensor(make_paths(rng, 32, 64, 4), device=dev)
+    for _ in range(100):
+        sk.sig_kernel(x, y)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(n):
+        sk.sig_kernel(x, y)
+    torch.cuda.synchronize()
+    per_call = (time.perf_counter() - t0) / n
+    ts = []
+    for _ in range(200):
+        t1 = time.perf_counter()
+        sk.sig_kernel(x, y)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t1)
+    return {"config": "BASELINE configs[0]: sig_kernel fwd, 32 pairs, L=64, d=4, lambda=0",
+            "us_per_call_pipelined": per_call * 1e6,
+            "us_blocking_median": statistics.median(ts) * 1e6,
+            "api": "paper_2509_10613_b200.sig_kernel"}
 
 
 def config_dict(name, world):
@@ -457,6 +488,8 @@ def main():
         except (OSError, ValueError):
             traffic = None
 
+    latency = small_call_latency(dev) if (rank == 0 and world == 1 and not args.no_e2e) else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(24 if args.config == "c3" else 8, L, d, lam)
@@ -501,7 +534,7 @@ def main():
                          "executed_fma_per_cell": 27 + 4 * d,
                          "executed_frac": my_cells * (27 + 4 * d) / t_step / peak_fma},
             "e2e_autograd": e2e_autograd,
-            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks, "latency_c1": latency,
             "gpu_launches": launches_per_step * args.steps,
         }
         print(json.dumps(out), flush=True)

@@ -132,9 +132,27 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   } while (0)
   for (int k = u; k < DP; k += NL) sZero[k] = 0.0;
   SK_BAR();
-#define SK_TR(q) sTR[(q) * NL + u]
-#define SK_KB(kap, s, f, r) sK[((((kap) * S + (s)) * F + (f)) * R + (r)) * NL + u]
-#define SK_PB(kap, s, c) sP[(((kap) * S + (s)) * RC + (c)) * NL + u]
+  // small blocks (<= 32 recomputed values per lane, e.g. one coarse column of
+  // 4 x 4 fine cells): the block's forward values, top row and coarse p live in
+  // registers (every index is a compile-time constant after unrolling) instead
+  // of the per-lane shared-memory columns
+  constexpr bool REGK = SM::NK <= 32;
+  double rK[REGK ? SM::NK : 1], rP[REGK ? SM::NP : 1], rT[REGK ? SM::NTR : 1];
+  auto kb_ref = [&](int i) -> double& {
+    if constexpr (REGK) return rK[i];
+    else return sK[i * NL + u];
+  };
+  auto pb_ref = [&](int i) -> double& {
+    if constexpr (REGK) return rP[i];
+    else return sP[i * NL + u];
+  };
+  auto tr_ref = [&](int i) -> double& {
+    if constexpr (REGK) return rT[i];
+    else return sTR[i * NL + u];
+  };
+#define SK_TR(q) tr_ref(q)
+#define SK_KB(kap, s, f, r) kb_ref((((kap) * S + (s)) * F + (f)) * R + (r))
+#define SK_PB(kap, s, c) pb_ref(((kap) * S + (s)) * RC + (c))
 #define SK_REC(col)                                                                     \
   (ring + ((SLOTS & (SLOTS - 1)) == 0 ? ((col) & (SLOTS - 1))                              \
                                       : (((col) + 4 * SLOTS) % SLOTS)) * REC)
@@ -409,6 +427,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
     for (int strip = nstrips - 1; strip >= 0; --strip) {
       const int rbase = strip * H + u * R;
       const int i0 = rbase >> pb.lam1;
+      const bool seed_lane = strip == last_strip && u == u_star;
       RowRegs<KIND, DP, RC> rr;
       load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
 
@@ -579,6 +598,14 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             const int jj = js * S + s;  // column
             const bool colv = (jj >= 0) && (jj < NC);
             const double* rec = SK_REC(jj);
+            // the seed dF/dk(M1, M2) = cot enters as the final cell's "message
+            // from the right" (exactly 0 there: right of it every cell is dead),
+            // once per step instead of a test per cell: (0 + cot) + m == (0 + m) + cot
+            if (seed_lane && jj == NC - 1) {
+#pragma unroll
+              for (int r = 0; r < R; ++r)
+                if (r == r_star) aR[r] += wcot;
+            }
             double Dp[RC];
 #pragma unroll
             for (int c = 0; c < RC; ++c) Dp[c] = 0.0;
@@ -593,27 +620,26 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             for (int f = F - 1; f >= 0; --f) {
               const int q = s * F + f;                 // fine column within the step
               const int qb = (kap * S + s) * F + f;    // fine column within the block
-              const int t = jj * F + f + 1;
               double m = recv[q];
+              // no masks: dead rows (> M1) and columns (>= NC) lie below / right
+              // of the seeded final cell and their p is finite (zero-filled
+              // rows and records), so their adjoint is exactly 0; columns < 0
+              // only feed cells further left, and their D is never consumed
 #pragma unroll
               for (int r = R - 1; r >= 0; --r) {
-                const int srow = rbase + r + 1;
-                const bool live = colv && (srow <= M1);
-                double lam = aR[r] + m;
-                if (srow == M1 && t == M2) lam += wcot;
-                lam = live ? lam : 0.0;
+                const double lam = aR[r] + m;
                 const int c = r / FR;
                 const double a = cf[c].A * lam;
                 const double b = cf[c].B * lam;
                 // forward values around the cell: left, up, up-left
-                const double kL = (qb > 0) ? sK[((qb - 1) * R + r) * NL + u] : kleft[r];
-                const double kU = (r > 0) ? sK[(qb * R + r - 1) * NL + u] : SK_TR(qb + 1);
-                const double kD = (r > 0) ? ((qb > 0) ? sK[((qb - 1) * R + r - 1) * NL + u]
+                const double kL = (qb > 0) ? kb_ref((qb - 1) * R + r) : kleft[r];
+                const double kU = (r > 0) ? kb_ref(qb * R + r - 1) : SK_TR(qb + 1);
+                const double kD = (r > 0) ? ((qb > 0) ? kb_ref((qb - 1) * R + r - 1)
                                                       : kleft[r - 1])
                                           : SK_TR(qb);
                 const double p6 = pk[c] * (1.0 / 6.0);
                 const double wv = fma(kL + kU, 0.5 + p6, kD * p6);
-                if (live) Dp[c] = fma(lam, wv, Dp[c]);
+                Dp[c] = fma(lam, wv, Dp[c]);
                 m = a - bR[r];
                 aR[r] = a;
                 bR[r] = b;

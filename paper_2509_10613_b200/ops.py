@@ -17,8 +17,34 @@ def _ptr(t):
     return t.data_ptr() if t is not None else None
 
 
+def _dev_index(device) -> int:
+    if device is None:
+        return torch.cuda.current_device()
+    return device.index if device.index is not None else torch.cuda.current_device()
+
+
 def _stream(device=None):
-    return torch.cuda.current_stream(device).cuda_stream
+    """Raw handle of torch's current stream on `device` (no Stream object)."""
+    return torch._C._cuda_getCurrentRawStream(_dev_index(device))
+
+
+class _NoDevSwitch:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
+_NO_SWITCH = _NoDevSwitch()
+
+
+def _on(device):
+    """Make `device` current for the enclosed launches; free when it already is
+    (the common case: small calls pay no device switch)."""
+    if device.index is None or device.index == torch.cuda.current_device():
+        return _NO_SWITCH
+    return torch.cuda.device(device)
 
 
 def _same_device(t, ref, name):
@@ -37,8 +63,25 @@ def _cotangent(cot, shape, ref, name="cotangent"):
     return cot.to(torch.float64).contiguous()
 
 
+_WS_CACHE: dict = {}
+_WS_CACHE_MAX = 64 << 20  # small workspaces are kept per (device, stream)
+
+
 def _workspace(nbytes: int, device) -> torch.Tensor:
-    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+    """Scratch for one C-ABI call.  Workspaces up to 64 MiB are cached per
+    (device, current stream) and reused: calls on one stream run in order, so
+    a later call never overwrites scratch a queued kernel still reads.  Larger
+    ones come from the caching allocator per call."""
+    nbytes = max(int(nbytes), 1)
+    if nbytes > _WS_CACHE_MAX:
+        return torch.empty(nbytes, dtype=torch.uint8, device=device)
+    idx = _dev_index(device)
+    key = (idx, torch._C._cuda_getCurrentRawStream(idx))
+    buf = _WS_CACHE.get(key)
+    if buf is None or buf.numel() < nbytes:
+        buf = torch.empty(max(nbytes, 1 << 20), dtype=torch.uint8, device=device)
+        _WS_CACHE[key] = buf
+    return buf[:nbytes]
 
 
 def _paths(t: torch.Tensor, name: str) -> torch.Tensor:
@@ -103,7 +146,7 @@ def forward_batch(x, y, lam1: int, lam2: int, kind: int, sigma: float,
     out = torch.empty(B, dtype=torch.float64, device=x.device)
     if B == 0:
         return out
-    with torch.cuda.device(x.device):
+    with _on(x.device):
         nb = lib.sk_forward_batch_tf_workspace_bytes(B, L1, L2, d, lam1, lam2, kind, tf)
         ws = _workspace(nb, x.device)
         _lib.check(lib.sk_forward_batch_tf(_ptr(x), _ptr(y), B, L1, L2, d, lam1, lam2, kind,
@@ -124,7 +167,7 @@ def forward_gram(x, y, lam1: int, lam2: int, kind: int, sigma: float,
         out = torch.empty((r1 - r0, n2), dtype=torch.float64, device=x.device)
     if n1 == 0 or n2 == 0 or r1 <= r0:
         return out
-    with torch.cuda.device(x.device):
+    with _on(x.device):
         nb = lib.sk_forward_gram_tf_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind, int(sym),
                                                     tf)
         ws = _workspace(nb, x.device)
@@ -157,7 +200,7 @@ def forward_batch_f32(x, y, lam1: int, lam2: int, transform=None) -> torch.Tenso
     out = torch.empty(B, dtype=torch.float32, device=x.device)
     if B == 0:
         return out
-    with torch.cuda.device(x.device):
+    with _on(x.device):
         nb = lib.sk_forward_batch_f32_workspace_bytes(B, L1, y.shape[1], d, lam1, lam2, tf)
         ws = _workspace(nb, x.device)
         _lib.check(lib.sk_forward_batch_f32(_ptr(x), _ptr(y), B, L1, y.shape[1], d, lam1, lam2,
@@ -182,7 +225,7 @@ def forward_gram_f32(x, y, lam1: int, lam2: int, rows=None, transform=None) -> t
     out = torch.empty((r1 - r0, n2), dtype=torch.float32, device=x.device)
     if n1 == 0 or n2 == 0 or r1 <= r0:
         return out
-    with torch.cuda.device(x.device):
+    with _on(x.device):
         nb = lib.sk_forward_gram_f32_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, int(sym), tf)
         ws = _workspace(nb, x.device)
         _lib.check(lib.sk_forward_gram_f32(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
@@ -197,7 +240,7 @@ def solve_delta(delta: torch.Tensor, lam1: int, lam2: int) -> torch.Tensor:
     delta = delta.to(torch.float64).contiguous()
     B, r1, r2 = delta.shape
     out = torch.empty(B, dtype=torch.float64, device=delta.device)
-    with torch.cuda.device(delta.device):
+    with _on(delta.device):
         nb = lib.sk_solve_delta_workspace_bytes(B, r1, r2, lam1, lam2)
         ws = _workspace(nb, delta.device)
         _lib.check(lib.sk_solve_delta(_ptr(delta), B, r1, r2, lam1, lam2, _ptr(out), _ptr(ws),
@@ -211,7 +254,7 @@ def solve_delta_grid(delta: torch.Tensor, lam1: int, lam2: int) -> torch.Tensor:
     r1, r2 = delta.shape
     grid = torch.empty(((r1 << lam1) + 1, (r2 << lam2) + 1), dtype=torch.float64,
                        device=delta.device)
-    with torch.cuda.device(delta.device):
+    with _on(delta.device):
         _lib.check(lib.sk_solve_delta_grid(_ptr(delta), r1, r2, lam1, lam2, _ptr(grid),
                                            _stream(delta.device)))
     return grid
@@ -236,7 +279,7 @@ def backward_batch(x, y, lam1, lam2, kind, sigma, cot, want_values=False, transf
     vals = torch.empty(B, dtype=torch.float64, device=x.device) if want_values else None
     if B == 0:
         return vals, gx, gy
-    with torch.cuda.device(x.device):
+    with _on(x.device):
         nb = lib.sk_backward_batch_tf_workspace_bytes(B, L1, L2, d, lam1, lam2, kind, tf)
         ws = _workspace(nb, x.device)
         _lib.check(lib.sk_backward_batch_tf(_ptr(x), _ptr(y), B, L1, L2, d, lam1, lam2, kind,
@@ -274,7 +317,7 @@ class GradAcc:
         (every call and rank sharing this gradient must pass the same one)."""
         lib = _lib.load()
         cot = _cotangent(cot, (n1, n2), self.blob)
-        with torch.cuda.device(self.blob.device):
+        with _on(self.blob.device):
             _lib.check(lib.sk_grad_acc_init(_ptr(self.blob), *self.tshape, _ptr(cot), n1, n2,
                                             int(bool(symmetric)), _stream(self.blob.device)))
         return self
@@ -290,7 +333,7 @@ class GradAcc:
             raise InvalidArgument(f"out must be a contiguous float64 tensor of shape {self.shape}")
         _same_device(out, self.blob, "out")
         dev = self.blob.device
-        with torch.cuda.device(dev):
+        with _on(dev):
             if self.tf == 0:
                 _lib.check(lib.sk_grad_acc_finalize(_ptr(self.blob), *self.tshape, _ptr(out),
                                                     int(bool(accumulate)), _stream(dev)))
@@ -344,7 +387,7 @@ def _gram_backward(x, y, lam1, lam2, kind, sigma, cot, rows, out, grad_x, grad_y
             _check_acc(acc_y, n2, L2, d, tf, x, "acc_y")
         if n1 == 0 or n2 == 0 or r1 <= r0:
             return acc_x, acc_y
-        with torch.cuda.device(dev):
+        with _on(dev):
             nb = lib.sk_backward_gram_acc_tf_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind,
                                                              int(sym), tf)
             ws = _workspace(nb, dev)
@@ -362,7 +405,7 @@ def _gram_backward(x, y, lam1, lam2, kind, sigma, cot, rows, out, grad_x, grad_y
         _grad_buffer(grad_y, yy, "grad_y")
     if n1 == 0 or n2 == 0 or r1 <= r0:
         return grad_x, grad_y
-    with torch.cuda.device(dev):
+    with _on(dev):
         nb = lib.sk_backward_gram_tf_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind,
                                                      int(sym), tf)
         ws = _workspace(nb, dev)
@@ -411,7 +454,7 @@ def mirror_upper(G: torch.Tensor) -> torch.Tensor:
     """In place: lower triangle := upper triangle (kernel.py:177-179)."""
     lib = _lib.load()
     n = G.shape[0]
-    with torch.cuda.device(G.device):
+    with _on(G.device):
         _lib.check(lib.sk_mirror_upper(_ptr(G), n, G.stride(0), _stream(G.device)))
     return G
 

@@ -104,7 +104,7 @@ def signature_forward(x, depth: int, transform=None, times=None) -> torch.Tensor
         raise InvalidArgument("signature too large")
     t = _times(times, L, x.device)
     out = torch.empty((B, total), dtype=torch.float64, device=x.device)
-    with torch.cuda.device(x.device):
+    with ops._on(x.device):
         nb = lib.sk_signature_workspace_bytes(B, L, d, depth, tf)
         if B and nb == 0:
             _lib.check(lib.sk_signature(None, None, B, L, d, depth, tf, None, None, 0, None))
@@ -127,7 +127,7 @@ def signature_backward_t(x, depth: int, cot, transform=None, times=None) -> torc
     grad = torch.empty_like(x)
     if B == 0:
         return grad
-    with torch.cuda.device(x.device):
+    with ops._on(x.device):
         nb = lib.sk_signature_backward_workspace_bytes(B, L, d, depth, tf)
         if nb == 0:
             _lib.check(lib.sk_signature_backward(None, None, B, L, d, depth, tf, None, None, None,

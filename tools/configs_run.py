@@ -74,4 +74,21 @@ t = timed(lambda: sk.sig_kernel_gram_value_and_grad(X, None, ones), 1)
 c = 2048 * 2049 // 2 * 1023 ** 2
 out["C5-shape sub-Gram 2048^2 L1024 d8 fused G+grad (full 8192^2: profiles/r01_c5_full_1gpu_fused.json)"] = {
     "s": t, "cells_per_s": c / t, "frac": c * sum(dp(8, 0, 0)) / t / peak}
+# FP32-arithmetic forward kernels (precision='fp32', linear kernel) against the
+# FP32 FMA pipe: 148 SMs x 128 lanes x 1.965 GHz (max SM clock) (FP32 instr/cell: the
+# small-correction cell is 5 + (d + 4)/2^(l1+l2), sk_cell.cuh Coef32)
+peak32 = 148 * 128 * 1.965e9
+X32 = paths(rng, 1024, 512, 16).float()
+t = timed(lambda: ops.forward_gram_f32(X32, None, 0, 0), 2)
+c = 1024 * 1025 // 2 * 511 ** 2
+out["C3-shape Gram fwd FP32 arithmetic"] = {"s": t, "cells_per_s": c / t,
+                                            "frac_fp32": c * (5 + 20) / t / peak32,
+                                            "peak_fp32_fma_per_s": peak32}
+x, y = paths(rng, 128, 8192, 4).float(), paths(rng, 128, 8192, 4).float()
+t = timed(lambda: ops.forward_batch_f32(x, y, 1, 1), 5)
+c = 128 * 16382 ** 2
+out["C4 sig_kernel fwd FP32 arithmetic"] = {"s": t, "cells_per_s": c / t,
+                                            "frac_fp32": c * (5 + 8 / 4) / t / peak32}
+import bench  # noqa: E402
+out["C1 latency"] = bench.small_call_latency(torch.device("cuda", 0))
 print(json.dumps(out, indent=1))
