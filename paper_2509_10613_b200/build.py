@@ -28,8 +28,8 @@ def _deps():
         os.path.join(HERE, "..", "include", "sigkernel.h")]
 
 
-def _compile(src: str, extra: list[str]) -> str:
-    obj = os.path.join(OUT, os.path.splitext(src)[0] + ".o")
+def _compile(src: str, extra: list[str], out: str = OUT) -> str:
+    obj = os.path.join(out, os.path.splitext(src)[0] + ".o")
     newest = max(os.path.getmtime(p) for p in _deps())
     if os.path.exists(obj) and os.path.getmtime(obj) >= newest:
         return obj
@@ -40,20 +40,31 @@ def _compile(src: str, extra: list[str]) -> str:
     return obj
 
 
-def build(verbose: bool = False, extra: list[str] | None = None) -> str:
-    os.makedirs(OUT, exist_ok=True)
+def build(verbose: bool = False, extra: list[str] | None = None, out: str = OUT) -> str:
+    """Compile every translation unit into `out` (default: the in-tree
+    _native/; experiment variants with extra flags go to their own directory,
+    selected at run time with SK_LIBSIGKERNEL)."""
+    os.makedirs(out, exist_ok=True)
+    so = os.path.join(out, "libsigkernel.so")
     extra = list(extra or [])
     if verbose:
         extra += ["-Xptxas", "-v"]
     with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, extra), SOURCES))
-    if not os.path.exists(SO) or os.path.getmtime(SO) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", SO, *objs, "-lcudart"]
+        objs = list(ex.map(lambda s: _compile(s, extra, out), SOURCES))
+    if not os.path.exists(so) or os.path.getmtime(so) < max(os.path.getmtime(o) for o in objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", so, *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    return SO
+    return so
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    # python -m paper_2509_10613_b200.build [-v] [--variant NAME -DFLAG ...]
+    args = sys.argv[1:]
+    if "--variant" in args:
+        i = args.index("--variant")
+        name, flags = args[i + 1], [a for a in args[i + 2:] if a != "-v"]
+        print(build(verbose="-v" in args, extra=flags, out=os.path.join(OUT, "variants", name)))
+    else:
+        print(build(verbose="-v" in args))

@@ -59,7 +59,7 @@ inline BwdFn sk_bwd_select(const BwdShape& s, int& smem_doubles) {
 template <int KIND, int DP, int R, int FR, int F, int NW>
 inline void sk_bwd_leaf_xw(BwdFn& fn, int& smem_doubles) {
   constexpr int S = bwd_steps_cols(DP, F);
-  constexpr int CB = bwd_block_steps(DP, R, F, S);
+  constexpr int CB = bwd_block_steps_xw(R, F, S);
   constexpr int MAP = (KIND == LINEAR) ? FUSED : DBUF;
   fn = bwd_kernel<KIND, DP, R, FR, F, CB, MAP, S, NW>;
   smem_doubles = BwdSmem<DP, R, R / FR, F, CB, S, 32 * NW>::TOTAL;  // per CTA

@@ -1009,7 +1009,9 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   pl.slots = pl.blocks * warps;
   const int64_t M1 = M1c << lamR, M2 = M2c << lamC;
   const int64_t Sc = bwd_steps_cols(s.DP, s.F), NC = M2 / s.F, NSTEP = (NC + Sc - 1) / Sc,
-                NT = NSTEP + NL - 1, CB = bwd_block_steps(s.DP, s.R, s.F, (int)Sc),
+                NT = NSTEP + NL - 1,
+                CB = s.NW > 1 ? bwd_block_steps_xw(s.R, s.F, (int)Sc)
+                              : bwd_block_steps(s.DP, s.R, s.F, (int)Sc),
                 NB = (NT + CB - 1) / CB;
   const int64_t nstrips = (M1 + NL * s.R - 1) / (NL * s.R);
   pl.rowck_stride = (int64_t)align_up((size_t)(nstrips * NT * Sc * s.F * NL), 32);

@@ -69,6 +69,14 @@ constexpr int bwd_block_steps(int DP, int R, int F, int S) {
                                                    : (DP >= 16 ? 8 : 16) / (F * R * S);
 }
 
+// cross-warp (one pair per CTA) backward: fine cells per lane per block
+#ifndef SK_XW_CBV
+#define SK_XW_CBV 32  // measured at C2: 16 -> 2.02 ms, 32 -> 1.61 ms, 64 (shared memory) 2.98 ms
+#endif
+constexpr int bwd_block_steps_xw(int R, int F, int S) {
+  return (SK_XW_CBV / (F * R * S)) < 1 ? 1 : (SK_XW_CBV / (F * R * S)) > 8 ? 8 : SK_XW_CBV / (F * R * S);
+}
+
 inline int bwd_rows_per_lane(int DP) {
   if (DP != 16) return rows_per_lane(DP);
   const char* e = std::getenv("SK_BWD_R16");  // tuning override (1 or 2)
