@@ -45,6 +45,20 @@ __host__ __device__ constexpr int ring_slots(int lanes, int S, int PF) {
          : ((lanes + PF + 1) * S) <= 512 ? 512 : ((lanes + PF + 1) * S) <= 1024 ? 1024 : 2048;
 }
 
+// Cross-warp (XW) pairs: lane 0 of warp w runs SK_XW_LAG steps behind lane 31
+// of warp w-1 (instead of one), so the cross-warp hops of SK_XW_LAG steps
+// travel together and the CTA meets at a barrier once per SK_XW_LAG steps
+// (measured at BASELINE config 2: the per-step barrier was the top stall).
+// Costs (LAG-1)(W-1) extra skew steps per strip.
+#ifndef SK_XW_LAG
+#define SK_XW_LAG 4
+#endif
+// ring records in flight for an XW CTA of `lanes` lanes: every lane's column,
+// the extra inter-warp skew, a LAG-step chunk of drift, LAG + PF - 1 prefetched steps
+__host__ __device__ constexpr int xw_ring_slots(int lanes, int S, int PF) {
+  return ring_slots(lanes + (SK_XW_LAG - 1) * (lanes / 32) + 2 * SK_XW_LAG, S, PF);
+}
+
 template <bool XW, int G, int S>
 struct FwdRing {
   static constexpr int PF = 2;  // steps in flight
@@ -116,7 +130,8 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
   extern __shared__ double smem_fwd_raw[];
   T* smem_fwd = reinterpret_cast<T*>(smem_fwd_raw);
   T* hand = reinterpret_cast<T*>(hand_);
-  __shared__ T xbuf[XW ? 2 : 1][XW ? 16 : 1][SF];
+  constexpr int XK = XW ? SK_XW_LAG : 1;  // steps per cross-warp chunk
+  __shared__ T xbuf[XW ? 2 * XK : 1][XW ? 16 : 1][SF];
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -125,7 +140,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
   const int g = XW ? 0 : lane / G;
   const int u = XW ? (int)threadIdx.x : lane % G;
   T* ring = XW ? smem_fwd : smem_fwd + (size_t)warp * SLOTS * REC;
-  const int smask = (XW ? ring_slots((int)blockDim.x, S, PF) : SLOTS) - 1;
+  const int smask = (XW ? xw_ring_slots((int)blockDim.x, S, PF) : SLOTS) - 1;
 
   const int M1 = pb.M1c << pb.lam1;
   const int M2 = pb.M2c << pb.lam2;
@@ -176,8 +191,11 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
 #pragma unroll
         for (int c = 0; c <= RC; ++c) Kl[c] = Kr[c];
       }
+      // XW: records of LAG + PF - 1 steps ahead, so a whole LAG-step chunk has
+      // landed at the chunk's barrier with PF groups still in flight
+      constexpr int LOOK = XW ? XK + PF - 1 : PF;
       if (issuer) {
-        for (int q = 0; q < PF; ++q)
+        for (int q = 0; q < LOOK; ++q)
           fwd_issue<KIND, DP, F, P, S, T>(ring, smask, pb, pc, hrow0, hand_stride, q * S, NC,
                                           strip, lane);
       }
@@ -277,7 +295,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
       for (int q = 0; q < SF; ++q) bot[q] = T(1);
       // wide paths (DP >= 16) pipeline the next step's coefficients behind the
       // recurrence; narrow ones keep the registers for S columns per step
-      constexpr bool PIPE = DP >= 16 || (!XW && G == 32 && R <= 2);  // (short paths: latency)
+      constexpr bool PIPE = !XW && (DP >= 16 || (G == 32 && R <= 2));  // (short paths: latency)
       Cf cf[S][RC];
       if constexpr (PIPE) {
         if (issuer) cp_async_wait<PF - 1>();  // step 0 landed
@@ -285,16 +303,28 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
         step_coefs(-u, cf);
       }
 
-      const int nsteps = NSTEP + Grt - 1;
+      const int lagw = XW ? (XK - 1) * warp : 0;  // extra skew of this warp (XW)
+      const int nsteps = NSTEP + Grt - 1 + (XW ? (XK - 1) * (nw - 1) : 0);
       for (int tau = 0; tau < nsteps; ++tau) {
-        if (issuer) {
-          fwd_issue<KIND, DP, F, P, S, T>(ring, smask, pb, pc, hrow0, hand_stride,
-                                          (tau + PF) * S, NC, strip, lane);
-          if constexpr (PIPE) cp_async_wait<PF - 1>();  // steps <= tau + 1 landed
-          else cp_async_wait<PF>();                     // step tau landed
+        if constexpr (XW) {
+          // once per chunk: steps tau .. tau + XK - 1 landed, hops of the last
+          // chunk visible, the chunk before it consumed
+          if (issuer) {
+            fwd_issue<KIND, DP, F, P, S, T>(ring, smask, pb, pc, hrow0, hand_stride,
+                                            (tau + LOOK) * S, NC, strip, lane);
+            if (tau % XK == 0) cp_async_wait<PF>();
+          }
+          if (tau % XK == 0) __syncthreads();
+        } else {
+          if (issuer) {
+            fwd_issue<KIND, DP, F, P, S, T>(ring, smask, pb, pc, hrow0, hand_stride,
+                                            (tau + PF) * S, NC, strip, lane);
+            if constexpr (PIPE) cp_async_wait<PF - 1>();  // steps <= tau + 1 landed
+            else cp_async_wait<PF>();                     // step tau landed
+          }
+          __syncwarp();
         }
-        if (XW) __syncthreads(); else __syncwarp();
-        const int js = tau - u;
+        const int js = tau - u - lagw;
         const bool active = (js >= 0) && (js < NSTEP);
         // software pipeline: next step's coefficients overlap this step's recurrence
         Cf cfn[PIPE ? S : 1][RC];
@@ -306,7 +336,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
           for (int q = 0; q < SF; ++q) tv[q] = __shfl_up_sync(0xffffffffu, bot[q], 1);
           if (lane == 0 && warp > 0) {
 #pragma unroll
-            for (int q = 0; q < SF; ++q) tv[q] = xbuf[(tau + 1) & 1][warp - 1][q];
+            for (int q = 0; q < SF; ++q) tv[q] = xbuf[(tau + XK) % (2 * XK)][warp - 1][q];
           }
         } else {
 #pragma unroll
@@ -366,7 +396,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
         if constexpr (XW) {
           if (lane == 31) {
 #pragma unroll
-            for (int q = 0; q < SF; ++q) xbuf[tau & 1][warp][q] = bot[q];
+            for (int q = 0; q < SF; ++q) xbuf[tau % (2 * XK)][warp][q] = bot[q];
           }
         }
       }
@@ -381,7 +411,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
 template <int KIND, int DP, int F, int G, bool XW, int S, typename T = double>
 constexpr int fwd_smem_bytes(int warps) {
   using Rec = FwdRec<KIND, DP, F, XW ? 1 : 32 / G, T>;
-  return XW ? ring_slots(32 * warps, S, FwdRing<XW, G, S>::PF) * Rec::REC * (int)sizeof(T)
+  return XW ? xw_ring_slots(32 * warps, S, FwdRing<XW, G, S>::PF) * Rec::REC * (int)sizeof(T)
             : warps * FwdRing<XW, G, S>::SLOTS * Rec::REC * (int)sizeof(T);
 }
 

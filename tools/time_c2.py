@@ -8,7 +8,7 @@ import torch
 sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
 from paper_2509_10613_b200 import ops  # noqa: E402
 
-kind = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+kind = int(sys.argv[1]) if len(sys.argv) > 1 and __name__ == "__main__" else 1
 rng = np.random.default_rng(0)
 
 
@@ -28,7 +28,8 @@ def timed(fn, reps=10):
     return a.elapsed_time(b) / reps
 
 
-x, y = paths(256, 256, 8), paths(256, 256, 8)
-tf = timed(lambda: ops.forward_batch(x, y, 2, 2, kind, 1.0))
-tb = timed(lambda: ops.backward_batch(x, y, 2, 2, kind, 1.0, None, want_values=True))
-print(f"C2 kind={kind}: fwd {tf:.3f} ms, bwd {tb:.3f} ms, total {tf + tb:.3f} ms")
+if __name__ == "__main__":
+    x, y = paths(256, 256, 8), paths(256, 256, 8)
+    tf = timed(lambda: ops.forward_batch(x, y, 2, 2, kind, 1.0))
+    tb = timed(lambda: ops.backward_batch(x, y, 2, 2, kind, 1.0, None, want_values=True))
+    print(f"C2 kind={kind}: fwd {tf:.3f} ms, bwd {tb:.3f} ms, total {tf + tb:.3f} ms")
