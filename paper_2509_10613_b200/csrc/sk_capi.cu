@@ -946,10 +946,13 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
     pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + s.WPC - 1) / s.WPC,
                                                        (int64_t)occ * sms));
     pl.slots = pl.blocks * s.WPC;
-    const int64_t nstrips = (M1c + 7) / 8, NT8 = (M2c + 10) / 8, NTS = 8 * (NT8 + 2);
-    pl.rowck_stride = nstrips * NTS * 32;
+    const int64_t nstrips = (M1c + 7) / 8, NT8 = (M2c + 10) / 8;
+    // rowck: the strips' top rows [strip][8 pairs][8 (NT8 + 5)]; colck: every
+    // lane's two values per block (double2); pck: its bottom value a column
+    // before (sk_mma_bwd.cuh)
+    pl.rowck_stride = nstrips * 8 * 8 * (NT8 + 5);
     pl.colck_stride = nstrips * NT8 * 32 * 2;
-    pl.pck_stride = 0;
+    pl.pck_stride = nstrips * NT8 * 32;
     // per pair, 8 pairs per slot: the adjoint row sits at column + 3 and the
     // handoff row is prefetched 4 iterations (32 columns) ahead
     pl.row_stride = 8 * (NT8 + 5);
@@ -957,8 +960,8 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
     pl.gscr_stride = 8 * NT8 * s.DP;
     pl.rsum_stride = 8 * M1c * s.DP;
     cap_slots(pl.blocks, pl.slots, s.WPC,
-              8.0 * (pl.rowck_stride + pl.colck_stride + pl.gscr_stride + pl.rsum_stride +
-                     16 * pl.row_stride));
+              8.0 * (pl.rowck_stride + pl.colck_stride + pl.pck_stride + pl.gscr_stride +
+                     pl.rsum_stride + 16 * pl.row_stride));
     return SK_OK;
   }
   s.R = bwd_rows_per_lane(s.DP);

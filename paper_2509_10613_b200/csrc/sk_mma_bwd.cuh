@@ -76,7 +76,8 @@ struct MmaBwdCfg {
   static constexpr int XSTR = DP;              // doubles per staged dX row
   // block-input staging (cp.async, lane-private, double buffered): 9 top-row
   // values + 2 left values per lane, 8 strip-below messages per lane group
-  static constexpr int STG = 11 * 32 + 8 * 8;
+  // + the block's column checkpoints of all 32 lanes' previous bottom value
+  static constexpr int STG = 11 * 32 + 8 * 8 + 32;
   static constexpr int WARP_DOUBLES = 2 * PTILE * 2 + 2 * DTILE + 64 * XSTR + STG;
 };
 
@@ -104,12 +105,16 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
   const int M1 = pb.M1c, NC = pb.M2c;
   const int nstrips = (M1 + 7) >> 3;
   const int NT8 = (NC + 3 + 7) >> 3;
-  const int NTS = 8 * (NT8 + 2);  // diagonal rows per strip in rowck
+  const int TRS = 8 * (NT8 + 5);  // doubles per strip top row (per pair)
   const int u_star = ((M1 - 1) & 7) >> 1, r_star = (M1 - 1) & 1;  // lane/row of the final cell
   const int64_t slot = (int64_t)blockIdx.x * WPC + warp;
-  double* __restrict__ rowck = ba.rowck + slot * ba.rowck_stride;
+  // strip top rows trow[strip][pair g][TRS] (= lane u = 3's bottom row of the
+  // strip above, written in phase A, read by lane u = 0 in both phases)
+  double* __restrict__ trows = ba.rowck + slot * ba.rowck_stride + (int64_t)g * TRS;
+  // the lane's bottom value one column before its block boundary,
+  // colck2[strip][blk][lane] (with colck: lane u-1's inputs to lane u's recompute)
+  double* __restrict__ colck2 = ba.pck + slot * ba.pck_stride;
   double2* __restrict__ colck = reinterpret_cast<double2*>(ba.colck + slot * ba.colck_stride);
-  double* __restrict__ hrow = ba.hand + (slot * 8 + g) * ba.row_stride;
   double* __restrict__ arow = ba.adj + (slot * 8 + g) * ba.row_stride;
   double* __restrict__ gcs = ba.gscr + slot * ba.gscr_stride;  // column gradients [8*NT8][DP]
   const FixAcc fxR = fix_make(ba.accR, ba.metaR), fxC = fix_make(ba.accC, ba.metaC);
@@ -190,6 +195,8 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
     if (PFB) load_bf(0, bfn);
     for (int strip = 0; strip < ((ba.exp & 2) ? 0 : nstrips); ++strip) {
       __syncwarp();
+      const double* __restrict__ trow_cur = trows + (int64_t)strip * 8 * TRS;
+      double* __restrict__ trow_next = trows + (int64_t)(strip + 1) * 8 * TRS;
       double bf[8][KS];
       if constexpr (PFB) {
 #pragma unroll
@@ -226,7 +233,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         if (strip > 0 && u == 0) {
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            cp_async16(sH + (T & 7) * 64 + g * 8 + 2 * q, hrow + 8 * T + 2 * q, true);
+            cp_async16(sH + (T & 7) * 64 + g * 8 + 2 * q, trow_cur + 8 * T + 2 * q, true);
         }
         const int t = T + 2;
 #pragma unroll
@@ -242,9 +249,10 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       for (int T = 0; T < HPD; ++T) issue_in(T);
       // checkpoint rows keep lane (g, u) at position 8u + g, so lane u = 3's
       // values (the strip handoff) are one contiguous 64-B quarter row
-      double* __restrict__ rck = rowck + (int64_t)strip * NTS * 32 + 8 * u + g;
       double2* __restrict__ cck = colck + (int64_t)strip * NT8 * 32 + lane;
+      double* __restrict__ cck2 = colck2 + (int64_t)strip * NT8 * 32 + lane;
       double kl0 = 1.0, kl1 = 1.0, topc = 1.0, bot = 1.0;
+      double bprev = 1.0;  // the lane's bottom value one column before kl1
       const bool last = strip == nstrips - 1;
       __syncwarp();
       // one 8-step iteration; EDGE iterations hold columns outside [0, NC)
@@ -263,8 +271,10 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         for (int kk = 0; kk < KS; ++kk) acur[kk] = sA[(((T + 2) % RA) * 8 + g) * DP + 4 * kk + u];
         // checkpoints are read back only after the whole item's forward: for
         // d = 16 stream them past L2 (evict-first; measured +0.5 %, -2.5 % at d = 8)
-        if constexpr (DP == 16) __stcs(cck + (int64_t)T * 32, make_double2(kl0, kl1));
-        else cck[(int64_t)T * 32] = make_double2(kl0, kl1);  // values at node column 8T - u
+        // values at node column 8T - u (and the bottom one a column before):
+        // read back only after the item's forward, so stream them past L2
+        __stcs(cck + (int64_t)T * 32, make_double2(kl0, kl1));
+        __stcs(cck2 + (int64_t)T * 32, bprev);
         double2* __restrict__ r0 = aslot(T);
         double2* __restrict__ r1 = aslot(T - 1);
         const int s0 = T & 1, s1 = (T - 1) & 1;  // slot within the ring half
@@ -282,13 +292,12 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
             const double k1 = cell(k0, kl1, kl0, c1);
             topc = tv;
             kl0 = k0;
+            bprev = kl1;
             kl1 = k1;
             bot = k1;
-            if (u == 3 && !last) hrow[c] = k1;
+            if (u == 3 && !last) trow_next[c] = k1;
             if (EDGE && last && u == u_star && c == NC - 1) kval = r_star ? k1 : k0;
           }
-          if constexpr (DP == 16) __stcs(rck + (int64_t)(8 * T + m) * 32, bot);
-          else rck[(int64_t)(8 * T + m) * 32] = bot;  // diagonal index = column + lane
         }
         __syncwarp();  // tile T+2 visible, tile T-1 dead
       };
@@ -296,8 +305,6 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         if (T == 0 || 8 * T + 8 > NC) iterA(std::true_type{}, T);
         else iterA(std::false_type{}, T);
       }
-      // rows read by the phase-B recompute past the last step: keep them finite
-      for (int e = 8 * NT8; e < NTS; ++e) rck[(int64_t)e * 32] = bot;
       cp_async_wait<0>();
     }
 
@@ -312,26 +319,26 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       __syncwarp();
       const int rb = strip * 8 + 2 * u;  // lane's first fine row (0-based)
       const bool fin0 = (rb == M1 - 1), fin1 = (rb + 1 == M1 - 1);
-      const double* __restrict__ rck_own = rowck + (int64_t)strip * NTS * 32;
-      const double* __restrict__ rck_up = rowck + (int64_t)max(strip - 1, 0) * NTS * 32;
+      const double* __restrict__ trow_cur = trows + (int64_t)strip * 8 * TRS;
       const double2* __restrict__ cck0 = colck + (int64_t)strip * NT8 * 32;
+      const double* __restrict__ cck20 = colck2 + (int64_t)strip * NT8 * 32;
       const bool below = strip < nstrips - 1;
 
-      // block inputs staged by cp.async one block ahead (lane-private records):
-      // top row tv[i] = node column 8blk-u+i of the row above the lane (i = 0..8),
-      // the lane's two values at node column 8blk-u, and (lane u = 3) the
-      // adjoint messages of the strip below at columns 8blk-3 .. 8blk+4, which
-      // arow holds at index column + 3 (16-byte aligned per block)
+      // block inputs staged by cp.async one block ahead: lane u = 0's top row
+      // tv[i] = node column 8blk+i of the strip's top row (i = 0..8), every
+      // lane's two values at its node column 8blk-u and its bottom value a
+      // column before (lane u > 0 starts its recompute from lane u-1's), and
+      // (lane u = 3) the adjoint messages of the strip below at columns
+      // 8blk-3 .. 8blk+4, which arow holds at index column + 3
       auto stage_block = [&](int blk) {
         double* st = sS;
-        // lane-private: the 9 checkpoint values above the lane (lane u-1 of this
-        // strip, or lane 3 of the strip above: a contiguous 64-B quarter row)
-        const double* src0 = (u > 0) ? rck_own + 8 * (u - 1) + g : rck_up + 24 + g;
-        const int t0 = (u > 0) ? 8 * blk - 2 : 8 * blk + 2;
+        if (u == 0) {
 #pragma unroll
-        for (int i = 0; i < 9; ++i)
-          cp_async8(st + i * 32 + lane, src0 + (int64_t)max(t0 + i, 0) * 32, u > 0 || strip > 0);
+          for (int i = 0; i < 9; ++i)
+            cp_async8(st + i * 32 + lane, trow_cur + max(8 * blk - 1 + i, 0), strip > 0);
+        }
         cp_async16(st + 9 * 32 + 2 * lane, cck0 + (int64_t)blk * 32 + lane, true);
+        cp_async8(st + 11 * 32 + 64 + lane, cck20 + (int64_t)blk * 32 + lane, true);
         if (u == 3) {
 #pragma unroll
           for (int i = 0; i < 8; i += 2)
@@ -379,16 +386,26 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
 #pragma unroll
         for (int n = 0; n < NN; ++n)
           gco[n] = *reinterpret_cast<const double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u);
+        // the row above the lane: lane u = 0 from the strip's top row; lane
+        // u > 0 starts from lane u-1's checkpoints (node columns 8blk-u,
+        // 8blk-u+1) and receives the rest from lane u-1's recompute below
         double tv[9];
+        if (u == 0) {
 #pragma unroll
-        for (int i = 0; i < 9; ++i) {
-          const double v = (u == 0 && strip == 0) ? 1.0 : st[i * 32 + lane];
-          if constexpr (EDGE) {
-            const int cc = 8 * blk - u + i;
-            tv[i] = (cc <= 0) ? 1.0 : (cc > NC ? 0.0 : v);
-          } else {
-            tv[i] = v;
+          for (int i = 0; i < 9; ++i) {
+            const double v = (strip == 0) ? 1.0 : st[i * 32 + lane];
+            if constexpr (EDGE) {
+              const int cc = 8 * blk + i;
+              tv[i] = (cc <= 0) ? 1.0 : (cc > NC ? 0.0 : v);
+            } else {
+              tv[i] = v;
+            }
           }
+        } else {
+          tv[0] = st[11 * 32 + 64 + lane - 1];
+          tv[1] = st[9 * 32 + 2 * (lane - 1) + 1];
+#pragma unroll
+          for (int i = 2; i < 9; ++i) tv[i] = 0.0;
         }
         const double2 kleft = *reinterpret_cast<const double2*>(st + 9 * 32 + 2 * lane);
         double av[8];  // lane u = 3: adjoint messages of the strip below
@@ -397,15 +414,22 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           av[i] = st[11 * 32 + g * 8 + i];
           if (EDGE && 8 * blk - 3 + i < 0) av[i] = 0.0;  // left of column 0: never written
         }
-        // the staging records are lane-private: refill them for block blk-1
+        // refill the staging records for block blk-1 (lanes read lane u-1's)
+        __syncwarp();
         if (blk > 0) stage_block(blk - 1);
 
-        // ---- 1. recompute the lane's 2 x 8 forward values (registers)
+        // ---- 1. recompute the lane's 2 x 8 forward values (registers): the
+        // skewed wavefront of phase A over the block (lane u-1's bottom row
+        // arrives by shuffle one step ahead), bitwise phase A's values
         double K0[8], K1[8];
         {
           double k0 = kleft.x, k1 = kleft.y;
 #pragma unroll
           for (int kap = 0; kap < 8; ++kap) {
+            if (kap > 0) {
+              const double sh = __shfl_up_sync(0xffffffffu, k1, 1, 4);
+              if (u > 0) tv[kap + 1] = sh;
+            }
             const int c = 8 * blk - u + kap;
             double2 pv = sP[((((c >> 3) & 1) * 8) + (c & 7)) * PSTR + psw(c, lane)];
             if (EDGE && (c < 0 || c >= NC)) pv = make_double2(0.0, 0.0);
