@@ -107,12 +107,21 @@ def load(require_device: bool = True):
         if lib.sk_abi_version() != 1:
             raise NativeUnavailable("libsigkernel ABI version mismatch")
         _lib = lib
-    if require_device:
+    if require_device and not _device_ok:
         import torch
         if not torch.cuda.is_available():
             raise NativeUnavailable("no CUDA device: the B200 kernels cannot run here "
                                     "(there is no CPU fallback)")
+        _set_device_ok()
     return _lib
+
+
+_device_ok = False
+
+
+def _set_device_ok():
+    global _device_ok
+    _device_ok = True
 
 
 def check(rc: int) -> None:

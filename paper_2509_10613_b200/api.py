@@ -160,6 +160,10 @@ def _precision(precision, kind):
     return precision == "fp32"
 
 
+def _needs_graph(*ts) -> bool:
+    return torch.is_grad_enabled() and any(t is not None and t.requires_grad for t in ts)
+
+
 def _prep(t, name):
     if not t.is_cuda:
         raise InvalidArgument(f"{name} must be a CUDA tensor (no CPU fallback)")
@@ -227,7 +231,10 @@ def sig_kernel(x, y, dyadic_order=0, static_kernel=None, transform=None, precisi
         k = _SigKernelF32Fn.apply(x.to(torch.float32), y.to(torch.float32), l1, l2, tf)
         return k[0] if sq else k
     out_dtype = torch.promote_types(x.dtype, y.dtype)
-    k = _SigKernelFn.apply(x.to(torch.float64), y.to(torch.float64), l1, l2, kind, sigma, tf)
+    if _needs_graph(x, y):
+        k = _SigKernelFn.apply(x.to(torch.float64), y.to(torch.float64), l1, l2, kind, sigma, tf)
+    else:  # nothing to differentiate: skip the autograd node (small-call latency)
+        k = ops.forward_batch(x, y, l1, l2, kind, sigma, tf)
     k = k.to(out_dtype)
     return k[0] if sq else k
 
@@ -250,11 +257,18 @@ def sig_kernel_gram(x, y=None, dyadic_order=0, static_kernel=None, transform=Non
         y, _ = _batched(_prep(y, "y"), "y")
         return _SigKernelGramF32Fn.apply(x.to(torch.float32), y.to(torch.float32), l1, l2, tf)
     if sym:
-        G = _SigKernelGramFn.apply(x.to(torch.float64), None, l1, l2, kind, sigma, tf)
+        if _needs_graph(x):
+            G = _SigKernelGramFn.apply(x.to(torch.float64), None, l1, l2, kind, sigma, tf)
+        else:
+            G = ops.forward_gram(x, None, l1, l2, kind, sigma, transform=tf)
         return G.to(x.dtype)
     y, _ = _batched(_prep(y, "y"), "y")
     out_dtype = torch.promote_types(x.dtype, y.dtype)
-    G = _SigKernelGramFn.apply(x.to(torch.float64), y.to(torch.float64), l1, l2, kind, sigma, tf)
+    if _needs_graph(x, y):
+        G = _SigKernelGramFn.apply(x.to(torch.float64), y.to(torch.float64), l1, l2, kind, sigma,
+                                   tf)
+    else:
+        G = ops.forward_gram(x, y, l1, l2, kind, sigma, transform=tf)
     return G.to(out_dtype)
 
 

@@ -7,6 +7,8 @@ workspaces are torch allocations handed to the C ABI as borrowed pointers.
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _lib
@@ -61,6 +63,22 @@ def _cotangent(cot, shape, ref, name="cotangent"):
         raise InvalidArgument(f"{name} must have shape {tuple(shape)}, got {tuple(cot.shape)}")
     _same_device(cot, ref, name)
     return cot.to(torch.float64).contiguous()
+
+
+_WSQ_CACHE: dict = {}
+
+
+def _wsq(fn, *args) -> int:
+    """Workspace-size query of the C ABI, memoised per (entry point, current
+    device, arguments): the answer depends only on those (plans are cached per
+    device on the C side too)."""
+    # SK_NO_MMA (read per plan on the C side) selects other instances
+    key = (fn.__name__, torch.cuda.current_device(), os.environ.get("SK_NO_MMA"), args)
+    nb = _WSQ_CACHE.get(key)
+    if nb is None:
+        nb = fn(*args)
+        _WSQ_CACHE[key] = nb
+    return nb
 
 
 _WS_CACHE: dict = {}
@@ -147,7 +165,7 @@ def forward_batch(x, y, lam1: int, lam2: int, kind: int, sigma: float,
     if B == 0:
         return out
     with _on(x.device):
-        nb = lib.sk_forward_batch_tf_workspace_bytes(B, L1, L2, d, lam1, lam2, kind, tf)
+        nb = _wsq(lib.sk_forward_batch_tf_workspace_bytes, B, L1, L2, d, lam1, lam2, kind, tf)
         ws = _workspace(nb, x.device)
         _lib.check(lib.sk_forward_batch_tf(_ptr(x), _ptr(y), B, L1, L2, d, lam1, lam2, kind,
                                            sigma, tf, _ptr(out), _ptr(ws), ws.numel(),
@@ -168,7 +186,7 @@ def forward_gram(x, y, lam1: int, lam2: int, kind: int, sigma: float,
     if n1 == 0 or n2 == 0 or r1 <= r0:
         return out
     with _on(x.device):
-        nb = lib.sk_forward_gram_tf_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind, int(sym),
+        nb = _wsq(lib.sk_forward_gram_tf_workspace_bytes, n1, n2, L1, L2, d, lam1, lam2, kind, int(sym),
                                                     tf)
         ws = _workspace(nb, x.device)
         _lib.check(lib.sk_forward_gram_tf(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
@@ -201,7 +219,7 @@ def forward_batch_f32(x, y, lam1: int, lam2: int, transform=None) -> torch.Tenso
     if B == 0:
         return out
     with _on(x.device):
-        nb = lib.sk_forward_batch_f32_workspace_bytes(B, L1, y.shape[1], d, lam1, lam2, tf)
+        nb = _wsq(lib.sk_forward_batch_f32_workspace_bytes, B, L1, y.shape[1], d, lam1, lam2, tf)
         ws = _workspace(nb, x.device)
         _lib.check(lib.sk_forward_batch_f32(_ptr(x), _ptr(y), B, L1, y.shape[1], d, lam1, lam2,
                                             tf, _ptr(out), _ptr(ws), ws.numel(),
@@ -226,7 +244,7 @@ def forward_gram_f32(x, y, lam1: int, lam2: int, rows=None, transform=None) -> t
     if n1 == 0 or n2 == 0 or r1 <= r0:
         return out
     with _on(x.device):
-        nb = lib.sk_forward_gram_f32_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, int(sym), tf)
+        nb = _wsq(lib.sk_forward_gram_f32_workspace_bytes, n1, n2, L1, L2, d, lam1, lam2, int(sym), tf)
         ws = _workspace(nb, x.device)
         _lib.check(lib.sk_forward_gram_f32(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
                                            lam1, lam2, tf, r0, r1, _ptr(out), _ptr(ws),
@@ -241,7 +259,7 @@ def solve_delta(delta: torch.Tensor, lam1: int, lam2: int) -> torch.Tensor:
     B, r1, r2 = delta.shape
     out = torch.empty(B, dtype=torch.float64, device=delta.device)
     with _on(delta.device):
-        nb = lib.sk_solve_delta_workspace_bytes(B, r1, r2, lam1, lam2)
+        nb = _wsq(lib.sk_solve_delta_workspace_bytes, B, r1, r2, lam1, lam2)
         ws = _workspace(nb, delta.device)
         _lib.check(lib.sk_solve_delta(_ptr(delta), B, r1, r2, lam1, lam2, _ptr(out), _ptr(ws),
                                       ws.numel(), _stream(delta.device)))
@@ -280,7 +298,7 @@ def backward_batch(x, y, lam1, lam2, kind, sigma, cot, want_values=False, transf
     if B == 0:
         return vals, gx, gy
     with _on(x.device):
-        nb = lib.sk_backward_batch_tf_workspace_bytes(B, L1, L2, d, lam1, lam2, kind, tf)
+        nb = _wsq(lib.sk_backward_batch_tf_workspace_bytes, B, L1, L2, d, lam1, lam2, kind, tf)
         ws = _workspace(nb, x.device)
         _lib.check(lib.sk_backward_batch_tf(_ptr(x), _ptr(y), B, L1, L2, d, lam1, lam2, kind,
                                             sigma, tf, _ptr(cot), _ptr(vals), _ptr(gx), _ptr(gy),
@@ -388,7 +406,7 @@ def _gram_backward(x, y, lam1, lam2, kind, sigma, cot, rows, out, grad_x, grad_y
         if n1 == 0 or n2 == 0 or r1 <= r0:
             return acc_x, acc_y
         with _on(dev):
-            nb = lib.sk_backward_gram_acc_tf_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind,
+            nb = _wsq(lib.sk_backward_gram_acc_tf_workspace_bytes, n1, n2, L1, L2, d, lam1, lam2, kind,
                                                              int(sym), tf)
             ws = _workspace(nb, dev)
             _lib.check(lib.sk_backward_gram_acc_tf(
@@ -406,7 +424,7 @@ def _gram_backward(x, y, lam1, lam2, kind, sigma, cot, rows, out, grad_x, grad_y
     if n1 == 0 or n2 == 0 or r1 <= r0:
         return grad_x, grad_y
     with _on(dev):
-        nb = lib.sk_backward_gram_tf_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, kind,
+        nb = _wsq(lib.sk_backward_gram_tf_workspace_bytes, n1, n2, L1, L2, d, lam1, lam2, kind,
                                                      int(sym), tf)
         ws = _workspace(nb, dev)
         _lib.check(lib.sk_backward_gram_tf(_ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d,
