@@ -92,6 +92,7 @@ inline BwdFn sk_bwd_select_xw(const BwdShape& s, int& smem_doubles) {
   BwdFn fn = nullptr;
   if (s.DP == 4 && s.NW == 4) sk_bwd_table_xw<KIND, 4, 8, 4>(s, fn, smem_doubles);
   else if (s.DP == 4 && s.NW == 8) sk_bwd_table_xw<KIND, 4, 8, 8>(s, fn, smem_doubles);
+  else if (s.DP == 8 && s.NW == 4 && s.R == 8) sk_bwd_table_xw<KIND, 8, 8, 4>(s, fn, smem_doubles);
   else if (s.DP == 8 && s.NW == 4) sk_bwd_table_xw<KIND, 8, 4, 4>(s, fn, smem_doubles);
   else if (s.DP == 8 && s.NW == 8) sk_bwd_table_xw<KIND, 8, 4, 8>(s, fn, smem_doubles);
   return fn;

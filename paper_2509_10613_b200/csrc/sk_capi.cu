@@ -437,8 +437,20 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
     }();
     // widen until the GPU is full or one strip covers the pair (measured at
     // BASELINE config 2: one 8-warp strip 0.60 ms vs two 4-warp strips 0.70 ms)
+    // DP = 8 pairs taller than 512 fine rows: 8 rows per lane, half the lanes
+    // (C2: RBF 0.60 -> 0.56 ms, linear 0.35 -> 0.28 ms)
+    static const int xr = [] {
+      const char* e = std::getenv("SK_FWD_XW_R");  // tuning knob: 4 or 8 rows per lane (DP = 8)
+      return (e && e[0] == '8') ? 8 : (e && e[0] == '4') ? 4 : 0;
+    }();
+    int64_t lanes = lanes_per_pair;
+    if ((xr ? xr == 8 : M1 > 512) && s.DP == 8 && !f32) {
+      s.R = 8;
+      s.FR = std::min(1 << std::min(lamR, 3), s.R);
+      lanes = (M1 + s.R - 1) / s.R;
+    }
     int W = 2;
-    while (W < wmax && npairs * 32 * W < target_lanes && 32 * W < lanes_per_pair) W *= 2;
+    while (W < wmax && npairs * 32 * W < target_lanes && 32 * W < lanes) W *= 2;
     static const int wforce = [] {
       const char* e = std::getenv("SK_FWD_XW_W");  // tuning knob: force the CTA width
       const int v = (e && e[0]) ? std::atoi(e) : 0;
@@ -984,6 +996,17 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
         lanes_per_pair > 64) {
       s.NW = 4;
       if (nw_force) s.NW = nw_force;
+      // pairs taller than one 4-row strip: 8 rows per lane, one strip (C2:
+      // RBF backward 1.62 -> 1.39 ms, linear 1.35 -> 1.03 ms)
+      static const int r_force = [] {
+        const char* e = std::getenv("SK_BWD_XW_R");  // tuning knob: 4 or 8 (DP = 8, NW = 4)
+        return (e && e[0] == '4') ? 4 : (e && e[0] == '8') ? 8 : 0;
+      }();
+      const bool r8 = r_force ? r_force == 8 : M1 > 32 * s.NW * s.R;
+      if (r8 && s.DP == 8 && s.NW == 4) {
+        s.R = 8;
+        s.FR = std::min(1 << std::min(lamR, 3), s.R);
+      }
     }
   }
   int smd = 0;

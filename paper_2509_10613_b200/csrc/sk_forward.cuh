@@ -59,9 +59,16 @@ __host__ __device__ constexpr int xw_ring_slots(int lanes, int S, int PF) {
   return ring_slots(lanes + (SK_XW_LAG - 1) * (lanes / 32) + 2 * SK_XW_LAG, S, PF);
 }
 
+#ifndef SK_FWD_PF
+#define SK_FWD_PF 2  // measured: 6 slower at C1 (32.3 vs 29.0 us) and on Gram tiles
+#endif
+
 template <bool XW, int G, int S>
 struct FwdRing {
-  static constexpr int PF = 2;  // steps in flight
+  // steps in flight.  Short steps (few rows per lane, e.g. BASELINE config 1:
+  // 2 rows) finish long before an L2 / HBM round trip, so lane groups keep
+  // more steps of column records in flight; XW CTAs add their LAG chunk
+  static constexpr int PF = XW ? 2 : SK_FWD_PF;
   static constexpr int NEED = ((XW ? 512 : G) + PF + 1) * S;
   static constexpr int SLOTS = NEED <= 32 ? 32 : NEED <= 64 ? 64 : NEED <= 128 ? 128
                                : NEED <= 256 ? 256 : NEED <= 512 ? 512 : NEED <= 1024 ? 1024
