@@ -20,7 +20,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "-ccbin", "/usr/bin/g++", "--expt-relaxed-constexpr"]
 SOURCES = ["sk_capi.cu", "sk_fwd_linear.cu", "sk_fwd_rbf.cu", "sk_fwd_delta.cu", "sk_fwd_f32.cu", "sk_fwd_short.cu",
-           "sk_bwd_linear.cu", "sk_bwd_rbf.cu", "sk_bwd_wide.cu", "sk_bwd_xw_linear.cu", "sk_bwd_xw_rbf.cu", "sk_signature.cu", "sk_fwd_mma.cu", "sk_bwd_mma.cu"]
+           "sk_bwd_linear.cu", "sk_bwd_rbf.cu", "sk_bwd_wide.cu", "sk_bwd_xw_linear.cu", "sk_bwd_xw_rbf.cu", "sk_signature.cu", "sk_fwd_mma.cu", "sk_bwd_mma.cu",
+           "sk_small.cu"]
 
 
 def _deps():

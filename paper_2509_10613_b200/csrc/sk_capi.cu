@@ -651,6 +651,25 @@ static int forward_impl(const void* x, const void* y, int64_t n1, int64_t n2, in
   pb.ldo = n2;
   FwdPlan pl;
   const int64_t npairs = mode == BATCH ? n1 : (r1 - r0) * n2;
+  // few short pairs (BASELINE config 1): one warp per pair from a shared
+  // coefficient tile, no workspace, no prep launch (sk_small.cu)
+  static const bool no_small = std::getenv("SK_NO_SMALL") && std::getenv("SK_NO_SMALL")[0] == '1';
+  if (!no_small && mode == BATCH && kind == LINEAR && !f32 && tf == TF_NONE &&
+      npairs <= 4 * (int64_t)device_sms() && pb.M1c << g.lamR <= 64 &&
+      pb.M2c << g.lamC <= 64 && d <= 32) {
+    if (query) {
+      *query = 0;
+      return SK_OK;
+    }
+    const double* xr = static_cast<const double*>(g.swap ? y : x);
+    const double* xc = static_cast<const double*>(g.swap ? x : y);
+    if (launch_small_fwd(xr, xc, n1, g.LR, g.LC, d, g.lamR, g.lamC, pb.scale,
+                         static_cast<double*>(out), device_sms(), st)) {
+      SK_CUDA(cudaGetLastError());
+      return SK_OK;
+    }
+    return fail(SK_CUDA_ERROR, "small-pair forward could not be launched");
+  }
   if (int rc = plan_forward(pl, kind, d, g.lamR, g.lamC, pb.M1c, pb.M2c, npairs,
                             mode != BATCH && !(mode == GRAM_CROSS && g.swap), mode, (int)n2,
                             (int)r0, (int)r1, f32))

@@ -45,6 +45,10 @@ FwdFn select_fwd_short(const FwdShape& s, int& smem);       // short paths, fp64
 FwdFn select_fwd_rbf(const FwdShape& s, int& smem);
 FwdFn select_fwd_delta(const FwdShape& s, int& smem);
 FwdFn select_fwd_mma(int DP, int& smem_per_warp);
+// few short pairs (sk_small.cu); false when the shape does not apply
+bool launch_small_fwd(const double* xr, const double* xc, int64_t B, int64_t LR, int64_t LC,
+                      int64_t d, int lamR, int lamC, double scale, double* out, int sms,
+                      cudaStream_t st);
 
 inline int rows_per_lane(int DP) {
   switch (DP) {

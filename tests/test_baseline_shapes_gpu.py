@@ -117,3 +117,20 @@ def test_c5_cross_block(sk, oracle):
     wx, wy = oracle.gram_backward(X, Y, C, 0, 0)
     assert rel_err(gx.cpu().numpy(), wx) < TOL
     assert rel_err(gy.cpu().numpy(), wy) < TOL
+
+
+@pytest.mark.parametrize("L1,L2,d,lam", [(64, 64, 4, 0), (40, 64, 3, 0), (17, 9, 8, 1),
+                                         (33, 33, 20, 0), (2, 65, 1, 0), (9, 5, 4, 3)])
+def test_small_pairs_path(sk, oracle, L1, L2, d, lam):
+    """Few short pairs run the small-pair kernel (sk_small.cu: one warp per pair
+    from a shared coefficient tile); the same pairs inside a large batch run the
+    general batch kernel -- values are bitwise equal, and match the oracle."""
+    s, ops = sk
+    rng = np.random.default_rng(L1 * 31 + L2 + d)
+    n_big = 4 * torch.cuda.get_device_properties(0).multi_processor_count + 8
+    x = make_paths(rng, n_big, L1, d)
+    y = make_paths(rng, n_big, L2, d)
+    small = ops.forward_batch(cu(x[:32]), cu(y[:32]), lam, lam, 0, 1.0).cpu().numpy()
+    big = ops.forward_batch(cu(x), cu(y), lam, lam, 0, 1.0).cpu().numpy()
+    np.testing.assert_array_equal(small, big[:32])
+    assert rel_err(small, oracle.kernel_batch(x[:32], y[:32], lam, lam)) < TOL
