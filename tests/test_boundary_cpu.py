@@ -67,7 +67,9 @@ def test_errors_map_to_reference_exceptions(lib):
 
 
 def test_workspace_queries_positive(lib):
-    assert lib.sk_forward_batch_workspace_bytes(32, 64, 64, 4, 0, 0, 0) > 0
+    # few short pairs (BASELINE config 1) take the small-pair kernel: no workspace
+    assert lib.sk_forward_batch_workspace_bytes(32, 64, 64, 4, 0, 0, 0) == 0
+    assert lib.sk_forward_batch_workspace_bytes(32, 128, 128, 4, 0, 0, 0) > 0
     assert lib.sk_forward_gram_workspace_bytes(16, 16, 30, 30, 3, 1, 1, 0, 1) > 0
     assert lib.sk_backward_batch_workspace_bytes(8, 40, 50, 8, 2, 2, 1) > 0
     assert lib.sk_backward_gram_workspace_bytes(8, 8, 40, 40, 16, 0, 0, 0, 1) > 0
