@@ -1,3 +1,7 @@
+# time the C3 step (prof_c3.py at n given) under SK_EXP switches of the profiling build
 mkdir -p gpurun_out
-for a in "256" "256 1024 8"; do
-for e in 0 1 2 6 10 14; do SK_EXP=$e timeout 300 python tools/prof_c3.py $a | sed "s/^/exp$e /" >> gpurun_out/exp.log 2>&1; done; done
+export SK_LIBSIGKERNEL=$PWD/paper_2509_10613_b200/_native/variants/prof/libsigkernel.so
+for e in 0 8 4 1; do
+  echo "== SK_EXP=$e" >> gpurun_out/exp.log
+  SK_EXP=$e python tools/prof_c3.py ${1:-512} >> gpurun_out/exp.log 2>&1
+done
