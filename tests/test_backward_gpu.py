@@ -218,3 +218,30 @@ def test_wide_gram_vs_oracle(sk, oracle, n1, n2, L, d, lam):
     Gt = s.sig_kernel_gram(xt, None if Y is None else cu(Y), dyadic_order=lam)
     (Gt * cu(C)).sum().backward()
     assert rel_err(xt.grad.cpu().numpy(), want if Y is None else want[0]) < TOL
+
+
+@pytest.mark.parametrize("B,L1,L2,d,l1,l2,static", [
+    (6, 130, 120, 8, 2, 2, (1, 0.8)),   # 516 fine rows: 8 rows per lane, one 4-warp strip
+    (5, 700, 650, 7, 0, 0, (0, 1.0)),   # cross-warp, lambda 0, d padded to 8
+    (4, 400, 390, 5, 1, 2, (1, 1.3)),   # RBF, mixed orders
+    (3, 300, 310, 8, 2, 1, (0, 1.0)),   # 1196 fine rows: taller than one 4-row strip of 128 lanes
+    (4, 65, 80, 3, 3, 3, (0, 1.0)),     # short axis at order 3
+])
+def test_cross_warp_pairs_vs_oracle(sk, oracle, B, L1, L2, d, l1, l2, static):
+    """Few long pairs take the cross-warp kernels (one pair per CTA: 8 rows per
+    lane past 512 fine rows, LAG-chunked forward hops); values and both
+    gradients vs the oracle at shapes around the instance boundaries."""
+    rng = np.random.default_rng(B * 1000 + L1 + d)
+    x = make_paths(rng, B, L1, d)
+    y = make_paths(rng, B, L2, d)
+    cot = rng.standard_normal(B)
+    kind, sigma = static
+    st = ("rbf", sigma) if kind == 1 else None
+    _, ops = sk
+    wv, wx, wy = oracle.kernel_batch_backward(x, y, l1, l2, cot, st)
+    v, gx, gy = ops.backward_batch(cu(x), cu(y), l1, l2, kind, sigma, cu(cot), want_values=True)
+    assert rel_err(v.cpu().numpy(), wv) < TOL
+    assert rel_err(gx.cpu().numpy(), wx) < TOL
+    assert rel_err(gy.cpu().numpy(), wy) < TOL
+    f = ops.forward_batch(cu(x), cu(y), l1, l2, kind, sigma).cpu().numpy()
+    np.testing.assert_array_equal(f, v.cpu().numpy())
