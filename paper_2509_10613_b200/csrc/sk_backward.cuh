@@ -86,7 +86,7 @@ struct BwdSmem {
   // EH node rows x NL node columns -- D tile (EH+1) x (NL+1), weights EH x
   // (NL+1), the band's row nodes, the chunk's column nodes
   static constexpr int EH = NL >= 128 ? 16 : 8;
-  static constexpr int EPI = (EH + 1) * (NL + 1) + EH * (NL + 1) + EH * DP + NL * DP;
+  static constexpr int EPI = (EH + 1) * (NL + 1) + EH * (NL + 1) + 2 * EH * DP + NL * DP;
   static constexpr int TOTAL = MAIN > EPI ? MAIN : EPI;
 };
 
@@ -885,8 +885,8 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       const int nchunk = (L2n + NL - 1) / NL;
       double* sDt = smem + (XW ? 0 : (size_t)warp * SM::TOTAL);  // [EH+1][TW]
       double* sW = sDt + (EH + 1) * TW;                             // [EH][TW]
-      double* sXb = sW + EH * TW;                                   // [EH][DP]
-      double* sYc = sXb + EH * DP;                                  // [NL][DP]
+      double* sXb0 = sW + EH * TW;                                  // [2][EH][DP]
+      double* sYc = sXb0 + 2 * EH * DP;                             // [NL][DP]
       double* gxa = gxs;  // [L1n][DP] dF/dx chains between column chunks
       for (int ch = 0; ch < nchunk; ++ch) {
         const int j0 = ch * NL, j = j0 + u;
@@ -899,19 +899,29 @@ bwd_kernel(Problem pb, BwdArgs ba) {
           gy[k] = 0.0;
           sYc[u * DP + k] = yj[k];
         }
-        for (int i0 = 0; i0 < L1n; i0 += EH) {
-          SK_BAR();  // previous band's W consumed
+        // band staging by cp.async (zero-filled outside the grid): the D tile
+        // and the band's row nodes; the next band's is issued under the
+        // current band's dF/dx pass (the D tile is dead by then)
+        auto stage_band = [&](int i0, double* sXb) {
           for (int e = u; e < (EH + 1) * TW; e += NL) {
             const int rr = e / TW, cc = e % TW;
             const int i = i0 - 1 + rr, jd = j0 - 1 + cc;
-            sDt[e] = (i >= 0 && jd >= 0 && i < pb.M1c && jd < pb.M2c)
-                         ? D[(int64_t)i * pb.M2c + jd] : 0.0;
+            const bool v = i >= 0 && jd >= 0 && i < pb.M1c && jd < pb.M2c;
+            cp_async8(sDt + e, D + (v ? (int64_t)i * pb.M2c + jd : 0), v);
           }
           for (int e = u; e < EH * DP; e += NL) {
             const int i = i0 + e / DP;
-            sXb[e] = i < L1n ? xp[(int64_t)i * pb.dpad + (e % DP)] : 0.0;
+            const bool v = i < L1n;
+            cp_async8(sXb + e, xp + (v ? (int64_t)i * pb.dpad + (e % DP) : 0), v);
           }
-          SK_BAR();
+          cp_async_commit();
+        };
+        SK_BAR();  // the previous chunk's band buffers consumed
+        stage_band(0, sXb0);
+        for (int i0 = 0, bb = 0; i0 < L1n; i0 += EH, bb ^= 1) {
+          double* sXb = sXb0 + bb * EH * DP;
+          cp_async_wait<0>();
+          SK_BAR();  // band staged, the previous band's W consumed
 #pragma unroll 2
           for (int r = 0; r < EH; ++r) {
             const double G = sDt[r * TW + u] - sDt[r * TW + u + 1] - sDt[(r + 1) * TW + u] +
@@ -931,6 +941,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             sW[r * TW + u] = w;
           }
           SK_BAR();
+          if (i0 + EH < L1n) stage_band(i0 + EH, sXb0 + (bb ^ 1) * EH * DP);
           // dF/dx chains of the band's rows over the chunk's columns
           for (int e = u; e < EH * dR; e += NL) {
             const int r = e / dR, k = e % dR, i = i0 + r;
