@@ -121,8 +121,11 @@ __device__ __forceinline__ void fwd_issue(T* ring, int smask, const Problem& pb,
 //         (the fp32 kernels: LINEAR only, small-correction cell, path data,
 //         handoff rows and outputs are float arrays behind the same pointers)
 // Every group of a warp must share the column path (Gram tiles / one pair).
-template <int KIND, int DP, int R, int FR, int F, int G, bool XW, int S, typename T = double>
-__global__ void __launch_bounds__(XW ? 512 : 128)
+//   XWT   XW CTAs: threads at most (256: 255 registers per thread, up to 8
+//         warps; 512: 128 registers, 16 warps for the longest pairs)
+template <int KIND, int DP, int R, int FR, int F, int G, bool XW, int S, typename T = double,
+          int XWT = 512>
+__global__ void __launch_bounds__(XW ? XWT : 128)
 fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
   constexpr int RC = R / FR;
   constexpr int P = XW ? 1 : 32 / G;

@@ -11,7 +11,10 @@ template <int KIND, int DP, int R, int FR, int F, typename T, bool XWONLY = fals
 inline void sk_fwd_leaf(const FwdShape& s, FwdFn& fn, int& smem) {
   if (XWONLY || s.XW) {
     if constexpr (KIND != DELTA) {
-      fn = fwd_kernel<KIND, DP, R, FR, F, 32, true, 2, T>;
+      // up to 8 warps: the 255-register instance (measured at BASELINE config 2:
+      // RBF forward 0.57 -> 0.50 ms, the 128-register one spills)
+      if (s.W <= 8) fn = fwd_kernel<KIND, DP, R, FR, F, 32, true, 2, T, 256>;
+      else fn = fwd_kernel<KIND, DP, R, FR, F, 32, true, 2, T, 512>;
       smem = fwd_smem_bytes<KIND, DP, F, 32, true, 2, T>(s.W);
     }
     return;
