@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "sk_cell.cuh"
 #include "sk_plan.h"
@@ -39,6 +40,9 @@ small_fwd_kernel(const double* __restrict__ xr, const double* __restrict__ xc, i
   double* __restrict__ dyc = smem_small;                                  // [M2c][DP]
   double2* __restrict__ ab = reinterpret_cast<double2*>(dyc + M2c * DP);  // [M2c][M1c]
   const int u_star = (M1 - 1) >> 1, r_star = (M1 - 1) & 1;
+#ifdef SK_SMALL_CLOCKS
+  long long c0_ = clock64(), c1_ = 0, c2_ = 0, c3_ = 0;
+#endif
   for (int64_t b = blockIdx.x; b < B; b += gridDim.x) {
     const double* xp = xr + b * (int64_t)LR * d;
     const double* yp = xc + b * (int64_t)LC * d;
@@ -57,6 +61,9 @@ small_fwd_kernel(const double* __restrict__ xr, const double* __restrict__ xc, i
     for (int k = 0; k < DP; ++k)
       dx[k] = (iv && k < d) ? (xp[(i + 1) * d + k] - xp[i * d + k]) * scale : 0.0;
     __syncthreads();
+#ifdef SK_SMALL_CLOCKS
+    c1_ = clock64();
+#endif
     if (iv) {
       for (int j = jp; j < M2c; j += 4) {
         const int j1 = min(j + 2, M2c - 1);
@@ -72,31 +79,49 @@ small_fwd_kernel(const double* __restrict__ xr, const double* __restrict__ xc, i
       }
     }
     __syncthreads();
+#ifdef SK_SMALL_CLOCKS
+    c2_ = clock64();
+#endif
     // 2. wavefront (warp 0): lane u, fine rows s0 = 2u+1, s1 = 2u+2 (1-based),
     //    column t = tau - u + 1 at step tau; row 0 and column 0 are the boundary
     if (tid < 32) {
       const int i0 = min((2 * lane) >> lamR, M1c - 1), i1 = min((2 * lane + 1) >> lamR, M1c - 1);
+      // branch-free steps (inactive lanes compute and discard), the next
+      // step's coefficients loaded one step ahead: the lane chain is the
+      // shuffle and four dependent FP64 operations per step (measured: 180 ->
+      // 123 cycles per step; two columns per step measured 203)
       double kl0 = 1.0, kl1 = 1.0, topc = 1.0, bot = 1.0;
       const int nsteps = M2 + 31;
+      auto coefs_at = [&](int t, double2& a0, double2& a1) {
+        const int jc = min(max(t - 1, 0), M2 - 1) >> lamC;
+        a0 = ab[jc * M1c + i0];
+        a1 = ab[jc * M1c + i1];
+      };
+      double2 n0, n1;
+      coefs_at(1 - lane, n0, n1);
+#pragma unroll 2
       for (int tau = 0; tau < nsteps; ++tau) {
+        const int t = tau - lane + 1;
+        const double2 c0 = n0, c1 = n1;
+        coefs_at(t + 1, n0, n1);
         double top = __shfl_up_sync(0xffffffffu, bot, 1);
         if (lane == 0) top = 1.0;
-        const int t = tau - lane + 1;
-        if (t >= 1 && t <= M2) {
-          const int jc = (t - 1) >> lamC;
-          const double2 c0 = ab[jc * M1c + i0], c1 = ab[jc * M1c + i1];
-          const double k0 = cell(top, kl0, topc, Coef{c0.x, c0.y});
-          const double k1 = cell(k0, kl1, kl0, Coef{c1.x, c1.y});
-          topc = top;
-          kl0 = k0;
-          kl1 = k1;
-          bot = k1;
-        }
+        const double k0 = cell(top, kl0, topc, Coef{c0.x, c0.y});
+        const double k1 = cell(k0, kl1, kl0, Coef{c1.x, c1.y});
+        const bool act = t >= 1 && t <= M2;
+        topc = act ? top : topc;
+        kl0 = act ? k0 : kl0;
+        kl1 = act ? k1 : kl1;
+        bot = act ? k1 : bot;
       }
       // column M2 is the lane's last: its row values are the final ones
       if (lane == u_star) out[b] = r_star ? kl1 : kl0;
     }
   }
+#ifdef SK_SMALL_CLOCKS
+  c3_ = clock64();
+  if (tid == 0 && blockIdx.x == 0) printf("small_fwd cycles: load %lld, tile %lld, wave %lld\n", c1_ - c0_, c2_ - c1_, c3_ - c2_);
+#endif
 }
 
 // dynamic shared memory of the tile (bytes)

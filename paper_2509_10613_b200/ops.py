@@ -111,6 +111,8 @@ def _paths(t: torch.Tensor, name: str) -> torch.Tensor:
         raise InvalidArgument(f"{name} needs at least 2 points per path")
     if not t.is_cuda:
         raise InvalidArgument(f"{name} must live on a CUDA device")
+    if t.dtype is torch.float64 and t.is_contiguous():
+        return t
     return t.to(torch.float64).contiguous()
 
 
@@ -164,12 +166,14 @@ def forward_batch(x, y, lam1: int, lam2: int, kind: int, sigma: float,
     out = torch.empty(B, dtype=torch.float64, device=x.device)
     if B == 0:
         return out
-    with _on(x.device):
+    dev = x.device
+    with _on(dev):
         nb = _wsq(lib.sk_forward_batch_tf_workspace_bytes, B, L1, L2, d, lam1, lam2, kind, tf)
-        ws = _workspace(nb, x.device)
-        _lib.check(lib.sk_forward_batch_tf(_ptr(x), _ptr(y), B, L1, L2, d, lam1, lam2, kind,
-                                           sigma, tf, _ptr(out), _ptr(ws), ws.numel(),
-                                           _stream(x.device)))
+        # (few short pairs need no workspace: BASELINE config 1's small-pair kernel)
+        ws = _workspace(nb, dev) if nb else None
+        _lib.check(lib.sk_forward_batch_tf(x.data_ptr(), y.data_ptr(), B, L1, L2, d, lam1, lam2,
+                                           kind, sigma, tf, out.data_ptr(), _ptr(ws),
+                                           ws.numel() if nb else 0, _stream(dev)))
     return out
 
 
