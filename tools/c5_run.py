@@ -67,4 +67,18 @@ out["subblock_rel_err"] = float(np.abs(Gs - want).max() / np.abs(want).max())
 out["symmetric_exact"] = bool(torch.equal(G, G.T))
 out["grad_finite"] = bool(torch.isfinite(gx).all().item())
 out["grad_abs_max"] = float(gx.abs().max().item())
+# full-size parity of one Gram row and one path's gradient: G[0, :] is k(x_0, x_b)
+# over all n paths, and with cotangent ones dF/dx_0 = 2 sum_b d1 k(x_0, x_b)
+# (k(x, y) = k(y, x): the column-side terms equal the row-side ones), i.e. the
+# cross Gram backward of x_0 against every path with cotangent 2 -- n pairs of
+# the full L = 1024 grid on the CPU oracle (all host threads)
+t1 = time.time()
+row = orc.kernel_gram(X[:1], X, 0, 0)
+out["row0_rel_err"] = float(np.abs(G[0].cpu().numpy() - row[0]).max() / np.abs(row[0]).max())
+g0, _ = orc.gram_backward(X[:1], X, 2.0 * np.ones((1, n)), 0, 0)
+got0 = gx[0].cpu().numpy()
+out["grad_path0_rel_err"] = float(np.abs(got0 - g0[0]).max() / np.abs(g0[0]).max())
+out["oracle_check_s"] = time.time() - t1
+out["oracle_check"] = (f"G[:6,:6], G[0,:] ({n} pairs) and dF/dx_0 ({n} pairs, cross Gram backward "
+                       f"with cotangent 2) vs oracle/sk_oracle.c; tolerance 1e-10")
 print(json.dumps(out, indent=1))
