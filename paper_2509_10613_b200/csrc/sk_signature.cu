@@ -227,12 +227,14 @@ sig_fwd_kernel(const double* __restrict__ inc, int64_t B, int64_t M, SigGeom g,
 // ------------------------------------------------------------------- backward
 // Deterministic CTA-wide contractions (fixed chunking and combine order).
 // out[c] += sum_r a[r] * M[r*C + c]
-__device__ void cta_vecmat(double* out, const double* a, const double* Mx, int64_t R, int64_t C,
-                           double* part) {
+__device__ void cta_vecmat(double* __restrict__ out, const double* __restrict__ a,
+                           const double* __restrict__ Mx, int64_t R, int64_t C,
+                           double* __restrict__ part) {
   const int T = blockDim.x, t = threadIdx.x;
   if (C >= T / 4 || R <= 4) {
     for (int64_t cc = t; cc < C; cc += T) {
       double acc = out[cc];
+#pragma unroll 8
       for (int64_t r = 0; r < R; ++r) acc = add(acc, mul(a[r], Mx[r * C + cc]));
       out[cc] = acc;
     }
@@ -245,6 +247,7 @@ __device__ void cta_vecmat(double* out, const double* a, const double* Mx, int64
     const int64_t cc = t % C, q = t / C;
     double acc = 0.0;
     const int64_t r1 = lmin(R, (q + 1) * Rc);
+#pragma unroll 8
     for (int64_t r = q * Rc; r < r1; ++r) acc = add(acc, mul(a[r], Mx[r * C + cc]));
     part[q * C + cc] = acc;
   }
@@ -258,12 +261,14 @@ __device__ void cta_vecmat(double* out, const double* a, const double* Mx, int64
 }
 
 // out[r] += sum_c M[r*C + c] * v[c]   (the dot formed first, then added)
-__device__ void cta_matvec(double* out, const double* Mx, const double* v, int64_t R, int64_t C,
-                           double* part) {
+__device__ void cta_matvec(double* __restrict__ out, const double* __restrict__ Mx,
+                           const double* __restrict__ v, int64_t R, int64_t C,
+                           double* __restrict__ part) {
   const int T = blockDim.x, t = threadIdx.x;
   if (R >= T / 4 || C <= 4) {
     for (int64_t r = t; r < R; r += T) {
       double acc = 0.0;
+#pragma unroll 8
       for (int64_t cc = 0; cc < C; ++cc) acc = add(acc, mul(Mx[r * C + cc], v[cc]));
       out[r] = add(out[r], acc);
     }
@@ -276,6 +281,7 @@ __device__ void cta_matvec(double* out, const double* Mx, const double* v, int64
     const int64_t r = t % R, q = t / R;
     double acc = 0.0;
     const int64_t c1 = lmin(C, (q + 1) * Cc);
+#pragma unroll 8
     for (int64_t cc = q * Cc; cc < c1; ++cc) acc = add(acc, mul(Mx[r * C + cc], v[cc]));
     part[q * R + r] = acc;
   }
@@ -290,22 +296,26 @@ __device__ void cta_matvec(double* out, const double* Mx, const double* v, int64
 
 // E = exp(zs) with zs = sign * z: level m entry J = ((z_j1 (1/2)) z_j2 (1/3)) ...
 // exactly as exp_into (_kernels.py:26-42)
-__device__ void cta_exp(double* E, const double* z, double sign, const SigGeom& g) {
-  const int d = g.d, N = g.N;
-  for (int m = 1; m <= N; ++m) {
-    const int64_t n = g.pw[m];
-    for (int64_t J = threadIdx.x; J < n; J += blockDim.x) {
-      // digits of J, most significant first
-      int64_t div = g.pw[m - 1];
-      double v = sign * z[(J / div) % d];
-      for (int k = 2; k <= m; ++k) {
-        div /= d;
-        v = mul(mul(v, c_inv[k]), sign * z[(J / div) % d]);
-      }
-      E[g.off[m - 1] + J] = v;
-    }
-  }
+// Level by level: entry J of level m is level m-1's entry J / d (its leading
+// digits) times 1/m times z of its last digit -- the very operations of the
+// digit loop, so every value is bitwise unchanged, at one multiply pair per
+// entry instead of m (the per-digit 64-bit divisions were the kernel's top cost).
+// 32-bit indices: the planner's (d, N) range keeps every level below 2^24 entries.
+__device__ void cta_exp(double* __restrict__ E, const double* __restrict__ z, double sign,
+                        const SigGeom& g) {
+  const unsigned d = (unsigned)g.d;
+  const int N = g.N;
+  for (unsigned J = threadIdx.x; J < d; J += blockDim.x) E[J] = sign * z[J];
   __syncthreads();
+  for (int m = 2; m <= N; ++m) {
+    const unsigned n = (unsigned)g.pw[m];
+    const double* __restrict__ prev = E + g.off[m - 2];
+    double* __restrict__ cur = E + g.off[m - 1];
+    const double im = c_inv[m];
+    for (unsigned J = threadIdx.x; J < n; J += blockDim.x)
+      cur[J] = mul(mul(prev[J / d], im), sign * z[J % d]);
+    __syncthreads();
+  }
 }
 
 // One CTA per path: the reverse walk of sig_backward_path (_kernels.py:182-266).
@@ -339,13 +349,19 @@ sig_bwd_kernel(const double* __restrict__ inc, int64_t M, SigGeom g, double* __r
       cta_exp(EX, z, -1.0, g);
       for (int k = N; k >= 1; --k) {  // top-down: level k reads the old lower levels
         const int64_t n = g.pw[k];
+        // level k (written) and the levels below / EX (read) do not overlap
+        double* __restrict__ dst = SIG + g.off[k - 1];
+        const double* __restrict__ low = SIG;
+        const double* __restrict__ ex = EX;
+#pragma unroll 4
         for (int64_t I = threadIdx.x; I < n; I += blockDim.x) {
-          double v = SIG[g.off[k - 1] + I];
+          double v = dst[I];
           for (int i = 1; i < k; ++i) {
-            const int64_t head = I / g.pw[k - i], tail = I % g.pw[k - i];
-            v = add(v, mul(SIG[g.off[i - 1] + head], EX[g.off[k - i - 1] + tail]));
+            const unsigned pk = (unsigned)g.pw[k - i];
+            const unsigned head = (unsigned)I / pk, tail = (unsigned)I % pk;
+            v = add(v, mul(low[g.off[i - 1] + head], ex[g.off[k - i - 1] + tail]));
           }
-          SIG[g.off[k - 1] + I] = add(v, EX[g.off[k - 1] + I]);
+          dst[I] = add(v, ex[g.off[k - 1] + I]);
         }
         __syncthreads();
       }
@@ -386,6 +402,7 @@ sig_bwd_kernel(const double* __restrict__ inc, int64_t M, SigGeom g, double* __r
           const int64_t q = t / d;
           double acc = 0.0;
           const int64_t r1 = lmin(rows, (q + 1) * Rc);
+#pragma unroll 8
           for (int64_t r = q * Rc; r < r1; ++r) acc = add(acc, mul(Em1[r], mul(Bm[r * d + j], im)));
           part[q * d + j] = acc;
         }
