@@ -59,6 +59,9 @@ __host__ __device__ constexpr int xw_ring_slots(int lanes, int S, int PF) {
   return ring_slots(lanes + (SK_XW_LAG - 1) * (lanes / 32) + 2 * SK_XW_LAG, S, PF);
 }
 
+#ifndef SK_XW_PIPE
+#define SK_XW_PIPE 1
+#endif
 #ifndef SK_FWD_PF
 #define SK_FWD_PF 2  // measured: 6 slower at C1 (32.3 vs 29.0 us) and on Gram tiles
 #endif
@@ -305,15 +308,25 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
       for (int q = 0; q < SF; ++q) bot[q] = T(1);
       // wide paths (DP >= 16) pipeline the next step's coefficients behind the
       // recurrence; narrow ones keep the registers for S columns per step
-      constexpr bool PIPE = !XW && (DP >= 16 || (G == 32 && R <= 2));  // (short paths: latency)
+      // (short paths: latency; XW RBF with the 255-register instance: the next
+      // step's exps under this step's recurrence instead of on the lane chain,
+      // measured at BASELINE config 2: 0.46 -> 0.40 ms; the linear XW forward
+      // is faster without it, 0.26 vs 0.30 ms)
+      constexpr bool PIPE = XW ? (KIND == RBF && XWT <= 256 && SK_XW_PIPE != 0)
+                               : (DP >= 16 || (G == 32 && R <= 2));
+      const int lagw = XW ? (XK - 1) * warp : 0;  // extra skew of this warp (XW)
       Cf cf[S][RC];
       if constexpr (PIPE) {
-        if (issuer) cp_async_wait<PF - 1>();  // step 0 landed
-        if (XW) __syncthreads(); else __syncwarp();
-        step_coefs(-u, cf);
+        if constexpr (XW) {
+          if (issuer) cp_async_wait<LOOK - 1>();  // step 0 landed
+          __syncthreads();
+        } else {
+          if (issuer) cp_async_wait<PF - 1>();  // step 0 landed
+          __syncwarp();
+        }
+        step_coefs(-u - lagw, cf);
       }
 
-      const int lagw = XW ? (XK - 1) * warp : 0;  // extra skew of this warp (XW)
       const int nsteps = NSTEP + Grt - 1 + (XW ? (XK - 1) * (nw - 1) : 0);
       for (int tau = 0; tau < nsteps; ++tau) {
         if constexpr (XW) {
@@ -322,7 +335,10 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
           if (issuer) {
             fwd_issue<KIND, DP, F, P, S, T>(ring, smask, pb, pc, hrow0, hand_stride,
                                             (tau + LOOK) * S, NC, strip, lane);
-            if (tau % XK == 0) cp_async_wait<PF>();
+            if (tau % XK == 0) {
+              if constexpr (PIPE) cp_async_wait<PF - 1>();  // ... and step tau + XK (next coefs)
+              else cp_async_wait<PF>();
+            }
           }
           if (tau % XK == 0) __syncthreads();
         } else {
