@@ -495,9 +495,12 @@ def main():
         cpu = cpu_baseline(24 if args.config == "c3" else 8, L, d, lam)
 
     if rank == 0:
-        # per row range: prep + fused DMMA kernel + mirror of the block
-        launches_per_step = 3 * len(ranges)
-        launches_per_step += 1 if world > 1 else 0  # mirror after gather
+        # our kernels per step (ncu launch list, profiles/r02_launches_c3_final.csv):
+        # one GPU: prep_sides, fix_init (exact accumulators), gram_bwd_mma,
+        # fix_finalize, mirror_upper; sharded: accumulator init, per row range
+        # prep + fused kernel + block mirror, then the mirror after the gather
+        # and the finalize
+        launches_per_step = 5 if world == 1 else 3 * len(ranges) + 3
         out = {
             "metric": METRIC, "value": value, "unit": "cells/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
