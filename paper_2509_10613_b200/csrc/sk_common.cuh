@@ -121,6 +121,25 @@ __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + 
 //   the finalize step writes NaN (never a silent wrong value).
 // meta[0]: max|cot| bit pattern (atomicMax; non-negative doubles order like
 // their bits), meta[1]: flags, meta[2]: nscale (double bits).
+// L2 residency hints (sm_80+ cache-policy operands): scratch that one warp
+// re-reads many times (the DMMA backward's column-gradient rows) is marked
+// evict-last so the streaming checkpoint traffic does not push it to HBM.
+__device__ __forceinline__ unsigned long long l2_evict_last_policy() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld_l2hint(const double2* a, unsigned long long pol) {
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_l2hint(double2* a, double2 v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;"
+               :: "l"(a), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+
 struct FixAcc {
   unsigned long long* acc;  // [elements][4]
   unsigned long long* meta;

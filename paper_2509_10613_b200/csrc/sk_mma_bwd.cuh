@@ -117,6 +117,8 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
   double2* __restrict__ colck = reinterpret_cast<double2*>(ba.colck + slot * ba.colck_stride);
   double* __restrict__ arow = ba.adj + (slot * 8 + g) * ba.row_stride;
   double* __restrict__ gcs = ba.gscr + slot * ba.gscr_stride;  // column gradients [8*NT8][DP]
+  // read-modified-written once per strip and block: keep it in L2
+  const unsigned long long pol_keep = l2_evict_last_policy();
   const FixAcc fxR = fix_make(ba.accR, ba.metaR), fxC = fix_make(ba.accC, ba.metaC);
   double* __restrict__ rs = ba.rsum + slot * ba.rsum_stride;  // [8][M1][DP]
 
@@ -385,7 +387,8 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         double2 gco[NN];  // column-gradient scratch of tile blk, read early
 #pragma unroll
         for (int n = 0; n < NN; ++n)
-          gco[n] = *reinterpret_cast<const double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u);
+          gco[n] = ld_l2hint(reinterpret_cast<const double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u),
+                             pol_keep);
         // the row above the lane: lane u = 0 from the strip's top row; lane
         // u > 0 starts from lane u-1's checkpoints (node columns 8blk-u,
         // 8blk-u+1) and receives the rest from lane u-1's recompute below
@@ -542,9 +545,10 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           }
 #pragma unroll
           for (int n = 0; n < NN; ++n)
-            *reinterpret_cast<double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u) =
-                make_double2(gco[n].x + ((c[n][0][0] + c[n][1][0]) + (c[n][2][0] + c[n][3][0])),
-                             gco[n].y + ((c[n][0][1] + c[n][1][1]) + (c[n][2][1] + c[n][3][1])));
+            st_l2hint(reinterpret_cast<double2*>(gcs + (int64_t)(8 * blk + g) * DP + 8 * n + 2 * u),
+                      make_double2(gco[n].x + ((c[n][0][0] + c[n][1][0]) + (c[n][2][0] + c[n][3][0])),
+                                   gco[n].y + ((c[n][0][1] + c[n][1][1]) + (c[n][2][1] + c[n][3][1]))),
+                      pol_keep);
         }
         }
         __syncwarp();
