@@ -59,6 +59,11 @@ __host__ __device__ constexpr int xw_ring_slots(int lanes, int S, int PF) {
   return ring_slots(lanes + (SK_XW_LAG - 1) * (lanes / 32) + 2 * SK_XW_LAG, S, PF);
 }
 
+// the same pipeline for the one-pair-per-warp / Gram-tile RBF instances:
+// measured slower (RBF Gram 256 x 256, L = 128: 3.2 -> 4.6 ms), off
+#ifndef SK_RBF_PIPE
+#define SK_RBF_PIPE 0
+#endif
 #ifndef SK_XW_PIPE
 #define SK_XW_PIPE 1
 #endif
@@ -313,7 +318,7 @@ fwd_kernel(Problem pb, double* __restrict__ hand_, int64_t hand_stride) {
       // measured at BASELINE config 2: 0.46 -> 0.40 ms; the linear XW forward
       // is faster without it, 0.26 vs 0.30 ms)
       constexpr bool PIPE = XW ? (KIND == RBF && XWT <= 256 && SK_XW_PIPE != 0)
-                               : (DP >= 16 || (G == 32 && R <= 2));
+                               : (DP >= 16 || (G == 32 && R <= 2) || (KIND == RBF && SK_RBF_PIPE));
       const int lagw = XW ? (XK - 1) * warp : 0;  // extra skew of this warp (XW)
       Cf cf[S][RC];
       if constexpr (PIPE) {
