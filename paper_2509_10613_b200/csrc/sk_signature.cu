@@ -371,8 +371,10 @@ sig_bwd_kernel(const double* __restrict__ inc, int64_t M, SigGeom g, double* __r
     }
     // ---- the segment exponential E = exp(z)
     cta_exp(EX, z, 1.0, g);
-    // ---- EB = adjoint w.r.t. E: EB_m = SB_m + sum_{k>m} A_{k-m}^T SB_k
-    for (int64_t t = threadIdx.x; t < total; t += blockDim.x) EB[t] = SB[t];
+    // ---- EB = adjoint w.r.t. E: EB_m = SB_m + sum_{k>m} A_{k-m}^T SB_k.  The
+    // top level has no correction (EB_N = SB_N, and SB_N is never updated), so
+    // it is read from SB below and only the lower levels are copied
+    for (int64_t t = threadIdx.x; t < g.off[N - 1]; t += blockDim.x) EB[t] = SB[t];
     __syncthreads();
     for (int m = 1; m < N; ++m)
       for (int k = m + 1; k <= N; ++k)
@@ -390,7 +392,7 @@ sig_bwd_kernel(const double* __restrict__ inc, int64_t M, SigGeom g, double* __r
       const double im = c_inv[m];
       const int64_t rows = g.pw[m - 1];
       const double* Em1 = EX + g.off[m - 2];
-      double* Bm = EB + g.off[m - 1];
+      double* Bm = (m == N ? SB : EB) + g.off[m - 1];
       double* Bm1 = EB + g.off[m - 2];
       // g[j] += sum_rows E_{m-1}[row] * (Bm[row, j] / m)   (chunked, fixed order)
       {
@@ -421,7 +423,8 @@ sig_bwd_kernel(const double* __restrict__ inc, int64_t M, SigGeom g, double* __r
       }
       __syncthreads();
     }
-    for (int j = threadIdx.x; j < d; j += blockDim.x) go[step * d + j] = add(gz[j], EB[j]);
+    for (int j = threadIdx.x; j < d; j += blockDim.x)
+      go[step * d + j] = add(gz[j], (N == 1 ? SB : EB)[j]);
     __syncthreads();
   }
 }
