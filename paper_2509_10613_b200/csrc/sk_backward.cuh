@@ -80,8 +80,14 @@ struct BwdSmem {
   static constexpr int GSTR = DP + 2;                // row stride: conflict-free 16-B accesses
   static constexpr int PS = CB * S * RC * NL;        // coarse p checkpoints of the next block
   static constexpr int XCH = NL > 32 ? 4 * (NL / 32) * SF : 0;  // cross-warp hops (2 x 2 buffers)
-  static constexpr int MAIN = SLOTS * REC + (NK + NP + NTR) * NL + TS + T0 + LS + 2 * GS +
-                              GROWS * GSTR + 2 * DP + PS + XCH;
+  // block values, coarse p and top row: registers when <= 32 values per lane
+  // (REGK in bwd_kernel), else per-lane shared-memory columns
+  static constexpr int KPT = NK <= 32 ? 0 : NK + NP + NTR;
+  // staged block inputs, double-buffered by block parity (the next block's
+  // staging is issued before this block's recompute, no barrier between)
+  static constexpr int STG = TS + T0 + LS + PS;
+  static constexpr int MAIN = SLOTS * REC + KPT * NL + 2 * STG + 2 * GS + GROWS * GSTR + 2 * DP +
+                              XCH;
   // RBF node-adjoint epilogue (after the sweep, reuses the region): a band of
   // EH node rows x NL node columns -- D tile (EH+1) x (NL+1), weights EH x
   // (NL+1), the band's row nodes, the chunk's column nodes
@@ -113,17 +119,20 @@ bwd_kernel(Problem pb, BwdArgs ba) {
   const int u = XW ? (int)threadIdx.x : lane;  // lane of the pair's wavefront
   double* ring = smem + (XW ? 0 : (size_t)warp * SM::TOTAL);
   double* sK = ring + SLOTS * REC;
-  double* sP = sK + SM::NK * NL;
-  double* sTR = sP + SM::NP * NL;
-  double* sTS = sTR + SM::NTR * NL;
-  double* sT0 = sTS + SM::TS;
-  double* sLS = sT0 + SM::T0;
-  double* sGS0 = sLS + SM::LS;
+  double* sP = sK + (SM::KPT ? SM::NK * NL : 0);
+  double* sTR = sP + (SM::KPT ? SM::NP * NL : 0);
+  double* sSTG = sTR + (SM::KPT ? SM::NTR * NL : 0);  // [2][STG] staged block inputs
+  // staging of block parity par: top-row checkpoints, lane 0's top row, left
+  // column checkpoint, coarse p
+  auto stg_ts = [&](int par) { return sSTG + par * SM::STG; };
+  auto stg_t0 = [&](int par) { return sSTG + par * SM::STG + SM::TS; };
+  auto stg_ls = [&](int par) { return sSTG + par * SM::STG + SM::TS + SM::T0; };
+  auto stg_ps = [&](int par) { return sSTG + par * SM::STG + SM::TS + SM::T0 + SM::LS; };
+  double* sGS0 = sSTG + 2 * SM::STG;
   double* sGW = sGS0 + 2 * SM::GS;
   double* sZero = sGW + SM::GROWS * SM::GSTR;  // DP zeros (the last lane's unseeded rows)
   double* sGA = sZero + DP;                    // lane 0's coarse-column sums (2^lam2 > F)
-  double* sPS = sGA + DP;                      // staged coarse p of the next block
-  double* sXA = sPS + SM::PS;                  // XW: [2][NW][SF] forward hops (bottom rows)
+  double* sXA = sGA + DP;                      // XW: [2][NW][SF] forward hops (bottom rows)
   double* sXB = sXA + (XW ? 2 * NW * SF : 0);  // XW: [2][NW][SF] backward hops (messages)
 #define SK_BAR()                          \
   do {                                     \
@@ -431,10 +440,14 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       RowRegs<KIND, DP, RC> rr;
       load_rows<KIND, DP, RC>(rr, pb, pr, i0, 0);
 
-      // records + staging of block blk: top-row checkpoints, lane 0's top row,
-      // left checkpoint (single buffers, consumed by the recompute) and lane
-      // 31's incoming column gradients (double buffered, used by the sweep)
+      // records + staging of block blk (buffers of parity blk & 1): top-row
+      // checkpoints, lane 0's top row, left checkpoint, coarse p (consumed by
+      // the recompute) and lane 31's incoming column gradients (the sweep)
       auto issue_block = [&](int blk, bool first) {
+        double* sTS = stg_ts(blk & 1);
+        double* sT0 = stg_t0(blk & 1);
+        double* sLS = stg_ls(blk & 1);
+        double* sPS = stg_ps(blk & 1);
         if (first) issue_cols((blk * CB - (NL - 1)) * S, (CB + NL - 1) * S, arow, true);
         else issue_cols((blk * CB - (NL - 1)) * S, CB * S, arow, true);  // the new columns only
         {
@@ -503,7 +516,13 @@ bwd_kernel(Problem pb, BwdArgs ba) {
       issue_block(NB - 1, true);
       for (int blk = NB - 1; blk >= 0; --blk) {
         cp_async_wait<0>();
-        SK_BAR();
+        SK_BAR();  // block blk staged; block blk+1's buffers (parity of blk-1) consumed
+        const double* sTS = stg_ts(blk & 1);
+        const double* sT0 = stg_t0(blk & 1);
+        const double* sLS = stg_ls(blk & 1);
+        const double* sPS = stg_ps(blk & 1);
+        // the next block's staging goes into the other parity's buffers at once
+        if (blk > 0) issue_block(blk - 1, false);
         const double* sGS = sGS0 + (blk & 1) * SM::GS;
         const int js0 = blk * CB - u;  // lane's first step in this block
         double kleft[R];
@@ -565,9 +584,7 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             }
           }
         }
-        SK_BAR();
-        // staging buffers are free again: prefetch the next block under the sweep
-        if (blk > 0) issue_block(blk - 1, false);
+        if constexpr (SM::KPT != 0) SK_BAR();  // shared-memory block values visible
 
         // ---- reverse sweep over the block, one step per kap
 #pragma unroll
@@ -758,9 +775,10 @@ bwd_kernel(Problem pb, BwdArgs ba) {
             if (!excl) SK_BAR();
           }
         }
-        SK_BAR();
+        // (no barrier: the next block starts with one)
       }
       cp_async_wait<0>();
+      SK_BAR();
       if constexpr (MAP == FUSED) {
         // row-side dF/d(dx_i) into the pair's scratch.  A coarse row owned by
         // one lane is stored once; when 2^lam1 > R a coarse row spans lanes
