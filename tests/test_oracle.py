@@ -166,3 +166,48 @@ def test_signature_oracle_pinned_to_reference(oracle):
         np.testing.assert_array_equal(sig, g[f"s{i}_sig"])
         grad = oracle.signature_backward(x, depth, g[f"s{i}_cot"], kinds[tf], times)
         np.testing.assert_array_equal(grad, g[f"s{i}_grad"])
+
+
+def _rbf_sigkernel_torch(x, y, lam1, lam2, sigma):
+    """Independent differentiable restatement (torch fp64, autograd) of the RBF
+    signature kernel: node kernel K, coarse second difference, the reference's
+    cell recurrence (_kernels.py:286-290, dyadic refinement as in
+    goursat_strip, _kernels.py:293-338) -- reverse-mode of the same
+    discretisation, no hand-written adjoint."""
+    import torch
+    K = torch.exp(-((x[:, None, :] - y[None, :, :]) ** 2).sum(-1) / (2.0 * sigma * sigma))
+    delta = (K[1:, 1:] - K[1:, :-1]) - (K[:-1, 1:] - K[:-1, :-1])
+    scale = 2.0 ** -(lam1 + lam2)
+    M1, M2 = (x.shape[0] - 1) << lam1, (y.shape[0] - 1) << lam2
+    one = torch.ones((), dtype=torch.float64)
+    prev = [one] * (M2 + 1)
+    for s in range(1, M1 + 1):
+        cur = [one]
+        for t in range(1, M2 + 1):
+            p = delta[(s - 1) >> lam1, (t - 1) >> lam2] * scale
+            a = 1.0 + p * 0.5 + p * p * (1.0 / 12.0)
+            b = 1.0 - p * p * (1.0 / 12.0)
+            cur.append((prev[t] + cur[t - 1]) * a - prev[t - 1] * b)
+        prev = cur
+    return prev[M2]
+
+
+@pytest.mark.parametrize("L1,L2,d,lam1,lam2,sigma", [(5, 4, 2, 1, 1, 0.7), (4, 6, 3, 2, 0, 1.3),
+                                                      (6, 5, 1, 0, 2, 0.5)])
+def test_rbf_adjoint_pinned_by_autograd(oracle, L1, L2, d, lam1, lam2, sigma):
+    """The RBF kappa adjoint (no reference counterpart) against torch autograd of
+    an independent restatement: values and both gradients to 1e-12 -- pins the
+    oracle the GPU RBF backward tests compare with."""
+    import torch
+    rng = np.random.default_rng(L1 * 10 + L2 + d)
+    x = rng.standard_normal((L1, d)) * 0.5
+    y = rng.standard_normal((L2, d)) * 0.5
+    xt = torch.tensor(x, requires_grad=True)
+    yt = torch.tensor(y, requires_grad=True)
+    k = _rbf_sigkernel_torch(xt, yt, lam1, lam2, sigma)
+    k.backward()
+    v, gx, gy = oracle.kernel_batch_backward(x[None], y[None], lam1, lam2,
+                                             static_kernel=("rbf", sigma))
+    assert abs(v[0] - k.item()) <= 1e-12 * abs(k.item())
+    assert rel_err(gx[0], xt.grad.numpy()) < 1e-12
+    assert rel_err(gy[0], yt.grad.numpy()) < 1e-12
