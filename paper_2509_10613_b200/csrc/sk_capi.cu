@@ -475,7 +475,7 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
   }
   // Gram tiles of the linear kernel at dyadic order 0: increment products on
   // the FP64 tensor cores (sk_mma_fwd.cuh).  SK_NO_MMA=1 keeps the r01 kernels.
-  s.MMA = gram && !f32 && kind == LINEAR && lamR == 0 && lamC == 0 && nch == 1 && s.DP <= 16 &&
+  s.MMA = gram && !f32 && kind == LINEAR && lamR == 0 && lamC == 0 && nch == 1 && s.DP <= 32 &&
           !(std::getenv("SK_NO_MMA") && std::getenv("SK_NO_MMA")[0] == '1');
   if (s.MMA) {
     int per_warp = 0;

@@ -8,6 +8,7 @@ FwdFn select_fwd_mma(int DP, int& smem_per_warp) {
     case 4: return gram_fwd_mma<4>;
     case 8: return gram_fwd_mma<8>;
     case 16: return gram_fwd_mma<16>;
+    case 32: return gram_fwd_mma<32>;
     default: return nullptr;
   }
 }

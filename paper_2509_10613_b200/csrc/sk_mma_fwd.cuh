@@ -56,7 +56,7 @@ struct MmaFwdCfg {
 };
 
 template <int DP>
-__global__ void __launch_bounds__(MmaFwdCfg::THREADS, 3)
+__global__ void __launch_bounds__(MmaFwdCfg::THREADS, DP >= 32 ? 2 : 3)
 gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
   constexpr int KS = DP / 4;
   constexpr int PSTR = MmaFwdCfg::PSTR;

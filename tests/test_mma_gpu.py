@@ -39,6 +39,7 @@ class _NoMMA:
 SHAPES = [  # (n1, n2, L, d)
     (1, 1, 2, 1), (3, 3, 3, 2), (9, 9, 9, 4), (8, 8, 17, 5), (17, 17, 33, 8),
     (5, 12, 64, 3), (16, 16, 70, 16), (11, 11, 130, 13), (24, 24, 41, 7), (4, 4, 300, 16),
+    (10, 10, 45, 17), (9, 13, 60, 32), (12, 12, 129, 24),  # DP = 32 instance
 ]
 
 
