@@ -231,6 +231,21 @@ def test_sig_mmd(mods, lam):
     assert rel_err(gy2.cpu().numpy(), gyw) < TOL
 
 
+def test_sig_mmd_same_sample(mods):
+    """MMD^2(X, X) = 0 with zero gradients (a minimum), through the fused API
+    with the same tensor twice (the cross term must stay a cross
+    Gram); dtype follows the input."""
+    import paper_2509_10613_b200 as sk
+    rng = np.random.default_rng(5)
+    X = random_paths(rng, 6, 25, 4)
+    xt = cu(X)
+    v, gx, gy = sk.sig_mmd_value_and_grad(xt, xt)
+    assert abs(v.item()) < 1e-13
+    assert gx.abs().max().item() < 1e-12 and gy.abs().max().item() < 1e-12
+    v32, _, _ = sk.sig_mmd_value_and_grad(xt.float(), xt.float())
+    assert v32.dtype == torch.float32
+
+
 @pytest.mark.parametrize("no_mma", [False, True])
 def test_backward_workspace_budget_caps_slots(mods, no_mma):
     """With a tiny workspace budget the backward runs on fewer resident slots
