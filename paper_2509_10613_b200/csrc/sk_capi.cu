@@ -473,9 +473,14 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
       short_r = true;
     }
   }
-  // Gram tiles of the linear kernel at dyadic order 0: increment products on
+  // Gram tiles of the linear kernel (any dyadic order): increment products on
   // the FP64 tensor cores (sk_mma_fwd.cuh).  SK_NO_MMA=1 keeps the r01 kernels.
-  s.MMA = gram && !f32 && kind == LINEAR && lamR == 0 && lamC == 0 && nch == 1 && s.DP <= 32 &&
+  // (measured, n = 256-512 Grams: DMMA wins for DP >= 16 at any order --
+  // lambda 1: d = 16 11.5 -> 4.8 ms, d = 32 41 -> 7.3 ms; lambda 2, d = 16 6.8
+  // -> 4.2 ms -- and for DP = 8 at order 0; the FMA-pipe kernel wins for
+  // DP = 4 (d = 4, lambda 0: 8.4 vs 13.4 ms) and for DP = 8 at order > 0)
+  const bool mma_shape = s.DP >= 16 || (s.DP == 8 && lamR + lamC == 0);
+  s.MMA = gram && !f32 && kind == LINEAR && nch == 1 && s.DP <= 32 && mma_shape &&
           !(std::getenv("SK_NO_MMA") && std::getenv("SK_NO_MMA")[0] == '1');
   if (s.MMA) {
     int per_warp = 0;
@@ -492,8 +497,9 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
     const int occ = occupancy((const void*)fn, pl.threads, pl.smem_bytes);
     pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + fwpc - 1) / fwpc, (int64_t)occ * sms));
     pl.slots = pl.blocks * fwpc * pl.P;
-    // lane u = 0 prefetches the handoff row 8 columns ahead of an 8-step tile loop
-    pl.hand_stride = 8 * ((M2c + 10) / 8 + 2);
+    // lane u = 0 prefetches the handoff row 8 columns ahead of an 8-step tile
+    // loop (fine columns)
+    pl.hand_stride = 8 * (((M2c << lamC) + 10) / 8 + 2);
     return SK_OK;
   }
   int smem = 0;

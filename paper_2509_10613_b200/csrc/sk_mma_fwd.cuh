@@ -65,7 +65,16 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
   const int g = lane >> 2, u = lane & 3;
   double2* __restrict__ sP = smem_mf + (size_t)warp * MmaFwdCfg::RING * MmaFwdCfg::TILE;
 
-  const int M1 = pb.M1c, NC = pb.M2c;  // dyadic order 0: fine == coarse
+  // dyadic orders (round 2): fine rows / columns, coarse = fine >> lam.  The
+  // p tiles are coarse (8 coarse columns); their B operand row r is the coarse
+  // row of the strip's fine row r, so the C fragment of lane (g, u) still holds
+  // p of the lane's two fine rows (duplicated coarse rows cost redundant DMMA
+  // work, no layout change); a coarse tile spans 8 << lam2 fine columns and is
+  // formed during the first 8-column iteration of the tile two ahead.
+  const int lamR = pb.lam1, lamC = pb.lam2;
+  const int M1 = pb.M1c << lamR, NC = pb.M2c << lamC;  // fine rows / columns
+  const int M2c = pb.M2c;
+  const int LCm = (1 << lamC) - 1;
   const int nstrips = (M1 + 7) >> 3;
   const int NT8 = (NC + 3 + 7) >> 3;  // 8-step iterations per strip (skew 3)
   const int u_star = ((M1 - 1) & 7) >> 1, r_star = (M1 - 1) & 1;
@@ -85,20 +94,21 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
       // B fragments: dX of pair h, row strip*8 + lane/4, component 4kk + lane%4
       double bf[8][KS];
       {
-        const int row = strip * 8 + g;
+        const int row = strip * 8 + g;    // fine row
+        const int crow = row >> lamR;      // its coarse row
 #pragma unroll
         for (int h = 0; h < 8; ++h) {
           const int ah = min(a0 + h, pb.r1 - 1);
-          const double* rp = pb.R.p + (int64_t)ah * pb.R.path_stride + (int64_t)row * DP + u;
+          const double* rp = pb.R.p + (int64_t)ah * pb.R.path_stride + (int64_t)crow * DP + u;
 #pragma unroll
           for (int kk = 0; kk < KS; ++kk) bf[h][kk] = (row < M1) ? __ldg(rp + 4 * kk) : 0.0;
         }
       }
-      auto loadA = [&](int T, double (&af)[KS]) {
+      auto loadA = [&](int T, double (&af)[KS]) {  // coarse tile T: coarse columns 8T + g
         const int col = 8 * T + g;
         const double* cp = cpath + (int64_t)col * DP + u;
 #pragma unroll
-        for (int kk = 0; kk < KS; ++kk) af[kk] = (col < NC) ? __ldg(cp + 4 * kk) : 0.0;
+        for (int kk = 0; kk < KS; ++kk) af[kk] = (col < M2c) ? __ldg(cp + 4 * kk) : 0.0;
       };
       auto tile = [&](int T, int h, const double (&af)[KS]) {
         double c0 = 0.0, c1 = 0.0;
@@ -126,7 +136,13 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
         }
       }
       __syncwarp();
-      double2 pcur = sP[((((0 - u) >> 3) & 3) * 8 + ((0 - u) & 7)) * PSTR + lane];
+      // p of fine column c: coarse column jc = c >> lamC, tile jc >> 3 (c < 0:
+      // arithmetic shift keeps the skewed lanes' dead columns in tile -1)
+      auto pslot = [&](int c) {
+        const int jc = c >> lamC;
+        return (((jc >> 3) & 3) * 8 + (jc & 7)) * PSTR + lane;
+      };
+      double2 pcur = sP[pslot(0 - u)];
       double kl0 = 1.0, kl1 = 1.0, topc = 1.0, bot = 1.0;
       const bool last = strip == nstrips - 1;
 
@@ -134,7 +150,10 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
       // the final column (the only ones that need range checks)
       auto iter = [&](auto edge, int T) {
         constexpr bool EDGE = decltype(edge)::value;
-        loadA(T + 3, an);
+        // coarse tile Tc + 2 is formed in the first fine iteration of tile Tc
+        const bool newtile = (T & LCm) == 0;
+        const int Tc = T >> lamC;
+        if (newtile) loadA(Tc + 3, an);
         double hnxt[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) hnxt[m] = 1.0;
@@ -148,13 +167,10 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
         }
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
-          tile(T + 2, m, af);
-          const int c = 8 * T + m - u;  // this lane's column
+          if (newtile) tile(Tc + 2, m, af);
+          const int c = 8 * T + m - u;  // this lane's (fine) column
           const double2 pv = pcur;
-          {
-            const int cn = c + 1;
-            pcur = sP[(((cn >> 3) & 3) * 8 + (cn & 7)) * PSTR + lane];
-          }
+          pcur = sP[pslot(c + 1)];
           double tv = __shfl_up_sync(0xffffffffu, bot, 1, 4);
           if (u == 0) tv = hcur[m];
           if (!EDGE || (c >= 0 && c < NC)) {
@@ -169,8 +185,10 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
             if (EDGE && last && u == u_star && c == NC - 1) kval = r_star ? k1 : k0;
           }
         }
+        if (newtile) {
 #pragma unroll
-        for (int kk = 0; kk < KS; ++kk) af[kk] = an[kk];
+          for (int kk = 0; kk < KS; ++kk) af[kk] = an[kk];
+        }
 #pragma unroll
         for (int m = 0; m < 8; ++m) hcur[m] = hnxt[m];
         __syncwarp();  // tile T+2 visible; tile T-2's slot free

@@ -59,6 +59,27 @@ def test_gram_forward_mma(mods, n1, n2, L, d):
         np.testing.assert_array_equal(got, got.T)
 
 
+@pytest.mark.parametrize("n1,n2,L1,L2,d,l1,l2", [
+    (9, 9, 20, 20, 4, 1, 1), (7, 7, 13, 13, 8, 2, 2), (6, 11, 17, 15, 5, 1, 2),
+    (10, 10, 9, 9, 16, 3, 0), (5, 8, 30, 12, 3, 0, 2), (12, 12, 33, 33, 24, 1, 1),
+    (4, 6, 25, 40, 8, 2, 1),  # longer columns' fine axis: the cross Gram swaps
+])
+def test_gram_forward_mma_dyadic(mods, n1, n2, L1, L2, d, l1, l2):
+    """DMMA Gram forward at dyadic orders > 0 (coarse p tiles, duplicated
+    coarse rows in the B operand, a tile spanning 8 << lam2 fine columns):
+    vs the oracle, and bitwise the FMA-pipe kernels' values (same p chain)."""
+    ops, orc = mods
+    rng = np.random.default_rng(n1 * 100 + L1 + d + l1 + 7 * l2)
+    X = random_paths(rng, n1, L1, d)
+    Y = random_paths(rng, n2, L2, d) if (n1 != n2 or L1 != L2) else None
+    want = orc.kernel_gram(X, Y, l1, l2)
+    got = ops.forward_gram(cu(X), None if Y is None else cu(Y), l1, l2, 0, 1.0).cpu().numpy()
+    assert rel_err(got, want) < TOL
+    with _NoMMA():
+        old = ops.forward_gram(cu(X), None if Y is None else cu(Y), l1, l2, 0, 1.0).cpu().numpy()
+    np.testing.assert_array_equal(got, old)
+
+
 def test_gram_forward_mma_cross_lengths(mods):
     ops, orc = mods
     rng = np.random.default_rng(3)
