@@ -368,6 +368,29 @@ class GradAcc:
         return out
 
 
+def transform_adjoint(gt: torch.Tensor, L: int, d: int, transform) -> torch.Tensor:
+    """Point gradients of the transformed paths gt (n, L', d') -> the raw paths'
+    (n, L, d) (reference transform_adjoint, transforms.py:66-88, same addition
+    order) by the C-ABI kernel sk_transform_adjoint."""
+    lib = _lib.load()
+    tf = transform_code(transform)
+    if not isinstance(gt, torch.Tensor) or not gt.is_cuda or gt.dim() != 3:
+        raise InvalidArgument("gt must be a (n, L', d') CUDA tensor")
+    gt = gt.to(torch.float64).contiguous()
+    n = gt.shape[0]
+    Le, de = effective_shape(L, d, tf)
+    if tuple(gt.shape[1:]) != (Le, de):
+        raise InvalidArgument(f"gradient of the transformed paths must be ({n}, {Le}, {de}), "
+                              f"got {tuple(gt.shape)}")
+    out = torch.empty((n, L, d), dtype=torch.float64, device=gt.device)
+    if n == 0:
+        return out
+    with _on(gt.device):
+        _lib.check(lib.sk_transform_adjoint(gt.data_ptr(), n, L, d, tf, out.data_ptr(), 0,
+                                            _stream(gt.device)))
+    return out
+
+
 def _gram_args(x, y):
     x = _paths(x, "x")
     sym = y is None

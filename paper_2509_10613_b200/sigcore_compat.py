@@ -32,7 +32,11 @@ from .signatures import (PathBatch, SigOptions, TensorShape, sig_tensor_shape,  
 from .signatures import signature_backward_np as signature_backward  # noqa: E402
 from .signatures import signature_np as signature  # noqa: E402
 
-__all__ = ["KernelConfig", "SolveResult", "InvalidArgument", "InvalidState", "increment_gram",
+from .sgt_io import FormatError, read_array, write_array  # noqa: E402
+
+__all__ = ["KernelConfig", "SolveResult", "InvalidArgument", "InvalidState", "FormatError",
+           "read_array", "write_array", "transform", "transform_adjoint", "fused_increments",
+           "effective_dim", "effective_length", "default_times", "increment_gram",
            "fine_cells", "solve_workspace_elements", "solve_goursat", "kernel_batch",
            "kernel_gram", "kernel_backward", "kernel_batch_backward",
            # truncated signatures (reference signature.py, signature_grad.py, tensors.py)
@@ -221,3 +225,125 @@ def kernel_batch_backward(x, y, cfg: KernelConfig, cot=None, threads: int | None
     if squeeze:
         return vals[0], gx[0], gy[0]
     return vals, gx, gy
+
+
+# ------------------------------------------------------------ path transforms
+# The reference's numpy transform utilities (transforms.py:30-135) with the
+# same names, shapes, dtypes and errors; the work runs on the GPU (torch ops
+# for the index bookkeeping, the C-ABI adjoint kernel for transform_adjoint).
+# The kernels themselves never need them: sig_kernel(..., transform=...) builds
+# the transformed increments inside the kernels' input preparation.
+TRANSFORM_KINDS = ("time_augment", "lead_lag")
+
+
+def _check_kind(kind):
+    if kind not in TRANSFORM_KINDS:
+        raise InvalidArgument(f"unknown transform kind {kind!r}, expected one of {TRANSFORM_KINDS}")
+
+
+def _as_3d_np(data, name="path batch"):
+    data = np.asarray(data)
+    if data.ndim == 2:
+        return data[None], True
+    if data.ndim != 3:
+        raise InvalidArgument(f"{name} must be (L, d) or (B, L, d), got shape {data.shape}")
+    return data, False
+
+
+def default_times(length: int, dtype=np.float64) -> np.ndarray:
+    """Uniform time grid on [0, 1] (numpy.linspace); a single point sits at 0."""
+    if length == 1:
+        return np.zeros(1, dtype=dtype)
+    return np.linspace(0.0, 1.0, length, dtype=dtype)
+
+
+def _times_t(times, length, dtype, dev):
+    t = default_times(length, dtype) if times is None else np.asarray(times, dtype=dtype)
+    if t.shape != (length,):
+        raise InvalidArgument(f"time grid has shape {t.shape}, expected ({length},)")
+    return torch.as_tensor(t, device=dev)
+
+
+def transform(batch, kind: str, times=None):
+    """transforms.py:37-63: time_augment (B, L, d) -> (B, L, d+1), lead_lag ->
+    (B, 2L-1, 2d) with Z[2k] = (X[k], X[k]), Z[2k+1] = (X[k+1], X[k])."""
+    _check_kind(kind)
+    data, squeeze = _as_3d_np(batch)
+    b, length, d = data.shape
+    if length < 1:
+        raise InvalidArgument("transform needs at least one point")
+    dev = _device()
+    x = torch.as_tensor(np.ascontiguousarray(data), device=dev)
+    if kind == "time_augment":
+        t = _times_t(times, length, data.dtype, dev)
+        out = torch.cat([x, t.view(1, length, 1).expand(b, length, 1)], dim=2)
+    else:
+        out = torch.empty((b, 2 * length - 1, 2 * d), dtype=x.dtype, device=dev)
+        out[:, 0::2, :d] = x
+        out[:, 0::2, d:] = x
+        out[:, 1::2, :d] = x[:, 1:]
+        out[:, 1::2, d:] = x[:, :-1]
+    out = out.cpu().numpy()
+    return out[0] if squeeze else out
+
+
+def transform_adjoint(grad_out, kind: str):
+    """transforms.py:66-88 through the C-ABI adjoint kernel (sk_transform_adjoint,
+    the same addition order): the time column gets no gradient; each lead-lag
+    point sums the gradients of every slot that reads it."""
+    _check_kind(kind)
+    g, squeeze = _as_3d_np(grad_out, "gradient batch")
+    b, length, dim = g.shape
+    if kind == "time_augment":
+        if dim < 2:
+            raise InvalidArgument("time-augmented gradient needs at least 2 coordinates")
+        L, d = length, dim - 1
+    else:
+        if dim % 2 != 0 or length % 2 != 1:
+            raise InvalidArgument(
+                f"lead-lag gradient must be (B, 2L-1, 2d), got shape {g.shape}")
+        L, d = (length + 1) // 2, dim // 2
+    out_dtype = g.dtype
+    gt = torch.as_tensor(np.ascontiguousarray(g, dtype=np.float64), device=_device())
+    out = ops.transform_adjoint(gt, L, d, kind).cpu().numpy().astype(out_dtype, copy=False)
+    return out[0] if squeeze else out
+
+
+def fused_increments(batch, kind: str | None = None, times=None):
+    """transforms.py:91-120: the increments of the transformed path built from
+    the input points (none: (B, L-1, d); time_augment: (B, L-1, d+1); lead_lag:
+    (B, 2L-2, 2d), alternating (dX_k, 0) and (0, dX_k))."""
+    data, squeeze = _as_3d_np(batch)
+    b, length, d = data.shape
+    if length < 1:
+        raise InvalidArgument("increments need at least one point")
+    dev = _device()
+    x = torch.as_tensor(np.ascontiguousarray(data), device=dev)
+    dx = x[:, 1:] - x[:, :-1]
+    if kind is None or kind == "none":
+        out = dx
+    elif kind == "time_augment":
+        t = _times_t(times, length, data.dtype, dev)
+        out = torch.cat([dx, (t[1:] - t[:-1]).view(1, length - 1, 1).expand(b, length - 1, 1)],
+                        dim=2)
+    elif kind == "lead_lag":
+        out = torch.zeros((b, 2 * length - 2, 2 * d), dtype=x.dtype, device=dev)
+        out[:, 0::2, :d] = dx
+        out[:, 1::2, d:] = dx
+    else:
+        _check_kind(kind)
+    out = out.cpu().numpy()
+    return out[0] if squeeze else out
+
+
+def effective_dim(d: int, kind) -> int:
+    """transforms.py:123-128."""
+    if kind is None or kind == "none":
+        return d
+    _check_kind(kind)
+    return d + 1 if kind == "time_augment" else 2 * d
+
+
+def effective_length(length: int, kind) -> int:
+    """transforms.py:131-135."""
+    return 2 * length - 1 if kind == "lead_lag" else length

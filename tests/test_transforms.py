@@ -153,3 +153,24 @@ def test_fused_transform_fp32(oracle):
         xt = path_transform(torch.as_tensor(x.astype(np.float64)), kind).numpy()
         yt = path_transform(torch.as_tensor(y.astype(np.float64)), kind).numpy()
         assert rel_err(k, oracle.kernel_batch(xt, yt, 0, 0)) < 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,gkey,akey", [("time_augment", "g_ta", "adj_ta"),
+                                            ("lead_lag", "g_ll", "adj_ll")])
+def test_sigcore_facade_transforms_match_reference(kind, gkey, akey):
+    """The facade's reference-named utilities (transforms.py:37-135) against
+    the reference's own outputs (tests/golden/transforms.npz, bitwise), and
+    fused_increments == np.diff of the transformed path."""
+    from paper_2509_10613_b200 import sigcore_compat as sc
+    g = golden("transforms")
+    x = g["x"]
+    np.testing.assert_array_equal(sc.transform(x, kind), g[kind])
+    np.testing.assert_array_equal(sc.transform(x[0], kind), g[kind][0])
+    np.testing.assert_array_equal(sc.transform_adjoint(g[gkey], kind), g[akey])
+    inc = sc.fused_increments(x, kind)
+    np.testing.assert_array_equal(inc, np.diff(g[kind], axis=1))
+    assert sc.effective_dim(x.shape[2], kind) == g[kind].shape[2]
+    assert sc.effective_length(x.shape[1], kind) == g[kind].shape[1]
+    with pytest.raises(sc.InvalidArgument):
+        sc.transform(x, "bogus")
