@@ -484,7 +484,7 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
           !(std::getenv("SK_NO_MMA") && std::getenv("SK_NO_MMA")[0] == '1');
   if (s.MMA) {
     int per_warp = 0;
-    FwdFn fn = select_fwd_mma(s.DP, per_warp);
+    FwdFn fn = select_fwd_mma(s.DP, per_warp, lamR + lamC > 0);
     if (!fn) return fail(SK_INVALID_ARGUMENT, "no DMMA forward instance for this shape");
     pl.shape = s;
     pl.fn = fn;

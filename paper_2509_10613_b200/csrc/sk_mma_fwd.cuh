@@ -55,7 +55,9 @@ struct MmaFwdCfg {
   static constexpr int THREADS = 128;
 };
 
-template <int DP>
+//   DY  dyadic orders > 0 (runtime lam1 / lam2); false: order 0 at compile
+//       time, so the order-0 instance (C3, C5) carries no index shifts
+template <int DP, bool DY = false>
 __global__ void __launch_bounds__(MmaFwdCfg::THREADS, DP >= 32 ? 2 : 3)
 gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
   constexpr int KS = DP / 4;
@@ -71,7 +73,7 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
   // p of the lane's two fine rows (duplicated coarse rows cost redundant DMMA
   // work, no layout change); a coarse tile spans 8 << lam2 fine columns and is
   // formed during the first 8-column iteration of the tile two ahead.
-  const int lamR = pb.lam1, lamC = pb.lam2;
+  const int lamR = DY ? pb.lam1 : 0, lamC = DY ? pb.lam2 : 0;
   const int M1 = pb.M1c << lamR, NC = pb.M2c << lamC;  // fine rows / columns
   const int M2c = pb.M2c;
   const int LCm = (1 << lamC) - 1;
