@@ -964,14 +964,22 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   // (sk_mma_bwd.cuh).  SK_NO_MMA=1 keeps the r01 kernels.
   // (d <= 4 runs the DP = 8 instance on zero-padded increments: the padding
   // adds exact zeros to every FMA chain, so p is bitwise unchanged)
-  s.MMA = shared_cols && kind == LINEAR && lamR == 0 && lamC == 0 && s.DP <= 16 && !wide &&
+  // dyadic orders > 0: the DY instance (coarse p tiles) only on request
+  // (SK_MMA_DY=1, read per plan like SK_NO_MMA): its gradient maps run per
+  // fine cell where the FMA-pipe backward sums D per coarse cell first, and it
+  // measured no faster (n = 256 Grams, lambda 1: d = 16 30.3 vs 30.0 ms,
+  // d = 8 23.6 vs 14.8 ms; lambda 2, d = 16: 28.1 vs 25.8 ms)
+  const char* mdy = std::getenv("SK_MMA_DY");
+  const bool dy = lamR + lamC > 0;
+  const bool dy_ok = mdy && mdy[0] == '1';
+  s.MMA = shared_cols && kind == LINEAR && (!dy || dy_ok) && s.DP <= 16 && !wide &&
           !(std::getenv("SK_NO_MMA") && std::getenv("SK_NO_MMA")[0] == '1');
   if (s.MMA) {
     if (s.DP == 4) s.DP = 8;
     const char* w = std::getenv("SK_BWD_WPC");
     s.WPC = (w && (w[0] == '3' || w[0] == '4')) ? w[0] - '0' : 2;  // measured: 2 >= 4 > 3
     int per_warp = 0;
-    BwdFn fn = select_bwd_mma(s.DP, s.WPC, per_warp);
+    BwdFn fn = select_bwd_mma(s.DP, s.WPC, per_warp, dy);
     if (!fn) return fail(SK_INVALID_ARGUMENT, "no DMMA backward instance for this shape");
     pl.shape = s;
     pl.fn = fn;
@@ -983,7 +991,9 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
     pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + s.WPC - 1) / s.WPC,
                                                        (int64_t)occ * sms));
     pl.slots = pl.blocks * s.WPC;
-    const int64_t nstrips = (M1c + 7) / 8, NT8 = (M2c + 10) / 8;
+    // (fine rows / columns: the strips and blocks are fine-grid ones)
+    const int64_t M1f = M1c << lamR, M2f = M2c << lamC;
+    const int64_t nstrips = (M1f + 7) / 8, NT8 = (M2f + 10) / 8;
     // rowck: the strips' top rows [strip][8 pairs][8 (NT8 + 5)]; colck: every
     // lane's two values per block (double2); pck: its bottom value a column
     // before (sk_mma_bwd.cuh)
@@ -995,7 +1005,7 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
     pl.row_stride = 8 * (NT8 + 5);
     pl.dbuf_stride = 0;
     pl.gscr_stride = 8 * NT8 * s.DP;
-    pl.rsum_stride = 8 * M1c * s.DP;
+    pl.rsum_stride = 8 * M1f * s.DP;
     cap_slots(pl.blocks, pl.slots, s.WPC,
               8.0 * (pl.rowck_stride + pl.colck_stride + pl.pck_stride + pl.gscr_stride +
                      pl.rsum_stride + 16 * pl.row_stride));

@@ -81,7 +81,10 @@ struct MmaBwdCfg {
   static constexpr int WARP_DOUBLES = 2 * PTILE * 2 + 2 * DTILE + 64 * XSTR + STG;
 };
 
-template <int DP, int WPC>
+//   DY  dyadic orders > 0 (runtime lam1 / lam2: coarse p tiles, coarse rows /
+//       columns of the operands, fine -> coarse sums before the telescoping);
+//       false: order 0 at compile time (C3, C5), no index shifts
+template <int DP, int WPC, bool DY = false>
 __global__ void __launch_bounds__(32 * WPC, 1)
 gram_bwd_mma(Problem pb, BwdArgs ba) {
   using Cf = MmaBwdCfg<DP>;
@@ -102,7 +105,10 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
   for (int e = lane; e < Cf::WARP_DOUBLES; e += 32) wsm[e] = 0.0;
   __syncwarp();
 
-  const int M1 = pb.M1c, NC = pb.M2c;
+  const int lamR = DY ? pb.lam1 : 0, lamC = DY ? pb.lam2 : 0;
+  const int LCm = (1 << lamC) - 1;
+  const int M1c = pb.M1c, M2c = pb.M2c;
+  const int M1 = M1c << lamR, NC = M2c << lamC;  // fine rows / columns
   const int nstrips = (M1 + 7) >> 3;
   const int NT8 = (NC + 3 + 7) >> 3;
   const int TRS = 8 * (NT8 + 5);  // doubles per strip top row (per pair)
@@ -150,15 +156,15 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         double2 v = make_double2(0.0, 0.0);
         if (row < M1)
           v = __ldg(reinterpret_cast<const double2*>(pb.R.p + (int64_t)ah * pb.R.path_stride +
-                                                     (int64_t)row * DP) + k2);
+                                                     (int64_t)(row >> lamR) * DP) + k2);
         *reinterpret_cast<double2*>(sX + R * XSTR + xsw(R, 2 * k2)) = v;
       }
     };
-    auto loadA = [&](int T, double (&af)[KS]) {  // dY[col 8T + lane/4][4kk + lane%4]
+    auto loadA = [&](int T, double (&af)[KS]) {  // dY[col 8T + lane/4][4kk + lane%4], coarse tile T
       const int col = 8 * T + g;
       const double* cp = cpath + (int64_t)col * DP + u;
 #pragma unroll
-      for (int kk = 0; kk < KS; ++kk) af[kk] = (col >= 0 && col < NC) ? __ldg(cp + 4 * kk) : 0.0;
+      for (int kk = 0; kk < KS; ++kk) af[kk] = (col >= 0 && col < M2c) ? __ldg(cp + 4 * kk) : 0.0;
     };
     auto ptile = [&](double2* ring, int slotT, int h, const double (&af)[KS]) {
       double c0 = 0.0, c1 = 0.0;
@@ -187,7 +193,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
 #pragma unroll
       for (int h = 0; h < 8; ++h) {
         const int ah = min(a0 + h, pb.r1 - 1);
-        const double* rp = pb.R.p + (int64_t)ah * pb.R.path_stride + (int64_t)row * DP + u;
+        const double* rp = pb.R.p + (int64_t)ah * pb.R.path_stride + (int64_t)(row >> lamR) * DP + u;
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) b[h][kk] = (row < M1) ? __ldg(rp + 4 * kk) : 0.0;
       }
@@ -237,13 +243,15 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           for (int q = 0; q < 4; ++q)
             cp_async16(sH + (T & 7) * 64 + g * 8 + 2 * q, trow_cur + 8 * T + 2 * q, true);
         }
-        const int t = T + 2;
+        if ((T & LCm) == 0) {  // coarse tile (T >> lamC) + 2 is formed at iteration T
+          const int t = (T >> lamC) + 2;
 #pragma unroll
-        for (int e = lane; e < 8 * DP / 2; e += 32) {
-          const int col = 8 * t + e / (DP / 2), q = e % (DP / 2);
-          const bool v = col < NC;
-          cp_async16(sA + ((t % RA) * 8 + e / (DP / 2)) * DP + 2 * q,
-                     cpath + (int64_t)(v ? col : 0) * DP + 2 * q, v);
+          for (int e = lane; e < 8 * DP / 2; e += 32) {
+            const int col = 8 * t + e / (DP / 2), q = e % (DP / 2);
+            const bool v = col < M2c;
+            cp_async16(sA + ((t % RA) * 8 + e / (DP / 2)) * DP + 2 * q,
+                       cpath + (int64_t)(v ? col : 0) * DP + 2 * q, v);
+          }
         }
         cp_async_commit();
       };
@@ -268,9 +276,11 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         double hcur[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) hcur[m] = (strip > 0) ? sH[(T & 7) * 64 + g * 8 + m] : 1.0;
-        double acur[KS];  // A operand of tile T+2: dY[col 8(T+2) + lane/4][4kk + lane%4]
+        const bool newtile = (T & LCm) == 0;  // (always at order 0)
+        const int Tc = T >> lamC;             // coarse tile of this iteration
+        double acur[KS];  // A operand of coarse tile Tc+2: dY[col 8(Tc+2) + lane/4][4kk + lane%4]
 #pragma unroll
-        for (int kk = 0; kk < KS; ++kk) acur[kk] = sA[(((T + 2) % RA) * 8 + g) * DP + 4 * kk + u];
+        for (int kk = 0; kk < KS; ++kk) acur[kk] = sA[(((Tc + 2) % RA) * 8 + g) * DP + 4 * kk + u];
         // checkpoints are read back only after the whole item's forward: for
         // d = 16 stream them past L2 (evict-first; measured +0.5 %, -2.5 % at d = 8)
         // values at node column 8T - u (and the bottom one a column before):
@@ -282,10 +292,16 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         const int s0 = T & 1, s1 = (T - 1) & 1;  // slot within the ring half
 #pragma unroll
         for (int m = 0; m < 8; ++m) {
-          ptile_r(aslot(T + 2), (T + 2) & 1, m, acur, bf);  // tile T+2, pair m, under the recurrence
+          if (newtile) ptile_r(aslot(Tc + 2), (Tc + 2) & 1, m, acur, bf);  // pair m, under the recurrence
           const int c = 8 * T + m - u;
-          const int sl = (m - u < 0) ? s1 : s0;
-          const double2 pv = ((m - u < 0) ? r1 : r0)[(sl * 8 + ((m - u) & 7)) * PSTR + psw(m - u, lane)];
+          double2 pv;
+          if constexpr (DY) {  // coarse column of fine column c, its tile in the 4-slot ring
+            const int jc = c >> lamC, tj = jc >> 3;
+            pv = aslot(tj)[(((tj & 1) * 8) + (jc & 7)) * PSTR + psw(jc, lane)];
+          } else {
+            const int sl = (m - u < 0) ? s1 : s0;
+            pv = ((m - u < 0) ? r1 : r0)[(sl * 8 + ((m - u) & 7)) * PSTR + psw(m - u, lane)];
+          }
           double tv = __shfl_up_sync(0xffffffffu, bot, 1, 4);
           if (u == 0) tv = hcur[m];
           if (!EDGE || (c >= 0 && c < NC)) {
@@ -351,10 +367,11 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       auto loadGX = [&](int T, double (&gb)[2][NN]) {  // dY[col 8T + 4kk + lane%4][8n + lane/4]
 #pragma unroll
         for (int kk = 0; kk < 2; ++kk) {
-          const int col = 8 * T + 4 * kk + u;
+          const int col = 8 * T + 4 * kk + u;  // fine column; its coarse dY
 #pragma unroll
           for (int n = 0; n < NN; ++n)
-            gb[kk][n] = (col >= 0 && col < NC) ? __ldg(cpath + (int64_t)col * DP + 8 * n + g) : 0.0;
+            gb[kk][n] = (col >= 0 && col < NC) ? __ldg(cpath + (int64_t)(col >> lamC) * DP + 8 * n + g)
+                                               : 0.0;
         }
       };
 
@@ -364,13 +381,15 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
 #pragma unroll
         for (int n = 0; n < NN; ++n) gx[h][n][0] = gx[h][n][1] = 0.0;
       {
+        // coarse tiles of the last block and the one before (order 0: blocks)
+        const int Tl = (NT8 - 1) >> lamC;
         double af[KS];
-        loadA(NT8 - 1, af);
+        loadA(Tl, af);
 #pragma unroll
-        for (int h = 0; h < 8; ++h) ptile(sP, (NT8 - 1) & 1, h, af);
-        loadA(NT8 - 2, af);
+        for (int h = 0; h < 8; ++h) ptile(sP, Tl & 1, h, af);
+        loadA(Tl - 1, af);
 #pragma unroll
-        for (int h = 0; h < 8; ++h) ptile(sP, (NT8 - 2) & 1, h, af);
+        for (int h = 0; h < 8; ++h) ptile(sP, (Tl - 1) & 1, h, af);
       }
       stage_block(NT8 - 1);
       double aR0 = 0.0, aR1 = 0.0, bR0 = 0.0, bR1 = 0.0, sendm = 0.0;
@@ -379,7 +398,10 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       auto blockB = [&](auto edge, int blk) {
         constexpr bool EDGE = decltype(edge)::value;
         double af[KS], gb[2][NN];
-        loadA(blk - 2, af);   // p tile blk-2, computed after the sweep
+        // coarse tile Tc - 2 is formed after the sweep of Tc's leftmost block
+        const bool lefttile = (blk & LCm) == 0;  // (always at order 0)
+        const int Tcb = blk >> lamC;
+        loadA(Tcb - 2, af);
         loadGX(blk, gb);      // gx B operand of tile blk
         cp_async_wait<0>();
         __syncwarp();         // staged inputs, p tiles blk and blk-1 visible
@@ -434,7 +456,8 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
               if (u > 0) tv[kap + 1] = sh;
             }
             const int c = 8 * blk - u + kap;
-            double2 pv = sP[((((c >> 3) & 1) * 8) + (c & 7)) * PSTR + psw(c, lane)];
+            const int jc = c >> lamC;  // coarse column
+            double2 pv = sP[((((jc >> 3) & 1) * 8) + (jc & 7)) * PSTR + psw(jc, lane)];
             if (EDGE && (c < 0 || c >= NC)) pv = make_double2(0.0, 0.0);
             const Coef c0 = coef(pv.x), c1 = coef(pv.y);
             const double n0 = cell(tv[kap + 1], k0, tv[kap], c0);
@@ -456,7 +479,8 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           const int c = 8 * blk - u + kap;
           double recv = __shfl_down_sync(0xffffffffu, sendm, 1, 4);
           if (u == 3) recv = av[kap];
-          double2 pv = sP[((((c >> 3) & 1) * 8) + (c & 7)) * PSTR + psw(c, lane)];
+          const int jc = c >> lamC;
+          double2 pv = sP[((((jc >> 3) & 1) * 8) + (jc & 7)) * PSTR + psw(jc, lane)];
           if (EDGE && (c < 0 || c >= NC)) pv = make_double2(0.0, 0.0);
           const Coef c0 = coef(pv.x), c1 = coef(pv.y);
           double lam1, lam0;
@@ -501,7 +525,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         // ---- 3. p tile blk-2 into tile blk's slot (its latency hides under the
         // maps), then the gradient maps on tile blk
 #pragma unroll
-        for (int h = 0; h < 8 && !(ba.exp & 8); h += 8) {
+        for (int h = 0; h < 8 && !(ba.exp & 8) && lefttile; h += 8) {
           // all 8 pairs' chains side by side, k-step outermost (same per-chain
           // order as ptile, so the values are unchanged)
           double c[8][2];
@@ -514,7 +538,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
               dmma(c[q][0], c[q][1], af[kk], sX[(8 * q + g) * XSTR + xsw(8 * q + g, 4 * kk + u)]);
 #pragma unroll
           for (int q = 0; q < 8; ++q)
-            sP[(((blk & 1) * 8 + g) * PSTR) + psw(g, 4 * q + u)] = make_double2(c[q][0], c[q][1]);
+            sP[(((Tcb & 1) * 8 + g) * PSTR) + psw(g, 4 * q + u)] = make_double2(c[q][0], c[q][1]);
         }
         const double* __restrict__ Dt = sD + (blk & 1) * Cf::DTILE;
         if (!(ba.exp & 4)) {
@@ -568,6 +592,10 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
           for (int n = 0; n < NN; ++n) {
             double2* q = reinterpret_cast<double2*>(rs + ((int64_t)h * M1 + rho) * DP + 8 * n + 2 * u);
             double2 v = make_double2(gx[h][n][0], gx[h][n][1]);
+            if constexpr (DY) {  // dY is unscaled: dp/d(dx) carries the dyadic factor (exact)
+              v.x *= pb.scale;
+              v.y *= pb.scale;
+            }
             if (!first_tile) {
               const double2 o = *q;
               v = make_double2(o.x + v.x, o.y + v.y);
@@ -583,11 +611,17 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
     {
       const int dR = ba.d;
       const int64_t gC = (int64_t)b * ba.gC_path;
-      for (int e = lane; e < (NC + 1) * dR; e += 32) {
+      // (dyadic: the fine columns of a coarse column summed first, ascending)
+      auto csum = [&](int j, int k) {
+        double a = gcs[(int64_t)(j << lamC) * DP + k];
+        for (int c = (j << lamC) + 1; c < ((j + 1) << lamC); ++c) a += gcs[(int64_t)c * DP + k];
+        return a;
+      };
+      for (int e = lane; e < (M2c + 1) * dR; e += 32) {
         const int p = e / dR, k = e % dR;
         double v = 0.0;
-        if (p >= 1) v += gcs[(int64_t)(p - 1) * DP + k];
-        if (p < NC) v -= gcs[(int64_t)p * DP + k];
+        if (p >= 1) v += csum(p - 1, k);
+        if (p < M2c) v -= csum(p, k);
         fix_add(fxC, gC + e, v);
       }
     }
@@ -602,11 +636,16 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       if (ah >= pb.r1 || bbeg >= bend) continue;  // warp-uniform
       const double* rh = rs + (int64_t)h * M1 * DP;
       const int64_t gp = (int64_t)ah * ba.gR_path;
-      for (int e = lane; e < (M1 + 1) * dR; e += 32) {
+      auto rsumc = [&](int i, int k) {  // fine rows of coarse row i, ascending
+        double a = rh[(int64_t)(i << lamR) * DP + k];
+        for (int r = (i << lamR) + 1; r < ((i + 1) << lamR); ++r) a += rh[(int64_t)r * DP + k];
+        return a;
+      };
+      for (int e = lane; e < (M1c + 1) * dR; e += 32) {
         const int p = e / dR, k = e % dR;
         double v = 0.0;
-        if (p >= 1) v += rh[(int64_t)(p - 1) * DP + k];
-        if (p < M1) v -= rh[(int64_t)p * DP + k];
+        if (p >= 1) v += rsumc(p - 1, k);
+        if (p < M1c) v -= rsumc(p, k);
         fix_add(fxR, gp + e, v);
       }
     }

@@ -73,7 +73,8 @@ def _wsq(fn, *args) -> int:
     device, arguments): the answer depends only on those (plans are cached per
     device on the C side too)."""
     # SK_NO_MMA (read per plan on the C side) selects other instances
-    key = (fn.__name__, torch.cuda.current_device(), os.environ.get("SK_NO_MMA"), args)
+    key = (fn.__name__, torch.cuda.current_device(), os.environ.get("SK_NO_MMA"),
+           os.environ.get("SK_MMA_DY"), args)
     nb = _WSQ_CACHE.get(key)
     if nb is None:
         nb = fn(*args)

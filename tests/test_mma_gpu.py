@@ -80,6 +80,39 @@ def test_gram_forward_mma_dyadic(mods, n1, n2, L1, L2, d, l1, l2):
     np.testing.assert_array_equal(got, old)
 
 
+@pytest.mark.parametrize("n1,n2,L1,L2,d,l1,l2", [
+    (9, 9, 15, 15, 16, 1, 1), (7, 7, 11, 11, 12, 2, 1), (6, 9, 13, 10, 16, 0, 2),
+    (10, 10, 9, 9, 10, 1, 0), (5, 7, 12, 17, 16, 1, 1),  # longer columns: swapped cross Gram
+])
+def test_gram_backward_mma_dyadic(mods, n1, n2, L1, L2, d, l1, l2):
+    """DMMA Gram backward at dyadic orders > 0 (opt-in DY instance: coarse p
+    tiles, fine -> coarse sums of the increment gradients, the dyadic factor
+    on the dY side): G and both gradients vs the oracle and the FMA pipe."""
+    ops, orc = mods
+    rng = np.random.default_rng(n1 * 31 + L1 + d + 5 * l1 + l2)
+    X = random_paths(rng, n1, L1, d)
+    Y = random_paths(rng, n2, L2, d) if (n1 != n2 or L1 != L2) else None
+    C = rng.standard_normal((n1, n2))
+    os.environ["SK_MMA_DY"] = "1"  # the DY instance is opt-in (sk_capi.cu plan_backward)
+    try:
+        G, gx, gy = ops.value_and_grad_gram(cu(X), None if Y is None else cu(Y), l1, l2, 0,
+                                            1.0, cu(C))
+        bx, by = ops.backward_gram(cu(X), None if Y is None else cu(Y), l1, l2, 0, 1.0, cu(C))
+    finally:
+        os.environ.pop("SK_MMA_DY", None)
+    assert rel_err(G.cpu().numpy(), orc.kernel_gram(X, Y, l1, l2)) < TOL
+    want = orc.gram_backward(X, Y, C, l1, l2)
+    if Y is None:
+        assert rel_err(gx.cpu().numpy(), want) < TOL
+    else:
+        assert rel_err(gx.cpu().numpy(), want[0]) < TOL
+        assert rel_err(gy.cpu().numpy(), want[1]) < TOL
+    np.testing.assert_array_equal(bx.cpu().numpy(), gx.cpu().numpy())
+    with _NoMMA():
+        ox, oy = ops.backward_gram(cu(X), None if Y is None else cu(Y), l1, l2, 0, 1.0, cu(C))
+    assert rel_err(gx.cpu().numpy(), ox.cpu().numpy()) < 1e-12
+
+
 def test_gram_forward_mma_cross_lengths(mods):
     ops, orc = mods
     rng = np.random.default_rng(3)
