@@ -156,20 +156,20 @@ __device__ inline double time_point(int64_t i, int64_t L) {
   return i == L - 1 ? 1.0 : (double)i * (1.0 / (double)(L - 1));
 }
 
-template <typename T>
+template <typename T, typename TO = T>
 struct PrepSide {
   const T* x;
   int64_t n, L;  // raw points per path
   double scale;
-  T* out;
+  TO* out;       // (TO = double for float inputs of the FP32-recurrence DMMA forward)
 };
 // Both sides of a call in ONE launch (rows side, then the columns side):
 // increments (kernel.py:74-75 np.diff, scaled by the exact dyadic factor,
 // zero-padded to dpad) for the linear kernel, padded nodes for RBF, each of
 // the transformed path when tf != TF_NONE (bitwise the np.diff of the
 // materialised transform: the same subtractions, and exact zeros).
-template <typename T>
-__global__ void prep_sides(PrepSide<T> s0, PrepSide<T> s1, int nsides, int rbf, int tf,
+template <typename T, typename TO = T>
+__global__ void prep_sides(PrepSide<T, TO> s0, PrepSide<T, TO> s1, int nsides, int rbf, int tf,
                            int64_t d, int dpad) {
   const int64_t per0 = rbf ? eff_len(s0.L, tf) : eff_len(s0.L, tf) - 1;
   const int64_t per1 = rbf ? eff_len(s1.L, tf) : eff_len(s1.L, tf) - 1;
@@ -180,34 +180,34 @@ __global__ void prep_sides(PrepSide<T> s0, PrepSide<T> s1, int nsides, int rbf, 
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t rowg = e / dpad, k = e % dpad;
     const bool first = rowg < rows0;
-    const PrepSide<T>& sd = first ? s0 : s1;
+    const PrepSide<T, TO>& sd = first ? s0 : s1;
     const int64_t row = first ? rowg : rowg - rows0;
     const int64_t per = first ? per0 : per1;
     const int64_t p = row / per, r = row % per;
     const T* xp = sd.x + p * sd.L * d;
-    T v = 0;
+    TO v = 0;  // (computed in TO: the identity for TO == T)
     if (rbf) {  // node r of the transformed path
       if (tf == TF_NONE) {
-        if (k < d) v = xp[r * d + k];
+        if (k < d) v = (TO)xp[r * d + k];
       } else if (tf == TF_TIME) {
-        if (k < d) v = xp[r * d + k];
-        else if (k == d) v = (T)time_point(r, sd.L);
+        if (k < d) v = (TO)xp[r * d + k];
+        else if (k == d) v = (TO)time_point(r, sd.L);
       } else {  // lead-lag: Z[2i] = (X[i], X[i]), Z[2i+1] = (X[i+1], X[i])
-        if (k < d) v = xp[((r + 1) >> 1) * d + k];
-        else if (k < 2 * d) v = xp[(r >> 1) * d + (k - d)];
+        if (k < d) v = (TO)xp[((r + 1) >> 1) * d + k];
+        else if (k < 2 * d) v = (TO)xp[(r >> 1) * d + (k - d)];
       }
     } else {  // increment r of the transformed path
       if (tf == TF_NONE) {
-        if (k < d) v = (xp[(r + 1) * d + k] - xp[r * d + k]) * (T)sd.scale;
+        if (k < d) v = ((TO)xp[(r + 1) * d + k] - (TO)xp[r * d + k]) * (TO)sd.scale;
       } else if (tf == TF_TIME) {
-        if (k < d) v = (xp[(r + 1) * d + k] - xp[r * d + k]) * (T)sd.scale;
-        else if (k == d) v = ((T)time_point(r + 1, sd.L) - (T)time_point(r, sd.L)) * (T)sd.scale;
+        if (k < d) v = ((TO)xp[(r + 1) * d + k] - (TO)xp[r * d + k]) * (TO)sd.scale;
+        else if (k == d) v = ((TO)time_point(r + 1, sd.L) - (TO)time_point(r, sd.L)) * (TO)sd.scale;
       } else {  // lead-lag: (dX_i, 0), then (0, dX_i)
         const int64_t i = r >> 1;
         const bool lead = (r & 1) == 0;
-        if (lead && k < d) v = (xp[(i + 1) * d + k] - xp[i * d + k]) * (T)sd.scale;
+        if (lead && k < d) v = ((TO)xp[(i + 1) * d + k] - (TO)xp[i * d + k]) * (TO)sd.scale;
         else if (!lead && k >= d && k < 2 * d)
-          v = (xp[(i + 1) * d + (k - d)] - xp[i * d + (k - d)]) * (T)sd.scale;
+          v = ((TO)xp[(i + 1) * d + (k - d)] - (TO)xp[i * d + (k - d)]) * (TO)sd.scale;
       }
     }
     sd.out[row * dpad + k] = v;
@@ -479,12 +479,14 @@ static int plan_forward(FwdPlan& pl, int kind, int64_t d, int lamR, int lamC, in
   // lambda 1: d = 16 11.5 -> 4.8 ms, d = 32 41 -> 7.3 ms; lambda 2, d = 16 6.8
   // -> 4.2 ms -- and for DP = 8 at order 0; the FMA-pipe kernel wins for
   // DP = 4 (d = 4, lambda 0: 8.4 vs 13.4 ms) and for DP = 8 at order > 0)
-  const bool mma_shape = s.DP >= 16 || (s.DP == 8 && lamR + lamC == 0);
-  s.MMA = gram && !f32 && kind == LINEAR && nch == 1 && s.DP <= 32 && mma_shape &&
+  // FP32 arithmetic (float recurrence, fp64 DMMA p): DP >= 16 only (C3 shape
+  // 404 -> 189 ms; at DP = 8 the FP32 FMA-pipe kernel is faster, 185 vs 340 ms)
+  const bool mma_shape = s.DP >= 16 || (s.DP == 8 && lamR + lamC == 0 && !f32);
+  s.MMA = gram && kind == LINEAR && nch == 1 && s.DP <= 32 && mma_shape &&
           !(std::getenv("SK_NO_MMA") && std::getenv("SK_NO_MMA")[0] == '1');
   if (s.MMA) {
     int per_warp = 0;
-    FwdFn fn = select_fwd_mma(s.DP, per_warp, lamR + lamC > 0);
+    FwdFn fn = select_fwd_mma(s.DP, per_warp, lamR + lamC > 0, f32);
     if (!fn) return fail(SK_INVALID_ARGUMENT, "no DMMA forward instance for this shape");
     pl.shape = s;
     pl.fn = fn;
@@ -543,16 +545,17 @@ static size_t prep_elems(int kind, int64_t n, int64_t L, int dpad) {
 // Prepares the rows side (scaled by `scale`) and, unless `share`, the columns
 // side, in one launch (T: the arithmetic type of the kernels that read them).
 // LR, LC, d: RAW points / dimension (the prepared arrays hold the transformed path)
-template <typename T>
+template <typename T, typename TO = T>
 static void launch_prep(int kind, const T* xr, int64_t nR, int64_t LR, const T* xc, int64_t nC,
-                        int64_t LC, bool share, int64_t d, int dpad, T* outR, T* outC,
+                        int64_t LC, bool share, int64_t d, int dpad, TO* outR, TO* outC,
                         cudaStream_t st, double scale, int tf = TF_NONE) {
   const size_t total = prep_elems(kind, nR, eff_len(LR, tf), dpad) +
                        (share ? 0 : prep_elems(kind, nC, eff_len(LC, tf), dpad));
   if (total == 0) return;
   const int blocks = (int)std::min<size_t>((total + 255) / 256, 4096);
-  PrepSide<T> s0{xr, nR, LR, scale, outR}, s1{xc, nC, LC, 1.0, outC};
-  prep_sides<T><<<blocks, 256, 0, st>>>(s0, s1, share ? 1 : 2, kind == RBF ? 1 : 0, tf, d, dpad);
+  PrepSide<T, TO> s0{xr, nR, LR, scale, outR}, s1{xc, nC, LC, 1.0, outC};
+  prep_sides<T, TO><<<blocks, 256, 0, st>>>(s0, s1, share ? 1 : 2, kind == RBF ? 1 : 0, tf, d,
+                                            dpad);
 }
 
 static int launch_transform_adjoint(const double* gt, int64_t n, int64_t L, int64_t d, int tf,
@@ -604,11 +607,15 @@ struct FwdLayout {
   size_t prepR = 0, prepC = 0, hand = 0, total = 0;
 };
 
+// esz: the recurrence's element size (handoff rows); pesz: the prepared paths'
+// (8 for the DMMA kernels' fp64 operands, also under FP32 arithmetic)
 static FwdLayout fwd_layout(const FwdPlan& pl, int kind, int64_t nR, int64_t LR, int64_t nC,
-                            int64_t LC, int dpad, bool shared_paths, size_t esz = sizeof(double)) {
+                            int64_t LC, int dpad, bool shared_paths, size_t esz = sizeof(double),
+                            size_t pesz = 0) {
   FwdLayout lo;
-  lo.prepR = align_up(prep_elems(kind, nR, LR, dpad) * esz, 256);
-  lo.prepC = shared_paths ? 0 : align_up(prep_elems(kind, nC, LC, dpad) * esz, 256);
+  if (pesz == 0) pesz = esz;
+  lo.prepR = align_up(prep_elems(kind, nR, LR, dpad) * pesz, 256);
+  lo.prepC = shared_paths ? 0 : align_up(prep_elems(kind, nC, LC, dpad) * pesz, 256);
   lo.hand = align_up((size_t)pl.slots * pl.hand_stride * esz, 256);
   lo.total = lo.prepR + lo.prepC + lo.hand;
   return lo;
@@ -685,7 +692,11 @@ static int forward_impl(const void* x, const void* y, int64_t n1, int64_t n2, in
   // needs a separate (unscaled) column copy when the factor is not 1.
   const bool fold = kind == LINEAR;
   const bool share = sym && !(fold && pb.scale != 1.0);
-  FwdLayout lo = fwd_layout(pl, kind, g.nR, g.LR, g.nC, g.LC, pb.dpad, share, esz);
+  // FP32 arithmetic on the DMMA Gram forward: fp64 operands (exact increments
+  // of the float points), float recurrence
+  const bool f32mma = f32 && pl.shape.MMA;
+  FwdLayout lo = fwd_layout(pl, kind, g.nR, g.LR, g.nC, g.LC, pb.dpad, share, esz,
+                            f32mma ? sizeof(double) : esz);
   if (query) {
     *query = lo.total;
     return SK_OK;
@@ -700,7 +711,11 @@ static int forward_impl(const void* x, const void* y, int64_t n1, int64_t n2, in
   double* hand = reinterpret_cast<double*>(base + lo.prepR + lo.prepC);
   const void* xr = g.swap ? y : x;
   const void* xc = g.swap ? x : y;
-  if (f32)
+  if (f32mma)
+    launch_prep<float, double>(kind, (const float*)xr, g.nR, g.swap ? L2r : L1r, (const float*)xc,
+                               g.nC, g.swap ? L1r : L2r, share, dr, pb.dpad, (double*)prepR,
+                               (double*)prepC, st, fold ? pb.scale : 1.0, tf);
+  else if (f32)
     launch_prep<float>(kind, (const float*)xr, g.nR, g.swap ? L2r : L1r, (const float*)xc, g.nC,
                        g.swap ? L1r : L2r, share, dr, pb.dpad, (float*)prepR, (float*)prepC, st,
                        fold ? pb.scale : 1.0, tf);

@@ -57,7 +57,11 @@ struct MmaFwdCfg {
 
 //   DY  dyadic orders > 0 (runtime lam1 / lam2); false: order 0 at compile
 //       time, so the order-0 instance (C3, C5) carries no index shifts
-template <int DP, bool DY = false>
+//   TR  the recurrence's arithmetic type: double, or float for the FP32
+//       kernels (p from the fp64 DMMA, rounded once to float; the cell in the
+//       small-correction form of sk_cell.cuh Coef32); the handoff rows and
+//       the output are TR
+template <int DP, bool DY = false, typename TR = double>
 __global__ void __launch_bounds__(MmaFwdCfg::THREADS, DP >= 32 ? 2 : 3)
 gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
   constexpr int KS = DP / 4;
@@ -81,7 +85,19 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
   const int NT8 = (NC + 3 + 7) >> 3;  // 8-step iterations per strip (skew 3)
   const int u_star = ((M1 - 1) & 7) >> 1, r_star = (M1 - 1) & 1;
   const int64_t slot = (int64_t)blockIdx.x * nw + warp;
-  double* __restrict__ hrow = hand + (slot * 8 + g) * hand_stride;
+  TR* __restrict__ hrow = reinterpret_cast<TR*>(hand) + (slot * 8 + g) * hand_stride;
+  // two consecutive handoff values (8- or 16-byte aligned: m even)
+  auto load2 = [](const TR* p, TR& a, TR& b) {
+    if constexpr (sizeof(TR) == 8) {
+      const double2 t = *reinterpret_cast<const double2*>(p);
+      a = t.x;
+      b = t.y;
+    } else {
+      const float2 t = *reinterpret_cast<const float2*>(p);
+      a = t.x;
+      b = t.y;
+    }
+  };
 
   for (int64_t item = slot; item < pb.nitems; item += (int64_t)gridDim.x * nw) {
     int a0, b;
@@ -89,7 +105,7 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
     const int a = a0 + g;
     const bool valid = a < pb.r1 && !(pb.mode == GRAM_SYM && a > b);
     const double* __restrict__ cpath = pb.C.p + (int64_t)b * pb.C.path_stride;
-    double kval = 0.0;
+    TR kval = 0;
 
     for (int strip = 0; strip < nstrips; ++strip) {
       __syncwarp();  // previous strip's handoff row and ring reads are done
@@ -126,15 +142,13 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
 #pragma unroll
       for (int h = 0; h < 8; ++h) tile(1, h, af);
       loadA(2, af);
-      double hcur[8];
+      TR hcur[8];
 #pragma unroll
-      for (int m = 0; m < 8; ++m) hcur[m] = 1.0;
+      for (int m = 0; m < 8; ++m) hcur[m] = TR(1);
       if (strip > 0 && u == 0) {
 #pragma unroll
         for (int m = 0; m < 8; m += 2) {
-          const double2 t = *reinterpret_cast<const double2*>(hrow + m);
-          hcur[m] = t.x;
-          hcur[m + 1] = t.y;
+          load2(hrow + m, hcur[m], hcur[m + 1]);
         }
       }
       __syncwarp();
@@ -145,7 +159,7 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
         return (((jc >> 3) & 3) * 8 + (jc & 7)) * PSTR + lane;
       };
       double2 pcur = sP[pslot(0 - u)];
-      double kl0 = 1.0, kl1 = 1.0, topc = 1.0, bot = 1.0;
+      TR kl0 = 1, kl1 = 1, topc = 1, bot = 1;
       const bool last = strip == nstrips - 1;
 
       // one 8-step iteration; EDGE iterations hold columns outside [0, NC) or
@@ -156,15 +170,13 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
         const bool newtile = (T & LCm) == 0;
         const int Tc = T >> lamC;
         if (newtile) loadA(Tc + 3, an);
-        double hnxt[8];
+        TR hnxt[8];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) hnxt[m] = 1.0;
+        for (int m = 0; m < 8; ++m) hnxt[m] = TR(1);
         if (strip > 0 && u == 0) {
 #pragma unroll
           for (int m = 0; m < 8; m += 2) {
-            const double2 t = *reinterpret_cast<const double2*>(hrow + 8 * (T + 1) + m);
-            hnxt[m] = t.x;
-            hnxt[m + 1] = t.y;
+            load2(hrow + 8 * (T + 1) + m, hnxt[m], hnxt[m + 1]);
           }
         }
 #pragma unroll
@@ -173,12 +185,12 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
           const int c = 8 * T + m - u;  // this lane's (fine) column
           const double2 pv = pcur;
           pcur = sP[pslot(c + 1)];
-          double tv = __shfl_up_sync(0xffffffffu, bot, 1, 4);
+          TR tv = __shfl_up_sync(0xffffffffu, bot, 1, 4);
           if (u == 0) tv = hcur[m];
           if (!EDGE || (c >= 0 && c < NC)) {
-            const Coef c0 = coef(pv.x), c1 = coef(pv.y);
-            const double k0 = cell(tv, kl0, topc, c0);
-            const double k1 = cell(k0, kl1, kl0, c1);
+            const CoefOf<TR> c0 = coef((TR)pv.x), c1 = coef((TR)pv.y);
+            const TR k0 = cell(tv, kl0, topc, c0);
+            const TR k1 = cell(k0, kl1, kl0, c1);
             topc = tv;
             kl0 = k0;
             kl1 = k1;
@@ -200,7 +212,7 @@ gram_fwd_mma(Problem pb, double* __restrict__ hand, int64_t hand_stride) {
         else iter(std::false_type{}, T);
       }
     }
-    if (valid && u == u_star) pb.out[(int64_t)(a - pb.r0) * pb.ldo + b] = kval;
+    if (valid && u == u_star) reinterpret_cast<TR*>(pb.out)[(int64_t)(a - pb.r0) * pb.ldo + b] = kval;
   }
 }
 

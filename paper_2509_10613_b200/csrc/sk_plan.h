@@ -44,7 +44,7 @@ FwdFn select_fwd_linear_f32(const FwdShape& s, int& smem);  // FP32 arithmetic
 FwdFn select_fwd_short(const FwdShape& s, int& smem);       // short paths, fp64
 FwdFn select_fwd_rbf(const FwdShape& s, int& smem);
 FwdFn select_fwd_delta(const FwdShape& s, int& smem);
-FwdFn select_fwd_mma(int DP, int& smem_per_warp, bool dyadic);
+FwdFn select_fwd_mma(int DP, int& smem_per_warp, bool dyadic, bool f32);
 // few short pairs (sk_small.cu); false when the shape does not apply
 bool launch_small_fwd(const double* xr, const double* xc, int64_t B, int64_t LR, int64_t LC,
                       int64_t d, int lamR, int lamC, double scale, double* out, int sms,

@@ -83,7 +83,11 @@ t = timed(lambda: ops.forward_gram_f32(X32, None, 0, 0), 2)
 c = 1024 * 1025 // 2 * 511 ** 2
 out["C3-shape Gram fwd FP32 arithmetic"] = {"s": t, "cells_per_s": c / t,
                                             "frac_fp32": c * (5 + 20) / t / peak32,
-                                            "peak_fp32_fma_per_s": peak32}
+                                            "peak_fp32_fma_per_s": peak32,
+                                            "note": "float recurrence on the FMA pipe; p = <dx, dy> "
+                                                    "on the FP64 tensor cores (DMMA), rounded "
+                                                    "once to float -- frac_fp32 counts it as "
+                                                    "FP32 work (d + 4 per cell)"}
 x, y = paths(rng, 128, 8192, 4).float(), paths(rng, 128, 8192, 4).float()
 t = timed(lambda: ops.forward_batch_f32(x, y, 1, 1), 5)
 c = 128 * 16382 ** 2
