@@ -40,7 +40,8 @@ def test_batch_fp32_within_1e4(sk, oracle, B, L, d, lam):
     assert rel_err(k.cpu().numpy(), want) < TOL32
 
 
-@pytest.mark.parametrize("n,L,d,lam", [(24, 512, 16, 0), (20, 1024, 8, 0), (12, 100, 3, 2)])
+@pytest.mark.parametrize("n,L,d,lam", [(24, 512, 16, 0), (20, 1024, 8, 0), (12, 100, 3, 2),
+                                       (10, 300, 32, 0), (16, 130, 20, 1)])  # DMMA + float recurrence
 def test_gram_fp32_within_1e4(sk, oracle, n, L, d, lam):
     rng = np.random.default_rng(1)
     X = make_paths(rng, n, L, d).astype(np.float32)
