@@ -92,7 +92,8 @@ def _workspace(nbytes: int, device) -> torch.Tensor:
     a later call never overwrites scratch a queued kernel still reads.  Larger
     ones come from the caching allocator per call."""
     nbytes = max(int(nbytes), 1)
-    if nbytes > _WS_CACHE_MAX:
+    # (no caching under CUDA-graph capture: that memory belongs to the graph's pool)
+    if nbytes > _WS_CACHE_MAX or torch.cuda.is_current_stream_capturing():
         return torch.empty(nbytes, dtype=torch.uint8, device=device)
     idx = _dev_index(device)
     key = (idx, torch._C._cuda_getCurrentRawStream(idx))

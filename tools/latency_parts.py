@@ -41,3 +41,16 @@ print(f"raw C ABI launch call:              {per_call(lambda: lib.sk_forward_bat
 print(f"ops.forward_batch:                  {per_call(lambda: ops.forward_batch(x, y, 0, 0, 0, 1.0)):.2f} us")
 print(f"sig_kernel:                         {per_call(lambda: sk.sig_kernel(x, y)):.2f} us")
 print(f"torch.empty(32):                    {per_call(lambda: torch.empty(32, dtype=torch.float64, device=dev)):.2f} us")
+
+# the same call captured once in a CUDA graph and replayed (inputs copied into
+# the captured buffers): the small-call path without host-side launch work
+s = torch.cuda.Stream()
+s.wait_stream(torch.cuda.current_stream())
+with torch.cuda.stream(s):
+    for _ in range(3):
+        sk.sig_kernel(x, y)
+torch.cuda.current_stream().wait_stream(s)
+graph = torch.cuda.CUDAGraph()
+with torch.cuda.graph(graph):
+    kg = sk.sig_kernel(x, y)
+print(f"sig_kernel as a CUDA-graph replay:  {per_call(lambda: graph.replay()):.2f} us")
