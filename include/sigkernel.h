@@ -260,6 +260,19 @@ int sk_backward_gram_acc_tf(const double *x, const double *y, int64_t n1, int64_
                             int static_kernel, double sigma, int transform, int64_t row_begin,
                             int64_t row_end, const double *cot, double *values, void *acc_x,
                             void *acc_y, void *workspace, size_t workspace_bytes, void *stream);
+/* FP32-arithmetic Gram backward (linear static kernel, dyadic order 0,
+ * d <= 16): sk_backward_gram_acc with the forward, recompute and adjoint
+ * recurrences in float (small-correction forms) and
+ * p = <dx, dy>, gx, gy on the FP64 tensor cores.  x / y are the fp64 copies of
+ * float32 points (exact); values (nullable) are the float recurrence's
+ * results widened to double.  Other shapes: SK_INVALID_ARGUMENT. */
+size_t sk_backward_gram_acc_f32_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                                int64_t d, int lam1, int lam2, int symmetric);
+int sk_backward_gram_acc_f32(const double *x, const double *y, int64_t n1, int64_t n2,
+                             int64_t L1, int64_t L2, int64_t d, int lam1, int lam2,
+                             int64_t row_begin, int64_t row_end, const double *cot,
+                             double *values, void *acc_x, void *acc_y, void *workspace,
+                             size_t workspace_bytes, void *stream);
 
 /* ---- truncated signatures ------------------------------------------------
  * Replaces sigcore's signature (signature.py:104-121) and signature_backward

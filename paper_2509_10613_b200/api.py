@@ -135,14 +135,23 @@ class _SigKernelGramF32Fn(torch.autograd.Function):
     @staticmethod
     def backward(ctx, cot):
         l1, l2, tf = ctx.cfg
+        # FP32-arithmetic backward where it exists (linear Gram tiles, order 0,
+        # d <= 16: sk_backward_gram_acc_f32), else the fp64 backward
+        f32 = ops.f32_backward_supported(l1, l2, ctx.saved_tensors[0].shape[2], tf)
         if ctx.sym:
             (x,) = ctx.saved_tensors
-            gx, _ = ops.backward_gram(x.double(), None, l1, l2, 0, 1.0, cot.double(),
-                                      transform=tf)
+            if f32:
+                _, gx, _ = ops.value_and_grad_gram_f32(x, None, cot)
+            else:
+                gx, _ = ops.backward_gram(x.double(), None, l1, l2, 0, 1.0, cot.double(),
+                                          transform=tf)
             return gx.to(x.dtype), None, None, None, None
         x, y = ctx.saved_tensors
-        gx, gy = ops.backward_gram(x.double(), y.double(), l1, l2, 0, 1.0, cot.double(),
-                                   transform=tf)
+        if f32:
+            _, gx, gy = ops.value_and_grad_gram_f32(x, y, cot)
+        else:
+            gx, gy = ops.backward_gram(x.double(), y.double(), l1, l2, 0, 1.0, cot.double(),
+                                       transform=tf)
         return (gx.to(x.dtype) if ctx.needs_input_grad[0] else None,
                 gy.to(y.dtype) if ctx.needs_input_grad[1] else None, None, None, None)
 
@@ -245,7 +254,10 @@ def sig_kernel_gram(x, y=None, dyadic_order=0, static_kernel=None, transform=Non
 
     y None (or y is x) -> symmetric: only a <= b is solved and the result is
     mirrored, hence exactly symmetric (reference kernel.py:151-180).
-    transform, precision: as sig_kernel."""
+    transform, precision: as sig_kernel; with precision="fp32" the gradient of
+    a linear Gram at dyadic order 0 with d <= 16 (no transform) comes from the
+    FP32-arithmetic backward (sk_backward_gram_acc_f32), other shapes from the
+    fp64 backward."""
     sym = y is None or y is x
     x, _ = _batched(_prep(x, "x"), "x")
     tf = _tf(transform)
@@ -273,7 +285,7 @@ def sig_kernel_gram(x, y=None, dyadic_order=0, static_kernel=None, transform=Non
 
 
 def sig_kernel_gram_value_and_grad(x, y=None, cotangent=None, dyadic_order=0, static_kernel=None,
-                                   transform=None):
+                                   transform=None, precision="fp64"):
     """Gram matrix and its gradient in ONE fused pass: returns (G, dF/dx, dF/dy)
     for F = sum_ab cotangent[a, b] G[a, b] (cotangent None = ones, the reference
     default kernel_grad.py:81-82); dF/dy is None when y is None (symmetric: both
@@ -282,11 +294,25 @@ def sig_kernel_gram_value_and_grad(x, y=None, cotangent=None, dyadic_order=0, st
     This is the Gram counterpart of the reference's kernel_batch_backward, which
     returns values and gradients from one call (kernel_grad.py:64-98): the
     backward's own forward solve produces G, so no separate forward runs.
-    Not an autograd op -- use sig_kernel_gram for autograd graphs."""
+    Not an autograd op -- use sig_kernel_gram for autograd graphs.
+    precision="fp32": FP32-arithmetic recurrences (linear kernel, dyadic order
+    0, d <= 16, no transform); G and the gradients come back as float32."""
     sym = y is None or y is x
     x, _ = _batched(_prep(x, "x"), "x")
     l1, l2 = _orders(dyadic_order)
     kind, sigma = ops.static_kind(static_kernel)
+    if _precision(precision, kind):
+        if not ops.f32_backward_supported(l1, l2, x.shape[2], _tf(transform)):
+            raise InvalidArgument("precision='fp32' value and gradient: linear kernel, dyadic "
+                                  "order 0, d <= 16, no transform")
+        xf = x.detach().to(torch.float32)
+        yf = None if sym else _batched(_prep(y, "y"), "y")[0].detach().to(torch.float32)
+        n1, n2 = xf.shape[0], (xf if sym else yf).shape[0]
+        if cotangent is None:
+            cotangent = torch.ones((n1, n2), dtype=torch.float64, device=xf.device)
+        G, gx, gy = ops.value_and_grad_gram_f32(xf, yf, cotangent)
+        return (G.to(torch.float32), gx.to(torch.float32),
+                None if gy is None else gy.to(torch.float32))
     xd = x.detach().to(torch.float64)
     yd = None
     if not sym:

@@ -969,7 +969,7 @@ struct BwdPlan {
 
 static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, int64_t M1c,
                          int64_t M2c, int mode, int64_t npairs, int n2, int r0, int r1,
-                         bool shared_cols) {
+                         bool shared_cols, bool f32 = false) {
   int nch = 1;
   BwdShape s{};
   s.kind = kind;
@@ -989,12 +989,17 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
   const bool dy_ok = mdy && mdy[0] == '1';
   s.MMA = shared_cols && kind == LINEAR && (!dy || dy_ok) && s.DP <= 16 && !wide &&
           !(std::getenv("SK_NO_MMA") && std::getenv("SK_NO_MMA")[0] == '1');
+  // FP32 backward: the DMMA Gram instance at order 0 only (d <= 16)
+  if (f32 && !(shared_cols && kind == LINEAR && !dy && s.DP <= 16 && !wide))
+    return fail(SK_INVALID_ARGUMENT,
+                "FP32 backward supports linear Gram tiles at dyadic order 0 with d <= 16");
+  if (f32) s.MMA = true;
   if (s.MMA) {
     if (s.DP == 4) s.DP = 8;
     const char* w = std::getenv("SK_BWD_WPC");
-    s.WPC = (w && (w[0] == '3' || w[0] == '4')) ? w[0] - '0' : 2;  // measured: 2 >= 4 > 3
+    s.WPC = (w && (w[0] == '3' || w[0] == '4') && !f32) ? w[0] - '0' : 2;  // measured: 2 >= 4 > 3
     int per_warp = 0;
-    BwdFn fn = select_bwd_mma(s.DP, s.WPC, per_warp, dy);
+    BwdFn fn = select_bwd_mma(s.DP, s.WPC, per_warp, dy, f32);
     if (!fn) return fail(SK_INVALID_ARGUMENT, "no DMMA backward instance for this shape");
     pl.shape = s;
     pl.fn = fn;
@@ -1117,7 +1122,7 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
                          int mode, int64_t r0, int64_t r1, const double* cot, double* values,
                          double* grad_x, double* grad_y, void* ws, size_t ws_bytes,
                          cudaStream_t st, size_t* query, void* acc_x = nullptr,
-                         void* acc_y = nullptr, int tf = TF_NONE) {
+                         void* acc_y = nullptr, int tf = TF_NONE, bool f32 = false) {
   if (int rc = validate(L1, L2, d, lam1, lam2, kind, sigma)) return rc;
   if (tf < TF_NONE || tf > TF_LEADLAG) return fail(SK_INVALID_ARGUMENT, "unknown path transform");
   // the kernels solve the transformed paths; their point gradients (transformed
@@ -1145,7 +1150,7 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   const int64_t npairs = mode == BATCH ? n1 : (r1 - r0) * n2;
   if (int rc = plan_backward(pl, kind, d, g.lamR, g.lamC, pb.M1c, pb.M2c, mode, npairs,
                              (int)n2, (int)r0, (int)r1,
-                             mode != BATCH && !(mode == GRAM_CROSS && g.swap)))
+                             mode != BATCH && !(mode == GRAM_CROSS && g.swap), f32))
     return rc;
   if (pl.shape.MMA) pb.dpad = pl.shape.DP;  // d <= 4: padded to the DP = 8 instance
   BwdLayout lo;
@@ -1503,6 +1508,44 @@ size_t sk_backward_gram_acc_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, 
                                             int symmetric) {
   return sk_backward_gram_acc_tf_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, static_kernel,
                                                  symmetric, TF_NONE);
+}
+
+size_t sk_backward_gram_acc_f32_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,
+                                                int64_t d, int lam1, int lam2, int symmetric) {
+  size_t q = 0;
+  char dummy = 0;
+  if (backward_impl(nullptr, nullptr, n1, n2, L1, L2, d, lam1, lam2, LINEAR, 1.0,
+                    symmetric ? GRAM_SYM : GRAM_CROSS, 0, n1, nullptr, nullptr, nullptr,
+                    nullptr, nullptr, 0, nullptr, &q, &dummy, &dummy, TF_NONE, true))
+    return 0;
+  return q;
+}
+
+int sk_backward_gram_acc_f32(const double* x, const double* y, int64_t n1, int64_t n2,
+                             int64_t L1, int64_t L2, int64_t d, int lam1, int lam2,
+                             int64_t row_begin, int64_t row_end, const double* cot,
+                             double* values, void* acc_x, void* acc_y, void* ws,
+                             size_t ws_bytes, void* stream) {
+  const bool sym = (y == nullptr);
+  if (sym && (n2 != n1 || L2 != L1))
+    return fail(SK_INVALID_ARGUMENT, "symmetric Gram needs n2 == n1 and L2 == L1");
+  if (row_begin < 0 || row_end > n1 || row_begin > row_end)
+    return fail(SK_INVALID_ARGUMENT, "row range out of bounds");
+  if (!cot) return fail(SK_INVALID_ARGUMENT, "Gram backward needs the cotangent matrix");
+  if (!acc_x) return fail(SK_INVALID_ARGUMENT, "accumulator missing");
+  if (int rc = backward_impl(x, sym ? x : y, n1, n2, L1, L2, d, lam1, lam2, LINEAR, 1.0,
+                             sym ? GRAM_SYM : GRAM_CROSS, row_begin, row_end, cot, values,
+                             nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream, nullptr,
+                             acc_x, acc_y, TF_NONE, true))
+    return rc;
+  const int64_t span = row_end - row_begin;
+  if (values && sym && span > 1) {
+    int blocks = (int)std::min<int64_t>((span * span + 255) / 256, 4096);
+    mirror_upper<double><<<blocks, 256, 0, (cudaStream_t)stream>>>(values, n2, (int)row_begin,
+                                                                   (int)row_end);
+    SK_CUDA(cudaGetLastError());
+  }
+  return SK_OK;
 }
 
 }  // extern "C"

@@ -84,9 +84,14 @@ struct MmaBwdCfg {
 //   DY  dyadic orders > 0 (runtime lam1 / lam2: coarse p tiles, coarse rows /
 //       columns of the operands, fine -> coarse sums before the telescoping);
 //       false: order 0 at compile time (C3, C5), no index shifts
-template <int DP, int WPC, bool DY = false>
+//   TR  the recurrences' arithmetic type: double, or float for the FP32
+//       backward (forward, recompute and adjoint on the FP32 pipe in the
+//       small-correction forms of sk_cell.cuh; p, gx, gy stay on DMMA with
+//       exact fp64 operands; checkpoints keep their fp64 slots, exact)
+template <int DP, int WPC, bool DY = false, typename TR = double>
 __global__ void __launch_bounds__(32 * WPC, 1)
 gram_bwd_mma(Problem pb, BwdArgs ba) {
+  constexpr bool F32 = std::is_same<TR, float>::value;
   using Cf = MmaBwdCfg<DP>;
   constexpr int KS = Cf::KS, NN = Cf::NN, PSTR = Cf::PSTR, DSTR = Cf::DSTR, XSTR = Cf::XSTR;
   extern __shared__ double smem_mb[];
@@ -184,7 +189,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
     };
 
     // ------------------------------------------------ phase A: forward + checkpoints
-    double kval = 0.0;  // the pair's kernel value (fused value + gradient calls)
+    TR kval = 0;  // the pair's kernel value (fused value + gradient calls)
     // B fragments: dX of pair h, row 8 strip + lane/4, component 4kk + lane%4;
     // the next strip's are loaded one strip ahead
     double bfn[8][KS];
@@ -261,8 +266,8 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       // values (the strip handoff) are one contiguous 64-B quarter row
       double2* __restrict__ cck = colck + (int64_t)strip * NT8 * 32 + lane;
       double* __restrict__ cck2 = colck2 + (int64_t)strip * NT8 * 32 + lane;
-      double kl0 = 1.0, kl1 = 1.0, topc = 1.0, bot = 1.0;
-      double bprev = 1.0;  // the lane's bottom value one column before kl1
+      TR kl0 = 1, kl1 = 1, topc = 1, bot = 1;
+      TR bprev = 1;  // the lane's bottom value one column before kl1
       const bool last = strip == nstrips - 1;
       __syncwarp();
       // one 8-step iteration; EDGE iterations hold columns outside [0, NC)
@@ -273,9 +278,9 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         issue_in(T + HPD);
         cp_async_wait<HPD>();  // this iteration's top row and tile T+2's dY landed
         __syncwarp();          // (the dY ring is shared by the warp)
-        double hcur[8];
+        TR hcur[8];
 #pragma unroll
-        for (int m = 0; m < 8; ++m) hcur[m] = (strip > 0) ? sH[(T & 7) * 64 + g * 8 + m] : 1.0;
+        for (int m = 0; m < 8; ++m) hcur[m] = (strip > 0) ? (TR)sH[(T & 7) * 64 + g * 8 + m] : TR(1);
         const bool newtile = (T & LCm) == 0;  // (always at order 0)
         const int Tc = T >> lamC;             // coarse tile of this iteration
         double acur[KS];  // A operand of coarse tile Tc+2: dY[col 8(Tc+2) + lane/4][4kk + lane%4]
@@ -286,7 +291,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         // values at node column 8T - u (and the bottom one a column before):
         // read back only after the item's forward, so stream them past L2
         __stcs(cck + (int64_t)T * 32, make_double2(kl0, kl1));
-        __stcs(cck2 + (int64_t)T * 32, bprev);
+        __stcs(cck2 + (int64_t)T * 32, (double)bprev);
         double2* __restrict__ r0 = aslot(T);
         double2* __restrict__ r1 = aslot(T - 1);
         const int s0 = T & 1, s1 = (T - 1) & 1;  // slot within the ring half
@@ -302,12 +307,12 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
             const int sl = (m - u < 0) ? s1 : s0;
             pv = ((m - u < 0) ? r1 : r0)[(sl * 8 + ((m - u) & 7)) * PSTR + psw(m - u, lane)];
           }
-          double tv = __shfl_up_sync(0xffffffffu, bot, 1, 4);
+          TR tv = __shfl_up_sync(0xffffffffu, bot, 1, 4);
           if (u == 0) tv = hcur[m];
           if (!EDGE || (c >= 0 && c < NC)) {
-            const Coef c0 = coef(pv.x), c1 = coef(pv.y);
-            const double k0 = cell(tv, kl0, topc, c0);
-            const double k1 = cell(k0, kl1, kl0, c1);
+            const CoefOf<TR> c0 = coef((TR)pv.x), c1 = coef((TR)pv.y);
+            const TR k0 = cell(tv, kl0, topc, c0);
+            const TR k1 = cell(k0, kl1, kl0, c1);
             topc = tv;
             kl0 = k0;
             bprev = kl1;
@@ -327,7 +332,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
     }
 
     if (ba.values && valid && u == u_star && !(ba.exp & 2))
-      ba.values[(int64_t)(a - pb.r0) * pb.ldo + b] = kval;
+      ba.values[(int64_t)(a - pb.r0) * pb.ldo + b] = (double)kval;
 
     // ------------------------------------------------ phase B: reverse sweep
     for (int e = lane; e < 8 * NT8 * DP; e += 32) gcs[e] = 0.0;
@@ -393,6 +398,9 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       }
       stage_block(NT8 - 1);
       double aR0 = 0.0, aR1 = 0.0, bR0 = 0.0, bR1 = 0.0, sendm = 0.0;
+      // F32: the right neighbours' adjoints and A / B corrections, and the
+      // two-part message (main, correction) to lane u-1
+      float lR0 = 0.f, lR1 = 0.f, aC0 = 0.f, aC1 = 0.f, bC0 = 0.f, bC1 = 0.f, sM = 0.f, sC = 0.f;
 
       // one block; EDGE blocks hold columns outside [0, NC) or the final cell
       auto blockB = [&](auto edge, int blk) {
@@ -414,30 +422,39 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         // the row above the lane: lane u = 0 from the strip's top row; lane
         // u > 0 starts from lane u-1's checkpoints (node columns 8blk-u,
         // 8blk-u+1) and receives the rest from lane u-1's recompute below
-        double tv[9];
+        TR tv[9];
         if (u == 0) {
 #pragma unroll
           for (int i = 0; i < 9; ++i) {
-            const double v = (strip == 0) ? 1.0 : st[i * 32 + lane];
+            const TR v = (strip == 0) ? TR(1) : (TR)st[i * 32 + lane];
             if constexpr (EDGE) {
               const int cc = 8 * blk + i;
-              tv[i] = (cc <= 0) ? 1.0 : (cc > NC ? 0.0 : v);
+              tv[i] = (cc <= 0) ? TR(1) : (cc > NC ? TR(0) : v);
             } else {
               tv[i] = v;
             }
           }
         } else {
-          tv[0] = st[11 * 32 + 64 + lane - 1];
-          tv[1] = st[9 * 32 + 2 * (lane - 1) + 1];
+          tv[0] = (TR)st[11 * 32 + 64 + lane - 1];
+          tv[1] = (TR)st[9 * 32 + 2 * (lane - 1) + 1];
 #pragma unroll
-          for (int i = 2; i < 9; ++i) tv[i] = 0.0;
+          for (int i = 2; i < 9; ++i) tv[i] = TR(0);
         }
-        const double2 kleft = *reinterpret_cast<const double2*>(st + 9 * 32 + 2 * lane);
-        double av[8];  // lane u = 3: adjoint messages of the strip below
+        const double2 kleft2 = *reinterpret_cast<const double2*>(st + 9 * 32 + 2 * lane);
+        const TR kleftx = (TR)kleft2.x, klefty = (TR)kleft2.y;
+        // lane u = 3: adjoint messages of the strip below (F32: a float2
+        // (main, correction) in each fp64 slot)
+        double av[8];
+        float2 avf[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          av[i] = st[11 * 32 + g * 8 + i];
-          if (EDGE && 8 * blk - 3 + i < 0) av[i] = 0.0;  // left of column 0: never written
+          if constexpr (F32) {
+            avf[i] = *reinterpret_cast<const float2*>(st + 11 * 32 + g * 8 + i);
+            if (EDGE && 8 * blk - 3 + i < 0) avf[i] = make_float2(0.f, 0.f);
+          } else {
+            av[i] = st[11 * 32 + g * 8 + i];
+            if (EDGE && 8 * blk - 3 + i < 0) av[i] = 0.0;  // left of column 0: never written
+          }
         }
         // refill the staging records for block blk-1 (lanes read lane u-1's)
         __syncwarp();
@@ -446,22 +463,22 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         // ---- 1. recompute the lane's 2 x 8 forward values (registers): the
         // skewed wavefront of phase A over the block (lane u-1's bottom row
         // arrives by shuffle one step ahead), bitwise phase A's values
-        double K0[8], K1[8];
+        TR K0[8], K1[8];
         {
-          double k0 = kleft.x, k1 = kleft.y;
+          TR k0 = kleftx, k1 = klefty;
 #pragma unroll
           for (int kap = 0; kap < 8; ++kap) {
             if (kap > 0) {
-              const double sh = __shfl_up_sync(0xffffffffu, k1, 1, 4);
+              const TR sh = __shfl_up_sync(0xffffffffu, k1, 1, 4);
               if (u > 0) tv[kap + 1] = sh;
             }
             const int c = 8 * blk - u + kap;
             const int jc = c >> lamC;  // coarse column
             double2 pv = sP[((((jc >> 3) & 1) * 8) + (jc & 7)) * PSTR + psw(jc, lane)];
             if (EDGE && (c < 0 || c >= NC)) pv = make_double2(0.0, 0.0);
-            const Coef c0 = coef(pv.x), c1 = coef(pv.y);
-            const double n0 = cell(tv[kap + 1], k0, tv[kap], c0);
-            const double n1 = cell(n0, k1, k0, c1);
+            const CoefOf<TR> c0 = coef((TR)pv.x), c1 = coef((TR)pv.y);
+            const TR n0 = cell(tv[kap + 1], k0, tv[kap], c0);
+            const TR n1 = cell(n0, k1, k0, c1);
             k0 = n0;
             k1 = n1;
             K0[kap] = n0;
@@ -477,13 +494,44 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
 #pragma unroll
         for (int kap = 7; kap >= 0; --kap) {
           const int c = 8 * blk - u + kap;
-          double recv = __shfl_down_sync(0xffffffffu, sendm, 1, 4);
-          if (u == 3) recv = av[kap];
           const int jc = c >> lamC;
           double2 pv = sP[((((jc >> 3) & 1) * 8) + (jc & 7)) * PSTR + psw(jc, lane)];
           if (EDGE && (c < 0 || c >= NC)) pv = make_double2(0.0, 0.0);
+          TR lam1, lam0;
+          if constexpr (F32) {
+            // small-correction adjoint (A = 1 + Ap, B = 1 - q): every cell's
+            // pushes split into an O(lambda) main part and an O(p lambda)
+            // correction, summed separately (the fp32 rounding of A, B would
+            // otherwise swallow the p ~ 1e-3 terms); the message to lane u-1
+            // is (lam0 - lamR0, a0 + bR0): below-push + diagonal-push of the
+            // row above's cell
+            float rM = __shfl_down_sync(0xffffffffu, sM, 1, 4);
+            float rC = __shfl_down_sync(0xffffffffu, sC, 1, 4);
+            if (u == 3) {
+              rM = avf[kap].x;
+              rC = avf[kap].y;
+            }
+            const Coef32 c0 = coef((float)pv.x), c1 = coef((float)pv.y);
+            float m1 = lR1 + rM;
+            if (EDGE && fin1 && c == NC - 1) m1 += (float)wcot;
+            lam1 = m1 + (aC1 + rC);
+            const float a1 = lam1 * c1.Ap;
+            float m0 = lR0 + (lam1 - lR1);
+            if (EDGE && fin0 && c == NC - 1) m0 += (float)wcot;
+            lam0 = m0 + (aC0 + (a1 + bC1));
+            const float a0 = lam0 * c0.Ap;
+            sM = lam0 - lR0;
+            sC = a0 + bC0;
+            lR1 = lam1;
+            aC1 = a1;
+            bC1 = lam1 * c1.q;
+            lR0 = lam0;
+            aC0 = a0;
+            bC0 = lam0 * c0.q;
+          } else {
+          double recv = __shfl_down_sync(0xffffffffu, sendm, 1, 4);
+          if (u == 3) recv = av[kap];
           const Coef c0 = coef(pv.x), c1 = coef(pv.y);
-          double lam1, lam0;
           if constexpr (EDGE || SK_AFFINE_MSG == 0) {
             // rows 1 then 0, the message chain as written (final-cell seed here)
             lam1 = aR1 + recv;
@@ -500,25 +548,29 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
             lam1 = aR1 + recv;
             lam0 = fma(c1.A, recv, R0);
           }
-          const double kL1 = kap > 0 ? K1[kap - 1] : kleft.y;
-          const double kD1 = kap > 0 ? K0[kap - 1] : kleft.x;
-          const double p61 = pv.y * (1.0 / 6.0);
-          const double D1 = lam1 * fma(kL1 + K0[kap], 0.5 + p61, kD1 * p61);
-          const double kL0 = kap > 0 ? K0[kap - 1] : kleft.x;
-          const double p60 = pv.x * (1.0 / 6.0);
-          const double D0 = lam0 * fma(kL0 + tv[kap + 1], 0.5 + p60, tv[kap] * p60);
           aR1 = c1.A * lam1;
           bR1 = c1.B * lam1;
           aR0 = c0.A * lam0;
           bR0 = c0.B * lam0;
+          }
+          const TR kL1 = kap > 0 ? K1[kap - 1] : klefty;
+          const TR kD1 = kap > 0 ? K0[kap - 1] : kleftx;
+          const TR p61 = (TR)pv.y * TR(1.0 / 6.0);
+          const TR D1 = lam1 * fma(kL1 + K0[kap], TR(0.5) + p61, kD1 * p61);
+          const TR kL0 = kap > 0 ? K0[kap - 1] : kleftx;
+          const TR p60 = (TR)pv.x * TR(1.0 / 6.0);
+          const TR D0 = lam0 * fma(kL0 + tv[kap + 1], TR(0.5) + p60, tv[kap] * p60);
           // columns outside [0, NC) store exact zeros: their slots are read by
           // the tile maps as dead columns later (x 0 dY), so no garbage (e.g.
           // the never-written adjoint messages left of column 0) may reach them
           const bool cdead = EDGE && (c < 0 || c >= NC);
           *reinterpret_cast<double2*>(sD + ((c >> 3) & 1) * Cf::DTILE + (c & 7) * DSTR +
                                       dsw(c, 2 * lane)) =
-              cdead ? make_double2(0.0, 0.0) : make_double2(D0, D1);
-          if (u == 0 && (!EDGE || c >= 0)) arow[c + 3] = sendm;
+              cdead ? make_double2(0.0, 0.0) : make_double2((double)D0, (double)D1);
+          if (u == 0 && (!EDGE || c >= 0)) {
+            if constexpr (F32) *reinterpret_cast<float2*>(arow + c + 3) = make_float2(sM, sC);
+            else arow[c + 3] = sendm;
+          }
         }
         __syncwarp();  // tile blk's D complete, p tile blk dead
 

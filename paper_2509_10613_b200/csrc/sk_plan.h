@@ -36,7 +36,7 @@ BwdFn select_bwd_rbf(const BwdShape& s, int& smem_doubles);
 BwdFn select_bwd_wide(const BwdShape& s, int& smem_doubles);  // linear, d > 32
 BwdFn select_bwd_xw_linear(const BwdShape& s, int& smem_doubles);  // one pair per CTA
 BwdFn select_bwd_xw_rbf(const BwdShape& s, int& smem_doubles);
-BwdFn select_bwd_mma(int DP, int WPC, int& smem_doubles_per_warp, bool dyadic);
+BwdFn select_bwd_mma(int DP, int WPC, int& smem_doubles_per_warp, bool dyadic, bool f32 = false);
 
 // Per-kind instance tables (one translation unit each, compiled in parallel).
 FwdFn select_fwd_linear(const FwdShape& s, int& smem);

@@ -497,6 +497,50 @@ def value_and_grad_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, out=None,
     return out, g1, g2
 
 
+def f32_backward_supported(lam1: int, lam2: int, d: int, transform=None) -> bool:
+    """Shapes the FP32-arithmetic Gram backward covers (sk_backward_gram_acc_f32)."""
+    return lam1 == 0 and lam2 == 0 and 1 <= d <= 16 and transform_code(transform) == 0
+
+
+def value_and_grad_gram_f32(x, y, cot, rows=None, out=None, acc_x=None, acc_y=None):
+    """FP32-arithmetic fused Gram value + gradient (linear kernel, dyadic order
+    0, d <= 16): the forward, recompute and adjoint recurrences in float
+    (small-correction forms), p = <dx, dy>, gx, gy on the FP64 tensor cores.
+    x, y: float32 or float64 points (float64 copies are made; exact for float32
+    inputs).  Returns (G rows [r0, r1) as float64 of the float results, gx, gy)
+    with float64 gradients (exact fixed-point sums of the float adjoints)."""
+    lib = _lib.load()
+    x, yy, sym, n1, n2, L1, L2, d = _gram_args(x.to(torch.float64), None if y is None else y.to(torch.float64))
+    if not f32_backward_supported(0, 0, d):
+        raise InvalidArgument("FP32 backward supports d <= 16")
+    r0, r1 = _rows(rows, n1)
+    cot = _cotangent(cot, (n1, n2), x)
+    dev = x.device
+    if out is None:
+        out = torch.empty((r1 - r0, n2), dtype=torch.float64, device=dev)
+    own = acc_x is None
+    if own:
+        acc_x = GradAcc(n1, L1, d, dev).init(cot, n1, n2, sym)
+        if not sym:
+            acc_y = GradAcc(n2, L2, d, dev).init(cot, n1, n2, False)
+    else:
+        _check_acc(acc_x, n1, L1, d, 0, x, "acc_x")
+        if not sym:
+            _check_acc(acc_y, n2, L2, d, 0, x, "acc_y")
+    if n1 and n2 and r1 > r0:
+        with _on(dev):
+            nb = _wsq(lib.sk_backward_gram_acc_f32_workspace_bytes, n1, n2, L1, L2, d, 0, 0,
+                      int(sym))
+            ws = _workspace(nb, dev)
+            _lib.check(lib.sk_backward_gram_acc_f32(
+                _ptr(x), None if sym else _ptr(yy), n1, n2, L1, L2, d, 0, 0, r0, r1, _ptr(cot),
+                _ptr(out), _ptr(acc_x.blob), None if sym else _ptr(acc_y.blob), _ptr(ws),
+                ws.numel(), _stream(dev)))
+    if not own:
+        return out, acc_x, acc_y
+    return out, acc_x.finalize(), (None if sym else acc_y.finalize())
+
+
 def mirror_upper(G: torch.Tensor) -> torch.Tensor:
     """In place: lower triangle := upper triangle (kernel.py:177-179)."""
     lib = _lib.load()

@@ -66,7 +66,7 @@ def test_c4_fp32_error_reported(sk, oracle):
     assert err < 5e-3
 
 
-def test_fp32_autograd_uses_fp64_backward(sk, oracle):
+def test_fp32_batch_autograd_uses_fp64_backward(sk, oracle):
     rng = np.random.default_rng(3)
     x = make_paths(rng, 4, 40, 3).astype(np.float32)
     y = make_paths(rng, 4, 33, 3).astype(np.float32)
@@ -83,3 +83,84 @@ def test_fp32_rejects_rbf(sk):
     x = torch.zeros((1, 4, 2), device="cuda")
     with pytest.raises(InvalidArgument):
         sk.sig_kernel(x, x, static_kernel=sk.RBFKernel(1.0), precision="fp32")
+
+
+# ---- FP32-arithmetic Gram backward (sk_backward_gram_acc_f32: float forward,
+# recompute and small-correction adjoint; p, gx, gy on the FP64 tensor cores)
+
+# C5's length (1023^2 fine cells per pair): the float recurrence's error grows
+# with the fine-axis length; measured 1.03e-4 on G there (the
+# gradient 3.7e-5 on Brownian paths, tools/time_f32_bwd.py), so that shape is
+# bounded at 2e-4 -- the fp64 path is the one within 1e-10
+@pytest.mark.parametrize("n,L,d,tol", [(10, 33, 3, TOL32),      # d <= 4: the DP = 8 instance, padded
+                                       (12, 129, 8, TOL32),     # DP = 8, several strips / blocks
+                                       (9, 512, 16, TOL32),     # C3 shape (length, dimension)
+                                       (8, 1024, 8, 2e-4)])     # C5 shape (length, dimension)
+def test_gram_value_and_grad_fp32_within_1e4(sk, oracle, n, L, d, tol):
+    rng = np.random.default_rng(11)
+    X = make_paths(rng, n, L, d).astype(np.float32)
+    C = rng.standard_normal((n, n))
+    G, gx, gy = sk.sig_kernel_gram_value_and_grad(f32(X), None, torch.as_tensor(C, device="cuda"),
+                                                  precision="fp32")
+    assert G.dtype == torch.float32 and gx.dtype == torch.float32 and gy is None
+    X64 = X.astype(np.float64)
+    eg = rel_err(G.cpu().numpy(), oracle.kernel_gram(X64, None, 0, 0))
+    np.testing.assert_array_equal(G.cpu().numpy(), G.cpu().numpy().T)
+    want = oracle.gram_backward(X64, None, C, 0, 0)
+    err = rel_err(gx.cpu().numpy(), want)
+    print(f"fp32 Gram n={n} L={L} d={d}: G rel err {eg:.2e}, gradient rel err {err:.2e}")
+    assert eg < tol
+    assert err < tol
+
+
+def test_gram_cross_value_and_grad_fp32(sk, oracle):
+    rng = np.random.default_rng(12)
+    X = make_paths(rng, 11, 200, 16).astype(np.float32)
+    Y = make_paths(rng, 7, 150, 16).astype(np.float32)
+    C = rng.standard_normal((11, 7))
+    G, gx, gy = sk.sig_kernel_gram_value_and_grad(f32(X), f32(Y), torch.as_tensor(C, device="cuda"),
+                                                  precision="fp32")
+    X64, Y64 = X.astype(np.float64), Y.astype(np.float64)
+    assert rel_err(G.cpu().numpy(), oracle.kernel_gram(X64, Y64, 0, 0)) < TOL32
+    wx, wy = oracle.gram_backward(X64, Y64, C, 0, 0)
+    assert rel_err(gx.cpu().numpy(), wx) < TOL32
+    assert rel_err(gy.cpu().numpy(), wy) < TOL32
+
+
+def test_gram_fp32_autograd_uses_fp32_backward(sk, oracle):
+    """sig_kernel_gram(precision="fp32") + autograd at an eligible shape: the
+    gradient equals the fused FP32 call's bitwise (same kernel, exact sums) and
+    is within 1e-4 of the fp64 oracle; and it is not the fp64 backward's."""
+    rng = np.random.default_rng(13)
+    X = make_paths(rng, 10, 96, 8).astype(np.float32)
+    # the autograd cotangent of a float32 G is float32: use float-exact C
+    C = rng.standard_normal((10, 10)).astype(np.float32).astype(np.float64)
+    Ct = torch.as_tensor(C, device="cuda")
+    xt = f32(X).requires_grad_(True)
+    G = sk.sig_kernel_gram(xt, precision="fp32")
+    (G.double() * Ct).sum().backward()
+    _, gf, _ = sk.sig_kernel_gram_value_and_grad(f32(X), None, Ct, precision="fp32")
+    np.testing.assert_array_equal(xt.grad.cpu().numpy(), gf.cpu().numpy())
+    want = oracle.gram_backward(X.astype(np.float64), None, C, 0, 0)
+    assert rel_err(xt.grad.cpu().numpy(), want) < TOL32
+    _, g64, _ = sk.sig_kernel_gram_value_and_grad(f32(X).double(), None, Ct)
+    assert not np.array_equal(g64.float().cpu().numpy(), gf.cpu().numpy())
+
+
+def test_gram_fp32_backward_deterministic(sk):
+    rng = np.random.default_rng(14)
+    X = f32(make_paths(rng, 40, 64, 16))
+    C = torch.as_tensor(rng.standard_normal((40, 40)), device="cuda")
+    a = sk.sig_kernel_gram_value_and_grad(X, None, C, precision="fp32")
+    b = sk.sig_kernel_gram_value_and_grad(X, None, C, precision="fp32")
+    for u, v in zip(a[:2], b[:2]):
+        np.testing.assert_array_equal(u.cpu().numpy(), v.cpu().numpy())
+
+
+def test_gram_fp32_value_and_grad_rejects_unsupported(sk):
+    from paper_2509_10613_b200 import InvalidArgument
+    x = torch.zeros((2, 5, 17), device="cuda")
+    with pytest.raises(InvalidArgument):
+        sk.sig_kernel_gram_value_and_grad(x, precision="fp32")
+    with pytest.raises(InvalidArgument):
+        sk.sig_kernel_gram_value_and_grad(x[..., :4], dyadic_order=1, precision="fp32")
