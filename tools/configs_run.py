@@ -88,6 +88,12 @@ out["C3-shape Gram fwd FP32 arithmetic"] = {"s": t, "cells_per_s": c / t,
                                                     "on the FP64 tensor cores (DMMA), rounded "
                                                     "once to float -- frac_fp32 counts it as "
                                                     "FP32 work (d + 4 per cell)"}
+ones = torch.ones((1024, 1024), dtype=torch.float64, device="cuda")
+t = timed(lambda: sk.sig_kernel_gram_value_and_grad(X32, None, ones, precision="fp32"), 2)
+out["C3 Gram fused G+grad FP32 arithmetic"] = {
+    "s": t, "cells_per_s": c / t,
+    "note": "float forward / recompute / small-correction adjoint on the FP32 pipe, p, gx, gy "
+            "on the FP64 tensor cores (gram_bwd_mma<16,2,false,float>); same shape as C3"}
 x, y = paths(rng, 128, 8192, 4).float(), paths(rng, 128, 8192, 4).float()
 t = timed(lambda: ops.forward_batch_f32(x, y, 1, 1), 5)
 c = 128 * 16382 ** 2
