@@ -52,6 +52,14 @@
 
 namespace sk {
 
+// 1: the gx map of block blk + 1 (32 DMMAs at DP = 16) is issued inside block
+// blk's reverse sweep, to fill the sweep chain's latency bubbles (same
+// accumulation order: bitwise equal -- measured slower: C3 fp64 1175 -> 1208
+// ms, FP32 1106 -> 1122 ms); 0 (default): after the sweep, with gy
+#ifndef SK_GX_DEFER
+#define SK_GX_DEFER 0
+#endif
+
 // 1: the adjoint message to lane u-1 as one FMA of the received one (+3 DP ops
 // per column, shorter lane chain); 0: the chain as written (measured faster)
 #ifndef SK_AFFINE_MSG
@@ -402,6 +410,17 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
       // two-part message (main, correction) to lane u-1
       float lR0 = 0.f, lR1 = 0.f, aC0 = 0.f, aC1 = 0.f, bC0 = 0.f, bC1 = 0.f, sM = 0.f, sC = 0.f;
 
+      // gx += D dY for one k-half and four pairs of tile t (D slot t & 1)
+      double gbp[2][NN];  // SK_GX_DEFER: tile blk + 1's gx B operand, mapped in blk's sweep
+      auto gx_part = [&](int t, const double (&gbx)[2][NN], int kk, int h0) {
+        const double* __restrict__ Dx = sD + (t & 1) * Cf::DTILE;
+#pragma unroll
+        for (int h = h0; h < h0 + 4; ++h) {
+          const double av_ = Dx[(4 * kk + u) * DSTR + dsw(u, 8 * h + g)];
+#pragma unroll
+          for (int n = 0; n < NN; ++n) dmma(gx[h][n][0], gx[h][n][1], av_, gbx[kk][n]);
+        }
+      };
       // one block; EDGE blocks hold columns outside [0, NC) or the final cell
       auto blockB = [&](auto edge, int blk) {
         constexpr bool EDGE = decltype(edge)::value;
@@ -493,6 +512,11 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         // (block 0) only feed D slots that are never consumed.
 #pragma unroll
         for (int kap = 7; kap >= 0; --kap) {
+          if (SK_GX_DEFER && kap >= 4 && blk + 1 < NT8 && !(ba.exp & 4))
+            gx_part(blk + 1, gbp, (7 - kap) >> 1, ((7 - kap) & 1) * 4);
+          // tile blk+1's D is read (above) before this sweep stores tile
+          // blk-1's columns into the same slot (lanes u > kap, kap <= 2)
+          if (SK_GX_DEFER && kap == 3) __syncwarp();
           const int c = 8 * blk - u + kap;
           const int jc = c >> lamC;
           double2 pv = sP[((((jc >> 3) & 1) * 8) + (jc & 7)) * PSTR + psw(jc, lane)];
@@ -594,14 +618,9 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
         }
         const double* __restrict__ Dt = sD + (blk & 1) * Cf::DTILE;
         if (!(ba.exp & 4)) {
+        if (!SK_GX_DEFER) {
 #pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-#pragma unroll
-          for (int h = 0; h < 8; ++h) {
-            const double av_ = Dt[(4 * kk + u) * DSTR + dsw(u, 8 * h + g)];
-#pragma unroll
-            for (int n = 0; n < NN; ++n) dmma(gx[h][n][0], gx[h][n][1], av_, gb[kk][n]);
-          }
+          for (int q = 0; q < 4; ++q) gx_part(blk, gb, q >> 1, (q & 1) * 4);
         }
         // gy = D^T dX over the tile's 64 rows: four independent DMMA chains per
         // component tile, all chains side by side (fixed order: deterministic)
@@ -627,11 +646,21 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
                       pol_keep);
         }
         }
+        if (SK_GX_DEFER) {
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+            for (int n = 0; n < NN; ++n) gbp[kk][n] = gb[kk][n];
+        }
         __syncwarp();
       };
       for (int blk = NT8 - 1; blk >= 0; --blk) {
         if (blk == 0 || 8 * blk + 8 >= NC) blockB(std::true_type{}, blk);
         else blockB(std::false_type{}, blk);
+      }
+      if (SK_GX_DEFER && !(ba.exp & 4)) {  // block 0's gx map (D slot 0 is intact)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) gx_part(0, gbp, q >> 1, (q & 1) * 4);
       }
 
       // row-side increment gradients of the strip into the super-item's sums
