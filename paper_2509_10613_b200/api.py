@@ -284,6 +284,31 @@ def sig_kernel_gram(x, y=None, dyadic_order=0, static_kernel=None, transform=Non
     return G.to(out_dtype)
 
 
+def sig_kernel_value_and_grad(x, y, cotangent=None, dyadic_order=0, static_kernel=None,
+                              transform=None):
+    """k(x_b, y_b) and the gradients of F = sum_b cotangent[b] k(x_b, y_b) in ONE
+    pass: returns (k, dF/dx, dF/dy).  cotangent None = ones.
+
+    The torch form of the reference's kernel_batch_backward, which returns the
+    values with the gradients from one call (kernel_grad.py:64-98): the
+    backward's own forward solve (phase A) writes k, so no separate forward
+    runs.  Not an autograd op -- use sig_kernel for autograd graphs.  Outputs
+    follow promote_types(x.dtype, y.dtype); a pair of (L, d) paths gives a 0-d k."""
+    x, sq = _batched(_prep(x, "x"), "x")
+    y, _ = _batched(_prep(y, "y"), "y")
+    out_dtype = torch.promote_types(x.dtype, y.dtype)
+    l1, l2 = _orders(dyadic_order)
+    kind, sigma = ops.static_kind(static_kernel)
+    cot = None if cotangent is None else torch.as_tensor(cotangent, device=x.device).reshape(-1)
+    k, gx, gy = ops.backward_batch(x.detach().to(torch.float64), y.detach().to(torch.float64),
+                                   l1, l2, kind, sigma, cot, want_values=True,
+                                   transform=_tf(transform))
+    k, gx, gy = k.to(out_dtype), gx.to(out_dtype), gy.to(out_dtype)
+    if sq:
+        return k[0], gx[0], gy[0]
+    return k, gx, gy
+
+
 def sig_kernel_gram_value_and_grad(x, y=None, cotangent=None, dyadic_order=0, static_kernel=None,
                                    transform=None, precision="fp64"):
     """Gram matrix and its gradient in ONE fused pass: returns (G, dF/dx, dF/dy)

@@ -245,3 +245,30 @@ def test_cross_warp_pairs_vs_oracle(sk, oracle, B, L1, L2, d, l1, l2, static):
     assert rel_err(gy.cpu().numpy(), wy) < TOL
     f = ops.forward_batch(cu(x), cu(y), l1, l2, kind, sigma).cpu().numpy()
     np.testing.assert_array_equal(f, v.cpu().numpy())
+
+
+@pytest.mark.parametrize("B,L1,L2,d,lam,sk_kind", [(6, 40, 33, 3, 0, None),
+                                                   (5, 50, 50, 8, (1, 2), None),
+                                                   (4, 30, 41, 5, 1, ("rbf", 0.8)),
+                                                   (256, 256, 256, 8, 2, ("rbf", 1.0))])  # C2
+def test_sig_kernel_value_and_grad_matches_oracle(B, L1, L2, d, lam, sk_kind):
+    """The torch form of kernel_batch_backward (kernel_grad.py:64-98): values
+    and both gradients from one pass, against the oracle's batch backward."""
+    import paper_2509_10613_b200 as sk
+    from oracle import oracle as orc
+    rng = np.random.default_rng(21)
+    x = np.cumsum(rng.standard_normal((B, L1, d)) / np.sqrt(L1), axis=1)
+    y = np.cumsum(rng.standard_normal((B, L2, d)) / np.sqrt(L2), axis=1)
+    cot = rng.standard_normal(B)
+    l1, l2 = (lam, lam) if isinstance(lam, int) else lam
+    static = None if sk_kind is None else sk.RBFKernel(sk_kind[1])
+    k, gx, gy = sk.sig_kernel_value_and_grad(torch.as_tensor(x, device="cuda"),
+                                             torch.as_tensor(y, device="cuda"),
+                                             torch.as_tensor(cot, device="cuda"),
+                                             dyadic_order=(l1, l2), static_kernel=static)
+    wv, wx, wy = orc.kernel_batch_backward(x, y, l1, l2, cot, sk_kind)
+    for got, want in ((k, wv), (gx, wx), (gy, wy)):
+        assert np.abs(got.cpu().numpy() - want).max() / np.abs(want).max() < 1e-10
+    k2 = sk.sig_kernel(torch.as_tensor(x, device="cuda"), torch.as_tensor(y, device="cuda"),
+                       dyadic_order=(l1, l2), static_kernel=static)
+    assert np.abs(k.cpu().numpy() - k2.cpu().numpy()).max() / np.abs(wv).max() < 1e-13

@@ -53,6 +53,9 @@ tb = timed(lambda: ops.backward_batch(x, y, 2, 2, 1, 1.0, None, want_values=True
 c = 256 * 1020 ** 2
 out["C2 sig_kernel fwd+bwd B256 L256 d8 lam2 RBF"] = {
     "fwd_s": tf, "bwd_s": tb, "fwd_cells_per_s": c / tf, "bwd_cells_per_s": c / tb,
+    "values_and_grad_one_call_s": tb,
+    "one_call": "bwd_s is the backward WITH the values (want_values=True): the reference's "
+                "kernel_batch_backward contract (kernel_grad.py:64-98), sig_kernel_value_and_grad",
     "note": "RBF adds an exp per coarse node; frac not reported (SURVEY 8d counts linear)"}
 
 X = paths(rng, 1024, 512, 16)
