@@ -321,6 +321,11 @@ __device__ void cta_exp(double* __restrict__ E, const double* __restrict__ z, do
 // One CTA per path: the reverse walk of sig_backward_path (_kernels.py:182-266).
 // W: per-path workspace [SIG | SB | EB | EX] (4 x total); SIG enters as the
 // full signature, SB as the cotangent.  gout: [M][d] increment gradients.
+// ONCHIP: the four tensors live in shared memory (4 x total doubles fit, e.g.
+// d = 4, N = 6: 175 KB); SIG and SB are copied in once, every per-segment sweep
+// then stays on chip (the global walk is L2 / DRAM latency bound).  Same
+// operations in the same order: bitwise the global-memory walk.
+template <bool ONCHIP>
 __global__ void __launch_bounds__(512)
 sig_bwd_kernel(const double* __restrict__ inc, int64_t M, SigGeom g, double* __restrict__ work,
                int64_t wstride, double* __restrict__ gout) {
@@ -332,6 +337,12 @@ sig_bwd_kernel(const double* __restrict__ inc, int64_t M, SigGeom g, double* __r
   double* part = gz + 32;                 // [blockDim]
   const int64_t path = blockIdx.x;
   double* SIG = work + path * wstride;
+  if constexpr (ONCHIP) {
+    double* t4 = part + ((blockDim.x + 1) & ~1u);
+    for (int64_t t = threadIdx.x; t < 2 * total; t += blockDim.x) t4[t] = SIG[t];
+    SIG = t4;
+    __syncthreads();
+  }
   double* SB = SIG + total;
   double* EB = SB + total;
   double* EX = EB + total;
@@ -596,7 +607,23 @@ int sk_signature_backward(const double* x, const double* times, int64_t B, int64
   }
   const int threads = 512;
   const size_t smem = (64 + threads) * sizeof(double);
-  sig_bwd_kernel<<<(unsigned)B, threads, smem, st>>>(inc, p.M, p.g, work, wstride, gin);
+  const size_t smem_on = smem + 4 * (size_t)p.total * sizeof(double);
+  static bool opted[64] = {};
+  int dev = 0;
+  (void)cudaGetDevice(&dev);
+  bool onchip = smem_on <= 227 * 1024 && dev >= 0 && dev < 64;
+  if (onchip && !opted[dev]) {
+    if (cudaFuncSetAttribute(sig_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024) == cudaSuccess)
+      opted[dev] = true;
+    else
+      (void)cudaGetLastError();
+  }
+  onchip = onchip && opted[dev];
+  if (onchip)
+    sig_bwd_kernel<true><<<(unsigned)B, threads, smem_on, st>>>(inc, p.M, p.g, work, wstride, gin);
+  else
+    sig_bwd_kernel<false><<<(unsigned)B, threads, smem, st>>>(inc, p.M, p.g, work, wstride, gin);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(SK_CUDA_ERROR, cudaGetErrorString(e));
   const int64_t np = B * L * d;
