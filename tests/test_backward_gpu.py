@@ -272,3 +272,20 @@ def test_sig_kernel_value_and_grad_matches_oracle(B, L1, L2, d, lam, sk_kind):
     k2 = sk.sig_kernel(torch.as_tensor(x, device="cuda"), torch.as_tensor(y, device="cuda"),
                        dyadic_order=(l1, l2), static_kernel=static)
     assert np.abs(k.cpu().numpy() - k2.cpu().numpy()).max() / np.abs(wv).max() < 1e-13
+
+
+def test_sig_kernel_value_and_grad_single_pair_and_transform():
+    """(L, d) inputs give a 0-d k; a transform runs inside the kernels and the
+    result equals sig_kernel + autograd on the same call (values and gradients)."""
+    import paper_2509_10613_b200 as sk
+    rng = np.random.default_rng(22)
+    x = torch.as_tensor(np.cumsum(rng.standard_normal((30, 3)) / 6, axis=0), device="cuda")
+    y = torch.as_tensor(np.cumsum(rng.standard_normal((25, 3)) / 5, axis=0), device="cuda")
+    k, gx, gy = sk.sig_kernel_value_and_grad(x, y, dyadic_order=1, transform="lead_lag")
+    assert k.dim() == 0 and gx.shape == x.shape and gy.shape == y.shape
+    xr, yr = x.clone().requires_grad_(True), y.clone().requires_grad_(True)
+    k2 = sk.sig_kernel(xr, yr, dyadic_order=1, transform="lead_lag")
+    k2.backward()
+    assert abs(k.item() - k2.item()) <= 1e-13 * abs(k2.item())
+    assert torch.allclose(gx, xr.grad, rtol=0, atol=1e-13 * xr.grad.abs().max().item())
+    assert torch.allclose(gy, yr.grad, rtol=0, atol=1e-13 * yr.grad.abs().max().item())
