@@ -261,7 +261,7 @@ int sk_backward_gram_acc_tf(const double *x, const double *y, int64_t n1, int64_
                             int64_t row_end, const double *cot, double *values, void *acc_x,
                             void *acc_y, void *workspace, size_t workspace_bytes, void *stream);
 /* FP32-arithmetic Gram backward (linear static kernel, dyadic order 0,
- * d <= 16): sk_backward_gram_acc with the forward, recompute and adjoint
+ * d <= 16, cross Grams with L2 <= L1): sk_backward_gram_acc with the forward, recompute and adjoint
  * recurrences in float (small-correction forms) and
  * p = <dx, dy>, gx, gy on the FP64 tensor cores.  x / y are the fp64 copies of
  * float32 points (exact); values (nullable) are the float recurrence's

@@ -137,7 +137,9 @@ class _SigKernelGramF32Fn(torch.autograd.Function):
         l1, l2, tf = ctx.cfg
         # FP32-arithmetic backward where it exists (linear Gram tiles, order 0,
         # d <= 16: sk_backward_gram_acc_f32), else the fp64 backward
-        f32 = ops.f32_backward_supported(l1, l2, ctx.saved_tensors[0].shape[2], tf)
+        sv = ctx.saved_tensors
+        f32 = ops.f32_backward_supported(l1, l2, sv[0].shape[2], tf, sv[0].shape[1],
+                                         sv[-1].shape[1])
         if ctx.sym:
             (x,) = ctx.saved_tensors
             if f32:
@@ -327,11 +329,12 @@ def sig_kernel_gram_value_and_grad(x, y=None, cotangent=None, dyadic_order=0, st
     l1, l2 = _orders(dyadic_order)
     kind, sigma = ops.static_kind(static_kernel)
     if _precision(precision, kind):
-        if not ops.f32_backward_supported(l1, l2, x.shape[2], _tf(transform)):
-            raise InvalidArgument("precision='fp32' value and gradient: linear kernel, dyadic "
-                                  "order 0, d <= 16, no transform")
         xf = x.detach().to(torch.float32)
         yf = None if sym else _batched(_prep(y, "y"), "y")[0].detach().to(torch.float32)
+        if not ops.f32_backward_supported(l1, l2, x.shape[2], _tf(transform), xf.shape[1],
+                                          (xf if yf is None else yf).shape[1]):
+            raise InvalidArgument("precision='fp32' value and gradient: linear kernel, dyadic "
+                                  "order 0, d <= 16, no transform, y no longer than x")
         n1, n2 = xf.shape[0], (xf if sym else yf).shape[0]
         if cotangent is None:
             cotangent = torch.ones((n1, n2), dtype=torch.float64, device=xf.device)

@@ -497,9 +497,14 @@ def value_and_grad_gram(x, y, lam1, lam2, kind, sigma, cot, rows=None, out=None,
     return out, g1, g2
 
 
-def f32_backward_supported(lam1: int, lam2: int, d: int, transform=None) -> bool:
-    """Shapes the FP32-arithmetic Gram backward covers (sk_backward_gram_acc_f32)."""
-    return lam1 == 0 and lam2 == 0 and 1 <= d <= 16 and transform_code(transform) == 0
+def f32_backward_supported(lam1: int, lam2: int, d: int, transform=None, L1=None,
+                           L2=None) -> bool:
+    """Shapes the FP32-arithmetic Gram backward covers (sk_backward_gram_acc_f32):
+    linear, order 0, d <= 16, no transform, and (cross Grams) y no longer than
+    x -- a longer y puts the y paths on the grid rows (kernel.py:137-140), which
+    the DMMA Gram tiles (shared column path) do not cover."""
+    return (lam1 == 0 and lam2 == 0 and 1 <= d <= 16 and transform_code(transform) == 0
+            and (L1 is None or L2 is None or L2 <= L1))
 
 
 def value_and_grad_gram_f32(x, y, cot, rows=None, out=None, acc_x=None, acc_y=None):
@@ -511,8 +516,9 @@ def value_and_grad_gram_f32(x, y, cot, rows=None, out=None, acc_x=None, acc_y=No
     with float64 gradients (exact fixed-point sums of the float adjoints)."""
     lib = _lib.load()
     x, yy, sym, n1, n2, L1, L2, d = _gram_args(x.to(torch.float64), None if y is None else y.to(torch.float64))
-    if not f32_backward_supported(0, 0, d):
-        raise InvalidArgument("FP32 backward supports d <= 16")
+    if not f32_backward_supported(0, 0, d, None, L1, L2):
+        raise InvalidArgument("FP32 backward supports d <= 16 and (cross Grams) y no longer "
+                              "than x")
     r0, r1 = _rows(rows, n1)
     cot = _cotangent(cot, (n1, n2), x)
     dev = x.device

@@ -164,3 +164,23 @@ def test_gram_fp32_value_and_grad_rejects_unsupported(sk):
         sk.sig_kernel_gram_value_and_grad(x, precision="fp32")
     with pytest.raises(InvalidArgument):
         sk.sig_kernel_gram_value_and_grad(x[..., :4], dyadic_order=1, precision="fp32")
+
+
+def test_gram_fp32_cross_longer_y_falls_back_to_fp64_backward(sk, oracle):
+    """A cross Gram whose y paths are longer puts y on the grid rows (outside
+    the FP32 DMMA backward): autograd takes the fp64 backward there, the fused
+    FP32 call refuses with InvalidArgument."""
+    from paper_2509_10613_b200 import InvalidArgument
+    rng = np.random.default_rng(15)
+    X = make_paths(rng, 5, 40, 4).astype(np.float32)
+    Y = make_paths(rng, 4, 61, 4).astype(np.float32)
+    C = rng.standard_normal((5, 4)).astype(np.float32).astype(np.float64)
+    xt, yt = f32(X).requires_grad_(True), f32(Y).requires_grad_(True)
+    G = sk.sig_kernel_gram(xt, yt, precision="fp32")
+    (G.double() * torch.as_tensor(C, device="cuda")).sum().backward()
+    wx, wy = oracle.gram_backward(X.astype(np.float64), Y.astype(np.float64), C, 0, 0)
+    assert rel_err(xt.grad.cpu().numpy(), wx) < 1e-6
+    assert rel_err(yt.grad.cpu().numpy(), wy) < 1e-6
+    with pytest.raises(InvalidArgument):
+        sk.sig_kernel_gram_value_and_grad(f32(X), f32(Y), torch.as_tensor(C, device="cuda"),
+                                          precision="fp32")
