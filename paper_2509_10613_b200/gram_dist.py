@@ -1,8 +1,9 @@
 """Gram matrices sharded across the GPUs of one box.
 
-One process per GPU (torch.distributed, NCCL over NVLink).  Rows of the Gram
-are split into 2P equal blocks and rank r solves blocks r and 2P-1-r, which
-balances the upper-triangle work of a symmetric Gram (row a holds n-a pairs).
+One process per GPU (torch.distributed, NCCL over NVLink).  Each rank solves
+one contiguous range of Gram rows, cut so every rank holds the same number of
+the fused kernel's work units (the upper triangle of a symmetric Gram: row a
+holds n-a pairs, so the top ranges are short), in one kernel launch.
 The only data-path collectives are all-gathers: one for the assembled Gram
 matrix, one for the gradients (each rank's partial gradient is gathered and
 summed in fixed rank order, so every rank holds bit-identical results and
@@ -25,14 +26,28 @@ from .errors import InvalidArgument
 TILE = 8  # Gram tile height of the DMMA kernels (pairs (a0 + g, b), g < 8)
 
 
+SUPER_B = 8  # column chunk of the DMMA kernels' super-items (SK_SUPER_B, sk_common.cuh)
+
+
+def _super_items_per_block(n: int) -> list[int]:
+    """Super-items (8 rows x SUPER_B column paths, the fused kernel's work unit,
+    sk_common.cuh super_chunks) of each 8-row block of a symmetric (n, n) Gram."""
+    return [(n - 1) // SUPER_B - (TILE * ab) // SUPER_B + 1 for ab in range(-(-n // TILE))]
+
+
 def row_blocks(n: int, world: int, rank: int, symmetric: bool = True) -> list[tuple[int, int]]:
     """Row ranges owned by `rank`.
 
-    symmetric: 2*world equal blocks, rank gets blocks rank and 2*world-1-rank
-    (balanced upper-triangle pair counts); otherwise one contiguous block.
-    Block boundaries are multiples of TILE (the kernels' 8-path Gram tile
-    height), so every rank sees the same tiles as a one-GPU run and the exact
-    gradient accumulators sum to bitwise the one-GPU gradient."""
+    symmetric: ONE contiguous range per rank, its boundaries chosen so every
+    rank holds the same number of the kernel's work units (super-items; row a
+    of the upper triangle holds n - a pairs, so the top ranges are short) --
+    one kernel launch per rank.  (Round 1/2 gave each rank two equal row
+    blocks, r and 2P-1-r: two launches, the second a nearly empty wave -- C3 on
+    8 GPUs would have taken 2 waves per rank against 7 on one GPU.)
+    Otherwise one contiguous block of equal rows.  Boundaries are multiples of
+    TILE (the kernels' 8-path Gram tile height), so every rank sees the same
+    tiles as a one-GPU run and the exact gradient accumulators sum to bitwise
+    the one-GPU gradient."""
     if world <= 1:
         return [(0, n)]
     if not symmetric:
@@ -40,14 +55,28 @@ def row_blocks(n: int, world: int, rank: int, symmetric: bool = True) -> list[tu
         step = -(-step // TILE) * TILE
         lo, hi = min(n, rank * step), min(n, (rank + 1) * step)
         return [(lo, hi)] if hi > lo else []
-    nb = 2 * world
-    bounds = [min(n, TILE * round(k * n / nb / TILE)) for k in range(nb)] + [n]
-    out = []
-    for k in (rank, nb - 1 - rank):
-        lo, hi = bounds[k], bounds[k + 1]
-        if hi > lo:
-            out.append((lo, hi))
-    return sorted(out)
+    w = _super_items_per_block(n)
+    cum = [0]
+    for v in w:
+        cum.append(cum[-1] + v)
+    total = cum[-1]
+
+    def cut(r):  # 8-row block index of boundary r (nearest to r / world of the items)
+        if r <= 0:
+            return 0
+        if r >= world:
+            return len(w)
+        t = total * r / world
+        return min(range(len(cum)), key=lambda k: (abs(cum[k] - t), k))
+
+    lo, hi = min(n, TILE * cut(rank)), min(n, TILE * cut(rank + 1))
+    return [(lo, hi)] if hi > lo else []
+
+
+def super_item_count(ranges, n: int) -> int:
+    """Super-items (kernel work units) of the given row ranges of a symmetric Gram."""
+    w = _super_items_per_block(n)
+    return sum(sum(w[lo // TILE: -(-hi // TILE)]) for lo, hi in ranges)
 
 
 def pair_count(ranges, n: int, symmetric: bool, n2: int | None = None) -> int:

@@ -23,8 +23,22 @@ def test_row_blocks_cover_and_balance(n, world):
         counts.append(gram_dist.pair_count(rg, n, True))
     assert sorted(seen) == list(range(n))
     assert sum(counts) == n * (n + 1) // 2
-    if n >= 64 * world:
-        assert max(counts) / (sum(counts) / world) < 1.01  # balanced to 1%
+    # one contiguous range per rank (one kernel launch), balanced in the fused
+    # kernel's work units (super-items) to within one 8-row block of them
+    items = [gram_dist.super_item_count(gram_dist.row_blocks(n, world, r, True), n)
+             for r in range(world)]
+    assert sum(items) == gram_dist.super_item_count([(0, n)], n)
+    gran = max(gram_dist._super_items_per_block(n))
+    assert max(items) - sum(items) / world <= gran
+    assert all(len(gram_dist.row_blocks(n, world, r, True)) <= 1 for r in range(world))
+
+
+def test_row_blocks_c3_one_wave_per_rank_at_8():
+    """C3 (n = 1024) on 8 GPUs: every rank's items fit one wave of the fused
+    kernel's 1184 resident warps (148 SMs x 8), against 7 waves on one GPU."""
+    items = [gram_dist.super_item_count(gram_dist.row_blocks(1024, 8, r, True), 1024)
+             for r in range(8)]
+    assert max(items) <= 148 * 8 < gram_dist.super_item_count([(0, 1024)], 1024)
 
 
 def test_row_blocks_cross():
