@@ -179,6 +179,22 @@ def forward_batch(x, y, lam1: int, lam2: int, kind: int, sigma: float,
     return out
 
 
+def _transpose_cross(y, rows, kind, L1, L2, lam1, lam2, tf) -> bool:
+    """Whole linear cross Grams whose y paths have the longer fine axis: the
+    kernels put the longer axis on the grid rows (kernel.py:137-140), and only
+    the un-swapped orientation shares one column path across a Gram tile (the
+    DMMA kernels), so the forward solves G^T = Gram(y, x) instead.
+    k(x, y) == k(y, x) bitwise and the DMMA forward is bitwise the FMA-pipe
+    forward, so the values equal the swapped-orientation (row-range) call's.
+    (The backward keeps the swapped orientation: its tile sums would differ in
+    the last bits from row-split calls, which must stay bitwise equal.)"""
+    if y is None or rows is not None or kind != 0:
+        return False
+    L1e, _ = effective_shape(L1, 1, tf)
+    L2e, _ = effective_shape(L2, 1, tf)
+    return ((L2e - 1) << lam2) > ((L1e - 1) << lam1)
+
+
 def forward_gram(x, y, lam1: int, lam2: int, kind: int, sigma: float,
                  rows: tuple[int, int] | None = None, out: torch.Tensor | None = None,
                  transform=None):
@@ -186,6 +202,14 @@ def forward_gram(x, y, lam1: int, lam2: int, kind: int, sigma: float,
     lib = _lib.load()
     tf = transform_code(transform)
     x, yy, sym, n1, n2, L1, L2, d = _gram_args(x, y)
+    if not sym and _transpose_cross(y, rows, kind, L1, L2, lam1, lam2, tf):
+        gt = forward_gram(yy, x, lam2, lam1, kind, sigma, transform=transform)
+        if out is None:
+            return gt.t().contiguous()
+        if tuple(out.shape) != (n1, n2):
+            raise InvalidArgument(f"out must have shape {(n1, n2)}")
+        out.copy_(gt.t())
+        return out
     r0, r1 = _rows(rows, n1)
     if out is None:
         out = torch.empty((r1 - r0, n2), dtype=torch.float64, device=x.device)

@@ -319,3 +319,21 @@ def test_backward_workspace_budget_caps_slots(mods, no_mma):
         os.environ.pop("SK_NO_MMA", None)
     assert rel_err(capped.cpu().numpy(), full.cpu().numpy()) < 1e-13
     assert rel_err(full.cpu().numpy(), orc.gram_backward(X, None, C, 0, 0)) < TOL
+
+
+def test_cross_gram_forward_longer_y_bitwise_row_range():
+    """A whole cross Gram whose y paths are longer is solved as G^T on the DMMA
+    tiles (ops._transpose_cross): bitwise equal to the swapped-orientation
+    row-range call and to the oracle within 1e-10."""
+    from paper_2509_10613_b200 import ops
+    from oracle import oracle as orc
+    rng = np.random.default_rng(31)
+    X = np.cumsum(rng.standard_normal((13, 40, 16)) / 7, axis=1)
+    Y = np.cumsum(rng.standard_normal((9, 57, 16)) / 7, axis=1)
+    xt, yt = torch.as_tensor(X, device="cuda"), torch.as_tensor(Y, device="cuda")
+    for lam in ((0, 0), (1, 0)):
+        G = ops.forward_gram(xt, yt, lam[0], lam[1], 0, 1.0)
+        Gr = ops.forward_gram(xt, yt, lam[0], lam[1], 0, 1.0, rows=(0, 13))
+        assert torch.equal(G, Gr)
+        want = orc.kernel_gram(X, Y, lam[0], lam[1])
+        assert np.abs(G.cpu().numpy() - want).max() / np.abs(want).max() < 1e-10
