@@ -260,6 +260,21 @@ int sk_backward_gram_acc_tf(const double *x, const double *y, int64_t n1, int64_
                             int static_kernel, double sigma, int transform, int64_t row_begin,
                             int64_t row_end, const double *cot, double *values, void *acc_x,
                             void *acc_y, void *workspace, size_t workspace_bytes, void *stream);
+/* sk_backward_gram_acc_tf for the cross-Gram pairs with rows in
+ * [row_begin, row_end) AND columns in [col_begin, col_end) (col_begin a
+ * multiple of 8): a column split sees the same DMMA work items as the whole
+ * call, so its accumulated gradients are bitwise the whole call's.  Linear
+ * static kernel on the DMMA backward only (dyadic order 0, d <= 16, x's fine
+ * axis not shorter than y's), else SK_INVALID_ARGUMENT.  values (nullable):
+ * (row_end - row_begin) x (col_end - col_begin).  The torch layer uses it to
+ * solve cross Grams whose y paths are longer as G^T with the row range of G
+ * as the column range of G^T.  Workspace: sk_backward_gram_acc_tf_workspace_bytes. */
+int sk_backward_gram_acc_cols(const double *x, const double *y, int64_t n1, int64_t n2,
+                              int64_t L1, int64_t L2, int64_t d, int lam1, int lam2,
+                              int transform, int64_t row_begin, int64_t row_end,
+                              int64_t col_begin, int64_t col_end, const double *cot,
+                              double *values, void *acc_x, void *acc_y, void *workspace,
+                              size_t workspace_bytes, void *stream);
 /* FP32-arithmetic Gram backward (linear static kernel, dyadic order 0,
  * d <= 16, cross Grams with L2 <= L1): sk_backward_gram_acc with the forward, recompute and adjoint
  * recurrences in float (small-correction forms) and

@@ -86,6 +86,8 @@ SIGNATURES = {
                                              _sz),
     "sk_backward_gram_acc": ([_dp, _dp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _cd, _i64,
                               _i64, _dp, _dp, _vp, _vp, _vp, _sz, _vp], _ci),
+    "sk_backward_gram_acc_cols": ([_dp, _dp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci, _i64,
+                                   _i64, _i64, _i64, _dp, _dp, _vp, _vp, _vp, _sz, _vp], _ci),
     "sk_backward_gram_acc_f32_workspace_bytes": ([_i64, _i64, _i64, _i64, _i64, _ci, _ci, _ci],
                                                  _sz),
     "sk_backward_gram_acc_f32": ([_dp, _dp, _i64, _i64, _i64, _i64, _i64, _ci, _ci, _i64, _i64,

@@ -659,6 +659,8 @@ static int forward_impl(const void* x, const void* y, int64_t n1, int64_t n2, in
   pb.n2 = (int)n2;
   pb.r0 = (int)r0;
   pb.r1 = (int)r1;
+  pb.c0 = 0;
+  pb.c1 = (int)n2;
   pb.swap = g.swap ? 1 : 0;
   pb.npairs = mode == BATCH ? n1 : 0;
   pb.ldo = n2;
@@ -969,7 +971,7 @@ struct BwdPlan {
 
 static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, int64_t M1c,
                          int64_t M2c, int mode, int64_t npairs, int n2, int r0, int r1,
-                         bool shared_cols, bool f32 = false) {
+                         bool shared_cols, bool f32 = false, int c0 = 0, int c1 = -1) {
   int nch = 1;
   BwdShape s{};
   s.kind = kind;
@@ -1005,7 +1007,7 @@ static int plan_backward(BwdPlan& pl, int kind, int64_t d, int lamR, int lamC, i
     pl.fn = fn;
     pl.threads = 32 * s.WPC;
     pl.smem_bytes = per_warp * (int)sizeof(double) * s.WPC;
-    pl.nitems = super_items(mode, n2, r0, r1);
+    pl.nitems = super_items(mode, n2, r0, r1, c0, c1);
     const int sms = device_sms();
     const int occ = occupancy((const void*)fn, pl.threads, pl.smem_bytes);
     pl.blocks = std::max<int64_t>(1, std::min<int64_t>((pl.nitems + s.WPC - 1) / s.WPC,
@@ -1122,7 +1124,8 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
                          int mode, int64_t r0, int64_t r1, const double* cot, double* values,
                          double* grad_x, double* grad_y, void* ws, size_t ws_bytes,
                          cudaStream_t st, size_t* query, void* acc_x = nullptr,
-                         void* acc_y = nullptr, int tf = TF_NONE, bool f32 = false) {
+                         void* acc_y = nullptr, int tf = TF_NONE, bool f32 = false,
+                         int64_t c0 = 0, int64_t c1 = -1) {
   if (int rc = validate(L1, L2, d, lam1, lam2, kind, sigma)) return rc;
   if (tf < TF_NONE || tf > TF_LEADLAG) return fail(SK_INVALID_ARGUMENT, "unknown path transform");
   // the kernels solve the transformed paths; their point gradients (transformed
@@ -1139,19 +1142,30 @@ static int backward_impl(const double* x, const double* y, int64_t n1, int64_t n
   pb.n2 = (int)n2;
   pb.r0 = (int)r0;
   pb.r1 = (int)r1;
+  // column range (GRAM_CROSS on the DMMA backward; the values buffer is then
+  // (r1 - r0) x (c1 - c0))
+  if (c1 < 0) c1 = n2;
+  if (c0 < 0 || c1 > n2 || c0 > c1 || c0 % SK_SUPER_B != 0 || ((c0 != 0 || c1 != n2) && mode != GRAM_CROSS))
+    return fail(SK_INVALID_ARGUMENT, "column range must be 8-aligned, in bounds, cross Gram only");
+  pb.c0 = (int)c0;
+  pb.c1 = (int)c1;
   pb.swap = g.swap ? 1 : 0;
   pb.npairs = mode == BATCH ? n1 : 0;
-  pb.ldo = n2;
+  pb.ldo = c1 - c0;
   // row-block-major tiles (gram_item_amajor) keep the row accumulators in L2 but put
   // hundreds of warps on the same few paths (atomic contention): measured 1.29 s vs
   // 1.25 s per C3 step with the column-major order, so it stays off
   pb.amajor = 0;
   BwdPlan pl;
-  const int64_t npairs = mode == BATCH ? n1 : (r1 - r0) * n2;
+  const int64_t npairs = mode == BATCH ? n1 : (r1 - r0) * (c1 - c0);
   if (int rc = plan_backward(pl, kind, d, g.lamR, g.lamC, pb.M1c, pb.M2c, mode, npairs,
                              (int)n2, (int)r0, (int)r1,
-                             mode != BATCH && !(mode == GRAM_CROSS && g.swap), f32))
+                             mode != BATCH && !(mode == GRAM_CROSS && g.swap), f32, (int)c0,
+                             (int)c1))
     return rc;
+  if ((c0 != 0 || c1 != n2) && !pl.shape.MMA)
+    return fail(SK_INVALID_ARGUMENT, "column ranges need the DMMA Gram backward (linear, dyadic "
+                                     "order 0, d <= 16, x paths not shorter than y)");
   if (pl.shape.MMA) pb.dpad = pl.shape.DP;  // d <= 4: padded to the DP = 8 instance
   BwdLayout lo;
   lo.prepR = align_up(prep_elems(kind, g.nR, g.LR, pb.dpad) * sizeof(double), 256);
@@ -1508,6 +1522,22 @@ size_t sk_backward_gram_acc_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, 
                                             int symmetric) {
   return sk_backward_gram_acc_tf_workspace_bytes(n1, n2, L1, L2, d, lam1, lam2, static_kernel,
                                                  symmetric, TF_NONE);
+}
+
+int sk_backward_gram_acc_cols(const double* x, const double* y, int64_t n1, int64_t n2,
+                              int64_t L1, int64_t L2, int64_t d, int lam1, int lam2,
+                              int transform, int64_t row_begin, int64_t row_end,
+                              int64_t col_begin, int64_t col_end, const double* cot,
+                              double* values, void* acc_x, void* acc_y, void* ws,
+                              size_t ws_bytes, void* stream) {
+  if (!y) return fail(SK_INVALID_ARGUMENT, "column ranges are for cross Grams (y != NULL)");
+  if (row_begin < 0 || row_end > n1 || row_begin > row_end)
+    return fail(SK_INVALID_ARGUMENT, "row range out of bounds");
+  if (!cot) return fail(SK_INVALID_ARGUMENT, "Gram backward needs the cotangent matrix");
+  if (!acc_x || !acc_y) return fail(SK_INVALID_ARGUMENT, "accumulators missing");
+  return backward_impl(x, y, n1, n2, L1, L2, d, lam1, lam2, LINEAR, 1.0, GRAM_CROSS, row_begin,
+                       row_end, cot, values, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream,
+                       nullptr, acc_x, acc_y, transform, false, col_begin, col_end);
 }
 
 size_t sk_backward_gram_acc_f32_workspace_bytes(int64_t n1, int64_t n2, int64_t L1, int64_t L2,

@@ -49,6 +49,7 @@ struct Problem {
   int64_t npairs;  // BATCH: number of pairs
   int n1, n2;      // Gram sizes (X count, Y count)
   int r0, r1;      // Gram: X rows [r0, r1) handled by this call
+  int c0, c1;      // GRAM_CROSS, DMMA backward: Y columns [c0, c1) (c0 % 8 == 0; 0, n2 = all)
   int swap;        // grid rows are the Y path (fine-axis orientation rule)
   int amajor;      // Gram backward: items enumerated row-block major (see gram_item)
   // output
@@ -265,23 +266,27 @@ __device__ inline void gram_item(const Problem& pb, int64_t item, int P, int& a0
 // result does not depend on how rows are split across calls / GPUs (the
 // chunks and row blocks are the same in every split aligned to 8 rows).
 #define SK_SUPER_B 8
-__host__ __device__ inline int64_t super_chunks(int mode, int n2, int r0, int ab) {
-  if (mode == GRAM_CROSS) return (n2 + SK_SUPER_B - 1) / SK_SUPER_B;
+// (GRAM_CROSS: the chunks of the column range [c0, c1), c0 a multiple of
+// SK_SUPER_B, so a column split sees the same chunks as the whole call)
+__host__ __device__ inline int64_t super_chunks(int mode, int n2, int r0, int ab, int c0 = 0,
+                                                int c1 = -1) {
+  if (mode == GRAM_CROSS)
+    return (int64_t)((c1 < 0 ? n2 : c1) + SK_SUPER_B - 1) / SK_SUPER_B - c0 / SK_SUPER_B;
   return (int64_t)((n2 - 1) / SK_SUPER_B) - (r0 + 8 * ab) / SK_SUPER_B + 1;
 }
-__host__ inline int64_t super_items(int mode, int n2, int r0, int r1) {
+__host__ inline int64_t super_items(int mode, int n2, int r0, int r1, int c0 = 0, int c1 = -1) {
   const int nblk = (r1 - r0 + 7) / 8;
   if (r1 <= r0) return 0;
-  if (mode == GRAM_CROSS) return (int64_t)nblk * super_chunks(mode, n2, r0, 0);
+  if (mode == GRAM_CROSS) return (int64_t)nblk * super_chunks(mode, n2, r0, 0, c0, c1);
   int64_t n = 0;
   for (int ab = 0; ab < nblk; ++ab) n += super_chunks(mode, n2, r0, ab);
   return n;
 }
 __device__ inline void super_item(const Problem& pb, int64_t s, int& ab, int& ch) {
   if (pb.mode == GRAM_CROSS) {
-    const int64_t nc = super_chunks(pb.mode, pb.n2, pb.r0, 0);
+    const int64_t nc = super_chunks(pb.mode, pb.n2, pb.r0, 0, pb.c0, pb.c1);
     ab = (int)(s / nc);
-    ch = (int)(s % nc);
+    ch = pb.c0 / SK_SUPER_B + (int)(s % nc);
     return;
   }
   const int nblk = (pb.r1 - pb.r0 + 7) / 8;

@@ -146,7 +146,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
   super_item(pb, sitem, ab, chunk);
   const int a0 = pb.r0 + 8 * ab;
   const int bbeg = max(chunk * SK_SUPER_B, pb.mode == GRAM_SYM ? a0 : 0);
-  const int bend = min(pb.n2, (chunk + 1) * SK_SUPER_B);
+  const int bend = min(pb.mode == GRAM_CROSS ? pb.c1 : pb.n2, (chunk + 1) * SK_SUPER_B);
   for (int b = bbeg; b < bend; ++b) {
     const bool first_tile = b == bbeg;
     const int a = a0 + g;
@@ -340,7 +340,7 @@ gram_bwd_mma(Problem pb, BwdArgs ba) {
     }
 
     if (ba.values && valid && u == u_star && !(ba.exp & 2))
-      ba.values[(int64_t)(a - pb.r0) * pb.ldo + b] = (double)kval;
+      ba.values[(int64_t)(a - pb.r0) * pb.ldo + (b - pb.c0)] = (double)kval;
 
     // ------------------------------------------------ phase B: reverse sweep
     for (int e = lane; e < 8 * NT8 * DP; e += 32) gcs[e] = 0.0;

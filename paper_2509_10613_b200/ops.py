@@ -443,6 +443,50 @@ def _check_acc(acc, n, L, d, tf, x, name):
     _same_device(acc.blob, x, name)
 
 
+def _transpose_cross_bwd(kind, L1, L2, lam1, lam2, d, tf) -> bool:
+    """Cross-Gram backwards whose y paths are longer run as G^T on the DMMA
+    backward (sk_backward_gram_acc_cols: the row range of G is the column range
+    of G^T, so row splits stay bitwise the whole call): linear kernel, dyadic
+    order 0, transformed dimension <= 16."""
+    if kind != 0 or lam1 or lam2 or os.environ.get("SK_NO_MMA") == "1":
+        return False
+    L1e, de = effective_shape(L1, d, tf)
+    L2e, _ = effective_shape(L2, d, tf)
+    return de <= 16 and L2e > L1e
+
+
+def _gram_backward_t(x, yy, n1, n2, L1, L2, d, lam1, lam2, kind, cot, r0, r1, out, grad_x,
+                     grad_y, acc_x, acc_y, transform, tf):
+    """The transposed cross-Gram backward (see _transpose_cross_bwd)."""
+    lib = _lib.load()
+    dev = x.device
+    own = acc_x is None
+    if own:  # anchors from the original (n1, n2) cotangent, as the C path would
+        ax = GradAcc(n1, L1, d, dev, transform).init(cot, n1, n2, False)
+        ay = GradAcc(n2, L2, d, dev, transform).init(cot, n1, n2, False)
+    else:
+        _check_acc(acc_x, n1, L1, d, tf, x, "acc_x")
+        _check_acc(acc_y, n2, L2, d, tf, x, "acc_y")
+        ax, ay = acc_x, acc_y
+    out_t = None if out is None else torch.empty((n2, r1 - r0), dtype=torch.float64, device=dev)
+    if n1 and n2 and r1 > r0:
+        cot_t = cot.t().contiguous()
+        with _on(dev):
+            nb = _wsq(lib.sk_backward_gram_acc_tf_workspace_bytes, n2, n1, L2, L1, d, lam2, lam1,
+                      kind, 0, tf)
+            ws = _workspace(nb, dev)
+            _lib.check(lib.sk_backward_gram_acc_cols(
+                _ptr(yy), _ptr(x), n2, n1, L2, L1, d, lam2, lam1, tf, 0, n2, r0, r1, _ptr(cot_t),
+                _ptr(out_t), _ptr(ay.blob), _ptr(ax.blob), _ptr(ws), ws.numel(), _stream(dev)))
+    if out is not None and out_t is not None:
+        out.copy_(out_t.t())
+    if not own:
+        return acc_x, acc_y
+    gx = ax.finalize() if grad_x is None else ax.finalize(out=grad_x, accumulate=True)
+    gy = ay.finalize() if grad_y is None else ay.finalize(out=grad_y, accumulate=True)
+    return gx, gy
+
+
 def _gram_backward(x, y, lam1, lam2, kind, sigma, cot, rows, out, grad_x, grad_y, acc_x, acc_y,
                    transform):
     """Shared body of backward_gram (out None) and value_and_grad_gram."""
@@ -450,6 +494,14 @@ def _gram_backward(x, y, lam1, lam2, kind, sigma, cot, rows, out, grad_x, grad_y
     tf = transform_code(transform)
     x, yy, sym, n1, n2, L1, L2, d = _gram_args(x, y)
     r0, r1 = _rows(rows, n1)
+    if not sym and _transpose_cross_bwd(kind, L1, L2, lam1, lam2, d, tf):
+        if grad_x is not None:
+            _grad_buffer(grad_x, x, "grad_x")
+        if grad_y is not None:
+            _grad_buffer(grad_y, yy, "grad_y")
+        return _gram_backward_t(x, yy, n1, n2, L1, L2, d, lam1, lam2, kind,
+                                _cotangent(cot, (n1, n2), x), r0, r1, out, grad_x, grad_y,
+                                acc_x, acc_y, transform, tf)
     cot = _cotangent(cot, (n1, n2), x)
     dev = x.device
     if acc_x is not None:

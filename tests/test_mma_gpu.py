@@ -337,3 +337,32 @@ def test_cross_gram_forward_longer_y_bitwise_row_range():
         assert torch.equal(G, Gr)
         want = orc.kernel_gram(X, Y, lam[0], lam[1])
         assert np.abs(G.cpu().numpy() - want).max() / np.abs(want).max() < 1e-10
+
+
+@pytest.mark.parametrize("tf", [None, "lead_lag"])
+def test_cross_gram_backward_longer_y_transposed(tf):
+    """Cross Grams whose y paths are longer: the backward runs as G^T on the
+    DMMA kernels with the row range of G as the column range of G^T
+    (sk_backward_gram_acc_cols).  Whole call vs the oracle, row splits with
+    accumulators bitwise the whole call, values bitwise the forward."""
+    from paper_2509_10613_b200 import ops
+    from oracle import oracle as orc
+    rng = np.random.default_rng(32)
+    d = 3 if tf else 8
+    X = np.cumsum(rng.standard_normal((21, 30, d)) / 6, axis=1)
+    Y = np.cumsum(rng.standard_normal((11, 45, d)) / 6, axis=1)
+    C = rng.standard_normal((21, 11))
+    xt, yt = torch.as_tensor(X, device="cuda"), torch.as_tensor(Y, device="cuda")
+    Ct = torch.as_tensor(C, device="cuda")
+    G, gx, gy = ops.value_and_grad_gram(xt, yt, 0, 0, 0, 1.0, Ct, transform=tf)
+    assert torch.equal(G, ops.forward_gram(xt, yt, 0, 0, 0, 1.0, transform=tf))
+    if tf is None:
+        wx, wy = orc.gram_backward(X, Y, C, 0, 0)
+        assert rel_err(gx.cpu().numpy(), wx) < 1e-10
+        assert rel_err(gy.cpu().numpy(), wy) < 1e-10
+        assert rel_err(G.cpu().numpy(), orc.kernel_gram(X, Y, 0, 0)) < 1e-10
+    ax = ops.GradAcc(21, 30, d, xt.device, tf).init(Ct, 21, 11, False)
+    ay = ops.GradAcc(11, 45, d, xt.device, tf).init(Ct, 21, 11, False)
+    for rg in ((0, 8), (8, 16), (16, 21)):
+        ops.backward_gram(xt, yt, 0, 0, 0, 1.0, Ct, rows=rg, acc_x=ax, acc_y=ay, transform=tf)
+    assert torch.equal(ax.finalize(), gx) and torch.equal(ay.finalize(), gy)

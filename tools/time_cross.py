@@ -1,7 +1,7 @@
 """Cross Gram with the longer paths on the y side: the whole-Gram call (solved
 as G^T on the DMMA tiles) against the same call with an explicit full row
-range (kept in the swapped orientation, FMA-pipe kernels), and the error
-between the two.  python tools/time_cross.py [n] [Lx] [Ly] [d]"""
+range (the forward keeps the swapped orientation, FMA-pipe kernels; the
+backward is transposed either way), and the difference between the two.  python tools/time_cross.py [n] [Lx] [Ly] [d]"""
 import sys
 
 import numpy as np
